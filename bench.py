@@ -1,0 +1,296 @@
+"""Benchmark: (-Delta + V1)^{-1} apply at 1024^3 FP64 on B200 (BASELINE.json configs[1]).
+
+One step = one SeparableOperator::solve (operators.cpp:42-61) of a 1024^3 real field: 3 forward
+mode-product passes (T^{-1}), the fused spectral divide, 3 backward passes (T). SEM Q^5, 205 cells,
+L = 8 (n = 1024), harmonic V1 = x^2 per axis, rhs = SplitMix64(seed = 1) uniform [-1, 1)
+(harness.cpp:184-189). Fields are 8 GiB each (>> 126 MB L2), so no L2 flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kronop|reference] [--n 1024]
+
+--impl reference times the reference algorithm's CPU implementation (the numpy oracle port: the
+C++ reference cannot be built here) on the host cores, on a bounded sample.
+Multi-GPU: the path does not shard for a single solve at this size (one GPU holds it); N > 1 runs
+N independent replicas (weak scaling, no collective), timed as max over ranks.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAK_FP64_FALLBACK = 35.4  # TFLOP/s, cuBLAS DGEMM sustained measured on this pool (profiles/)
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6449.1, "fp64_tflops": PEAK_FP64_FALLBACK, "fp64_src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        peaks["hbm_gbs"] = m.get("hbm_gbs", peaks["hbm_gbs"])
+    except OSError:
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_dgemm_peak.json")) as f:
+            m = json.load(f)
+        peaks["fp64_tflops"] = m["fp64_tflops_sustained"]
+        peaks["fp64_src"] = "measured cuBLAS DGEMM sustained (profiles/r01_fp64_dgemm_peak.json)"
+    except (OSError, KeyError):
+        pass
+    return peaks
+
+
+class ClockSampler:
+    def __init__(self, gpu_index=0):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out = self.proc.communicate()[0]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in out.strip().splitlines():
+            p = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, v, device):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def workload_config(n):
+    cells = (n + 1) // 5
+    assert cells * 5 - 1 == n, "n must be 5*cells - 1 ... use n = 1024 (205 cells)"
+    return cells
+
+
+# -------------------------------------------------------------------------- CPU arm --
+def cpu_reference_sample(n_sample=514, reps=1):
+    """Oracle (numpy/OpenBLAS, all host threads) solve at n_sample^3 of the same workload family;
+    returns (seconds per sample solve, n_sample)."""
+    from oracle import kronop_oracle as K
+    cells = (n_sample + 1) // 5
+    g = K.Grid.sem(8.0, cells, 5, 3)
+    pot = K.build_potential("harmonic", g)
+    op = g.separable_operator(pot.separable)
+    b = K.seeded_field(g.shape, 1)
+    op.solve(b)  # warm
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        op.solve(b)
+    return (time.perf_counter() - t0) / reps, g.shape[0]
+
+
+def run_reference(args):
+    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return 0
+    n = args.n
+    N = n ** 3
+    times = []
+    ns = None
+    for _ in range(args.warmup):
+        cpu_reference_sample()
+    for _ in range(args.steps):
+        t, ns = cpu_reference_sample()
+        times.append(t)
+    t = float(np.median(times))
+    t_full = t * (n / ns) ** 4  # 12 n^4 flops per solve
+    gdofs = N / t_full / 1e9
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": "(-Delta+V1)^-1 apply GDoF/s at 1024^3 fp64",
+        "value": gdofs, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "3D (-Delta+V1)^-1 solve, harmonic V1, SEM Q5 205 cells L=8, n=%d" % n,
+                   "n": n, "dof": N, "sample_n": ns},
+        "cpu_baseline": {"value": gdofs, "unit": "GDoF/s", "cores": cores, "kind": "port",
+                         "sample": "numpy/OpenBLAS oracle solve at %d^3 (same SEM Q5 family), "
+                                   "median of %d, scaled to %d^3 by n^4 (12 n^4 flops)" % (
+                                       ns, args.steps, n)},
+        "e2e": {"value": gdofs, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------------------- GPU arm --
+def run_kronop(args):
+    import torch
+    world, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    from paper_2605_20491_b200 import api as A
+    from paper_2605_20491_b200 import potentials as P
+    peaks = load_peaks()
+    n = args.n
+    cells = workload_config(n)
+    grid = A.Grid.sem(8.0, cells, 5, 3)
+    pot = P.build_potential("harmonic", grid)
+    ctx = A.Context(local)
+    op = grid.separable_operator(ctx, pot.separable)
+    N = grid.node_count()
+    b = A.splitmix_uniform(ctx, 1, N)
+    x = torch.empty_like(b)
+    stream = ctx.stream
+    # warm-up (also sizes the workspace)
+    for _ in range(args.warmup):
+        op.solve(b, out=x)
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    sampler = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        op.solve(b, out=x)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop()
+    t_step = e0.elapsed_time(e1) / 1e3 / args.steps
+    launches = ctx.launch_count() - launches0
+    t_step = max_over_ranks(world, t_step, "cuda:%d" % local)
+    value = world * N / t_step / 1e9
+
+    # dominant kernel: one mode-product pass (axis 2, forward), CUDA events on the ctx stream
+    y = torch.empty_like(b)
+    for _ in range(2):
+        op.transform_pass(b, 2, True, out=y)
+    reps = 5
+    pe0 = torch.cuda.Event(enable_timing=True)
+    pe1 = torch.cuda.Event(enable_timing=True)
+    per_axis = []
+    for axis in range(3):
+        torch.cuda.synchronize()
+        pe0.record(stream)
+        for _ in range(reps):
+            op.transform_pass(b, axis, True, out=y)
+        pe1.record(stream)
+        torch.cuda.synchronize()
+        per_axis.append(pe0.elapsed_time(pe1) / 1e3 / reps)
+    t_pass = float(np.mean(per_axis))
+    pass_flops = 2.0 * n * N
+    achieved = pass_flops / t_pass / 1e12
+    del y
+
+    # end-to-end through the C-ABI host entry point (pinned host buffers, H2D + D2H inside)
+    bh = torch.empty(N, dtype=torch.float64, pin_memory=True)
+    xh = torch.empty(N, dtype=torch.float64, pin_memory=True)
+    bh.copy_(b.cpu())
+    bn, xn = bh.numpy(), xh.numpy()
+    op.solve_host(bn, xn)  # warm (sizes the staging buffers)
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        op.solve_host(bn, xn)
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    t_e2e = max_over_ranks(world, t_e2e, "cuda:%d" % local)
+    e2e_value = world * N / t_e2e / 1e9
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        ts, ns = cpu_reference_sample()
+        t_full = ts * (n / ns) ** 4
+        cpu = {"value": N / t_full / 1e9, "unit": "GDoF/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": "numpy/OpenBLAS oracle solve at %d^3 (same SEM Q5 family), scaled to "
+                         "%d^3 by n^4" % (ns, n)}
+    if rank == 0:
+        line = {
+            "metric": "(-Delta+V1)^-1 apply GDoF/s at 1024^3 fp64",
+            "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "3D (-Delta+V1)^-1 solve, harmonic V1, SEM Q5 205 cells L=8, "
+                                   "n=%d (BASELINE configs[1])" % n,
+                       "n": n, "dof": N, "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs (8 GiB/field) larger than L2; no flush"},
+            "tflops": 12.0 * n ** 4 / t_step / 1e12,
+            "roofline": {"bound": "tensor", "achieved": achieved,
+                         "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                         "frac": achieved / peaks["fp64_tflops"], "traffic": None,
+                         "kernel": "mode_product_kernel (FP64 DMMA), 1024^3 pass = 2 n^4 flops",
+                         "per_axis_ms": [t * 1e3 for t in per_axis],
+                         "peak_src": peaks["fp64_src"]},
+            "e2e": {"value": e2e_value, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * N,
+                    "d2h_bytes_per_step": 8 * N, "ms_per_step": t_e2e * 1e3},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kronop", choices=["kronop", "reference"])
+    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_kronop(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,616 @@
+"""Python mirror of the reference's operator API over the C-ABI (include/kronop_cuda.h).
+
+Used by the tests and bench.py. Names follow proj/include/kronop/*.hpp: Grid, SeparableOperator,
+FullOperator, pcg, inverse_iteration, gpe_gradient_flow, qhop_step, yoshida_step, evolve,
+mode_product, kron_apply, inner, mass_field, direct_sum_grid. Fields are torch CUDA tensors
+(float64 for RealField, complex128 for ComplexField, flat, axis 0 fastest). Device memory and the
+stream come from torch; all arithmetic runs in libkronop.so (there is no CPU path here).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import check, lib
+
+_PD = C.POINTER(C.c_double)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_PD)
+
+
+def _arr_of_ptrs(arrs):
+    t = (_PD * len(arrs))()
+    for i, a in enumerate(arrs):
+        t[i] = _dptr(a) if a is not None else _PD()
+    return t
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("kronop fields must be CUDA tensors")
+    if not t.is_contiguous():
+        raise ValueError("kronop fields must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+# ------------------------------------------------------------------------------ context --
+class Context:
+    """kronop_ctx on one device with its own CUDA stream, ordered against torch's current
+    stream at every call boundary (event waits, no host syncs)."""
+
+    def __init__(self, device: int = 0):
+        lib()
+        self.device = device
+        with torch.cuda.device(device):
+            self.stream = torch.cuda.Stream(device=device)
+        h = C.c_void_p()
+        check(lib().kronop_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h)))
+        self.h = h
+
+    def enter(self):
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+
+    def leave(self):
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
+
+    def synchronize(self):
+        check(lib().kronop_ctx_synchronize(self.h))
+
+    def launch_count(self) -> int:
+        v = C.c_uint64()
+        check(lib().kronop_ctx_launch_count(self.h, C.byref(v)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().kronop_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _Call:
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+
+    def __enter__(self):
+        self.ctx.enter()
+
+    def __exit__(self, *a):
+        self.ctx.leave()
+
+
+# ------------------------------------------------------------------ host setup (C++) --
+def gll_rule(degree: int):
+    n = degree + 1
+    x, w, d = np.zeros(n), np.zeros(n), np.zeros(n * n)
+    check(lib().kronop_host_gll_rule(degree, _dptr(x), _dptr(w), _dptr(d)))
+    return x, w, d.reshape(n, n, order="F")
+
+
+def gauss_legendre(points: int):
+    x, w = np.zeros(points), np.zeros(points)
+    check(lib().kronop_host_gauss_legendre(points, _dptr(x), _dptr(w)))
+    return x, w
+
+
+@dataclass
+class Basis1D:
+    """proj/include/kronop/basis1d.hpp:17-29 (SEM axis)."""
+    half_width: float
+    cell_count: int
+    degree: int
+    nodes: np.ndarray
+    mass: np.ndarray
+    stiffness: np.ndarray
+
+    @property
+    def size(self):
+        return len(self.nodes)
+
+
+def assemble_sem(half_width: float, cell_count: int, degree: int) -> Basis1D:
+    n = cell_count * degree - 1
+    if n < 1:
+        raise L.ParameterError(L.KRONOP_EPARAM, "assemble_sem: no interior nodes")
+    x, m, s = np.zeros(n), np.zeros(n), np.zeros(n * n)
+    check(lib().kronop_host_assemble_sem(half_width, cell_count, degree, _dptr(x), _dptr(m),
+                                         _dptr(s)))
+    return Basis1D(half_width, cell_count, degree, x, m, s.reshape(n, n, order="F"))
+
+
+def interp_matrix(coarse: Basis1D, fine: Basis1D) -> np.ndarray:
+    p = np.zeros(fine.size * coarse.size)
+    check(lib().kronop_host_interp_matrix(coarse.half_width, coarse.cell_count, coarse.degree,
+                                          fine.cell_count, fine.degree, _dptr(p)))
+    return p.reshape(fine.size, coarse.size, order="F")
+
+
+def sym_eig(a: np.ndarray):
+    n = a.shape[0]
+    af = np.asfortranarray(a, dtype=np.float64)
+    lam, q = np.zeros(n), np.zeros(n * n)
+    check(lib().kronop_host_sym_eig(n, af.ctypes.data_as(_PD), _dptr(lam), _dptr(q)))
+    return lam, q.reshape(n, n, order="F")
+
+
+@dataclass
+class AxisEigens:
+    """proj/include/kronop/axis.hpp:23-29."""
+    eigenvalues: np.ndarray
+    transform: np.ndarray
+    inverse_transform: np.ndarray
+
+    @property
+    def size(self):
+        return len(self.eigenvalues)
+
+
+_AXIS_CACHE = {}
+
+
+def build_axis(basis: Basis1D, f: Optional[Callable] = None, fvals: Optional[np.ndarray] = None):
+    """build_axis for an SEM basis (axis.cpp:55-74) via the C++ Householder+QL eigensolver."""
+    n = basis.size
+    if fvals is None:
+        fvals = np.array([f(float(x)) for x in basis.nodes]) if f is not None else np.zeros(n)
+    fvals = np.ascontiguousarray(fvals, dtype=np.float64)
+    key = (basis.half_width, basis.cell_count, basis.degree, fvals.tobytes())
+    if key in _AXIS_CACHE:
+        return _AXIS_CACHE[key]
+    lam, t, ti = np.zeros(n), np.zeros(n * n), np.zeros(n * n)
+    check(lib().kronop_host_build_sem_axis(basis.half_width, basis.cell_count, basis.degree,
+                                           _dptr(fvals), _dptr(lam), _dptr(t), _dptr(ti)))
+    ax = AxisEigens(lam, t.reshape(n, n, order="F"), ti.reshape(n, n, order="F"))
+    _AXIS_CACHE[key] = ax
+    return ax
+
+
+# ---------------------------------------------------------------------------- operators --
+class SeparableOperator:
+    """proj/include/kronop/operators.hpp:15-53, resident on the device."""
+
+    def __init__(self, ctx: Context, axes: Sequence[AxisEigens], shift: float = 0.0,
+                 mass: Optional[Sequence[np.ndarray]] = None):
+        self.ctx = ctx
+        self.axes = list(axes)
+        d = len(axes)
+        self.shape = tuple(a.size for a in axes)
+        n = (C.c_int * d)(*self.shape)
+        self._keep = [np.asfortranarray(a.transform) for a in axes] + \
+                     [np.asfortranarray(a.inverse_transform) for a in axes] + \
+                     [np.ascontiguousarray(a.eigenvalues) for a in axes]
+        T = _arr_of_ptrs(self._keep[:d])
+        Ti = _arr_of_ptrs(self._keep[d:2 * d])
+        lam = _arr_of_ptrs(self._keep[2 * d:])
+        self.mass = [np.ascontiguousarray(m, dtype=np.float64) for m in mass] if mass else None
+        mp = _arr_of_ptrs(self.mass) if self.mass else None
+        h = C.c_void_p()
+        check(lib().kronop_op_create(ctx.h, d, n, T, Ti, lam, mp, shift, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().kronop_op_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def dim(self):
+        return len(self.shape)
+
+    @property
+    def size(self):
+        return int(np.prod(self.shape))
+
+    def info(self):
+        s, lo, hi, n = C.c_double(), C.c_double(), C.c_double(), C.c_size_t()
+        check(lib().kronop_op_info(self.h, C.byref(s), C.byref(lo), C.byref(hi), C.byref(n)))
+        return s.value, lo.value, hi.value
+
+    @property
+    def shift(self):
+        return self.info()[0]
+
+    def set_shift(self, shift: float):
+        check(lib().kronop_op_set_shift(self.h, shift))
+
+    def min_eigenvalue(self):
+        return self.info()[1]
+
+    def max_eigenvalue(self):
+        return self.info()[2]
+
+    def _out(self, like, out):
+        return torch.empty_like(like) if out is None else out
+
+    def apply(self, u: torch.Tensor, out=None) -> torch.Tensor:
+        out = self._out(u, out)
+        with _Call(self.ctx):
+            check(lib().kronop_sep_apply(self.ctx.h, self.h, _ptr(u), int(u.is_complex()), _ptr(out)))
+        return out
+
+    def solve(self, b: torch.Tensor, out=None) -> torch.Tensor:
+        out = self._out(b, out)
+        with _Call(self.ctx):
+            check(lib().kronop_sep_solve(self.ctx.h, self.h, _ptr(b), int(b.is_complex()), _ptr(out)))
+        return out
+
+    def propagate(self, psi: torch.Tensor, dt: float, out=None) -> torch.Tensor:
+        if not psi.is_complex():
+            raise ValueError("propagate needs a complex128 field")
+        out = self._out(psi, out)
+        with _Call(self.ctx):
+            check(lib().kronop_sep_propagate(self.ctx.h, self.h, _ptr(psi), dt, _ptr(out)))
+        return out
+
+    def ground_state(self) -> torch.Tensor:
+        out = torch.empty(self.size, dtype=torch.float64, device="cuda:%d" % self.ctx.device)
+        with _Call(self.ctx):
+            check(lib().kronop_op_ground_state(self.ctx.h, self.h, _ptr(out)))
+        return out
+
+    def eigenvalue_grid(self) -> torch.Tensor:
+        out = torch.empty(self.size, dtype=torch.float64, device="cuda:%d" % self.ctx.device)
+        with _Call(self.ctx):
+            check(lib().kronop_op_eigenvalue_grid(self.ctx.h, self.h, _ptr(out)))
+        return out
+
+    def transform_pass(self, x: torch.Tensor, axis: int, forward: bool = True, out=None):
+        """One mode-product pass with the resident T^{-1} (forward) or T (kronop_op_pass)."""
+        out = self._out(x, out)
+        with _Call(self.ctx):
+            check(lib().kronop_op_pass(self.ctx.h, self.h, axis, int(forward), _ptr(x),
+                                       int(x.is_complex()), _ptr(out)))
+        return out
+
+    # host-buffer (end-to-end) variants
+    def solve_host(self, b: np.ndarray, out: np.ndarray, is_complex=False):
+        check(lib().kronop_sep_solve_host(self.ctx.h, self.h, C.c_void_p(b.ctypes.data),
+                                          int(is_complex), C.c_void_p(out.ctypes.data)))
+        return out
+
+
+@dataclass
+class FullOperator:
+    """sep + optional V2 diagonal (operators.hpp:56-62)."""
+    sep: SeparableOperator
+    diagonal: Optional[torch.Tensor] = None
+
+    def apply(self, u: torch.Tensor, sigma: float = 0.0, out=None) -> torch.Tensor:
+        out = torch.empty_like(u) if out is None else out
+        with _Call(self.sep.ctx):
+            check(lib().kronop_full_apply(self.sep.ctx.h, self.sep.h, _ptr(self.diagonal), sigma,
+                                          _ptr(u), int(u.is_complex()), _ptr(out)))
+        return out
+
+
+# ------------------------------------------------------------------------------ tensor --
+def _shape_arr(shape):
+    return (C.c_int * len(shape))(*shape)
+
+
+def mode_product(ctx: Context, x: torch.Tensor, shape, a: np.ndarray, axis: int) -> torch.Tensor:
+    """tensor.hpp:79-81."""
+    a = np.asfortranarray(a, dtype=np.float64)
+    m = a.shape[0]
+    out_shape = list(shape)
+    out_shape[axis] = m
+    out = torch.empty(int(np.prod(out_shape)), dtype=x.dtype, device=x.device)
+    with _Call(ctx):
+        check(lib().kronop_mode_product(ctx.h, _ptr(x), len(shape), _shape_arr(shape),
+                                        int(x.is_complex()), a.ctypes.data_as(_PD), m, axis,
+                                        _ptr(out)))
+    return out
+
+
+def kron_apply(ctx: Context, x: torch.Tensor, shape, mats) -> torch.Tensor:
+    """tensor.hpp:85-87 (None = identity)."""
+    keep = [np.asfortranarray(a, dtype=np.float64) if a is not None else None for a in mats]
+    ms = [a.shape[0] if a is not None else 0 for a in keep]
+    out_shape = [ms[i] if keep[i] is not None else shape[i] for i in range(len(shape))]
+    out = torch.empty(int(np.prod(out_shape)), dtype=x.dtype, device=x.device)
+    with _Call(ctx):
+        check(lib().kronop_kron_apply(ctx.h, _ptr(x), len(shape), _shape_arr(shape),
+                                      int(x.is_complex()), _arr_of_ptrs(keep),
+                                      _shape_arr(ms), _ptr(out)))
+    return out
+
+
+def inner(ctx: Context, u: torch.Tensor, v: torch.Tensor, shape, mass=None):
+    """tensor.hpp:89-98: conjugate-linear in u; mass = per-axis weights or None (plain)."""
+    res = np.zeros(2)
+    mk = [np.ascontiguousarray(m, dtype=np.float64) for m in mass] if mass is not None else None
+    with _Call(ctx):
+        check(lib().kronop_inner(ctx.h, _ptr(u), _ptr(v), len(shape), _shape_arr(shape),
+                                 int(u.is_complex()), _arr_of_ptrs(mk) if mk else None,
+                                 _dptr(res)))
+    return complex(res[0], res[1]) if u.is_complex() else float(res[0])
+
+
+def norm(ctx, u, shape, mass=None) -> float:
+    s = inner(ctx, u, u, shape, mass)
+    return math.sqrt(s.real if isinstance(s, complex) else s)
+
+
+def mass_field(ctx: Context, shape, mass) -> torch.Tensor:
+    out = torch.empty(int(np.prod(shape)), dtype=torch.float64, device="cuda:%d" % ctx.device)
+    mk = [np.ascontiguousarray(m, dtype=np.float64) for m in mass]
+    with _Call(ctx):
+        check(lib().kronop_mass_field(ctx.h, len(shape), _shape_arr(shape), _arr_of_ptrs(mk),
+                                      _ptr(out)))
+    return out
+
+
+def direct_sum_grid(ctx: Context, values) -> torch.Tensor:
+    shape = [len(v) for v in values]
+    out = torch.empty(int(np.prod(shape)), dtype=torch.float64, device="cuda:%d" % ctx.device)
+    vk = [np.ascontiguousarray(v, dtype=np.float64) for v in values]
+    with _Call(ctx):
+        check(lib().kronop_direct_sum_grid(ctx.h, len(shape), _shape_arr(shape), _arr_of_ptrs(vk),
+                                           _ptr(out)))
+    return out
+
+
+def splitmix_uniform(ctx: Context, seed: int, count: int, start: int = 0) -> torch.Tensor:
+    """SplitMix64 uniform_pm1 stream (rng.hpp:16-35) generated on the device."""
+    out = torch.empty(count, dtype=torch.float64, device="cuda:%d" % ctx.device)
+    with _Call(ctx):
+        check(lib().kronop_splitmix_uniform(ctx.h, seed, start, count, _ptr(out)))
+    return out
+
+
+# --------------------------------------------------------------------------------- grid --
+class Grid:
+    """Isotropic SEM tensor grid (proj/include/kronop/grid.hpp:16-39, grid.cpp:14-22)."""
+
+    def __init__(self, axes: List[Basis1D]):
+        self.axes = axes
+
+    @staticmethod
+    def sem(half_width: float, cell_count: int, degree: int, dimension: int) -> "Grid":
+        if dimension < 1 or dimension > 9:
+            raise L.ParameterError(L.KRONOP_EPARAM, "Grid: dimension must be in [1, 9]")
+        b = assemble_sem(half_width, cell_count, degree)
+        return Grid([b] * dimension)
+
+    @property
+    def dim(self):
+        return len(self.axes)
+
+    @property
+    def shape(self):
+        return tuple(a.size for a in self.axes)
+
+    @property
+    def mass(self):
+        return [a.mass for a in self.axes]
+
+    def node_count(self):
+        return int(np.prod(self.shape))
+
+    def coords(self):
+        d = self.dim
+        out = []
+        for a in range(d):
+            shp = [1] * d
+            shp[d - 1 - a] = self.axes[a].size
+            out.append(self.axes[a].nodes.reshape(shp))
+        return out
+
+    def sample(self, f_vec) -> np.ndarray:
+        """Nodal sampling (grid.cpp:53-69) on the host; f_vec gets per-axis coordinates."""
+        v = f_vec(self.coords())
+        return np.ascontiguousarray(np.broadcast_to(v, tuple(reversed(self.shape))).reshape(-1),
+                                    dtype=np.float64)
+
+    def separable_operator(self, ctx: Context, per_axis=None, shift: float = 0.0):
+        """grid.cpp:71-83: per_axis = list of scalar functions (or None = 0)."""
+        axes = []
+        for a in range(self.dim):
+            f = per_axis[a] if per_axis else None
+            fv = np.array([f(float(x)) for x in self.axes[a].nodes]) if f else None
+            axes.append(build_axis(self.axes[a], f=None, fvals=fv))
+        return SeparableOperator(ctx, axes, shift, mass=self.mass)
+
+    def laplacian(self, ctx: Context, shift: float = 0.0):
+        return self.separable_operator(ctx, None, shift)
+
+
+# ----------------------------------------------------------------------------- drivers --
+@dataclass
+class PcgConfig:
+    """pcg.hpp:10-20."""
+    rel_tol: float = 1e-12
+    max_iter: int = 500
+    record_history: bool = False
+    preconditioned_norm: bool = False
+    stagnation_window: int = 0
+
+    def c(self):
+        return L.PcgConfig(self.rel_tol, self.max_iter, int(self.record_history),
+                           int(self.preconditioned_norm), self.stagnation_window)
+
+
+@dataclass
+class PcgReport:
+    iterations: int = 0
+    final_residual: float = 0.0
+    converged: bool = False
+    history: list = field(default_factory=list)
+
+
+def apply_map(op: SeparableOperator, diag=None, sigma: float = 0.0):
+    """KRONOP_MAP_APPLY: v -> op.apply(v) + diag v - sigma v."""
+    return (L.LinearMap(op.h, L.KRONOP_MAP_APPLY, _ptr(diag), sigma, None), (op, diag))
+
+
+def solve_map(op: SeparableOperator, scale=None):
+    """KRONOP_MAP_SOLVE: r -> scale .* op.solve(scale .* r)."""
+    return (L.LinearMap(op.h, L.KRONOP_MAP_SOLVE, None, 0.0, _ptr(scale)), (op, scale))
+
+
+def pcg(apply_a, precond, b: torch.Tensor, x: torch.Tensor, config: PcgConfig = PcgConfig()):
+    """pcg.hpp:36-37; x is updated in place (warm start in, solution out)."""
+    ctx = apply_a[1][0].ctx
+    rep = L.PcgReport()
+    hist = np.zeros(config.max_iter + 2)
+    cfg = config.c()
+    with _Call(ctx):
+        check(lib().kronop_pcg(ctx.h, C.byref(apply_a[0]), C.byref(precond[0]), _ptr(b), _ptr(x),
+                               C.byref(cfg), C.byref(rep),
+                               _dptr(hist) if config.record_history else None))
+    return PcgReport(rep.iterations, rep.final_residual, bool(rep.converged),
+                     list(hist[:rep.history_len]) if config.record_history else [])
+
+
+@dataclass
+class InverseIterationConfig:
+    """ground_state.hpp:24-32."""
+    shift_mode: str = "fraction"
+    shift_fraction: float = 0.9
+    shift_offset: float = 1e-4
+    eig_rel_tol: float = 1e-12
+    max_outer: int = 60
+    inner: PcgConfig = field(default_factory=lambda: PcgConfig(stagnation_window=100))
+
+
+@dataclass
+class EigenpairResult:
+    eigenvalue: float
+    eigenvector: torch.Tensor
+    outer_iterations: int
+    total_inner_iterations: int
+    inner_per_outer: list
+    converged: bool
+
+
+def inverse_iteration(op: FullOperator, config: InverseIterationConfig, initial: torch.Tensor):
+    """ground_state.hpp:47-56 (op.sep must carry mass weights)."""
+    ctx = op.sep.ctx
+    mode = {"fraction": 0, "offset": 1, "zero": 2}[config.shift_mode]
+    cfg = L.InverseIterationConfig(mode, config.shift_fraction, config.shift_offset,
+                                   config.eig_rel_tol, config.max_outer, config.inner.c())
+    res = L.EigenpairResult()
+    per = (C.c_int * max(1, config.max_outer))()
+    vec = torch.empty_like(initial)
+    with _Call(ctx):
+        check(lib().kronop_inverse_iteration(ctx.h, op.sep.h, _ptr(op.diagonal), C.byref(cfg),
+                                             _ptr(initial), _ptr(vec), C.byref(res), per))
+    inner = list(per[:res.outer_iterations]) if op.diagonal is not None else []
+    return EigenpairResult(res.eigenvalue, vec, res.outer_iterations, res.total_inner_iterations,
+                           inner, bool(res.converged))
+
+
+@dataclass
+class GpeFlowConfig:
+    """gpe.hpp:30-40."""
+    kind: str = "h1"
+    step: float = 0.1
+    metric_shift: float = 20.0
+    energy_rel_tol: float = 1e-12
+    max_iterations: int = 20000
+    inner: PcgConfig = field(default_factory=lambda: PcgConfig(stagnation_window=100))
+    init: str = "eigenfunction"
+    record_history: bool = False
+
+
+@dataclass
+class GpeResult:
+    state: torch.Tensor
+    energy: float
+    eigenvalue: float
+    iterations: int
+    linear_solves: int
+    converged: bool
+    history: list
+
+
+def gpe_energy(ham: FullOperator, beta: float, u: torch.Tensor) -> float:
+    e = C.c_double()
+    ctx = ham.sep.ctx
+    with _Call(ctx):
+        check(lib().kronop_gpe_energy(ctx.h, ham.sep.h, _ptr(ham.diagonal), beta, _ptr(u),
+                                      C.byref(e)))
+    return e.value
+
+
+def gpe_gradient_flow(ham: FullOperator, laplacian: SeparableOperator, beta: float,
+                      config: GpeFlowConfig, initial: Optional[torch.Tensor] = None):
+    """gpe.hpp:65-66."""
+    ctx = ham.sep.ctx
+    cfg = L.GpeConfig({"h1": 0, "au": 1}[config.kind], config.step, config.metric_shift,
+                      config.energy_rel_tol, config.max_iterations, config.inner.c(),
+                      {"constant": 0, "eigenfunction": 1, "supplied": 2}[config.init],
+                      int(config.record_history))
+    res = L.GpeResult()
+    hist = np.zeros(5 * max(1, config.max_iterations)) if config.record_history else None
+    state = torch.empty(ham.sep.size, dtype=torch.float64, device="cuda:%d" % ctx.device)
+    with _Call(ctx):
+        check(lib().kronop_gpe_gradient_flow(ctx.h, ham.sep.h, _ptr(ham.diagonal), laplacian.h,
+                                             beta, C.byref(cfg), _ptr(initial), _ptr(state),
+                                             C.byref(res), _dptr(hist) if hist is not None else None))
+    rows = hist[:5 * res.history_len].reshape(-1, 5).tolist() if hist is not None else []
+    return GpeResult(state, res.energy, res.eigenvalue, res.iterations, res.linear_solves,
+                     bool(res.converged), rows)
+
+
+def yoshida_coeffs():
+    g1, g2 = C.c_double(), C.c_double()
+    check(lib().kronop_yoshida_coeffs(C.byref(g1), C.byref(g2)))
+    return g1.value, g2.value
+
+
+def qhop_step(a: SeparableOperator, b_diag: torch.Tensor, psi: torch.Tensor, h: float, m: int):
+    out = torch.empty_like(psi)
+    with _Call(a.ctx):
+        check(lib().kronop_qhop_step(a.ctx.h, a.h, _ptr(b_diag), _ptr(psi), h, m, _ptr(out)))
+    return out
+
+
+def yoshida_step(a: SeparableOperator, b_diag: torch.Tensor, psi: torch.Tensor, h: float, m: int):
+    out = torch.empty_like(psi)
+    with _Call(a.ctx):
+        check(lib().kronop_yoshida_step(a.ctx.h, a.h, _ptr(b_diag), _ptr(psi), h, m, _ptr(out)))
+    return out
+
+
+@dataclass
+class SplitSpec:
+    """splitting.hpp:26-33."""
+    quad_points: int = 1
+    composition: str = "single"
+    dt: float = 0.0
+    total_time: float = 0.0
+    merge_across_steps: bool = False
+    mass_weighted_error: bool = False
+
+
+def evolve(spec: SplitSpec, a: SeparableOperator, b_diag: torch.Tensor, psi0: torch.Tensor,
+           exact: Optional[SeparableOperator] = None, stationary_eigenvalue: float = 0.0):
+    """splitting.hpp:68-69. Returns (state, error, steps)."""
+    cs = L.SplitSpec(spec.quad_points, {"single": 0, "yoshida": 1}[spec.composition], spec.dt,
+                     spec.total_time, int(spec.merge_across_steps), int(spec.mass_weighted_error))
+    state = torch.empty_like(psi0)
+    err = C.c_double()
+    steps = C.c_int()
+    with _Call(a.ctx):
+        check(lib().kronop_evolve(a.ctx.h, C.byref(cs), a.h, _ptr(b_diag), _ptr(psi0),
+                                  exact.h if exact is not None else None, stationary_eigenvalue,
+                                  _ptr(state), C.byref(err), C.byref(steps)))
+    return state, err.value, steps.value

@@ -1,0 +1,654 @@
+// extern "C" boundary (include/kronop_cuda.h): context, operators, tensor ops and the host setup
+// entry points. Drivers (pcg / inverse iteration / gpe / splitting) are in drivers.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "context.cuh"
+#include "host_setup.hpp"
+
+namespace kronop_dev {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return KRONOP_OK;
+  } catch (const Error& e) {
+    set_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return KRONOP_ECAPABILITY;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return KRONOP_ERUNTIME;
+  }
+}
+
+View make_view(int d, const int* shape, int cplx) {
+  param_check(d >= 1 && d <= KRONOP_MAX_DIM, "TensorField: dimension must be in [1, 9]");
+  View v;
+  v.cplx = cplx ? 1 : 0;
+  v.nd = d + v.cplx;
+  if (v.cplx) v.ext[0] = 2;
+  for (int a = 0; a < d; ++a) {
+    param_check(shape[a] >= 1, "TensorField: extents must be positive");
+    v.ext[a + v.cplx] = shape[a];
+  }
+  return v;
+}
+
+void ensure_scratch(kronop_ctx& ctx, size_t doubles) {
+  if (doubles <= ctx.scratch_cap) return;
+  for (auto& p : ctx.scratch) {
+    if (p) KCUDA(cudaFreeAsync(p, ctx.stream));
+    p = nullptr;
+  }
+  ctx.scratch_cap = 0;
+  for (auto& p : ctx.scratch) KCUDA(cudaMallocAsync(&p, doubles * sizeof(double), ctx.stream));
+  ctx.scratch_cap = doubles;
+}
+
+double* ensure_tmp(kronop_ctx& ctx, size_t doubles) {
+  if (doubles > ctx.tmp_cap) {
+    if (ctx.tmp) KCUDA(cudaFreeAsync(ctx.tmp, ctx.stream));
+    ctx.tmp = nullptr;
+    KCUDA(cudaMallocAsync(&ctx.tmp, doubles * sizeof(double), ctx.stream));
+    ctx.tmp_cap = doubles;
+  }
+  return ctx.tmp;
+}
+
+void run_pass(kronop_ctx& ctx, const double* x, double* y, View& v, int raxis, const double* a,
+              int lda, int m, const EpiParams& ep) {
+  PassShape ps;
+  for (int i = 0; i < raxis; ++i) ps.pre *= v.ext[i];
+  for (int i = raxis + 1; i < v.nd; ++i) ps.post *= v.ext[i];
+  ps.nk = static_cast<int>(v.ext[raxis]);
+  ps.m = m;
+  launch_mode_product(ctx.stream, x, y, a, lda, ps, ep);
+  ctx.ws.launches += 1;
+  v.ext[raxis] = m;
+}
+
+void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
+                   SepKind kind, double shift, double dt, const double* diag, double sigma) {
+  View v = make_view(op.d, op.n, cplx);
+  ensure_scratch(ctx, static_cast<size_t>(v.total()));
+  const int d = op.d;
+  const double* cur = in;
+  for (int k = 0; k < 2 * d; ++k) {
+    const bool forward = k < d;
+    const int axis = forward ? k : k - d;
+    double* dst = (k == 2 * d - 1) ? out : ctx.scratch[k % 2];
+    EpiParams ep;
+    if (k == d - 1) {
+      ep.kind = kind == SEP_APPLY ? EPI_SPEC_MUL : kind == SEP_SOLVE ? EPI_SPEC_DIV : EPI_SPEC_PHASE;
+      ep.axis = axis + v.cplx;
+      ep.ndims = v.nd;
+      for (int i = 0; i < v.nd; ++i) ep.ext[i] = v.ext[i];
+      for (int a = 0; a < d; ++a) ep.lam[a + v.cplx] = op.lam[a];
+      ep.shift = shift;
+      ep.dt = dt;
+      ep.cplx = v.cplx;
+    }
+    if (k == 2 * d - 1 && (diag != nullptr || sigma != 0.0)) {
+      ep.kind = EPI_AXPY_DIAG;
+      ep.diag = diag;
+      ep.u = in;
+      ep.sigma = sigma;
+      ep.cplx = v.cplx;
+    }
+    run_pass(ctx, cur, dst, v, axis + v.cplx, forward ? op.fwd[axis] : op.bwd[axis], op.lda[axis],
+             op.n[axis], ep);
+    cur = dst;
+  }
+}
+
+// min |lambda - shift| over the direct-sum grid (device, deterministic min-reduction)
+struct GapArgs {
+  int d;
+  long long n[KRONOP_MAX_DIM];
+  const double* lam[KRONOP_MAX_DIM];
+  double shift;
+  long long total;
+};
+__global__ void k_gap_partial(GapArgs a, double* partials) {
+  __shared__ double sh[256];
+  double best = INFINITY;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < a.total;
+       i += stride) {
+    long long r = i;
+    double s = 0.0;
+    for (int ax = 0; ax < a.d; ++ax) {
+      const long long idx = r % a.n[ax];
+      r /= a.n[ax];
+      s = __dadd_rn(s, a.lam[ax][idx]);
+    }
+    best = fmin(best, fabs(__dsub_rn(s, a.shift)));
+  }
+  sh[threadIdx.x] = best;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = fmin(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
+void check_solve_shift(kronop_ctx& ctx, const kronop_op& op, double shift) {
+  const double floor = 1e-14 * std::max(std::abs(op.lmin), std::abs(op.lmax));
+  double closest = std::min(std::abs(op.lmin - shift), std::abs(op.lmax - shift));
+  if (shift > op.lmin && shift < op.lmax) {
+    GapArgs a{};
+    a.d = op.d;
+    for (int i = 0; i < op.d; ++i) {
+      a.n[i] = op.n[i];
+      a.lam[i] = op.lam[i];
+    }
+    a.shift = shift;
+    a.total = op.N;
+    k_gap_partial<<<kRedBlocks, 256, 0, ctx.stream>>>(a, ctx.ws.partials);
+    KCUDA(cudaGetLastError());
+    ctx.ws.launches += 1;
+    std::vector<double> part(kRedBlocks);
+    KCUDA(cudaMemcpyAsync(part.data(), ctx.ws.partials, kRedBlocks * sizeof(double),
+                          cudaMemcpyDeviceToHost, ctx.stream));
+    KCUDA(cudaStreamSynchronize(ctx.stream));
+    closest = *std::min_element(part.begin(), part.end());
+  }
+  if (closest < floor)
+    fail(KRONOP_ENUMERICAL, "SeparableOperator::solve: shift coincides with an eigenvalue");
+}
+
+IndexGeomHost mass_geom(const kronop_op& op) {
+  param_check(op.has_mass, "inner: field has no mass weights attached");
+  IndexGeomHost g;
+  g.d = op.d;
+  for (int a = 0; a < op.d; ++a) {
+    g.n[a] = op.n[a];
+    g.mass[a] = op.mass[a];
+  }
+  return g;
+}
+
+// Upload a host column-major m x k matrix into a zero-padded device copy (lda = pad(m,128),
+// pad(k,16) columns). Returns lda.
+static int upload_padded(kronop_ctx& ctx, const double* host, int m, int k, double** dev,
+                         bool allocate) {
+  const int lda = pad_up(m, kMatPadM), kp = pad_up(k, kMatPadK);
+  std::vector<double> hp(static_cast<size_t>(lda) * kp, 0.0);
+  for (int j = 0; j < k; ++j)
+    std::memcpy(&hp[static_cast<size_t>(lda) * j], host + static_cast<size_t>(m) * j,
+                sizeof(double) * m);
+  if (allocate) KCUDA(cudaMalloc(dev, hp.size() * sizeof(double)));
+  KCUDA(cudaMemcpyAsync(*dev, hp.data(), hp.size() * sizeof(double), cudaMemcpyHostToDevice,
+                        ctx.stream));
+  KCUDA(cudaStreamSynchronize(ctx.stream));  // hp is a stack temporary
+  return lda;
+}
+
+static void generic_kron(kronop_ctx& ctx, const double* x, int d, const int* shape, int cplx,
+                         const double* const* mats, const int* ms, double* out) {
+  View v = make_view(d, shape, cplx);
+  // plan: sizes of every intermediate
+  size_t maxsz = static_cast<size_t>(v.total());
+  {
+    View w = v;
+    for (int a = 0; a < d; ++a) {
+      if (!mats[a]) continue;
+      param_check(ms[a] >= 1, "kron_apply: matrix rows must be positive");
+      w.ext[a + w.cplx] = ms[a];
+      maxsz = std::max(maxsz, static_cast<size_t>(w.total()));
+    }
+  }
+  int nmat = 0, last = -1;
+  size_t matsz = 0;
+  for (int a = 0; a < d; ++a)
+    if (mats[a]) {
+      ++nmat;
+      last = a;
+      matsz += static_cast<size_t>(pad_up(ms[a], kMatPadM)) * pad_up(shape[a], kMatPadK);
+    }
+  if (nmat == 0) {
+    if (out != x)
+      KCUDA(cudaMemcpyAsync(out, x, v.total() * sizeof(double), cudaMemcpyDeviceToDevice,
+                            ctx.stream));
+    return;
+  }
+  ensure_scratch(ctx, maxsz);
+  double* mbuf = ensure_tmp(ctx, matsz);
+  std::vector<double*> dm(d, nullptr);
+  std::vector<int> lda(d, 0);
+  size_t off = 0;
+  for (int a = 0; a < d; ++a) {
+    if (!mats[a]) continue;
+    dm[a] = mbuf + off;
+    lda[a] = upload_padded(ctx, mats[a], ms[a], shape[a], &dm[a], false);
+    off += static_cast<size_t>(lda[a]) * pad_up(shape[a], kMatPadK);
+  }
+  const double* cur = x;
+  int k = 0;
+  for (int a = 0; a < d; ++a) {
+    if (!mats[a]) continue;
+    double* dst = (a == last) ? out : ctx.scratch[k % 2];
+    EpiParams ep;
+    run_pass(ctx, cur, dst, v, a + v.cplx, dm[a], lda[a], ms[a], ep);
+    cur = dst;
+    ++k;
+  }
+}
+
+}  // namespace kronop_dev
+
+using namespace kronop_dev;
+
+extern "C" {
+
+const char* kronop_last_error(void) { return g_last_error.c_str(); }
+const char* kronop_version(void) { return "kronop-b200 0.1.0 (sm_100a, FP64 DMMA)"; }
+
+int kronop_ctx_create(int device, void* stream, kronop_ctx** out) {
+  return guard([&] {
+    param_check(out != nullptr, "kronop_ctx_create: null out");
+    auto* c = new kronop_ctx();
+    try {
+      c->device = device;
+      KCUDA(cudaSetDevice(device));
+      if (stream) {
+        c->stream = static_cast<cudaStream_t>(stream);
+      } else {
+        KCUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+      }
+      KCUDA(cudaMalloc(&c->ws.partials, kRedBlocks * 4 * sizeof(double)));
+      KCUDA(cudaMalloc(&c->dscal, kScalarSlots * sizeof(double)));
+      KCUDA(cudaMemset(c->dscal, 0, kScalarSlots * sizeof(double)));
+      KCUDA(cudaMallocHost(&c->hscal, kScalarSlots * sizeof(double)));
+      prime_mode_product_kernels();
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int kronop_ctx_destroy(kronop_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto p : ctx->scratch) if (p) cudaFree(p);
+    for (auto p : ctx->io) if (p) cudaFree(p);
+    if (ctx->tmp) cudaFree(ctx->tmp);
+    if (ctx->ws.partials) cudaFree(ctx->ws.partials);
+    if (ctx->dscal) cudaFree(ctx->dscal);
+    if (ctx->hscal) cudaFreeHost(ctx->hscal);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int kronop_ctx_synchronize(kronop_ctx* ctx) {
+  return guard([&] { KCUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int kronop_ctx_workspace_bytes(kronop_ctx* ctx, size_t* bytes) {
+  return guard([&] {
+    *bytes = (2 * ctx->scratch_cap + ctx->tmp_cap + 2 * ctx->io_cap) * sizeof(double);
+  });
+}
+
+int kronop_ctx_launch_count(kronop_ctx* ctx, uint64_t* count) {
+  return guard([&] { *count = ctx->ws.launches; });
+}
+
+int kronop_mode_product(kronop_ctx* ctx, const double* x, int d, const int* shape, int is_complex,
+                        const double* a, int m, int axis, double* out) {
+  return guard([&] {
+    param_check(ctx && x && out && shape && a, "mode_product: null argument");
+    param_check(axis >= 0 && axis < d, "mode_product: axis out of range");
+    param_check(m >= 1, "mode_product: matrix rows must be positive");
+    param_check(out != x, "mode_product: out must not alias x");
+    std::vector<const double*> mats(d, nullptr);
+    std::vector<int> ms(d, 0);
+    mats[axis] = a;
+    ms[axis] = m;
+    generic_kron(*ctx, x, d, shape, is_complex, mats.data(), ms.data(), out);
+  });
+}
+
+int kronop_kron_apply(kronop_ctx* ctx, const double* x, int d, const int* shape, int is_complex,
+                      const double* const* mats, const int* m, double* out) {
+  return guard([&] {
+    param_check(ctx && x && out && shape && mats && m, "kron_apply: null argument");
+    make_view(d, shape, is_complex);
+    generic_kron(*ctx, x, d, shape, is_complex, mats, m, out);
+  });
+}
+
+int kronop_inner(kronop_ctx* ctx, const double* u, const double* v, int d, const int* shape,
+                 int is_complex, const double* const* mass, double* result) {
+  return guard([&] {
+    param_check(ctx && u && v && shape && result, "inner: null argument");
+    View vw = make_view(d, shape, 0);
+    const long long n = vw.total();
+    IndexGeomHost g;
+    IndexGeomHost* gp = nullptr;
+    if (mass) {
+      size_t tot = 0;
+      for (int a = 0; a < d; ++a) tot += shape[a];
+      double* mb = ensure_tmp(*ctx, tot);
+      g.d = d;
+      size_t off = 0;
+      for (int a = 0; a < d; ++a) {
+        KCUDA(cudaMemcpyAsync(mb + off, mass[a], shape[a] * sizeof(double), cudaMemcpyHostToDevice,
+                              ctx->stream));
+        g.n[a] = shape[a];
+        g.mass[a] = mb + off;
+        off += shape[a];
+      }
+      gp = &g;
+    }
+    launch_dot(ctx->stream, ctx->ws, u, v, n, is_complex, gp, ctx->dscal);
+    KCUDA(cudaMemcpyAsync(ctx->hscal, ctx->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+    KCUDA(cudaStreamSynchronize(ctx->stream));
+    result[0] = ctx->hscal[0];
+    if (is_complex) result[1] = ctx->hscal[1];
+  });
+}
+
+static void generate_from_host(kronop_ctx* ctx, int d, const int* shape,
+                               const double* const* vecs, int mode, double* out) {
+  View vw = make_view(d, shape, 0);
+  size_t tot = 0;
+  for (int a = 0; a < d; ++a) tot += shape[a];
+  double* mb = ensure_tmp(*ctx, tot);
+  IndexGeomHost g;
+  g.d = d;
+  std::vector<const double*> dv(d);
+  size_t off = 0;
+  for (int a = 0; a < d; ++a) {
+    param_check(vecs[a] != nullptr, "per-axis vector missing");
+    KCUDA(cudaMemcpyAsync(mb + off, vecs[a], shape[a] * sizeof(double), cudaMemcpyHostToDevice,
+                          ctx->stream));
+    g.n[a] = shape[a];
+    dv[a] = mb + off;
+    off += shape[a];
+  }
+  (void)vw;
+  launch_generate(ctx->stream, ctx->ws, out, g, dv.data(), mode);
+}
+
+int kronop_mass_field(kronop_ctx* ctx, int d, const int* shape, const double* const* mass,
+                      double* out) {
+  return guard([&] { generate_from_host(ctx, d, shape, mass, 0, out); });
+}
+
+int kronop_direct_sum_grid(kronop_ctx* ctx, int d, const int* shape, const double* const* values,
+                           double* out) {
+  return guard([&] { generate_from_host(ctx, d, shape, values, 1, out); });
+}
+
+int kronop_op_create(kronop_ctx* ctx, int d, const int* n, const double* const* T,
+                     const double* const* Tinv, const double* const* lambda,
+                     const double* const* mass, double shift, kronop_op** out) {
+  return guard([&] {
+    param_check(ctx && n && T && Tinv && lambda && out, "SeparableOperator: null argument");
+    param_check(d >= 1 && d <= KRONOP_MAX_DIM, "SeparableOperator: need at least one axis");
+    auto* op = new kronop_op();
+    try {
+      op->ctx = ctx;
+      op->d = d;
+      op->N = 1;
+      op->shift = shift;
+      op->has_mass = mass != nullptr;
+      double lmin = 0.0, lmax = 0.0;
+      for (int a = 0; a < d; ++a) {
+        param_check(n[a] >= 1 && T[a] && Tinv[a] && lambda[a], "SeparableOperator: bad axis");
+        op->n[a] = n[a];
+        op->N *= n[a];
+        op->hlam[a].assign(lambda[a], lambda[a] + n[a]);
+        op->lda[a] = upload_padded(*ctx, Tinv[a], n[a], n[a], &op->fwd[a], true);
+        upload_padded(*ctx, T[a], n[a], n[a], &op->bwd[a], true);
+        KCUDA(cudaMalloc(&op->lam[a], n[a] * sizeof(double)));
+        KCUDA(cudaMemcpy(op->lam[a], lambda[a], n[a] * sizeof(double), cudaMemcpyHostToDevice));
+        // direct-sum extremes in axis order from 0.0 (operators.cpp:13-15; rounding is
+        // monotone so the grid min/max sit at the per-axis min/max entries)
+        lmin += *std::min_element(lambda[a], lambda[a] + n[a]);
+        lmax += *std::max_element(lambda[a], lambda[a] + n[a]);
+        if (mass) {
+          param_check(mass[a] != nullptr, "SeparableOperator: mass vector missing");
+          op->hmass[a].assign(mass[a], mass[a] + n[a]);
+          KCUDA(cudaMalloc(&op->mass[a], n[a] * sizeof(double)));
+          KCUDA(cudaMemcpy(op->mass[a], mass[a], n[a] * sizeof(double), cudaMemcpyHostToDevice));
+        }
+      }
+      op->lmin = lmin;
+      op->lmax = lmax;
+    } catch (...) {
+      kronop_op_destroy(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
+int kronop_op_destroy(kronop_op* op) {
+  return guard([&] {
+    if (!op) return;
+    if (op->ctx) cudaStreamSynchronize(op->ctx->stream);
+    for (int a = 0; a < KRONOP_MAX_DIM; ++a) {
+      if (op->fwd[a]) cudaFree(op->fwd[a]);
+      if (op->bwd[a]) cudaFree(op->bwd[a]);
+      if (op->lam[a]) cudaFree(op->lam[a]);
+      if (op->mass[a]) cudaFree(op->mass[a]);
+    }
+    delete op;
+  });
+}
+
+int kronop_op_set_shift(kronop_op* op, double shift) {
+  return guard([&] { op->shift = shift; });
+}
+
+int kronop_op_info(const kronop_op* op, double* shift, double* lambda_min, double* lambda_max,
+                   size_t* size) {
+  return guard([&] {
+    if (shift) *shift = op->shift;
+    if (lambda_min) *lambda_min = op->lmin;
+    if (lambda_max) *lambda_max = op->lmax;
+    if (size) *size = static_cast<size_t>(op->N);
+  });
+}
+
+int kronop_op_eigenvalue_grid(kronop_ctx* ctx, const kronop_op* op, double* out) {
+  return guard([&] {
+    IndexGeomHost g;
+    g.d = op->d;
+    for (int a = 0; a < op->d; ++a) g.n[a] = op->n[a];
+    launch_generate(ctx->stream, ctx->ws, out, g, op->lam, 1);
+  });
+}
+
+int kronop_op_ground_state(kronop_ctx* ctx, const kronop_op* op, double* out) {
+  return guard([&] {
+    IndexGeomHost g;
+    g.d = op->d;
+    for (int a = 0; a < op->d; ++a) g.n[a] = op->n[a];
+    // column 0 of each padded T is its first n entries (operators.cpp:77-91)
+    launch_generate(ctx->stream, ctx->ws, out, g, op->bwd, 2);
+  });
+}
+
+int kronop_sep_apply(kronop_ctx* ctx, const kronop_op* op, const double* u, int is_complex,
+                     double* out) {
+  return guard([&] {
+    param_check(ctx && op && u && out, "apply: null argument");
+    sep_transform(*ctx, *op, u, out, is_complex, SEP_APPLY, op->shift, 0.0, nullptr, 0.0);
+  });
+}
+
+int kronop_sep_solve(kronop_ctx* ctx, const kronop_op* op, const double* b, int is_complex,
+                     double* out) {
+  return guard([&] {
+    param_check(ctx && op && b && out, "solve: null argument");
+    check_solve_shift(*ctx, *op, op->shift);
+    sep_transform(*ctx, *op, b, out, is_complex, SEP_SOLVE, op->shift, 0.0, nullptr, 0.0);
+  });
+}
+
+int kronop_sep_propagate(kronop_ctx* ctx, const kronop_op* op, const double* psi, double dt,
+                         double* out) {
+  return guard([&] {
+    param_check(ctx && op && psi && out, "propagate: null argument");
+    if (dt == 0.0) {  // operators.cpp:64
+      if (out != psi)
+        KCUDA(cudaMemcpyAsync(out, psi, 2 * op->N * sizeof(double), cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+      return;
+    }
+    sep_transform(*ctx, *op, psi, out, 1, SEP_PROPAGATE, op->shift, dt, nullptr, 0.0);
+  });
+}
+
+int kronop_full_apply(kronop_ctx* ctx, const kronop_op* op, const double* diag, double sigma,
+                      const double* u, int is_complex, double* out) {
+  return guard([&] {
+    param_check(ctx && op && u && out, "FullOperator::apply: null argument");
+    sep_transform(*ctx, *op, u, out, is_complex, SEP_APPLY, op->shift, 0.0, diag, sigma);
+  });
+}
+
+int kronop_op_pass(kronop_ctx* ctx, const kronop_op* op, int axis, int forward, const double* in,
+                   int is_complex, double* out) {
+  return guard([&] {
+    param_check(ctx && op && in && out && in != out, "op_pass: bad argument");
+    param_check(axis >= 0 && axis < op->d, "op_pass: axis out of range");
+    View v = make_view(op->d, op->n, is_complex);
+    EpiParams ep;
+    run_pass(*ctx, in, out, v, axis + v.cplx, forward ? op->fwd[axis] : op->bwd[axis],
+             op->lda[axis], op->n[axis], ep);
+  });
+}
+
+static void host_roundtrip(kronop_ctx* ctx, const kronop_op* op, const double* in_host, int cplx,
+                           double* out_host, SepKind kind, double dt) {
+  const size_t nd = static_cast<size_t>(op->N) * (cplx ? 2 : 1);
+  if (nd > ctx->io_cap) {
+    for (auto& p : ctx->io) {
+      if (p) KCUDA(cudaFree(p));
+      p = nullptr;
+    }
+    ctx->io_cap = 0;
+    for (auto& p : ctx->io) KCUDA(cudaMalloc(&p, nd * sizeof(double)));
+    ctx->io_cap = nd;
+  }
+  KCUDA(cudaMemcpyAsync(ctx->io[0], in_host, nd * sizeof(double), cudaMemcpyHostToDevice,
+                        ctx->stream));
+  if (kind == SEP_SOLVE) check_solve_shift(*ctx, *op, op->shift);
+  sep_transform(*ctx, *op, ctx->io[0], ctx->io[1], cplx, kind, op->shift, dt, nullptr, 0.0);
+  KCUDA(cudaMemcpyAsync(out_host, ctx->io[1], nd * sizeof(double), cudaMemcpyDeviceToHost,
+                        ctx->stream));
+  KCUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+int kronop_sep_solve_host(kronop_ctx* ctx, const kronop_op* op, const double* b_host,
+                          int is_complex, double* out_host) {
+  return guard([&] { host_roundtrip(ctx, op, b_host, is_complex, out_host, SEP_SOLVE, 0.0); });
+}
+
+int kronop_sep_apply_host(kronop_ctx* ctx, const kronop_op* op, const double* u_host,
+                          int is_complex, double* out_host) {
+  return guard([&] { host_roundtrip(ctx, op, u_host, is_complex, out_host, SEP_APPLY, 0.0); });
+}
+
+int kronop_sep_propagate_host(kronop_ctx* ctx, const kronop_op* op, const double* psi_host,
+                              double dt, double* out_host) {
+  return guard([&] {
+    if (dt == 0.0) {
+      std::memcpy(out_host, psi_host, 2 * op->N * sizeof(double));
+      return;
+    }
+    host_roundtrip(ctx, op, psi_host, 1, out_host, SEP_PROPAGATE, dt);
+  });
+}
+
+int kronop_splitmix_uniform(kronop_ctx* ctx, uint64_t seed, uint64_t start, size_t count,
+                            double* out) {
+  return guard([&] {
+    launch_splitmix(ctx->stream, ctx->ws, out, seed, start, static_cast<long long>(count));
+  });
+}
+
+// ------------------------------------------------------------------------ host setup --
+int kronop_host_gll_rule(int degree, double* nodes, double* weights, double* diff) {
+  return guard([&] {
+    const kronop_host::GllRule r = kronop_host::gll_rule(degree);
+    std::copy(r.nodes.begin(), r.nodes.end(), nodes);
+    std::copy(r.weights.begin(), r.weights.end(), weights);
+    if (diff) std::copy(r.diff.begin(), r.diff.end(), diff);
+  });
+}
+
+int kronop_host_gauss_legendre(int points, double* nodes, double* weights) {
+  return guard([&] {
+    std::vector<double> x, w;
+    kronop_host::gauss_legendre(points, x, w);
+    std::copy(x.begin(), x.end(), nodes);
+    std::copy(w.begin(), w.end(), weights);
+  });
+}
+
+int kronop_host_assemble_sem(double half_width, int cell_count, int degree, double* nodes,
+                             double* mass, double* stiffness) {
+  return guard([&] {
+    const kronop_host::SemBasis b = kronop_host::assemble_sem(half_width, cell_count, degree);
+    std::copy(b.nodes.begin(), b.nodes.end(), nodes);
+    std::copy(b.mass.begin(), b.mass.end(), mass);
+    if (stiffness) std::copy(b.stiffness.begin(), b.stiffness.end(), stiffness);
+  });
+}
+
+int kronop_host_interp_matrix(double half_width, int coarse_cells, int coarse_degree,
+                              int fine_cells, int fine_degree, double* p) {
+  return guard([&] {
+    const auto c = kronop_host::assemble_sem(half_width, coarse_cells, coarse_degree);
+    const auto f = kronop_host::assemble_sem(half_width, fine_cells, fine_degree);
+    const auto m = kronop_host::interp_matrix(c, f);
+    std::copy(m.begin(), m.end(), p);
+  });
+}
+
+int kronop_host_sym_eig(int n, const double* a, double* eigenvalues, double* q) {
+  return guard([&] {
+    std::vector<double> lam, qq;
+    kronop_host::sym_eig(n, a, lam, qq);
+    std::copy(lam.begin(), lam.end(), eigenvalues);
+    std::copy(qq.begin(), qq.end(), q);
+  });
+}
+
+int kronop_host_build_sem_axis(double half_width, int cell_count, int degree, const double* fvals,
+                               double* lambda, double* T, double* Tinv) {
+  return guard([&] {
+    const auto b = kronop_host::assemble_sem(half_width, cell_count, degree);
+    const auto f = kronop_host::build_sem_axis(b, fvals);
+    std::copy(f.eigenvalues.begin(), f.eigenvalues.end(), lambda);
+    std::copy(f.transform.begin(), f.transform.end(), T);
+    std::copy(f.inverse_transform.begin(), f.inverse_transform.end(), Tinv);
+  });
+}
+
+}  // extern "C"

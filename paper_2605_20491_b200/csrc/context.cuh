@@ -1,0 +1,77 @@
+// Context / operator objects behind the opaque C handles, and the transform-chain helpers shared
+// by the C-ABI entry points (capi.cu) and the device-resident drivers (drivers.cu).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "kronop_internal.cuh"
+#include "vector_ops.cuh"
+
+struct kronop_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  kronop_dev::Workspace ws;
+  double* scratch[2] = {nullptr, nullptr};  // ping-pong transform buffers
+  size_t scratch_cap = 0;                   // doubles each
+  double* dscal = nullptr;                  // device scalar slots
+  double* hscal = nullptr;                  // pinned host mirror
+  double* tmp = nullptr;                    // temp device buffer (host matrices, mass vectors)
+  size_t tmp_cap = 0;
+  double* io[2] = {nullptr, nullptr};       // device staging for the *_host entry points
+  size_t io_cap = 0;
+};
+
+constexpr int kScalarSlots = 256;
+
+struct kronop_op {
+  kronop_ctx* ctx = nullptr;
+  int d = 0;
+  int n[KRONOP_MAX_DIM] = {};
+  long long N = 0;
+  double* fwd[KRONOP_MAX_DIM] = {};  // T^{-1}, padded, lda[a]
+  double* bwd[KRONOP_MAX_DIM] = {};  // T, padded
+  int lda[KRONOP_MAX_DIM] = {};
+  double* lam[KRONOP_MAX_DIM] = {};
+  double* mass[KRONOP_MAX_DIM] = {};
+  bool has_mass = false;
+  std::vector<double> hlam[KRONOP_MAX_DIM];
+  std::vector<double> hmass[KRONOP_MAX_DIM];
+  double shift = 0.0, lmin = 0.0, lmax = 0.0;
+};
+
+namespace kronop_dev {
+
+// Real view of a field: an optional leading re/im axis of extent 2, then the spatial axes.
+struct View {
+  int nd = 0;
+  int cplx = 0;
+  long long ext[kMaxDims] = {};
+  long long total() const {
+    long long t = 1;
+    for (int i = 0; i < nd; ++i) t *= ext[i];
+    return t;
+  }
+};
+View make_view(int d, const int* shape, int cplx);
+
+void ensure_scratch(kronop_ctx& ctx, size_t doubles);
+double* ensure_tmp(kronop_ctx& ctx, size_t doubles);
+
+// One pass on real-view axis `raxis` of `v` (updated to the output shape).
+void run_pass(kronop_ctx& ctx, const double* x, double* y, View& v, int raxis, const double* a,
+              int lda, int m, const EpiParams& ep);
+
+enum SepKind { SEP_APPLY = 0, SEP_SOLVE = 1, SEP_PROPAGATE = 2 };
+// out = T (f(lambda - shift) . (T^{-1} in)) [+ diag .* in - sigma in], f = x, / or exp(-i . dt).
+// in may alias out. Uses ctx.scratch.
+void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
+                   SepKind kind, double shift, double dt, const double* diag, double sigma);
+// Singular-shift guard of SeparableOperator::solve (operators.cpp:44-52).
+void check_solve_shift(kronop_ctx& ctx, const kronop_op& op, double shift);
+
+IndexGeomHost mass_geom(const kronop_op& op);
+void set_error(const std::string& msg);
+
+}  // namespace kronop_dev

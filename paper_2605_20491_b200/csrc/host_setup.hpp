@@ -1,0 +1,48 @@
+// Host-side setup (quadrature, SEM basis, Eigen-free sym_eig, per-axis factorisation).
+// See host_setup.cpp; these mirror proj/include/kronop/{quadrature,basis1d,axis}.hpp without Eigen.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace kronop_host {
+
+// Carries a kronop status code (KRONOP_EPARAM / ENUMERICAL / ECAPABILITY / ERUNTIME) to the C-ABI
+// shim, which turns it into a return code + kronop_last_error() text (errors.hpp:9-30).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct GllRule {  // quadrature.hpp:13-18
+  int degree = 0;
+  std::vector<double> nodes, weights;
+  std::vector<double> diff;  // (k+1)^2 column-major, diff(i,j) = l_j'(x_i)
+};
+
+struct SemBasis {  // basis1d.hpp:17-29 (Basis1D)
+  double half_width = 0.0;
+  int cell_count = 0;
+  int degree = 0;
+  GllRule rule;
+  std::vector<double> nodes, mass;
+  std::vector<double> stiffness;  // n x n column-major
+  int size() const { return static_cast<int>(nodes.size()); }
+};
+
+struct AxisFactor {  // axis.hpp:23-29 (AxisEigens)
+  std::vector<double> eigenvalues;        // ascending
+  std::vector<double> transform;          // T, n x n column-major
+  std::vector<double> inverse_transform;  // T^{-1}
+};
+
+void legendre_pair(int k, double x, double& p, double& dp);
+void gauss_legendre(int m, std::vector<double>& nodes, std::vector<double>& weights);
+GllRule gll_rule(int degree);
+SemBasis assemble_sem(double half_width, int cell_count, int degree);
+std::vector<double> interp_matrix(const SemBasis& coarse, const SemBasis& fine);
+void sym_eig(int n, const double* a, std::vector<double>& lam, std::vector<double>& q);
+AxisFactor build_sem_axis(const SemBasis& basis, const double* fvals);
+
+}  // namespace kronop_host

@@ -1,0 +1,91 @@
+// Internal declarations shared by the kronop CUDA translation units.
+// Not part of the public boundary (that is include/kronop_cuda.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/kronop_cuda.h"
+#include "host_setup.hpp"
+
+namespace kronop_dev {
+
+// ---------------------------------------------------------------- errors --
+// Mirrors the reference's exception hierarchy (proj/include/kronop/errors.hpp:9-30) as status
+// codes at the C boundary; internally C++ exceptions carry the code to the extern "C" shim.
+using Error = kronop_host::Error;
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void param_check(bool ok, const std::string& msg) {
+  if (!ok) fail(KRONOP_EPARAM, msg);
+}
+
+#define KCUDA(expr)                                                                        \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      ::kronop_dev::fail(_e == cudaErrorMemoryAllocation ? KRONOP_ECAPABILITY : KRONOP_ERUNTIME, \
+                         std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " +   \
+                             __FILE__ + ":" + std::to_string(__LINE__));                   \
+  } while (0)
+
+// ------------------------------------------------------------ mode product --
+// One pass of the mode-k product on a field viewed as a real (pre x nk x post) array, axis 0
+// fastest:  Y[p, i, q] = sum_j A[i, j] X[p, j, q]  (proj/src/tensor.cpp:105-134).
+// Complex fields (interleaved re/im, the reference's std::complex layout) are the real view with a
+// leading axis of extent 2, exactly as contract_inner_axis reinterprets them (tensor.cpp:124-131).
+constexpr int kMatPadM = 128;  // row padding of device copies of per-axis matrices
+constexpr int kMatPadK = 16;   // column (contraction) padding
+
+inline int pad_up(int v, int p) { return (v + p - 1) / p * p; }
+
+enum EpiKind : int {
+  EPI_STORE = 0,       // y = acc
+  EPI_SPEC_MUL = 1,    // y = acc * (lambda - shift)              operators.cpp:36
+  EPI_SPEC_DIV = 2,    // y = acc / (lambda - shift)              operators.cpp:57
+  EPI_SPEC_PHASE = 3,  // complex: y = acc * exp(-i (lambda - shift) dt)   operators.cpp:68-71
+  EPI_AXPY_DIAG = 4,   // y = (acc + diag .* u) - sigma * u       operators.cpp:102, ground_state.cpp:70-72
+};
+
+constexpr int kMaxDims = 10;  // 9 spatial axes + the complex component axis
+
+struct EpiParams {
+  int kind = EPI_STORE;
+  int axis = 0;                  // real-view axis this pass contracts
+  // index decomposition of the real view (for lambda / diag indexing)
+  int ndims = 0;                 // real-view dimensions
+  long long ext[kMaxDims] = {};  // real-view extents (output shape of this pass)
+  const double* lam[kMaxDims] = {};  // per real-view axis eigenvalues, null for the re/im axis
+  double shift = 0.0;
+  double dt = 0.0;
+  const double* diag = nullptr;  // V2 / diag field (spatial index, real)
+  const double* u = nullptr;     // the operator's input field (same layout as y)
+  double sigma = 0.0;
+  int cplx = 0;                  // real view has a leading re/im axis
+};
+
+struct PassShape {
+  long long pre = 1, post = 1;
+  int nk = 0, m = 0;
+};
+
+// Launch one pass. a_pad: device matrix, column-major with leading dimension lda >= pad_up(m,128),
+// zero padded to pad_up(nk,16) columns. x and y must not alias.
+void prime_mode_product_kernels();
+void launch_mode_product(cudaStream_t s, const double* x, double* y, const double* a_pad, int lda,
+                         const PassShape& ps, const EpiParams& ep);
+
+// ------------------------------------------------------------- workspace --
+constexpr int kRedBlocks = 592;   // 4 x 148 SMs: reduction grid (fixed => deterministic)
+constexpr int kEltBlocks = 1184;  // 8 x 148 SMs: elementwise grid-stride kernels
+
+struct Workspace {
+  double* partials = nullptr;  // kRedBlocks * 4 doubles
+  unsigned long long launches = 0;
+};
+
+}  // namespace kronop_dev

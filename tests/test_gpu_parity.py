@@ -1,0 +1,427 @@
+"""GPU parity: libkronop.so (sm_100a) against the CPU oracle on identical inputs.
+
+Two levels, as in the reference's own tests:
+  * kernel parity — the oracle is handed the SAME per-axis factors (T, T^-1, lambda) the product
+    built, so differences are pure transform arithmetic (bound 1e-13 relative, the reference's
+    dense-Kronecker tolerance, proj/tests/test_tensor.cpp:64-84);
+  * end-to-end parity — each side builds its own setup (C++ Householder+QL vs LAPACK), compared
+    within the FP64 tolerances of SURVEY.md §8c (1e-12 for solutions / eigenvalues, equal PCG
+    iteration counts, splitting errors to 1e-9 relative).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import kronop_oracle as K
+
+pytestmark = pytest.mark.gpu
+
+
+def api():
+    from paper_2605_20491_b200 import api as a
+    return a
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def oracle_op_from(prod_op, shift=0.0):
+    """Oracle SeparableOperator built from the product's own axis factors (kernel parity)."""
+    axes = [K.AxisEigens(a.eigenvalues.copy(), a.transform.copy(), a.inverse_transform.copy())
+            for a in prod_op.axes]
+    return K.SeparableOperator(axes, shift)
+
+
+# ----------------------------------------------------------------------------- tensor --
+@pytest.mark.parametrize("shape", [(3, 4, 5), (64, 64, 64), (13, 7, 33), (129, 3, 130)])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_mode_product_matches_dense(ctx, shape, cplx):
+    A = api()
+    n = int(np.prod(shape))
+    x = K.uniform_pm1(17, 2 * n)
+    x = x[0::2] + 1j * x[1::2] if cplx else x[:n]
+    for axis in range(len(shape)):
+        for m in (shape[axis], 7, 150):
+            a = K.uniform_pm1(100 + axis + m, m * shape[axis]).reshape(m, shape[axis], order="F")
+            y = host(A.mode_product(ctx, dev(x), shape, a, axis))
+            ref = K.mode_product(x, shape, a, axis)
+            assert rel(y, ref) < 1e-13, (axis, m)
+
+
+def test_mode_product_rank_one_and_identity(ctx):
+    # proj/tests/test_tensor.cpp:46-62
+    A = api()
+    x = K.uniform_pm1(5, 20)
+    y = host(A.mode_product(ctx, dev(x), (4, 5), np.eye(4), 0))
+    assert np.array_equal(y, x)
+    e = np.zeros(6)
+    e[1 + 3 * 1] = 1.0
+    a = np.arange(1, 10, dtype=float).reshape(3, 3)
+    r = host(A.mode_product(ctx, dev(e), (3, 2), a, 0))
+    for i in range(3):
+        for j in range(2):
+            assert r[i + 3 * j] == (a[i, 1] if j == 1 else 0.0)
+
+
+def test_mode_product_shape_errors(ctx):
+    # proj/tests/test_tensor.cpp:86-91
+    from paper_2605_20491_b200 import ParameterError
+    A = api()
+    x = dev(np.zeros(12))
+    with pytest.raises(ParameterError):
+        A.mode_product(ctx, x, (3, 4), np.zeros((3, 5)), 0)
+    with pytest.raises(ParameterError):
+        A.mode_product(ctx, x, (3, 4), np.zeros((3, 5)), 2)
+
+
+def test_kron_apply_and_round_trip(ctx):
+    # proj/tests/test_tensor.cpp:93-117
+    A = api()
+    a = np.array([[0.3, -1.2], [0.7, 2.0]])
+    b = np.array([[1.5, 0.25], [-0.6, 0.1]])
+    x = K.uniform_pm1(23, 4)
+    y = host(A.kron_apply(ctx, dev(x), (2, 2), [a, b]))
+    full = np.kron(b, a)
+    assert np.abs(y - full @ x).max() < 1e-13
+    basis = A.assemble_sem(1.0, 5, 8)
+    ax = A.build_axis(basis, lambda t: t * t)
+    u = K.uniform_pm1(29, ax.size * ax.size)
+    shp = (ax.size, ax.size)
+    v = A.kron_apply(ctx, A.kron_apply(ctx, dev(u), shp, [ax.transform, ax.transform]), shp,
+                     [ax.inverse_transform, ax.inverse_transform])
+    assert np.abs(host(v) - u).max() < 1e-9 * np.abs(u).max()
+    # rectangular (multilevel prolongation shapes) + identity entries
+    c = A.assemble_sem(8.0, 2, 6)
+    f = A.assemble_sem(8.0, 4, 6)
+    p = A.interp_matrix(c, f)
+    g = K.uniform_pm1(3, c.size ** 3)
+    out = host(A.kron_apply(ctx, dev(g), (c.size,) * 3, [p, None, p]))
+    ref, _ = K.kron_apply(g, (c.size,) * 3, [p, None, p])
+    assert rel(out, ref) < 1e-13
+
+
+def test_inner_mass_direct_sum_splitmix(ctx):
+    A = api()
+    grid = A.Grid.sem(2.0, 3, 4, 3)
+    shape = grid.shape
+    u = K.uniform_pm1(3, grid.node_count())
+    v = K.uniform_pm1(4, grid.node_count())
+    mw = K.mass_field(shape, grid.mass)
+    assert abs(A.inner(ctx, dev(u), dev(v), shape) - float(u @ v)) < 1e-12 * np.abs(u * v).sum()
+    got = A.inner(ctx, dev(u), dev(v), shape, grid.mass)
+    assert abs(got - float(np.sum(mw * u * v))) < 1e-12 * np.abs(mw * u * v).sum()
+    uc = K.seeded_complex_field(shape, 9)
+    vc = K.seeded_complex_field(shape, 10)
+    gc = A.inner(ctx, dev(uc), dev(vc), shape)
+    assert abs(gc - np.vdot(uc, vc)) < 1e-12 * np.abs(uc).sum()
+    # mass_field / direct_sum_grid are bitwise: same operation order as tensor.cpp:183-209
+    assert np.array_equal(host(A.mass_field(ctx, shape, grid.mass)), mw)
+    vals = [K.uniform_pm1(7 + a, shape[a]) for a in range(3)]
+    assert np.array_equal(host(A.direct_sum_grid(ctx, vals)), K.direct_sum_grid(vals))
+    # SplitMix64 on the device is bit-identical to rng.hpp
+    assert np.array_equal(host(A.splitmix_uniform(ctx, 1, 100000)), K.uniform_pm1(1, 100000))
+    assert np.array_equal(host(A.splitmix_uniform(ctx, 7, 1000, start=123)),
+                          K.uniform_pm1(7, 1000, start=123))
+
+
+# -------------------------------------------------------------------------- operators --
+def _trap_op(A, ctx, grid, shift=0.0):
+    return grid.separable_operator(ctx, [lambda t: t * t] * grid.dim, shift)
+
+
+@pytest.mark.parametrize("spec", [(1.0, 4, 3, 2), (2.0, 3, 4, 3), (8.0, 13, 5, 3), (8.0, 8, 10, 3),
+                                  (1.5, 5, 6, 1)])
+def test_separable_apply_solve_propagate_kernel_parity(ctx, spec):
+    A = api()
+    grid = A.Grid.sem(*spec)
+    op = _trap_op(A, ctx, grid, 0.5)
+    ko = oracle_op_from(op, 0.5)
+    n = grid.node_count()
+    u = K.uniform_pm1(11, n)
+    psi = K.seeded_complex_field(grid.shape, 12)
+    assert rel(host(op.apply(dev(u))), ko.apply(u)) < 1e-13
+    assert rel(host(op.solve(dev(u))), ko.solve(u)) < 1e-13
+    assert rel(host(op.apply(dev(psi))), ko.apply(psi)) < 1e-13
+    assert rel(host(op.solve(dev(psi))), ko.solve(psi)) < 1e-13
+    for dt in (0.083, -0.2, 1e-3):
+        assert rel(host(op.propagate(dev(psi), dt)), ko.propagate(psi, dt)) < 1e-13
+    assert np.array_equal(host(op.propagate(dev(psi), 0.0)), psi)
+    assert np.array_equal(host(op.eigenvalue_grid()), ko.lam)
+    assert np.array_equal(host(op.ground_state()), ko.ground_state())
+    s, lo, hi = op.info()
+    assert (s, lo, hi) == (0.5, ko.lambda_min, ko.lambda_max)
+
+
+def test_full_operator_apply_with_v2_and_sigma(ctx):
+    A = api()
+    grid = A.Grid.sem(1.0, 7, 1, 3)  # 6^3, acceptance.cpp:131-200 instance
+    op = _trap_op(A, ctx, grid)
+    v2 = grid.sample(lambda c: 2.0 * np.exp(-((c[0] - 0.3) ** 2 + (c[1] - 0.3) ** 2 + (c[2] - 0.3) ** 2)))
+    ko = K.FullOperator(oracle_op_from(op), v2)
+    u = K.uniform_pm1(101, grid.node_count())
+    fo = A.FullOperator(op, dev(v2))
+    assert rel(host(fo.apply(dev(u))), ko.apply(u)) < 1e-13
+    assert rel(host(fo.apply(dev(u), sigma=1.7)), ko.apply(u) - 1.7 * u) < 1e-13
+    # dense-oracle equivalence at the acceptance tolerance (acceptance.cpp:131-200)
+    ops = [K.dense_axis_operator(K.assemble_sem(1.0, 7, 1), lambda t: t * t)] * 3
+    dense = K.dense_assemble(ops, v2)
+    assert rel(host(fo.apply(dev(u))), dense @ u) < 1e-10
+    uc = K.seeded_complex_field(grid.shape, 5)
+    assert rel(host(fo.apply(dev(uc))), ko.apply(uc)) < 1e-13
+
+
+def test_singular_shift_refused(ctx):
+    # proj/tests/test_operators.cpp:95-102
+    from paper_2605_20491_b200 import NumericalError
+    A = api()
+    grid = A.Grid.sem(1.0, 4, 3, 2)
+    op = _trap_op(A, ctx, grid)
+    lam = op.axes[0].eigenvalues[1] + op.axes[1].eigenvalues[2]
+    op.set_shift(lam)
+    with pytest.raises(NumericalError):
+        op.solve(dev(np.ones(grid.node_count())))
+    op.set_shift(op.axes[0].eigenvalues[0] + op.axes[1].eigenvalues[0])  # = lambda_min
+    with pytest.raises(NumericalError):
+        op.solve(dev(np.ones(grid.node_count())))
+
+
+def test_c1_manufactured_solve_64cubed(ctx):
+    """BASELINE config 1: 64^3 (SEM k=5, 13 cells, L=8) harmonic, manufactured solution
+    (harness.cpp:228-249): the GPU solution equals the oracle's own end-to-end solve."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, 13, 5, 3)
+    pot = P.build_potential("harmonic", grid)
+    op = grid.separable_operator(ctx, pot.separable)
+    kg = K.Grid.sem(8.0, 13, 5, 3)
+    kp = K.build_potential("harmonic", kg)
+    rhs, ustar = K.manufactured_rhs(kg, kp, 8.0)
+    kop = kg.separable_operator(kp.separable)
+    u_ref = kop.solve(rhs)
+    u = host(op.solve(dev(rhs)))
+    assert rel(u, u_ref) < 1e-12
+    err_gpu, err_ref = rel(u, ustar), rel(u_ref, ustar)
+    assert abs(err_gpu - err_ref) <= 1e-9 * err_ref
+    # residual (harness.cpp:269-274)
+    res = host(A.FullOperator(op).apply(dev(u))) - rhs
+    assert np.linalg.norm(res) / np.linalg.norm(rhs) < 1e-12
+
+
+# --------------------------------------------------------------------------------- pcg --
+def test_pcg_identity_and_exact_preconditioner(ctx):
+    # proj/tests/test_pcg.cpp:26-69: exact preconditioner converges in one iteration
+    A = api()
+    grid = A.Grid.sem(2.0, 3, 4, 3)
+    op = _trap_op(A, ctx, grid)
+    b = dev(K.uniform_pm1(3, grid.node_count()))
+    x = torch.zeros_like(b)
+    rep = A.pcg(A.apply_map(op), A.solve_map(op), b, x, A.PcgConfig(rel_tol=1e-10))
+    assert rep.converged and rep.iterations == 1
+    r = host(A.FullOperator(op).apply(x)) - host(b)
+    assert np.linalg.norm(r) / np.linalg.norm(host(b)) < 1e-10
+    # warm start at the solution: zero iterations (test_pcg.cpp:129-142)
+    rep2 = A.pcg(A.apply_map(op), A.solve_map(op), b, x, A.PcgConfig(rel_tol=1e-8))
+    assert rep2.converged and rep2.iterations == 0
+
+
+@pytest.mark.parametrize("kind,cells", [("stirrer", 8), ("quartic", 8)])
+def test_pcg_iteration_parity_with_oracle(ctx, kind, cells):
+    """acceptance.cpp:202-236 instances (Q6, L=8, seed 1, tol 1e-8): same iteration count and
+    history as the oracle; solution within tolerance."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, cells, 6, 3)
+    pot = P.build_potential(kind, grid)
+    op = grid.separable_operator(ctx, pot.separable)
+    v2 = pot.v2_device()
+    b_np = K.seeded_field(grid.shape, 1)
+    b = A.splitmix_uniform(ctx, 1, grid.node_count())
+    assert np.array_equal(host(b), b_np)
+    x = torch.zeros_like(b)
+    cfg = A.PcgConfig(rel_tol=1e-8, record_history=True)
+    rep = A.pcg(A.apply_map(op, v2), A.solve_map(op), b, x, cfg)
+    kg = K.Grid.sem(8.0, cells, 6, 3)
+    kop = K.build_full_operator(kg, K.build_potential(kind, kg))
+    xr = np.zeros_like(b_np)
+    krep = K.pcg(kop.apply, kop.sep.solve, b_np, xr, K.PcgConfig(rel_tol=1e-8, record_history=True))
+    assert rep.converged == krep.converged
+    assert rep.iterations == krep.iterations
+    assert np.allclose(rep.history, krep.history, rtol=1e-8, atol=0)
+    assert rel(host(x), xr) < 1e-10
+
+
+def test_pcg_max_iter_returns_best_and_breakdown(ctx):
+    from paper_2605_20491_b200 import NumericalError
+    A = api()
+    grid = A.Grid.sem(8.0, 4, 6, 3)
+    from paper_2605_20491_b200 import potentials as P
+    pot = P.build_potential("quartic", grid)
+    op = grid.separable_operator(ctx, pot.separable)
+    b = A.splitmix_uniform(ctx, 2, grid.node_count())
+    x = torch.zeros_like(b)
+    rep = A.pcg(A.apply_map(op, pot.v2_device()), A.solve_map(op), b, x,
+                A.PcgConfig(rel_tol=1e-14, max_iter=3))
+    assert not rep.converged and rep.iterations == 3
+    # indefinite operator: A = sep.apply - sigma with sigma above lambda_max (test_pcg.cpp:144-154)
+    s, lo, hi = op.info()
+    x.zero_()
+    with pytest.raises(NumericalError):
+        A.pcg(A.apply_map(op, None, sigma=2 * hi), A.solve_map(op), b, x, A.PcgConfig())
+
+
+# ------------------------------------------------------------------- inverse iteration --
+def test_inverse_iteration_separable_criterion5(ctx):
+    """acceptance.cpp:291-308 (79^3, sep-osc amp 100): eigenvalue equals the oracle's."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, 8, 10, 3)
+    pot = P.build_potential("sep-osc", grid, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    op = grid.separable_operator(ctx, pot.separable)
+    init = torch.ones(grid.node_count(), dtype=torch.float64, device="cuda")
+    r = A.inverse_iteration(A.FullOperator(op), A.InverseIterationConfig(), init)
+    kg = K.Grid.sem(8.0, 8, 10, 3)
+    kp = K.build_potential("sep-osc", kg, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    kr = K.inverse_iteration(K.FullOperator(kg.separable_operator(kp.separable)),
+                             K.InverseIterationConfig(), np.ones(kg.node_count()), kg.mass)
+    assert r.converged and r.outer_iterations == kr.outer_iterations
+    assert abs(r.eigenvalue - kr.eigenvalue) <= 1e-12 * kr.eigenvalue
+    assert rel(host(r.eigenvector), kr.eigenvector) < 1e-9
+
+
+def test_inverse_iteration_stirrer_pcg_path(ctx):
+    """Non-separable inverse iteration (stirrer, Q20 2 cells = 39^3; acceptance.cpp:347-368 level
+    0 / criterion 10 setup): eigenvalue and inner iteration counts equal the oracle's."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, 2, 20, 3)
+    pot = P.build_potential("stirrer", grid)
+    op = grid.separable_operator(ctx, pot.separable)
+    fo = A.FullOperator(op, pot.v2_device())
+    r = A.inverse_iteration(fo, A.InverseIterationConfig(), op.ground_state())
+    kg = K.Grid.sem(8.0, 2, 20, 3)
+    kop = K.build_full_operator(kg, K.build_potential("stirrer", kg))
+    kr = K.inverse_iteration(kop, K.InverseIterationConfig(), kop.sep.ground_state(), kg.mass)
+    assert r.outer_iterations == kr.outer_iterations
+    assert r.inner_per_outer == kr.inner_per_outer
+    assert abs(r.eigenvalue - kr.eigenvalue) <= 1e-12 * kr.eigenvalue
+
+
+# --------------------------------------------------------------------------------- gpe --
+@pytest.mark.parametrize("kind", ["h1", "au"])
+def test_gpe_flow_trace_parity(ctx, kind):
+    """GPE flows (gpe.cpp:55-165) on a 39^3 Q20 grid, beta = 10, 25 iterations: the energy
+    trace equals the oracle's to 1e-11 relative."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, 2, 20, 3)
+    pot = P.build_potential("sep-osc", grid, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    ham = A.FullOperator(grid.separable_operator(ctx, pot.separable))
+    lap = grid.laplacian(ctx)
+    step = 0.1 if kind == "h1" else 1.0
+    cfg = A.GpeFlowConfig(kind=kind, step=step, energy_rel_tol=1e-30, max_iterations=25,
+                          record_history=True, init="constant")
+    r = A.gpe_gradient_flow(ham, lap, 10.0, cfg)
+    kg = K.Grid.sem(8.0, 2, 20, 3)
+    kp = K.build_potential("sep-osc", kg, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    prob = K.GpeProblem(K.FullOperator(kg.separable_operator(kp.separable)), kg.laplacian(), 10.0,
+                        kg.mass)
+    kr = K.gpe_gradient_flow(prob, K.GpeFlowConfig(kind=kind, step=step, energy_rel_tol=1e-30,
+                                                   max_iterations=25, record_history=True,
+                                                   init="constant"))
+    assert r.iterations == kr.iterations == 25
+    e_gpu = np.array([h[1] for h in r.history])
+    e_ref = np.array([h[1] for h in kr.history])
+    assert np.max(np.abs(e_gpu - e_ref) / np.abs(e_ref)) < 1e-11
+    assert [int(h[3]) for h in r.history] == [h[3] for h in kr.history]
+    assert abs(r.energy - kr.energy) <= 1e-11 * abs(kr.energy)
+    assert abs(A.gpe_energy(ham, 10.0, r.state) - r.energy) <= 1e-12 * abs(r.energy)
+
+
+# --------------------------------------------------------------------------- splitting --
+def test_yoshida_coeffs():
+    # proj/tests/test_splitting.cpp:29-35
+    g1, g2 = api().yoshida_coeffs()
+    assert abs(2 * g1 + g2 - 1.0) < 1e-15
+    assert abs(2 * g1 ** 3 + g2 ** 3) < 1e-14
+    assert (g1, g2) == K.yoshida_coeffs()
+
+
+def test_qhop_and_yoshida_step_kernel_parity(ctx):
+    A = api()
+    grid = A.Grid.sem(8.0, 4, 7, 2)
+    a = grid.laplacian(ctx)
+    ko = oracle_op_from(a)
+    b = grid.sample(lambda c: c[0] ** 2 + 100 * np.sin(np.pi * c[0] / 4) ** 2 + c[1] ** 2)
+    psi = K.seeded_complex_field(grid.shape, 2)
+    for m in (1, 3, 5):
+        out = host(A.qhop_step(a, dev(b), dev(psi), 0.013, m))
+        assert rel(out, K.qhop_step(ko, b, psi, 0.013, m)) < 1e-12
+        out = host(A.yoshida_step(a, dev(b), dev(psi), -0.02, m))
+        assert rel(out, K.yoshida_step(ko, b, psi, -0.02, m)) < 1e-12
+    # M = 1 is the explicit Strang half-kick form (test_splitting.cpp:37-54)
+    ref = ko.propagate(psi, 0.013 / 2)
+    ref = K.pointwise_phase(ref, b, 0.013)
+    ref = ko.propagate(ref, 0.013 / 2)
+    assert np.abs(host(A.qhop_step(a, dev(b), dev(psi), 0.013, 1)) - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("m,comp,dt,total", [(1, "single", 0.01, 0.1), (3, "single", 0.005, 0.1),
+                                             (1, "yoshida", 0.05, 1.0), (3, "yoshida", 0.1, 1.0)])
+def test_evolve_criterion9_errors(ctx, m, comp, dt, total):
+    """acceptance.cpp:424-489 setup (31^3 sep-osc, box psi0, exact reference, merge on): the
+    split-step error equals the oracle's to 1e-9 relative."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, 4, 8, 3)
+    pot = P.build_potential("sep-osc", grid, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    full = grid.separable_operator(ctx, pot.separable)
+    lap = grid.laplacian(ctx)
+    b = P.separable_sum(grid, pot)
+    kg = K.Grid.sem(8.0, 4, 8, 3)
+    psi0 = K.box_state(kg, 8.0).astype(np.complex128)
+    spec = A.SplitSpec(quad_points=m, composition=comp, dt=dt, total_time=total,
+                       merge_across_steps=True)
+    state, err, steps = A.evolve(spec, lap, dev(b), dev(psi0), exact=full)
+    kp = K.build_potential("sep-osc", kg, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    kstate, kerr, ksteps = K.evolve(K.SplitSpec(quad_points=m, composition=comp, dt=dt,
+                                                total_time=total, merge_across_steps=True),
+                                    kg.laplacian(), K.separable_sum_field(kg, kp), psi0,
+                                    exact=kg.separable_operator(kp.separable))
+    assert steps == ksteps
+    assert abs(err - kerr) <= 1e-9 * kerr
+    assert rel(host(state), kstate) < 1e-10
+
+
+def test_evolve_unitarity_and_stationary(ctx):
+    """Mass-norm conservation (acceptance.cpp:611-645) over 200 steps and the stationary
+    reference path (splitting.cpp:129-134)."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, 4, 8, 3)
+    pot = P.build_potential("sep-osc", grid, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    full = grid.separable_operator(ctx, pot.separable)
+    lap = grid.laplacian(ctx)
+    b = dev(P.separable_sum(grid, pot))
+    psi0 = K.box_state(K.Grid.sem(8.0, 4, 8, 3), 8.0).astype(np.complex128)
+    spec = A.SplitSpec(quad_points=1, dt=1e-3, total_time=0.2, merge_across_steps=True)
+    state, err, steps = A.evolve(spec, lap, b, dev(psi0), exact=full)
+    n0 = A.norm(ctx, dev(psi0 / np.linalg.norm(psi0)), grid.shape, grid.mass)
+    drift = abs(A.norm(ctx, state, grid.shape, grid.mass) - n0) / n0
+    assert drift <= 1e-8
+    # stationary: psi0 = ground state of the separable full operator -> error ~ splitting error
+    gs = full.ground_state().to(torch.complex128)
+    st, e2, _ = A.evolve(A.SplitSpec(quad_points=1, dt=0.01, total_time=0.1,
+                                     merge_across_steps=True), full, torch.zeros_like(b), gs,
+                         stationary_eigenvalue=full.min_eigenvalue())
+    assert e2 < 1e-10
