@@ -308,6 +308,11 @@ def _shape_arr(shape):
 def mode_product(ctx: Context, x: torch.Tensor, shape, a: np.ndarray, axis: int) -> torch.Tensor:
     """tensor.hpp:79-81."""
     a = np.asfortranarray(a, dtype=np.float64)
+    if not 0 <= axis < len(shape):
+        raise L.ParameterError(L.KRONOP_EPARAM, "mode_product: axis out of range")
+    if a.ndim != 2 or a.shape[1] != shape[axis]:
+        raise L.ParameterError(L.KRONOP_EPARAM,
+                               "mode_product: matrix columns do not match axis extent")
     m = a.shape[0]
     out_shape = list(shape)
     out_shape[axis] = m
@@ -321,7 +326,13 @@ def mode_product(ctx: Context, x: torch.Tensor, shape, a: np.ndarray, axis: int)
 
 def kron_apply(ctx: Context, x: torch.Tensor, shape, mats) -> torch.Tensor:
     """tensor.hpp:85-87 (None = identity)."""
+    if len(mats) != len(shape):
+        raise L.ParameterError(L.KRONOP_EPARAM, "kron_apply: need one matrix (or null) per axis")
     keep = [np.asfortranarray(a, dtype=np.float64) if a is not None else None for a in mats]
+    for i, a in enumerate(keep):
+        if a is not None and (a.ndim != 2 or a.shape[1] != shape[i]):
+            raise L.ParameterError(L.KRONOP_EPARAM,
+                                   "mode_product: matrix columns do not match axis extent")
     ms = [a.shape[0] if a is not None else 0 for a in keep]
     out_shape = [ms[i] if keep[i] is not None else shape[i] for i in range(len(shape))]
     out = torch.empty(int(np.prod(out_shape)), dtype=x.dtype, device=x.device)

@@ -1,0 +1,144 @@
+"""CPU: the product's C++ host setup (libkronop.so, no GPU needed) against the oracle, and the
+C-ABI library surface: it loads without a GPU and exports every symbol include/kronop_cuda.h
+declares."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import kronop_oracle as K
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def api():
+    from paper_2605_20491_b200 import api as a
+    return a
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "kronop_cuda.h")) as f:
+        src = f.read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(kronop_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+    from paper_2605_20491_b200 import _lib
+    h = ctypes.CDLL(_lib.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 40
+    missing = [s for s in syms if not hasattr(h, s)]
+    assert not missing, missing
+    # the Python binding declares a prototype for every exported entry point
+    assert set(syms) == set(_lib.PROTOTYPES), set(syms) ^ set(_lib.PROTOTYPES)
+    assert b"sm_100a" in _lib.lib().kronop_version()
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+    from paper_2605_20491_b200 import _lib
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH],
+                          capture_output=True, text=True).stdout
+    assert "mode_product_kernel" in sass
+    assert "DMMA" in sass  # FP64 tensor-core MMA in the transform kernel
+    assert "LDGSTS" in sass  # cp.async producer pipeline
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 8, 10, 20, 25, 40])
+def test_gll_rule_bitwise(k):
+    x, w, d = api().gll_rule(k)
+    r = K.gll_rule(k)
+    assert np.array_equal(x, r.nodes) and np.array_equal(w, r.weights)
+    assert np.abs(d - r.diff).max() == 0.0
+
+
+def test_gauss_legendre_bitwise():
+    for m in range(1, 17):
+        x, w = api().gauss_legendre(m)
+        ox, ow = K.gauss_legendre(m)
+        assert np.array_equal(x, ox) and np.array_equal(w, ow)
+
+
+@pytest.mark.parametrize("spec", [(8.0, 13, 5), (1.0, 16, 2), (8.0, 8, 10), (8.0, 2, 20), (5.0, 3, 10)])
+def test_assemble_sem_bitwise(spec):
+    b = api().assemble_sem(*spec)
+    ob = K.assemble_sem(*spec)
+    assert np.array_equal(b.nodes, ob.nodes)
+    assert np.array_equal(b.mass, ob.mass)
+    assert np.array_equal(b.stiffness, ob.stiffness)
+
+
+def test_interp_matrix_bitwise():
+    A = api()
+    for (c, f) in [((8.0, 2, 20), (8.0, 4, 20)), ((8.0, 2, 10), (8.0, 3, 10)), ((1.0, 3, 2), (1.0, 7, 2))]:
+        p = A.interp_matrix(A.assemble_sem(*c), A.assemble_sem(*f))
+        op = K.interp_matrix(K.assemble_sem(*c), K.assemble_sem(*f))
+        assert np.array_equal(p, op)
+        assert np.all(p.sum(axis=1) <= 1.0 + 1e-15) and np.all(p >= 0)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 128])
+def test_sym_eig_against_lapack(n):
+    a = K.uniform_pm1(n, n * n).reshape(n, n)
+    a = a + a.T
+    lam, q = api().sym_eig(a)
+    olam, oq = K.sym_eig(a)
+    scale = np.abs(olam).max()
+    assert np.abs(lam - olam).max() < 1e-13 * scale * max(1, n / 10)
+    assert np.abs(q.T @ q - np.eye(n)).max() < 1e-13 * max(1, n / 10)
+    assert np.abs(q @ np.diag(lam) @ q.T - a).max() < 1e-13 * scale * max(1, n / 10)
+    # sign convention (axis.cpp:44-52)
+    for j in range(n):
+        col = q[:, j]
+        i = int(np.argmax(np.abs(col) >= (1 - 1e-8) * np.abs(col).max()))
+        assert col[i] > 0
+
+
+def test_sym_eig_analytic_tridiagonal():
+    # test_axis_eigen.cpp:42-58: tridiag(-1, 2, -1) has eigenvalues 2 - 2 cos(j pi / (n+1))
+    n = 50
+    a = 2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
+    lam, _ = api().sym_eig(a)
+    exact = 2 - 2 * np.cos(np.arange(1, n + 1) * np.pi / (n + 1))
+    assert np.abs(lam - np.sort(exact)).max() < 1e-13
+    from paper_2605_20491_b200 import ParameterError
+    with pytest.raises(ParameterError):
+        api().sym_eig(np.array([[1.0, 2.0], [0.0, 1.0]]))
+
+
+@pytest.mark.parametrize("spec,f", [((8.0, 13, 5), lambda t: t * t),
+                                    ((1.0, 8, 10), lambda t: 1600 * np.sin(np.pi * t / 4) ** 2 + 2 * t * t),
+                                    ((8.0, 2, 20), lambda t: 4 * t * t)])
+def test_build_axis_factorisation(spec, f):
+    """T diag(L) T^-1 is the axis operator M^-1 S + diag(f) (axis.cpp:55-74); eigenvalues equal
+    the oracle's; T T^-1 = I. (Eigenvectors of (near-)degenerate pairs are not unique, so T is
+    compared through the operator it factorises.)"""
+    A = api()
+    b = A.assemble_sem(*spec)
+    ax = A.build_axis(b, f)
+    ob = K.assemble_sem(*spec)
+    oax = K.build_axis(ob, f)
+    scale = np.abs(oax.eigenvalues).max()
+    assert np.abs(ax.eigenvalues - oax.eigenvalues).max() < 1e-12 * scale
+    n = b.size
+    assert np.abs(ax.transform @ ax.inverse_transform - np.eye(n)).max() < 1e-11
+    dense = K.dense_axis_operator(ob, f)
+    rec = ax.transform @ np.diag(ax.eigenvalues) @ ax.inverse_transform
+    assert np.abs(rec - dense).max() < 1e-11 * scale
+
+
+def test_host_error_codes():
+    from paper_2605_20491_b200 import ParameterError
+    A = api()
+    with pytest.raises(ParameterError):
+        A.gll_rule(0)
+    with pytest.raises(ParameterError):
+        A.gauss_legendre(17)
+    with pytest.raises(ParameterError):
+        A.assemble_sem(-1.0, 3, 2)
