@@ -1024,7 +1024,9 @@ def gpe_gradient_flow(problem: GpeProblem, cfg: GpeFlowConfig,
 
 def yoshida_coeffs():
     """proj/src/splitting.cpp:86-90."""
-    cbrt2 = math.cbrt(2.0)
+    # std::cbrt(2.0) in the reference is folded by GCC at compile time (correctly rounded); glibc's
+    # runtime cbrt is 1 ulp off for 2.0, so use the correctly rounded constant.
+    cbrt2 = 1.2599210498948732
     denom = 2.0 - cbrt2
     return 1.0 / denom, -cbrt2 / denom
 

@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkronop.so")
+LIB_PATH = os.environ.get("KRONOP_LIB") or os.path.join(_HERE, "libkronop.so")
 
 KRONOP_OK = 0
 KRONOP_EPARAM = 2
@@ -21,6 +21,8 @@ KRONOP_SHIFT_FRACTION, KRONOP_SHIFT_OFFSET, KRONOP_SHIFT_ZERO = 0, 1, 2
 KRONOP_GPE_H1, KRONOP_GPE_AU = 0, 1
 KRONOP_GPE_INIT_CONSTANT, KRONOP_GPE_INIT_EIGENFUNCTION, KRONOP_GPE_INIT_SUPPLIED = 0, 1, 2
 KRONOP_COMPOSITION_SINGLE, KRONOP_COMPOSITION_YOSHIDA = 0, 1
+KRONOP_EPI_STORE, KRONOP_EPI_SPEC_MUL, KRONOP_EPI_SPEC_DIV = 0, 1, 2
+KRONOP_EPI_SPEC_PHASE, KRONOP_EPI_AXPY_DIAG = 3, 4
 
 P = C.c_void_p
 D = C.c_double
@@ -76,6 +78,10 @@ PROTOTYPES = {
     "kronop_ctx_synchronize": (I, [P]),
     "kronop_ctx_workspace_bytes": (I, [P, C.POINTER(C.c_size_t)]),
     "kronop_ctx_launch_count": (I, [P, C.POINTER(C.c_uint64)]),
+    "kronop_field_alloc": (I, [P, C.c_size_t, C.POINTER(P)]),
+    "kronop_field_free": (I, [P, P]),
+    "kronop_field_upload": (I, [P, P, P, C.c_size_t]),
+    "kronop_field_download": (I, [P, P, P, C.c_size_t]),
     "kronop_mode_product": (I, [P, P, I, IP, I, DP, I, I, P]),
     "kronop_kron_apply": (I, [P, P, I, IP, I, C.POINTER(DP), IP, P]),
     "kronop_inner": (I, [P, P, P, I, IP, I, C.POINTER(DP), DP]),
@@ -93,6 +99,7 @@ PROTOTYPES = {
     "kronop_op_ground_state": (I, [P, P, P]),
     "kronop_full_apply": (I, [P, P, P, D, P, I, P]),
     "kronop_op_pass": (I, [P, P, I, I, P, I, P]),
+    "kronop_op_pass_ex": (I, [P, P, I, I, P, I, P, I, D, P, D, P]),
     "kronop_sep_solve_host": (I, [P, P, P, I, P]),
     "kronop_sep_apply_host": (I, [P, P, P, I, P]),
     "kronop_sep_propagate_host": (I, [P, P, P, D, P]),

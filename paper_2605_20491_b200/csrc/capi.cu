@@ -276,6 +276,7 @@ int kronop_ctx_create(int device, void* stream, kronop_ctx** out) {
       KCUDA(cudaMemset(c->dscal, 0, kScalarSlots * sizeof(double)));
       KCUDA(cudaMallocHost(&c->hscal, kScalarSlots * sizeof(double)));
       prime_mode_product_kernels();
+      prime_mode_product_tma_kernels();
     } catch (...) {
       delete c;
       throw;
@@ -311,6 +312,36 @@ int kronop_ctx_workspace_bytes(kronop_ctx* ctx, size_t* bytes) {
 
 int kronop_ctx_launch_count(kronop_ctx* ctx, uint64_t* count) {
   return guard([&] { *count = ctx->ws.launches; });
+}
+
+int kronop_field_alloc(kronop_ctx* ctx, size_t doubles, double** out) {
+  return guard([&] {
+    param_check(ctx && out, "field_alloc: null argument");
+    KCUDA(cudaMalloc(out, std::max<size_t>(doubles, 1) * sizeof(double)));
+  });
+}
+
+int kronop_field_free(kronop_ctx* ctx, double* p) {
+  return guard([&] {
+    if (ctx) KCUDA(cudaStreamSynchronize(ctx->stream));
+    if (p) KCUDA(cudaFree(p));
+  });
+}
+
+int kronop_field_upload(kronop_ctx* ctx, double* dst, const double* host, size_t doubles) {
+  return guard([&] {
+    KCUDA(cudaMemcpyAsync(dst, host, doubles * sizeof(double), cudaMemcpyHostToDevice,
+                          ctx->stream));
+    KCUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int kronop_field_download(kronop_ctx* ctx, double* host, const double* src, size_t doubles) {
+  return guard([&] {
+    KCUDA(cudaMemcpyAsync(host, src, doubles * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+    KCUDA(cudaStreamSynchronize(ctx->stream));
+  });
 }
 
 int kronop_mode_product(kronop_ctx* ctx, const double* x, int d, const int* shape, int is_complex,
@@ -538,6 +569,33 @@ int kronop_op_pass(kronop_ctx* ctx, const kronop_op* op, int axis, int forward, 
     param_check(axis >= 0 && axis < op->d, "op_pass: axis out of range");
     View v = make_view(op->d, op->n, is_complex);
     EpiParams ep;
+    run_pass(*ctx, in, out, v, axis + v.cplx, forward ? op->fwd[axis] : op->bwd[axis],
+             op->lda[axis], op->n[axis], ep);
+  });
+}
+
+int kronop_op_pass_ex(kronop_ctx* ctx, const kronop_op* op, int axis, int forward,
+                      const double* in, int is_complex, double* out, int epilogue, double dt,
+                      const double* diag, double sigma, const double* u) {
+  return guard([&] {
+    param_check(ctx && op && in && out && in != out, "op_pass: bad argument");
+    param_check(axis >= 0 && axis < op->d, "op_pass: axis out of range");
+    param_check(epilogue >= KRONOP_EPI_STORE && epilogue <= KRONOP_EPI_AXPY_DIAG,
+                "op_pass: bad epilogue");
+    View v = make_view(op->d, op->n, is_complex);
+    EpiParams ep;
+    ep.kind = epilogue;
+    ep.axis = axis + v.cplx;
+    ep.ndims = v.nd;
+    for (int i = 0; i < v.nd; ++i) ep.ext[i] = v.ext[i];
+    for (int a = 0; a < op->d; ++a) ep.lam[a + v.cplx] = op->lam[a];
+    ep.shift = op->shift;
+    ep.dt = dt;
+    ep.cplx = v.cplx;
+    ep.diag = diag;
+    ep.sigma = sigma;
+    ep.u = u;
+    if (epilogue == KRONOP_EPI_AXPY_DIAG) param_check(u != nullptr, "op_pass: AXPY needs u");
     run_pass(*ctx, in, out, v, axis + v.cplx, forward ? op->fwd[axis] : op->bwd[axis],
              op->lda[axis], op->n[axis], ep);
   });

@@ -76,6 +76,12 @@ struct PassShape {
 // Launch one pass. a_pad: device matrix, column-major with leading dimension lda >= pad_up(m,128),
 // zero padded to pad_up(nk,16) columns. x and y must not alias.
 void prime_mode_product_kernels();
+// TMA + mbarrier warp-specialised kernel (mode_product_tma.cu) for the STRIDED (pre % 128 == 0)
+// and CONTIG (pre == 1, even nk) geometries; launch_mode_product dispatches to it when eligible.
+void prime_mode_product_tma_kernels();
+bool mode_product_tma_eligible(const double* x, const PassShape& ps);
+void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const double* a_pad,
+                             int lda, const PassShape& ps, const EpiParams& ep);
 void launch_mode_product(cudaStream_t s, const double* x, double* y, const double* a_pad, int lda,
                          const PassShape& ps, const EpiParams& ep);
 

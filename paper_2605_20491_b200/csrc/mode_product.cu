@@ -22,15 +22,23 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
+#include "epilogue.cuh"
 #include "kronop_internal.cuh"
 
 namespace kronop_dev {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 16;
-constexpr int STAGES = 4;
+#ifndef KRONOP_BK
+#define KRONOP_BK 32
+#endif
+#ifndef KRONOP_STAGES
+#define KRONOP_STAGES 3
+#endif
+constexpr int BK = KRONOP_BK;          // contraction depth per pipeline stage
+constexpr int STAGES = KRONOP_STAGES;  // cp.async pipeline depth
 constexpr int NTHREADS = 256;
 
 enum LoaderKind : int { LD_CONTIG = 0, LD_STRIDED_R = 1, LD_STRIDED_K = 2 };
@@ -67,14 +75,17 @@ struct TileCfg {
   static constexpr int WTN = BN / WARPS_N;  // 32
   static constexpr int RB = WTM / 8;
   static constexpr int CB = WTN / 8;
-  static constexpr int SAN = BN + 8;        // A-tile row stride (doubles), = 8 mod 16
+  // A-tile row stride (doubles) = 4 mod 16: the 16 lanes of each half-warp phase of a 64-bit
+  // fragment load (g = 0..3 or 4..7, t = 0..3 at t*S + g) hit 16 distinct bank pairs.
+  static constexpr int SAN = BN + 4;
 };
 
 template <int LOADER>
 struct XLayout {
-  // CONTIG: [BM][BK+4] (k fastest, stride = 4 mod 16); strided: [BK][BM+8] (rows fastest).
-  static constexpr int STRIDE = LOADER == LD_CONTIG ? BK + 4 : BM + 8;
-  static constexpr int ELEMS = LOADER == LD_CONTIG ? BM * (BK + 4) : BK * (BM + 8);
+  // CONTIG: [BM][BK+4] (k fastest); strided: [BK][BM+4] (rows fastest). Both strides are
+  // 4 mod 16 doubles => conflict-free 64-bit fragment loads (see TileCfg::SAN).
+  static constexpr int STRIDE = LOADER == LD_CONTIG ? BK + 4 : BM + 4;
+  static constexpr int ELEMS = LOADER == LD_CONTIG ? BM * (BK + 4) : BK * (BM + 4);
 };
 
 template <int BN, int LOADER>
@@ -98,48 +109,6 @@ __device__ __forceinline__ long long x_row_base(long long r, long long pre, int 
   // X(r, j) lives at x_row_base(r) + pre * j (r = p + pre * q flattened).
   const long long q = r / pre;
   return (r - q * pre) + q * pre * nk;
-}
-
-// Sum of per-axis eigenvalues over the real-view axes below `axis` for row coordinate p, in axis
-// order starting from 0.0 (direct_sum_grid, proj/src/tensor.cpp:196-209).
-__device__ __forceinline__ double lambda_partial_low(const EpiParams& ep, long long p, int axis) {
-  double s = 0.0;
-  for (int a = 0; a < axis; ++a) {
-    const long long e = ep.ext[a];
-    const long long idx = p % e;
-    p /= e;
-    if (ep.lam[a]) s = __dadd_rn(s, ep.lam[a][idx]);
-  }
-  return s;
-}
-
-// Pointwise spectral operation on one accumulator (kept out of line: it is executed once per
-// output element, after the K loop, and inlining it into every unrolled fragment slot only bloats
-// the kernel). lambda = ((0 + L_0[i_0]) + L_1[i_1]) + ... in axis order, then (lambda - shift);
-// true division for the solve; complex(cos, sin) product for the phase (operators.cpp:36,57,68-71).
-__device__ __noinline__ double spectral_epilogue(const EpiParams& ep, double val, double other,
-                                                 double lam_lo, int pass_axis, int i,
-                                                 long long q, long long p) {
-  double lam = lam_lo;
-  if (ep.lam[pass_axis] && i >= 0) lam = __dadd_rn(lam, ep.lam[pass_axis][i]);
-  long long qq = q;  // axes above the pass axis (post > 1): continue the axis-order sum
-  for (int aa = pass_axis + 1; aa < ep.ndims; ++aa) {
-    const long long e = ep.ext[aa];
-    const long long idx = qq % e;
-    qq /= e;
-    if (ep.lam[aa]) lam = __dadd_rn(lam, ep.lam[aa][idx]);
-  }
-  const double ls = __dsub_rn(lam, ep.shift);
-  if (ep.kind == EPI_SPEC_MUL) return __dmul_rn(val, ls);
-  if (ep.kind == EPI_SPEC_DIV) return __ddiv_rn(val, ls);
-  const double phase = __dmul_rn(-ls, ep.dt);
-  double sn, cs;
-  sincos(phase, &sn, &cs);
-  const bool is_im = (p & 1) != 0;
-  const double re = is_im ? other : val;
-  const double im = is_im ? val : other;
-  return is_im ? __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs))
-               : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
 }
 
 template <int BN, int LOADER, int VEC>
@@ -285,7 +254,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) mode_product_kernel(const KArgs a
     double lam_lo = 0.0;
     const int pass_axis = ep.axis;
     if (ep.kind == EPI_SPEC_MUL || ep.kind == EPI_SPEC_DIV || ep.kind == EPI_SPEC_PHASE)
-      lam_lo = lambda_partial_low(ep, p, pass_axis);
+      lam_lo = lambda_partial_low_ext(ep, p, pass_axis);
 #pragma unroll
     for (int cb = 0; cb < TC::CB; ++cb) {
 #pragma unroll
@@ -301,7 +270,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) mode_product_kernel(const KArgs a
             // re/im rows are adjacent (leading re/im axis): partner lane holds row r ^ 1
             const double other =
                 ep.kind == EPI_SPEC_PHASE ? __shfl_xor_sync(0xffffffffu, val, 4) : 0.0;
-            val = spectral_epilogue(ep, val, other, lam_lo, pass_axis, ok ? i : -1, q, p);
+            val = spectral_epilogue_ext(ep, val, other, lam_lo, pass_axis, ok ? i : -1, q, p);
             break;
           }
           case EPI_AXPY_DIAG: {
@@ -377,6 +346,14 @@ void launch_mode_product(cudaStream_t s, const double* x, double* y, const doubl
   param_check(ps.nk >= 1 && ps.m >= 1 && ps.pre >= 1 && ps.post >= 1,
               "mode_product: empty pass shape");
   param_check(lda >= pad_up(ps.m, kMatPadM), "mode_product: matrix leading dimension too small");
+  static const bool no_tma = [] {
+    const char* e = getenv("KRONOP_DISABLE_TMA");  // A/B switch for profiling the cp.async kernel
+    return e && e[0] == '1';
+  }();
+  if (!no_tma && mode_product_tma_eligible(x, ps)) {
+    launch_mode_product_tma(s, x, y, a_pad, lda, ps, ep);
+    return;
+  }
   KArgs ka;
   ka.x = x;
   ka.y = y;

@@ -1,0 +1,402 @@
+// Mode-k eigenbasis transform, Blackwell-native pipeline: TMA (cp.async.bulk.tensor) tiles into
+// 128B-swizzled shared memory, mbarrier full/empty handshakes, one producer warp and eight
+// FP64-DMMA consumer warps (warp specialisation), 128-bit fragment loads.
+//
+// Same contraction as mode_product.cu (proj/src/tensor.cpp:31-84, mode_product :105-134) with the
+// same fused epilogues (operators.cpp:36,57,68-71,102); this kernel serves the two geometries that
+// carry ~all of the FLOPs at scale:
+//   STRIDED  pre % 128 == 0: X tile = 8 TMA boxes of [BK k][16 rows] (3-D tensor map pre x nk x post)
+//   CONTIG   pre == 1:       X tile = 2 TMA boxes of [128 rows][16 k] (2-D tensor map nk x rows)
+// and the per-axis matrix (B operand) = BN/16 boxes of [BK k][16 cols] (2-D, zero-padded lda x kp).
+// Everything else (complex axis 0 with pre = 2, odd strides) runs the cp.async kernel.
+//
+// Fragment layout (why 128-bit loads are conflict free): with 128B swizzle the 16-byte chunk c of
+// smem row y sits at chunk c ^ (y & 7). A thread loads one 16-byte chunk = two consecutive rows (or
+// k values) and feeds them to two different 8x8x4 DMMA tiles; the lane -> row map is permuted so
+// that the 8 lanes of each quarter-warp touch 8 distinct chunks:
+//   STRIDED / matrix boxes (row = k): chunk(g) = (g&1)*4 + (g>>1)  (k varies in bits 0-1)
+//   CONTIG X box (row = tile row):    row(g)   = (g&1)*4 + (g>>1), chunk spans an aligned 4-block
+//   CONTIG matrix box (k = 2t+s):     chunk(g) = g                   (k varies in bits 1-2)
+// The permutation is undone in the epilogue (row / column maps below). The contraction index may be
+// permuted freely as long as both operands agree, which the CONTIG path uses (lane t holds k = 2t, 2t+1).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "epilogue.cuh"
+#include "kronop_internal.cuh"
+
+namespace kronop_dev {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;
+constexpr int STAGES = 3;
+constexpr int NCONS = 8;                 // DMMA warps; warp 0 lane 0 also drives TMA
+constexpr int NTHREADS = NCONS * 32;
+constexpr int BOX_STRIDED_BYTES = BK * 128;  // [BK rows][16 doubles]
+constexpr int BOX_CONTIG_BYTES = BM * 128;   // [BM rows][16 doubles]
+
+enum { TL_STRIDED = 0, TL_CONTIG = 1 };
+
+template <int BN>
+struct Cfg {
+  static constexpr int WARPS_N = BN == 128 ? 4 : 2;
+  static constexpr int WARPS_M = NCONS / WARPS_N;
+  static constexpr int WTM = BM / WARPS_M;  // 64 | 32
+  static constexpr int WTN = BN / WARPS_N;  // 32
+  static constexpr int RT = WTM / 8;
+  static constexpr int CT = WTN / 8;
+  static constexpr int X_BYTES = BM * BK * 8;
+  static constexpr int A_BYTES = BN * BK * 8;
+  static constexpr int STAGE_BYTES = X_BYTES + A_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 64 /*barriers*/;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ double2 lds128(const char* base, uint32_t byte_off) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n"
+               : "=d"(v.x), "=d"(v.y)
+               : "r"(smem_u32(base) + byte_off));
+  return v;
+}
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ int chS(int g) { return ((g & 1) << 2) | (g >> 1); }
+
+struct TArgs {
+  double* y;
+  long long pre, post, R;
+  int nk, m;
+  int ntiles_n;
+  long long ntiles_m;
+  EpiParams ep;
+};
+
+template <int BN, int LOADER>
+__device__ __forceinline__ int row_map(int j, int g) {
+  // row (within the warp tile) of MMA row g of row-tile j
+  if (LOADER == TL_STRIDED) return (j >> 1) * 16 + 2 * chS(g) + (j & 1);
+  return j * 8 + chS(g);
+}
+template <int BN, int LOADER>
+__device__ __forceinline__ int col_map(int jc, int n) {
+  if (LOADER == TL_STRIDED) return (jc >> 1) * 16 + 2 * chS(n) + (jc & 1);
+  return (jc >> 1) * 16 + 2 * n + (jc & 1);
+}
+
+template <int BN, int LOADER>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    mode_product_tma_kernel(const __grid_constant__ CUtensorMap tmx,
+                            const __grid_constant__ CUtensorMap tma, const TArgs args) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const long long bid = blockIdx.x;
+  const int ntile = static_cast<int>(bid % args.ntiles_n);
+  const long long mtile = bid / args.ntiles_n;
+  const long long row0 = mtile * BM;
+  const int col0 = ntile * BN;
+  const int KT = (args.nk + BK - 1) / BK;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  __syncthreads();
+
+  // The TMA producer is lane 0 of warp 0 (a dedicated producer warp would cap the DMMA warps at
+  // 168 registers): it refills slot (kt + STAGES - 1) % STAGES once all eight warps released it.
+  const long long q_tile = row0 / args.pre;
+  const int p0 = static_cast<int>(row0 - q_tile * args.pre);
+  auto issue = [&](int kt) {
+    const int s = kt % STAGES;
+    mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
+    unsigned char* xs = smem + s * C::STAGE_BYTES;
+    unsigned char* as = xs + C::X_BYTES;
+    mbar_expect_tx(&full[s], C::STAGE_BYTES);
+    const int k0 = kt * BK;
+    if (LOADER == TL_STRIDED) {
+#pragma unroll
+      for (int b = 0; b < BM / 16; ++b)
+        tma_load_3d(xs + b * BOX_STRIDED_BYTES, &tmx, p0 + 16 * b, k0, static_cast<int>(q_tile),
+                    &full[s]);
+    } else {
+#pragma unroll
+      for (int h = 0; h < BK / 16; ++h)
+        tma_load_2d(xs + h * BOX_CONTIG_BYTES, &tmx, k0 + 16 * h, static_cast<int>(row0),
+                    &full[s]);
+    }
+#pragma unroll
+    for (int c = 0; c < BN / 16; ++c)
+      tma_load_2d(as + c * BOX_STRIDED_BYTES, &tma, col0 + 16 * c, k0, &full[s]);
+  };
+  const bool producer = tid == 0;
+  if (producer) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmx) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tma) : "memory");
+    for (int kt = 0; kt < STAGES - 1 && kt < KT; ++kt) issue(kt);
+  }
+
+  // ---------------------------------------------------------------- DMMA consumers --
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  double acc[C::RT][C::CT][2];
+#pragma unroll
+  for (int i = 0; i < C::RT; ++i)
+#pragma unroll
+    for (int j = 0; j < C::CT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int cs = chS(g);
+  for (int kt = 0; kt < KT; ++kt) {
+    if (producer && kt + STAGES - 1 < KT) issue(kt + STAGES - 1);
+    const int s = kt % STAGES;
+    mbar_wait(&full[s], (kt / STAGES) & 1);
+    const char* xs = reinterpret_cast<const char*>(smem + s * C::STAGE_BYTES);
+    const char* as = xs + C::X_BYTES;
+    if (LOADER == TL_STRIDED) {
+#pragma unroll
+      for (int k4 = 0; k4 < BK / 4; ++k4) {
+        const int kk = k4 * 4 + t;
+        const uint32_t rowoff = kk * 128 + ((cs ^ (kk & 7)) << 4);
+        double af[C::RT], bf[C::CT];
+#pragma unroll
+        for (int bb = 0; bb < C::RT / 2; ++bb) {
+          const double2 v = lds128(xs, (wm * (C::RT / 2) + bb) * BOX_STRIDED_BYTES + rowoff);
+          af[2 * bb] = v.x;
+          af[2 * bb + 1] = v.y;
+        }
+#pragma unroll
+        for (int cc = 0; cc < C::CT / 2; ++cc) {
+          const double2 w = lds128(as, (wn * (C::CT / 2) + cc) * BOX_STRIDED_BYTES + rowoff);
+          bf[2 * cc] = w.x;
+          bf[2 * cc + 1] = w.y;
+        }
+#pragma unroll
+        for (int i = 0; i < C::RT; ++i)
+#pragma unroll
+          for (int j = 0; j < C::CT; ++j) dmma884(acc[i][j], af[i], bf[j]);
+      }
+    } else {
+#pragma unroll
+      for (int kb = 0; kb < BK / 8; ++kb) {
+        double a0[C::RT], a1[C::RT];
+        const int h = kb >> 1;
+        const int chunk = ((kb & 1) << 2) | t;
+#pragma unroll
+        for (int rt = 0; rt < C::RT; ++rt) {
+          const int row = wm * C::WTM + rt * 8 + cs;  // cs = rowC(g): row & 7 == chS(g)
+          const double2 v =
+              lds128(xs, h * BOX_CONTIG_BYTES + row * 128 + ((chunk ^ (row & 7)) << 4));
+          a0[rt] = v.x;  // k = kb*8 + 2t
+          a1[rt] = v.y;  // k = kb*8 + 2t + 1
+        }
+#pragma unroll
+        for (int sstep = 0; sstep < 2; ++sstep) {
+          const int kk = kb * 8 + 2 * t + sstep;
+          const uint32_t rowoff = kk * 128 + ((g ^ (kk & 7)) << 4);
+          double bf[C::CT];
+#pragma unroll
+          for (int cc = 0; cc < C::CT / 2; ++cc) {
+            const double2 w = lds128(as, (wn * (C::CT / 2) + cc) * BOX_STRIDED_BYTES + rowoff);
+            bf[2 * cc] = w.x;
+            bf[2 * cc + 1] = w.y;
+          }
+#pragma unroll
+          for (int i = 0; i < C::RT; ++i)
+#pragma unroll
+            for (int j = 0; j < C::CT; ++j) dmma884(acc[i][j], sstep ? a1[i] : a0[i], bf[j]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ----------------------------------------------------------------------- epilogue --
+  const EpiParams& ep = args.ep;
+  const long long pre = args.pre, R = args.R;
+  const int m = args.m;
+  const bool spectral = ep.kind == EPI_SPEC_MUL || ep.kind == EPI_SPEC_DIV || ep.kind == EPI_SPEC_PHASE;
+#pragma unroll
+  for (int j = 0; j < C::RT; ++j) {
+    const long long r = row0 + wm * C::WTM + row_map<BN, LOADER>(j, g);
+    const bool rok = r < R;
+    const long long rr = rok ? r : 0;
+    const long long q = rr / pre;
+    const long long p = rr - q * pre;
+    const long long ybase = p + q * pre * m;
+    const double lam_lo = spectral ? lambda_partial_low_ext(ep, p, ep.axis) : 0.0;
+#pragma unroll
+    for (int jc = 0; jc < C::CT; ++jc) {
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
+        const bool ok = rok && i < m;
+        double val = acc[j][jc][v];
+        const long long yi = ybase + pre * static_cast<long long>(ok ? i : 0);
+        if (spectral) {
+          // PHASE: the re/im partner (row r ^ 1) is this thread's tile j ^ 1 (STRIDED map)
+          const double other = ep.kind == EPI_SPEC_PHASE ? acc[j ^ 1][jc][v] : 0.0;
+          val = spectral_epilogue_ext(ep, val, other, lam_lo, ep.axis, ok ? i : -1, q, p);
+        } else if (ep.kind == EPI_AXPY_DIAG && ok) {
+          const double uu = ep.u[yi];
+          if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (yi >> 1) : yi], uu));
+          if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+        }
+        if (ok) args.y[yi] = val;
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    KCUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p)
+      fail(KRONOP_ERUNTIME, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+void encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims,
+            const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base),
+                                 dims, strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(KRONOP_ERUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+template <int BN, int LOADER>
+void set_attr_tma() {
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+}
+
+}  // namespace
+
+void prime_mode_product_tma_kernels() {
+  set_attr_tma<128, TL_STRIDED>();
+  set_attr_tma<128, TL_CONTIG>();
+  set_attr_tma<64, TL_STRIDED>();
+  set_attr_tma<64, TL_CONTIG>();
+}
+
+bool mode_product_tma_eligible(const double* x, const PassShape& ps) {
+  if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
+  if (ps.pre == 1) return ps.nk % 2 == 0 && ps.post <= 0x7fffffffLL;
+  return ps.pre % BM == 0 && ps.pre <= 0x7fffffffLL && ps.post <= 0x7fffffffLL;
+}
+
+void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const double* a_pad,
+                             int lda, const PassShape& ps, const EpiParams& ep) {
+  TArgs ta;
+  ta.y = y;
+  ta.pre = ps.pre;
+  ta.post = ps.post;
+  ta.R = ps.pre * ps.post;
+  ta.nk = ps.nk;
+  ta.m = ps.m;
+  ta.ep = ep;
+  const int bn = ps.m > 64 ? 128 : 64;
+  ta.ntiles_n = (ps.m + bn - 1) / bn;
+  ta.ntiles_m = (ta.R + BM - 1) / BM;
+  CUtensorMap tmx, tmA;
+  const int kp = pad_up(ps.nk, kMatPadK);
+  {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(lda), static_cast<cuuint64_t>(kp)};
+    const cuuint64_t str[1] = {static_cast<cuuint64_t>(lda) * 8};
+    const cuuint32_t box[2] = {16, BK};
+    encode(&tmA, a_pad, 2, dims, str, box);
+  }
+  const bool contig = ps.pre == 1;
+  if (contig) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ps.nk), static_cast<cuuint64_t>(ta.R)};
+    const cuuint64_t str[1] = {static_cast<cuuint64_t>(ps.nk) * 8};
+    const cuuint32_t box[2] = {16, BM};
+    encode(&tmx, x, 2, dims, str, box);
+  } else {
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(ps.pre), static_cast<cuuint64_t>(ps.nk),
+                                static_cast<cuuint64_t>(ps.post)};
+    const cuuint64_t str[2] = {static_cast<cuuint64_t>(ps.pre) * 8,
+                               static_cast<cuuint64_t>(ps.pre) * ps.nk * 8};
+    const cuuint32_t box[3] = {16, BK, 1};
+    encode(&tmx, x, 3, dims, str, box);
+  }
+  const long long blocks = ta.ntiles_m * ta.ntiles_n;
+  if (bn == 128) {
+    if (contig)
+      mode_product_tma_kernel<128, TL_CONTIG><<<blocks, NTHREADS, Cfg<128>::SMEM, s>>>(tmx, tmA, ta);
+    else
+      mode_product_tma_kernel<128, TL_STRIDED><<<blocks, NTHREADS, Cfg<128>::SMEM, s>>>(tmx, tmA, ta);
+  } else {
+    if (contig)
+      mode_product_tma_kernel<64, TL_CONTIG><<<blocks, NTHREADS, Cfg<64>::SMEM, s>>>(tmx, tmA, ta);
+    else
+      mode_product_tma_kernel<64, TL_STRIDED><<<blocks, NTHREADS, Cfg<64>::SMEM, s>>>(tmx, tmA, ta);
+  }
+  KCUDA(cudaGetLastError());
+}
+
+}  // namespace kronop_dev
