@@ -166,6 +166,65 @@ def run_reference(args):
 
 
 # -------------------------------------------------------------------------- GPU arm --
+def secondary_metrics(A, P, ctx, device):
+    """The other two metrics BASELINE.json names, each timed on the device:
+    PCG time-to-tol (stirrer, 512^3 = Q19 x 27 cells, seed-1 rhs, tol 1e-8, (-Delta+V1)^-1
+    preconditioner; harness.cpp:501-582) and split-step steps/s (Strang = qHOP M=1 with merge,
+    499^3 complex128, sep-osc trap split=kinetic, box psi0, dt = 5e-3, T = 0.1;
+    splitting.cpp:107-146)."""
+    import torch
+    out = {}
+    g = A.Grid.sem(8.0, 27, 19, 3)
+    pot = P.build_potential("stirrer", g)
+    op = g.separable_operator(ctx, pot.separable)
+    v2 = pot.v2_device("cuda:%d" % device)
+    b = A.splitmix_uniform(ctx, 1, g.node_count())
+    x = torch.zeros_like(b)
+    cfg = A.PcgConfig(rel_tol=1e-8)
+    A.pcg(A.apply_map(op, v2), A.solve_map(op), b, x, A.PcgConfig(rel_tol=1e-8, max_iter=2))
+    x.zero_()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    rep = A.pcg(A.apply_map(op, v2), A.solve_map(op), b, x, cfg)
+    e1.record(ctx.stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3
+    n = g.shape[0]
+    out["pcg_time_to_tol"] = {
+        "value": t, "unit": "s", "iterations": rep.iterations, "final_residual": rep.final_residual,
+        "converged": rep.converged, "n": n, "dof": g.node_count(),
+        "tflops": (rep.iterations + 1) * 24.0 * n ** 4 / t / 1e12,
+        "config": "stirrer V=V1+V2, SEM Q19 x 27 cells (n=512), L=8, rhs SplitMix64(1), tol 1e-8, "
+                  "precond (-Delta+V1)^-1, device-resident PCG (one CUDA graph, WHILE node)"}
+    del op, v2, b, x
+    torch.cuda.empty_cache()
+    g = A.Grid.sem(8.0, 100, 5, 3)
+    pot = P.build_potential("sep-osc", g, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    lap = g.laplacian(ctx)
+    bdiag = torch.from_numpy(P.separable_sum(g, pot)).to("cuda:%d" % device)
+    box = g.sample(lambda c: np.sin(np.pi * (c[0] + 8.0) / 16.0) * np.sin(np.pi * (c[1] + 8.0) / 16.0)
+                   * np.sin(np.pi * (c[2] + 8.0) / 16.0))
+    psi0 = torch.from_numpy(box.astype(np.complex128)).to("cuda:%d" % device)
+    spec = A.SplitSpec(quad_points=1, composition="single", dt=5e-3, total_time=0.1,
+                       merge_across_steps=True)
+    A.evolve(A.SplitSpec(quad_points=1, dt=5e-3, total_time=1e-2, merge_across_steps=True), lap,
+             bdiag, psi0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    state, err, steps = A.evolve(spec, lap, bdiag, psi0)
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+    out["splitstep_steps_per_s"] = {
+        "value": steps / t, "unit": "steps/s", "steps": steps, "seconds": t, "n": g.shape[0],
+        "config": "Strang (qHOP M=1) with cross-step merge, 499^3 complex128 (SEM Q5 x 100 cells, "
+                  "L=8), A=-Delta, B=sep-osc V, box psi0, dt=5e-3, T=0.1 (PAPER.md:1381 setup)"}
+    del lap, bdiag, psi0, state
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_kronop(args):
     import torch
     world, rank, local = dist_init()
@@ -241,6 +300,7 @@ def run_kronop(args):
     t_e2e = max_over_ranks(world, t_e2e, "cuda:%d" % local)
     e2e_value = world * N / t_e2e / 1e9
 
+    extras = {} if args.no_extras else secondary_metrics(A, P, ctx, local)
     cpu = None
     if rank == 0 and not args.no_cpu:
         ts, ns = cpu_reference_sample()
@@ -268,6 +328,7 @@ def run_kronop(args):
             "e2e": {"value": e2e_value, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * N,
                     "d2h_bytes_per_step": 8 * N, "ms_per_step": t_e2e * 1e3},
             "gpu_launches": int(launches),
+            "secondary": extras,
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
@@ -286,6 +347,7 @@ def main():
     ap.add_argument("--impl", default="kronop", choices=["kronop", "reference"])
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

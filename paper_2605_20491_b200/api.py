@@ -280,9 +280,21 @@ class SeparableOperator:
         return out
 
     # host-buffer (end-to-end) variants
-    def solve_host(self, b: np.ndarray, out: np.ndarray, is_complex=False):
+    def solve_host(self, b: np.ndarray, out: np.ndarray, is_complex=None):
+        """kronop_sep_solve_host: host in / host out, copies overlapped with the passes."""
+        cplx = np.iscomplexobj(b) if is_complex is None else is_complex
         check(lib().kronop_sep_solve_host(self.ctx.h, self.h, C.c_void_p(b.ctypes.data),
-                                          int(is_complex), C.c_void_p(out.ctypes.data)))
+                                          int(cplx), C.c_void_p(out.ctypes.data)))
+        return out
+
+    def apply_host(self, u: np.ndarray, out: np.ndarray):
+        check(lib().kronop_sep_apply_host(self.ctx.h, self.h, C.c_void_p(u.ctypes.data),
+                                          int(np.iscomplexobj(u)), C.c_void_p(out.ctypes.data)))
+        return out
+
+    def propagate_host(self, psi: np.ndarray, dt: float, out: np.ndarray):
+        check(lib().kronop_sep_propagate_host(self.ctx.h, self.h, C.c_void_p(psi.ctypes.data), dt,
+                                              C.c_void_p(out.ctypes.data)))
         return out
 
 

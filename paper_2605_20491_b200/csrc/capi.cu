@@ -295,6 +295,12 @@ int kronop_ctx_destroy(kronop_ctx* ctx) {
     if (ctx->ws.partials) cudaFree(ctx->ws.partials);
     if (ctx->dscal) cudaFree(ctx->dscal);
     if (ctx->hscal) cudaFreeHost(ctx->hscal);
+    for (auto st : ctx->copy_stream) if (st) cudaStreamDestroy(st);
+    for (int i = 0; i < kronop_ctx::kMaxChunks; ++i) {
+      if (ctx->ev_in[i]) cudaEventDestroy(ctx->ev_in[i]);
+      if (ctx->ev_out[i]) cudaEventDestroy(ctx->ev_out[i]);
+    }
+    if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -601,25 +607,129 @@ int kronop_op_pass_ex(kronop_ctx* ctx, const kronop_op* op, int axis, int forwar
   });
 }
 
+// End-to-end path for host buffers (what a CPU caller of the reference API hands over). The
+// field is streamed in and out in slabs of the slowest axis on two copy streams so the PCIe
+// transfers overlap the transform: the forward passes on axes 0..d-2 of slab c run while slab
+// c+1 is still in flight; the last axis (forward, fused spectral op, backward) needs the whole
+// field; the backward passes on axes 0..d-2 of slab c run while slab c-1 is being copied out.
+// (Backward axis d-1 runs before axes 0..d-2 here: the Kronecker factors commute, results agree
+// with sep_transform to rounding.)
+static void ensure_io(kronop_ctx* ctx, size_t nd) {
+  if (nd <= ctx->io_cap) return;
+  for (auto& p : ctx->io) {
+    if (p) KCUDA(cudaFree(p));
+    p = nullptr;
+  }
+  ctx->io_cap = 0;
+  for (auto& p : ctx->io) KCUDA(cudaMalloc(&p, nd * sizeof(double)));
+  ctx->io_cap = nd;
+}
+
+static void ensure_copy_engines(kronop_ctx* ctx) {
+  if (ctx->copy_stream[0]) return;
+  for (auto& st : ctx->copy_stream) KCUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (int i = 0; i < kronop_ctx::kMaxChunks; ++i) {
+    KCUDA(cudaEventCreateWithFlags(&ctx->ev_in[i], cudaEventDisableTiming));
+    KCUDA(cudaEventCreateWithFlags(&ctx->ev_out[i], cudaEventDisableTiming));
+  }
+  KCUDA(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
+}
+
 static void host_roundtrip(kronop_ctx* ctx, const kronop_op* op, const double* in_host, int cplx,
                            double* out_host, SepKind kind, double dt) {
   const size_t nd = static_cast<size_t>(op->N) * (cplx ? 2 : 1);
-  if (nd > ctx->io_cap) {
-    for (auto& p : ctx->io) {
-      if (p) KCUDA(cudaFree(p));
-      p = nullptr;
-    }
-    ctx->io_cap = 0;
-    for (auto& p : ctx->io) KCUDA(cudaMalloc(&p, nd * sizeof(double)));
-    ctx->io_cap = nd;
-  }
-  KCUDA(cudaMemcpyAsync(ctx->io[0], in_host, nd * sizeof(double), cudaMemcpyHostToDevice,
-                        ctx->stream));
+  ensure_io(ctx, nd);
   if (kind == SEP_SOLVE) check_solve_shift(*ctx, *op, op->shift);
-  sep_transform(*ctx, *op, ctx->io[0], ctx->io[1], cplx, kind, op->shift, dt, nullptr, 0.0);
-  KCUDA(cudaMemcpyAsync(out_host, ctx->io[1], nd * sizeof(double), cudaMemcpyDeviceToHost,
-                        ctx->stream));
-  KCUDA(cudaStreamSynchronize(ctx->stream));
+  const int d = op->d;
+  const int nz = op->n[d - 1];
+  if (d < 2 || nz < 2) {
+    KCUDA(cudaMemcpyAsync(ctx->io[0], in_host, nd * sizeof(double), cudaMemcpyHostToDevice,
+                          ctx->stream));
+    sep_transform(*ctx, *op, ctx->io[0], ctx->io[1], cplx, kind, op->shift, dt, nullptr, 0.0);
+    KCUDA(cudaMemcpyAsync(out_host, ctx->io[1], nd * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+    KCUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
+  ensure_copy_engines(ctx);
+  ensure_scratch(*ctx, nd);
+  cudaStream_t sc = ctx->stream, sin = ctx->copy_stream[0], sout = ctx->copy_stream[1];
+  const int chunks = std::min(nz, 8);
+  const size_t plane = nd / nz;  // doubles per plane of the slowest axis
+  std::vector<int> zc(chunks), z0(chunks);
+  for (int c = 0, acc = 0; c < chunks; ++c) {
+    zc[c] = nz / chunks + (c < nz % chunks ? 1 : 0);
+    z0[c] = acc;
+    acc += zc[c];
+  }
+  // the copy streams must not start before earlier work on the compute stream is done
+  KCUDA(cudaEventRecord(ctx->ev_ready, sc));
+  KCUDA(cudaStreamWaitEvent(sin, ctx->ev_ready, 0));
+  KCUDA(cudaStreamWaitEvent(sout, ctx->ev_ready, 0));
+  double* io0 = ctx->io[0];
+  double* io1 = ctx->io[1];
+  double* s0 = ctx->scratch[0];
+  double* s1 = ctx->scratch[1];
+  // forward passes on axes 0..d-2, slab by slab, as the slabs arrive: io0 -> s0/s1 ping-pong
+  double* fwd_local = nullptr;
+  for (int c = 0; c < chunks; ++c) {
+    const size_t off = plane * z0[c], cnt = plane * zc[c];
+    KCUDA(cudaMemcpyAsync(io0 + off, in_host + off, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                          sin));
+    KCUDA(cudaEventRecord(ctx->ev_in[c], sin));
+    KCUDA(cudaStreamWaitEvent(sc, ctx->ev_in[c], 0));
+    std::vector<int> shp(op->n, op->n + d);
+    shp[d - 1] = zc[c];
+    View v = make_view(d, shp.data(), cplx);
+    const double* cur = io0 + off;
+    for (int a = 0; a < d - 1; ++a) {
+      double* dst = (a % 2 == 0 ? s0 : s1) + off;
+      EpiParams ep;
+      run_pass(*ctx, cur, dst, v, a + v.cplx, op->fwd[a], op->lda[a], op->n[a], ep);
+      cur = dst;
+    }
+    fwd_local = ((d - 2) % 2 == 0) ? s0 : s1;
+  }
+  // last axis on the whole field: forward + fused spectral op, then backward
+  double* other = (fwd_local == s0) ? s1 : s0;
+  {
+    View v = make_view(d, op->n, cplx);
+    EpiParams ep;
+    ep.kind = kind == SEP_APPLY ? EPI_SPEC_MUL : kind == SEP_SOLVE ? EPI_SPEC_DIV : EPI_SPEC_PHASE;
+    ep.axis = d - 1 + v.cplx;
+    ep.ndims = v.nd;
+    for (int i = 0; i < v.nd; ++i) ep.ext[i] = v.ext[i];
+    for (int a = 0; a < d; ++a) ep.lam[a + v.cplx] = op->lam[a];
+    ep.shift = op->shift;
+    ep.dt = dt;
+    ep.cplx = v.cplx;
+    run_pass(*ctx, fwd_local, other, v, d - 1 + v.cplx, op->fwd[d - 1], op->lda[d - 1],
+             op->n[d - 1], ep);
+    View v2 = make_view(d, op->n, cplx);
+    EpiParams plain;
+    run_pass(*ctx, other, io0, v2, d - 1 + v2.cplx, op->bwd[d - 1], op->lda[d - 1],
+             op->n[d - 1], plain);
+  }
+  // backward passes on axes 0..d-2 slab by slab, each slab copied out as soon as it is done
+  for (int c = 0; c < chunks; ++c) {
+    const size_t off = plane * z0[c], cnt = plane * zc[c];
+    std::vector<int> shp(op->n, op->n + d);
+    shp[d - 1] = zc[c];
+    View v = make_view(d, shp.data(), cplx);
+    const double* cur = io0 + off;
+    for (int a = 0; a < d - 1; ++a) {
+      double* dst = (a == d - 2) ? io1 + off : ((a % 2 == 0 ? s0 : s1) + off);
+      EpiParams ep;
+      run_pass(*ctx, cur, dst, v, a + v.cplx, op->bwd[a], op->lda[a], op->n[a], ep);
+      cur = dst;
+    }
+    KCUDA(cudaEventRecord(ctx->ev_out[c], sc));
+    KCUDA(cudaStreamWaitEvent(sout, ctx->ev_out[c], 0));
+    KCUDA(cudaMemcpyAsync(out_host + off, io1 + off, cnt * sizeof(double), cudaMemcpyDeviceToHost,
+                          sout));
+  }
+  KCUDA(cudaStreamSynchronize(sout));
+  KCUDA(cudaStreamSynchronize(sc));
 }
 
 int kronop_sep_solve_host(kronop_ctx* ctx, const kronop_op* op, const double* b_host,

@@ -21,6 +21,12 @@ struct kronop_ctx {
   size_t tmp_cap = 0;
   double* io[2] = {nullptr, nullptr};       // device staging for the *_host entry points
   size_t io_cap = 0;
+  // copy engines for the pipelined host path (H2D / D2H overlap the slab-local passes)
+  cudaStream_t copy_stream[2] = {nullptr, nullptr};
+  static constexpr int kMaxChunks = 16;
+  cudaEvent_t ev_in[kMaxChunks] = {};
+  cudaEvent_t ev_out[kMaxChunks] = {};
+  cudaEvent_t ev_ready = nullptr;
 };
 
 constexpr int kScalarSlots = 256;

@@ -1,0 +1,174 @@
+// The reference's C++ API (include/kronop/kronop.hpp) used the way the reference's own unit tests
+// use theirs (proj/tests/test_operators.cpp, test_pcg.cpp, test_splitting.cpp, test_ground_state.cpp).
+// Built and run by tests/test_cpp_api.py on the GPU box; prints one line per check, exits non-zero
+// on the first failure.
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <memory>
+
+#include "kronop/kronop.hpp"
+
+using namespace kronop;
+
+static int g_checks = 0;
+#define CHECK(cond)                                                      \
+  do {                                                                   \
+    ++g_checks;                                                          \
+    if (!(cond)) {                                                       \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+      std::exit(1);                                                      \
+    }                                                                    \
+  } while (0)
+
+static double uniform(std::uint64_t& state) {  // SplitMix64::uniform_pm1 (rng.hpp:16-31)
+  state += 0x9E3779B97F4A7C15ULL;
+  std::uint64_t z = state;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return static_cast<double>((z ^ (z >> 31)) >> 11) * 0x1.0p-52 - 1.0;
+}
+
+int main() {
+  Context ctx(0);
+  const auto osc = [](double x) { return x * x; };
+
+  // test_operators.cpp:30-46 — apply reproduces eigenvectors of the Kronecker sum
+  {
+    const Basis1D b = assemble_sem(2.0, 3, 4);
+    std::vector<AxisEigens> axes = {build_axis(b, osc), build_axis(b, osc)};
+    SeparableOperator op(ctx, axes, 0.5);
+    const int n = axes[0].size();
+    RealField u({n, n});
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i)
+        u[i + n * j] = axes[0].transform[i + n * 2] * axes[1].transform[j + n * 0];
+    const double lam = axes[0].eigenvalues[2] + axes[1].eigenvalues[0];
+    const RealField hu = op.apply(u);
+    double err = 0.0, umax = 0.0;
+    for (std::size_t k = 0; k < u.size(); ++k) {
+      err = std::max(err, std::abs(hu[k] - (lam - 0.5) * u[k]));
+      umax = std::max(umax, std::abs(u[k]));
+    }
+    CHECK(err < 1e-9 * std::abs(lam) * umax);
+    std::printf("ok apply-eigenvector err %.3e\n", err);
+  }
+
+  // test_operators.cpp:60-93 — solve inverts apply; singular shift refused (:95-102)
+  {
+    const Basis1D b = assemble_sem(1.0, 4, 3);
+    std::vector<AxisEigens> axes = {build_axis(b, osc), build_axis(b, osc)};
+    SeparableOperator op(ctx, axes, 0.0);
+    const int n = b.size();
+    RealField rhs({n, n});
+    std::uint64_t s = 3;
+    for (std::size_t k = 0; k < rhs.size(); ++k) rhs[k] = uniform(s);
+    const RealField x = op.solve(rhs);
+    const RealField back = op.apply(x);
+    double num = 0, den = 0;
+    for (std::size_t k = 0; k < rhs.size(); ++k) {
+      num += (back[k] - rhs[k]) * (back[k] - rhs[k]);
+      den += rhs[k] * rhs[k];
+    }
+    CHECK(std::sqrt(num / den) < 1e-12);
+    op.set_shift(axes[0].eigenvalues[1] + axes[1].eigenvalues[3]);
+    bool threw = false;
+    try {
+      op.solve(rhs);
+    } catch (const NumericalError&) {
+      threw = true;
+    }
+    CHECK(threw);
+    std::printf("ok solve residual %.3e, singular shift -> NumericalError\n", std::sqrt(num / den));
+  }
+
+  // test_operators.cpp:104-137 — propagation is unitary in the mass norm and reversible
+  {
+    const Basis1D b = assemble_sem(8.0, 4, 7);
+    auto mass = std::make_shared<MassWeights>(MassWeights{b.mass, b.mass, b.mass});
+    std::vector<AxisEigens> axes(3, build_axis(b, osc));
+    SeparableOperator op(ctx, axes, 0.0, mass);
+    const int n = b.size();
+    ComplexField psi({n, n, n});
+    std::uint64_t s = 9;
+    for (std::size_t k = 0; k < psi.size(); ++k) psi[k] = {uniform(s), uniform(s)};
+    const ComplexField fwd = op.propagate(psi, 0.37);
+    const ComplexField back = op.propagate(fwd, -0.37);
+    double err = 0, nrm = 0, m0 = 0, m1 = 0;
+    for (int k2 = 0; k2 < n; ++k2)
+      for (int k1 = 0; k1 < n; ++k1)
+        for (int k0 = 0; k0 < n; ++k0) {
+          const std::size_t k = k0 + n * (k1 + static_cast<std::size_t>(n) * k2);
+          const double w = b.mass[k0] * b.mass[k1] * b.mass[k2];
+          err += std::norm(back[k] - psi[k]);
+          nrm += std::norm(psi[k]);
+          m0 += w * std::norm(psi[k]);
+          m1 += w * std::norm(fwd[k]);
+        }
+    CHECK(std::sqrt(err / nrm) < 1e-11);
+    CHECK(std::abs(m1 - m0) < 1e-11 * m0);
+    std::printf("ok propagate reversible %.3e, mass-norm drift %.3e\n", std::sqrt(err / nrm),
+                std::abs(m1 - m0) / m0);
+  }
+
+  // test_pcg.cpp:36-69 — the exact preconditioner converges in one iteration (device-resident)
+  {
+    const Basis1D b = assemble_sem(2.0, 3, 4);
+    std::vector<AxisEigens> axes(3, build_axis(b, osc));
+    SeparableOperator op(ctx, axes, 0.0);
+    const int n = b.size();
+    RealField rhs({n, n, n});
+    std::uint64_t s = 5;
+    for (std::size_t k = 0; k < rhs.size(); ++k) rhs[k] = uniform(s);
+    DeviceField<double> db(ctx, rhs), dx(ctx, RealField({n, n, n}));
+    PcgConfig cfg;
+    cfg.rel_tol = 1e-10;
+    cfg.record_history = true;
+    const PcgReport rep = pcg(ctx, LinearMap::apply(op), LinearMap::solve(op), db, dx, cfg);
+    CHECK(rep.converged && rep.iterations == 1);
+    CHECK(rep.history.size() == 2 && rep.history[1] <= 1e-10);
+    std::printf("ok pcg exact preconditioner: %d iteration(s), residual %.3e\n", rep.iterations,
+                rep.final_residual);
+  }
+
+  // test_splitting.cpp:29-35 — Yoshida coefficients
+  {
+    const YoshidaCoeffs c = yoshida_coeffs();
+    CHECK(std::abs(2.0 * c.gamma1 + c.gamma2 - 1.0) < 1e-15);
+    CHECK(std::abs(2.0 * std::pow(c.gamma1, 3) + std::pow(c.gamma2, 3)) < 1e-14);
+    std::printf("ok yoshida %.15f %.15f\n", c.gamma1, c.gamma2);
+  }
+
+  // test_ground_state.cpp — separable inverse iteration matches the sum of axis minima
+  {
+    const Basis1D b = assemble_sem(8.0, 4, 8);
+    auto mass = std::make_shared<MassWeights>(MassWeights{b.mass, b.mass, b.mass});
+    const auto f = [](double x) { return x * x + 100.0 * std::pow(std::sin(M_PI * x / 4.0), 2); };
+    std::vector<AxisEigens> axes(3, build_axis(b, f));
+    SeparableOperator sep(ctx, axes, 0.0, mass);
+    const int n = b.size();
+    DeviceField<double> init(ctx, RealField::constant({n, n, n}, 1.0)), vec(ctx, Shape{n, n, n});
+    FullOperator op{&sep, nullptr};
+    const EigenpairResult r = inverse_iteration(op, InverseIterationConfig{}, init, vec);
+    const double exact = 3.0 * axes[0].eigenvalues[0];
+    CHECK(r.converged);
+    CHECK(std::abs(r.eigenvalue - exact) < 1e-11 * exact);
+    std::printf("ok inverse iteration lambda %.12f (exact %.12f) in %d outer\n", r.eigenvalue,
+                exact, r.outer_iterations);
+  }
+
+  // errors.hpp: ParameterError on bad input through the C-ABI
+  {
+    bool threw = false;
+    try {
+      assemble_sem(-1.0, 3, 2);
+    } catch (const ParameterError&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  std::printf("all %d checks passed\n", g_checks);
+  return 0;
+}

@@ -163,6 +163,23 @@ def test_separable_apply_solve_propagate_kernel_parity(ctx, spec):
     assert (s, lo, hi) == (0.5, ko.lambda_min, ko.lambda_max)
 
 
+@pytest.mark.parametrize("spec", [(8.0, 13, 5, 3), (1.0, 4, 3, 2), (2.0, 3, 4, 4), (1.5, 5, 6, 1)])
+def test_host_buffer_entry_points_pipelined(ctx, spec):
+    """kronop_sep_{solve,apply,propagate}_host (slab-pipelined H2D/D2H) equal the device path."""
+    A = api()
+    grid = A.Grid.sem(*spec)
+    op = _trap_op(A, ctx, grid, 0.25)
+    ko = oracle_op_from(op, 0.25)
+    n = grid.node_count()
+    u = K.uniform_pm1(21, n)
+    out = np.empty_like(u)
+    assert rel(op.solve_host(u, out), ko.solve(u)) < 1e-13
+    assert rel(op.apply_host(u, np.empty_like(u)), ko.apply(u)) < 1e-13
+    psi = K.seeded_complex_field(grid.shape, 22)
+    assert rel(op.propagate_host(psi, 0.07, np.empty_like(psi)), ko.propagate(psi, 0.07)) < 1e-13
+    assert rel(op.solve_host(psi, np.empty_like(psi)), ko.solve(psi)) < 1e-13
+
+
 def test_full_operator_apply_with_v2_and_sigma(ctx):
     A = api()
     grid = A.Grid.sem(1.0, 7, 1, 3)  # 6^3, acceptance.cpp:131-200 instance
