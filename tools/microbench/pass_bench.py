@@ -9,9 +9,12 @@ from paper_2605_20491_b200 import api as A
 def main():
     res = {"lib": os.environ.get("KRONOP_LIB", "default")}
     ctx = A.Context(0)
-    for n, cplx in [(1024, False), (512, False), (512, True), (64, False), (79, False)]:
-        cells = (n + 1) // 5 if (n + 1) % 5 == 0 else None
-        grid = A.Grid.sem(8.0, cells, 5, 3) if cells else A.Grid.sem(8.0, 8, 10, 3)
+    cfgs = {1024: (205, 5), 512: (27, 19), 499: (100, 5), 79: (8, 10), 64: (13, 5)}
+    which = os.environ.get("PASS_CASES", "1024r,1024c,512r,499c,79r,64r").split(",")
+    for case in which:
+        n, cplx = int(case[:-1]), case[-1] == "c"
+        cells, k = cfgs[n]
+        grid = A.Grid.sem(8.0, cells, k, 3)
         op = grid.separable_operator(ctx, [lambda t: t * t] * 3)
         N = grid.node_count()
         x = A.splitmix_uniform(ctx, 1, 2 * N if cplx else N)
