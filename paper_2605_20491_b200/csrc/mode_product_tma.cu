@@ -112,6 +112,7 @@ __device__ __forceinline__ int chS(int g) { return ((g & 1) << 2) | (g >> 1); }
 
 struct TArgs {
   double* y;
+  int x2d;  // STRIDED with post == 1: X is the 2-D (pre x nk) tensor map
   long long pre, post, R;
   int nk, m;
   int ntiles_n;
@@ -162,8 +163,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   // The TMA producer is lane 0 of warp 0 (a dedicated producer warp would cap the DMMA warps at
   // 168 registers): it refills slot (kt + STAGES - 1) % STAGES once all eight warps released it.
-  const long long q_tile = row0 / args.pre;
-  const int p0 = static_cast<int>(row0 - q_tile * args.pre);
   auto issue = [&](int kt) {
     const int s = kt % STAGES;
     mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
@@ -173,9 +172,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int k0 = kt * BK;
     if (LOADER == TL_STRIDED) {
 #pragma unroll
-      for (int b = 0; b < BM / 16; ++b)
-        tma_load_3d(xs + b * BOX_STRIDED_BYTES, &tmx, p0 + 16 * b, k0, static_cast<int>(q_tile),
-                    &full[s]);
+      for (int b = 0; b < BM / 16; ++b) {
+        // each 16-row box lies inside one (p, q) plane: pre % 16 == 0, or post == 1 (2-D map)
+        const long long r = row0 + 16 * b;
+        if (args.x2d) {
+          tma_load_2d(xs + b * BOX_STRIDED_BYTES, &tmx, static_cast<int>(r), k0, &full[s]);
+        } else {
+          const long long qb = r / args.pre;
+          tma_load_3d(xs + b * BOX_STRIDED_BYTES, &tmx, static_cast<int>(r - qb * args.pre), k0,
+                      static_cast<int>(qb), &full[s]);
+        }
+      }
     } else {
 #pragma unroll
       for (int h = 0; h < BK / 16; ++h)
@@ -345,14 +352,17 @@ void prime_mode_product_tma_kernels() {
 
 bool mode_product_tma_eligible(const double* x, const PassShape& ps) {
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
-  if (ps.pre == 1) return ps.nk % 2 == 0 && ps.post <= 0x7fffffffLL;
-  return ps.pre % BM == 0 && ps.pre <= 0x7fffffffLL && ps.post <= 0x7fffffffLL;
+  if (ps.pre * ps.post > 0x7fffffffLL) return false;  // TMA coordinates are 32-bit
+  if (ps.pre == 1) return ps.nk % 2 == 0;             // row stride nk * 8 must be 16-B aligned
+  if (ps.pre % 2 != 0) return false;                  // k stride pre * 8 must be 16-B aligned
+  return ps.post == 1 || ps.pre % 16 == 0;            // a 16-row box never straddles two q
 }
 
 void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const double* a_pad,
                              int lda, const PassShape& ps, const EpiParams& ep) {
   TArgs ta;
   ta.y = y;
+  ta.x2d = 0;
   ta.pre = ps.pre;
   ta.post = ps.post;
   ta.R = ps.pre * ps.post;
@@ -375,6 +385,12 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ps.nk), static_cast<cuuint64_t>(ta.R)};
     const cuuint64_t str[1] = {static_cast<cuuint64_t>(ps.nk) * 8};
     const cuuint32_t box[2] = {16, BM};
+    encode(&tmx, x, 2, dims, str, box);
+  } else if (ps.post == 1) {
+    ta.x2d = 1;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ps.pre), static_cast<cuuint64_t>(ps.nk)};
+    const cuuint64_t str[1] = {static_cast<cuuint64_t>(ps.pre) * 8};
+    const cuuint32_t box[2] = {16, BK};
     encode(&tmx, x, 2, dims, str, box);
   } else {
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(ps.pre), static_cast<cuuint64_t>(ps.nk),

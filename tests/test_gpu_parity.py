@@ -44,7 +44,8 @@ def oracle_op_from(prod_op, shift=0.0):
 
 
 # ----------------------------------------------------------------------------- tensor --
-@pytest.mark.parametrize("shape", [(3, 4, 5), (64, 64, 64), (13, 7, 33), (129, 3, 130)])
+@pytest.mark.parametrize("shape", [(3, 4, 5), (64, 64, 64), (13, 7, 33), (129, 3, 130), (32, 5, 6),
+                                   (48, 3, 10), (6, 200, 2)])
 @pytest.mark.parametrize("cplx", [False, True])
 def test_mode_product_matches_dense(ctx, shape, cplx):
     A = api()
