@@ -637,3 +637,38 @@ def evolve(spec: SplitSpec, a: SeparableOperator, b_diag: torch.Tensor, psi0: to
                                   exact.h if exact is not None else None, stationary_eigenvalue,
                                   _ptr(state), C.byref(err), C.byref(steps)))
     return state, err.value, steps.value
+
+
+@dataclass
+class LevelReport:
+    """ground_state.hpp:58-66."""
+    n: int
+    outer_iterations: int
+    total_inner_iterations: int
+    inner_per_outer: float
+    eigenvalue: float
+
+
+def multilevel_ground_state(ctx: Context, grids: Sequence[Grid], make_operator,
+                            config: InverseIterationConfig):
+    """Coarse-to-fine continuation (ground_state.cpp:101-154): solve on each SEM grid, prolong the
+    eigenvector with per-axis piecewise-linear interpolation (rectangular mode products on the
+    device), continue. make_operator(grid) -> FullOperator. Returns (EigenpairResult, [LevelReport])."""
+    if not grids:
+        raise L.ParameterError(L.KRONOP_EPARAM, "multilevel_ground_state: no levels")
+    guess, prev = None, None
+    levels, pair = [], None
+    for grid in grids:
+        op = make_operator(grid)
+        if guess is None:
+            initial = op.sep.ground_state()
+        else:
+            mats = [interp_matrix(prev.axes[a], grid.axes[a]) for a in range(grid.dim)]
+            initial = kron_apply(ctx, guess, prev.shape, mats)
+        pair = inverse_iteration(op, config, initial)
+        levels.append(LevelReport(grid.axes[0].size, pair.outer_iterations,
+                                  pair.total_inner_iterations,
+                                  pair.total_inner_iterations / max(1, pair.outer_iterations),
+                                  pair.eigenvalue))
+        guess, prev = pair.eigenvector, grid
+    return pair, levels

@@ -163,6 +163,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   // The TMA producer is lane 0 of warp 0 (a dedicated producer warp would cap the DMMA warps at
   // 168 registers): it refills slot (kt + STAGES - 1) % STAGES once all eight warps released it.
+  // (p, q) of each 16-row box of this tile, computed once (pre % 16 == 0: a box never straddles)
+  int box_p[BM / 16], box_q[BM / 16];
+  if (LOADER == TL_STRIDED && tid == 0 && !args.x2d) {
+    long long q = row0 / args.pre;
+    long long p = row0 - q * args.pre;
+#pragma unroll
+    for (int b = 0; b < BM / 16; ++b) {
+      box_p[b] = static_cast<int>(p);
+      box_q[b] = static_cast<int>(q);
+      p += 16;
+      if (p >= args.pre) {
+        p -= args.pre;
+        ++q;
+      }
+    }
+  }
   auto issue = [&](int kt) {
     const int s = kt % STAGES;
     mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
@@ -173,15 +189,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (LOADER == TL_STRIDED) {
 #pragma unroll
       for (int b = 0; b < BM / 16; ++b) {
-        // each 16-row box lies inside one (p, q) plane: pre % 16 == 0, or post == 1 (2-D map)
-        const long long r = row0 + 16 * b;
-        if (args.x2d) {
-          tma_load_2d(xs + b * BOX_STRIDED_BYTES, &tmx, static_cast<int>(r), k0, &full[s]);
-        } else {
-          const long long qb = r / args.pre;
-          tma_load_3d(xs + b * BOX_STRIDED_BYTES, &tmx, static_cast<int>(r - qb * args.pre), k0,
-                      static_cast<int>(qb), &full[s]);
-        }
+        if (args.x2d)
+          tma_load_2d(xs + b * BOX_STRIDED_BYTES, &tmx, static_cast<int>(row0) + 16 * b, k0,
+                      &full[s]);
+        else
+          tma_load_3d(xs + b * BOX_STRIDED_BYTES, &tmx, box_p[b], k0, box_q[b], &full[s]);
       }
     } else {
 #pragma unroll

@@ -443,3 +443,45 @@ def test_evolve_unitarity_and_stationary(ctx):
                                      merge_across_steps=True), full, torch.zeros_like(b), gs,
                          stationary_eigenvalue=full.min_eigenvalue())
     assert e2 < 1e-10
+
+
+def test_multilevel_ground_state_criterion7(ctx):
+    """acceptance.cpp:347-368: stirrer, Q20, 2 -> 4 cells (39^3 -> 79^3). Same per-level outer
+    and inner iteration counts as the oracle; eigenvalue equal to 1e-11 and to the reference's
+    golden 5.286155366963 within its 1e-6."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grids = [A.Grid.sem(8.0, 2, 20, 3), A.Grid.sem(8.0, 4, 20, 3)]
+
+    def mk(g):
+        pot = P.build_potential("stirrer", g)
+        return A.FullOperator(g.separable_operator(ctx, pot.separable), pot.v2_device())
+    pair, levels = A.multilevel_ground_state(ctx, grids, mk, A.InverseIterationConfig())
+    kgrids = [K.Grid.sem(8.0, 2, 20, 3), K.Grid.sem(8.0, 4, 20, 3)]
+    kpair, klevels = K.multilevel_ground_state(
+        kgrids, lambda g: K.build_full_operator(g, K.build_potential("stirrer", g)),
+        K.InverseIterationConfig())
+    assert [(lv.n, lv.outer_iterations, lv.total_inner_iterations) for lv in levels] == \
+        [(l[0], l[1], l[2]) for l in klevels]
+    assert abs(pair.eigenvalue - kpair.eigenvalue) <= 1e-11 * kpair.eigenvalue
+    assert abs(pair.eigenvalue - 5.286155366963) <= 1e-6 * 5.286155366963
+
+
+@pytest.mark.parametrize("spec", [(5.0, 2, 3, 6), (3.0, 2, 2, 9), (8.0, 2, 10, 4)])
+def test_high_dimensional_operators(ctx, spec):
+    """6D / 9D / 4D grids (config 5 families at parity-test size): apply / solve / propagate and
+    a qHOP step with the soft-Coulomb B equal the oracle given the same factors."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(*spec)
+    op = _trap_op(A, ctx, grid, 0.0)
+    ko = oracle_op_from(op)
+    u = K.uniform_pm1(31, grid.node_count())
+    psi = K.seeded_complex_field(grid.shape, 32)
+    assert rel(host(op.apply(dev(u))), ko.apply(u)) < 1e-13
+    assert rel(host(op.solve(dev(u))), ko.solve(u)) < 1e-13
+    assert rel(host(op.propagate(dev(psi), 0.01)), ko.propagate(psi, 0.01)) < 1e-13
+    kind = {6: "coulomb-3d2", 9: "coulomb-3d3", 4: "coulomb-2d2"}[grid.dim]
+    b = P.build_potential(kind, grid).nonseparable
+    out = host(A.qhop_step(op, dev(b), dev(psi), 0.02, 3))
+    assert rel(out, K.qhop_step(ko, b, psi, 0.02, 3)) < 1e-12

@@ -125,6 +125,16 @@ int main() {
     timeit(nm, [&] { k_dfma<<<blocks, threads>>>(out, 0.999); },
            2.0 * 16 * ITERS * double(blocks) * threads);
   }
+  for (int wps : {4, 8, 12, 16}) {
+    // one block per SM with wps warps: DMMA throughput vs resident warps
+    const int blocks = sms, threads = 32 * wps;
+    const double warps = double(blocks) * wps;
+    char nm[64];
+    snprintf(nm, sizeof nm, "DMMA m8n8k4 x8 warps/SM=%d", wps);
+    timeit(nm, [&] { k_dmma884<8><<<blocks, threads>>>(out, 0.5); }, warps * 8 * ITERS * 2.0 * 8 * 8 * 4);
+    snprintf(nm, sizeof nm, "DMMA m8n8k4 x32 warps/SM=%d", wps);
+    timeit(nm, [&] { k_dmma884<32><<<blocks, threads>>>(out, 0.5); }, warps * 32 * ITERS * 2.0 * 8 * 8 * 4);
+  }
   for (int bps : {2, 4}) {
     const int blocks = sms * bps, threads = 256;
     const double warps = double(blocks) * threads / 32;
