@@ -145,12 +145,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const long long bid = blockIdx.x;
-  const int ntile = static_cast<int>(bid % args.ntiles_n);
-  const long long mtile = bid / args.ntiles_n;
-  const long long row0 = mtile * BM;
-  const int col0 = ntile * BN;
   const int KT = (args.nk + BK - 1) / BK;
+  // Persistent CTAs: tile t = blockIdx.x + i * gridDim.x (N-tiles fastest, so the CTAs sharing an
+  // X panel are resident together). The k-stage counter `it` runs across tiles, so the producer
+  // streams the next tile's first stages while the consumers run the current tile's epilogue.
+  const long long ntiles = args.ntiles_m * args.ntiles_n;
+  const long long my_tiles =
+      blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long total_it = my_tiles * KT;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -161,27 +163,41 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   __syncthreads();
 
-  // The TMA producer is lane 0 of warp 0 (a dedicated producer warp would cap the DMMA warps at
-  // 168 registers): it refills slot (kt + STAGES - 1) % STAGES once all eight warps released it.
-  // (p, q) of each 16-row box of this tile, computed once (pre % 16 == 0: a box never straddles)
+  // ------------------------------------------------------------------ producer state --
+  // Lane 0 of warp 0 is the TMA producer (a dedicated producer warp would cap the DMMA warps at
+  // 168 registers): it refills slot (it + STAGES - 1) % STAGES once all eight warps released it.
+  const bool producer = tid == 0;
+  long long p_tile = -1;  // local tile index the producer state below describes
+  long long p_row0 = 0;
+  int p_col0 = 0;
   int box_p[BM / 16], box_q[BM / 16];
-  if (LOADER == TL_STRIDED && tid == 0 && !args.x2d) {
-    long long q = row0 / args.pre;
-    long long p = row0 - q * args.pre;
+  auto producer_tile = [&](long long lt) {
+    p_tile = lt;
+    const long long tile = blockIdx.x + lt * gridDim.x;
+    p_row0 = (tile / args.ntiles_n) * BM;
+    p_col0 = static_cast<int>(tile % args.ntiles_n) * BN;
+    if (LOADER == TL_STRIDED && !args.x2d) {
+      // (p, q) of each 16-row box (pre % 16 == 0: a box never straddles two q)
+      long long q = p_row0 / args.pre;
+      long long pp = p_row0 - q * args.pre;
 #pragma unroll
-    for (int b = 0; b < BM / 16; ++b) {
-      box_p[b] = static_cast<int>(p);
-      box_q[b] = static_cast<int>(q);
-      p += 16;
-      if (p >= args.pre) {
-        p -= args.pre;
-        ++q;
+      for (int b = 0; b < BM / 16; ++b) {
+        box_p[b] = static_cast<int>(pp);
+        box_q[b] = static_cast<int>(q);
+        pp += 16;
+        if (pp >= args.pre) {
+          pp -= args.pre;
+          ++q;
+        }
       }
     }
-  }
-  auto issue = [&](int kt) {
-    const int s = kt % STAGES;
-    mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
+  };
+  auto issue = [&](long long it) {
+    const long long lt = it / KT;
+    const int kt = static_cast<int>(it - lt * KT);
+    if (lt != p_tile) producer_tile(lt);
+    const int s = static_cast<int>(it % STAGES);
+    mbar_wait(&empty[s], static_cast<uint32_t>(((it / STAGES) & 1) ^ 1));
     unsigned char* xs = smem + s * C::STAGE_BYTES;
     unsigned char* as = xs + C::X_BYTES;
     mbar_expect_tx(&full[s], C::STAGE_BYTES);
@@ -190,7 +206,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
       for (int b = 0; b < BM / 16; ++b) {
         if (args.x2d)
-          tma_load_2d(xs + b * BOX_STRIDED_BYTES, &tmx, static_cast<int>(row0) + 16 * b, k0,
+          tma_load_2d(xs + b * BOX_STRIDED_BYTES, &tmx, static_cast<int>(p_row0) + 16 * b, k0,
                       &full[s]);
         else
           tma_load_3d(xs + b * BOX_STRIDED_BYTES, &tmx, box_p[b], k0, box_q[b], &full[s]);
@@ -198,78 +214,57 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else {
 #pragma unroll
       for (int h = 0; h < BK / 16; ++h)
-        tma_load_2d(xs + h * BOX_CONTIG_BYTES, &tmx, k0 + 16 * h, static_cast<int>(row0),
+        tma_load_2d(xs + h * BOX_CONTIG_BYTES, &tmx, k0 + 16 * h, static_cast<int>(p_row0),
                     &full[s]);
     }
 #pragma unroll
     for (int c = 0; c < BN / 16; ++c)
-      tma_load_2d(as + c * BOX_STRIDED_BYTES, &tma, col0 + 16 * c, k0, &full[s]);
+      tma_load_2d(as + c * BOX_STRIDED_BYTES, &tma, p_col0 + 16 * c, k0, &full[s]);
   };
-  const bool producer = tid == 0;
   if (producer) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmx) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tma) : "memory");
-    for (int kt = 0; kt < STAGES - 1 && kt < KT; ++kt) issue(kt);
+    for (long long it = 0; it < STAGES - 1 && it < total_it; ++it) issue(it);
   }
 
   // ---------------------------------------------------------------- DMMA consumers --
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
-  double acc[C::RT][C::CT][2];
-#pragma unroll
-  for (int i = 0; i < C::RT; ++i)
-#pragma unroll
-    for (int j = 0; j < C::CT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
   const int cs = chS(g);
-  for (int kt = 0; kt < KT; ++kt) {
-    if (producer && kt + STAGES - 1 < KT) issue(kt + STAGES - 1);
-    const int s = kt % STAGES;
-    mbar_wait(&full[s], (kt / STAGES) & 1);
-    const char* xs = reinterpret_cast<const char*>(smem + s * C::STAGE_BYTES);
-    const char* as = xs + C::X_BYTES;
-    if (LOADER == TL_STRIDED) {
+  const EpiParams& ep = args.ep;
+  const long long pre = args.pre, R = args.R;
+  const int m = args.m;
+  const bool spectral =
+      ep.kind == EPI_SPEC_MUL || ep.kind == EPI_SPEC_DIV || ep.kind == EPI_SPEC_PHASE;
+  long long it = 0;
+  for (long long lt = 0; lt < my_tiles; ++lt) {
+    const long long tile = blockIdx.x + lt * gridDim.x;
+    const long long row0 = (tile / args.ntiles_n) * BM;
+    const int col0 = static_cast<int>(tile % args.ntiles_n) * BN;
+    double acc[C::RT][C::CT][2];
 #pragma unroll
-      for (int k4 = 0; k4 < BK / 4; ++k4) {
-        const int kk = k4 * 4 + t;
-        const uint32_t rowoff = kk * 128 + ((cs ^ (kk & 7)) << 4);
-        double af[C::RT], bf[C::CT];
+    for (int i = 0; i < C::RT; ++i)
 #pragma unroll
-        for (int bb = 0; bb < C::RT / 2; ++bb) {
-          const double2 v = lds128(xs, (wm * (C::RT / 2) + bb) * BOX_STRIDED_BYTES + rowoff);
-          af[2 * bb] = v.x;
-          af[2 * bb + 1] = v.y;
-        }
+      for (int j = 0; j < C::CT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt, ++it) {
+      if (producer && it + STAGES - 1 < total_it) issue(it + STAGES - 1);
+      const int s = static_cast<int>(it % STAGES);
+      mbar_wait(&full[s], static_cast<uint32_t>((it / STAGES) & 1));
+      const char* xs = reinterpret_cast<const char*>(smem + s * C::STAGE_BYTES);
+      const char* as = xs + C::X_BYTES;
+      if (LOADER == TL_STRIDED) {
 #pragma unroll
-        for (int cc = 0; cc < C::CT / 2; ++cc) {
-          const double2 w = lds128(as, (wn * (C::CT / 2) + cc) * BOX_STRIDED_BYTES + rowoff);
-          bf[2 * cc] = w.x;
-          bf[2 * cc + 1] = w.y;
-        }
+        for (int k4 = 0; k4 < BK / 4; ++k4) {
+          const int kk = k4 * 4 + t;
+          const uint32_t rowoff = kk * 128 + ((cs ^ (kk & 7)) << 4);
+          double af[C::RT], bf[C::CT];
 #pragma unroll
-        for (int i = 0; i < C::RT; ++i)
-#pragma unroll
-          for (int j = 0; j < C::CT; ++j) dmma884(acc[i][j], af[i], bf[j]);
-      }
-    } else {
-#pragma unroll
-      for (int kb = 0; kb < BK / 8; ++kb) {
-        double a0[C::RT], a1[C::RT];
-        const int h = kb >> 1;
-        const int chunk = ((kb & 1) << 2) | t;
-#pragma unroll
-        for (int rt = 0; rt < C::RT; ++rt) {
-          const int row = wm * C::WTM + rt * 8 + cs;  // cs = rowC(g): row & 7 == chS(g)
-          const double2 v =
-              lds128(xs, h * BOX_CONTIG_BYTES + row * 128 + ((chunk ^ (row & 7)) << 4));
-          a0[rt] = v.x;  // k = kb*8 + 2t
-          a1[rt] = v.y;  // k = kb*8 + 2t + 1
-        }
-#pragma unroll
-        for (int sstep = 0; sstep < 2; ++sstep) {
-          const int kk = kb * 8 + 2 * t + sstep;
-          const uint32_t rowoff = kk * 128 + ((g ^ (kk & 7)) << 4);
-          double bf[C::CT];
+          for (int bb = 0; bb < C::RT / 2; ++bb) {
+            const double2 v = lds128(xs, (wm * (C::RT / 2) + bb) * BOX_STRIDED_BYTES + rowoff);
+            af[2 * bb] = v.x;
+            af[2 * bb + 1] = v.y;
+          }
 #pragma unroll
           for (int cc = 0; cc < C::CT / 2; ++cc) {
             const double2 w = lds128(as, (wn * (C::CT / 2) + cc) * BOX_STRIDED_BYTES + rowoff);
@@ -279,46 +274,73 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int i = 0; i < C::RT; ++i)
 #pragma unroll
-            for (int j = 0; j < C::CT; ++j) dmma884(acc[i][j], sstep ? a1[i] : a0[i], bf[j]);
+            for (int j = 0; j < C::CT; ++j) dmma884(acc[i][j], af[i], bf[j]);
+        }
+      } else {
+#pragma unroll
+        for (int kb = 0; kb < BK / 8; ++kb) {
+          double a0[C::RT], a1[C::RT];
+          const int h = kb >> 1;
+          const int chunk = ((kb & 1) << 2) | t;
+#pragma unroll
+          for (int rt = 0; rt < C::RT; ++rt) {
+            const int row = wm * C::WTM + rt * 8 + cs;  // row & 7 == chS(g)
+            const double2 v =
+                lds128(xs, h * BOX_CONTIG_BYTES + row * 128 + ((chunk ^ (row & 7)) << 4));
+            a0[rt] = v.x;  // k = kb*8 + 2t
+            a1[rt] = v.y;  // k = kb*8 + 2t + 1
+          }
+#pragma unroll
+          for (int sstep = 0; sstep < 2; ++sstep) {
+            const int kk = kb * 8 + 2 * t + sstep;
+            const uint32_t rowoff = kk * 128 + ((g ^ (kk & 7)) << 4);
+            double bf[C::CT];
+#pragma unroll
+            for (int cc = 0; cc < C::CT / 2; ++cc) {
+              const double2 w = lds128(as, (wn * (C::CT / 2) + cc) * BOX_STRIDED_BYTES + rowoff);
+              bf[2 * cc] = w.x;
+              bf[2 * cc + 1] = w.y;
+            }
+#pragma unroll
+            for (int i = 0; i < C::RT; ++i)
+#pragma unroll
+              for (int j = 0; j < C::CT; ++j) dmma884(acc[i][j], sstep ? a1[i] : a0[i], bf[j]);
+          }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
 
-  // ----------------------------------------------------------------------- epilogue --
-  const EpiParams& ep = args.ep;
-  const long long pre = args.pre, R = args.R;
-  const int m = args.m;
-  const bool spectral = ep.kind == EPI_SPEC_MUL || ep.kind == EPI_SPEC_DIV || ep.kind == EPI_SPEC_PHASE;
+    // --------------------------------------------------------------------- epilogue --
 #pragma unroll
-  for (int j = 0; j < C::RT; ++j) {
-    const long long r = row0 + wm * C::WTM + row_map<BN, LOADER>(j, g);
-    const bool rok = r < R;
-    const long long rr = rok ? r : 0;
-    const long long q = rr / pre;
-    const long long p = rr - q * pre;
-    const long long ybase = p + q * pre * m;
-    const double lam_lo = spectral ? lambda_partial_low_ext(ep, p, ep.axis) : 0.0;
+    for (int j = 0; j < C::RT; ++j) {
+      const long long r = row0 + wm * C::WTM + row_map<BN, LOADER>(j, g);
+      const bool rok = r < R;
+      const long long rr = rok ? r : 0;
+      const long long q = rr / pre;
+      const long long p = rr - q * pre;
+      const long long ybase = p + q * pre * m;
+      const double lam_lo = spectral ? lambda_partial_low_ext(ep, p, ep.axis) : 0.0;
 #pragma unroll
-    for (int jc = 0; jc < C::CT; ++jc) {
+      for (int jc = 0; jc < C::CT; ++jc) {
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
-        const bool ok = rok && i < m;
-        double val = acc[j][jc][v];
-        const long long yi = ybase + pre * static_cast<long long>(ok ? i : 0);
-        if (spectral) {
-          // PHASE: the re/im partner (row r ^ 1) is this thread's tile j ^ 1 (STRIDED map)
-          const double other = ep.kind == EPI_SPEC_PHASE ? acc[j ^ 1][jc][v] : 0.0;
-          val = spectral_epilogue_ext(ep, val, other, lam_lo, ep.axis, ok ? i : -1, q, p);
-        } else if (ep.kind == EPI_AXPY_DIAG && ok) {
-          const double uu = ep.u[yi];
-          if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (yi >> 1) : yi], uu));
-          if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+        for (int v = 0; v < 2; ++v) {
+          const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
+          const bool ok = rok && i < m;
+          double val = acc[j][jc][v];
+          const long long yi = ybase + pre * static_cast<long long>(ok ? i : 0);
+          if (spectral) {
+            // PHASE: the re/im partner (row r ^ 1) is this thread's tile j ^ 1 (STRIDED map)
+            const double other = ep.kind == EPI_SPEC_PHASE ? acc[j ^ 1][jc][v] : 0.0;
+            val = spectral_epilogue_ext(ep, val, other, lam_lo, ep.axis, ok ? i : -1, q, p);
+          } else if (ep.kind == EPI_AXPY_DIAG && ok) {
+            const double uu = ep.u[yi];
+            if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (yi >> 1) : yi], uu));
+            if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+          }
+          if (ok) args.y[yi] = val;
         }
-        if (ok) args.y[yi] = val;
       }
     }
   }
@@ -412,7 +434,14 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
     const cuuint32_t box[3] = {16, BK, 1};
     encode(&tmx, x, 3, dims, str, box);
   }
-  const long long blocks = ta.ntiles_m * ta.ntiles_n;
+  static int num_sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  const long long tiles = ta.ntiles_m * ta.ntiles_n;
+  const long long blocks = tiles < num_sms ? tiles : num_sms;  // one persistent CTA per SM
   if (bn == 128) {
     if (contig)
       mode_product_tma_kernel<128, TL_CONTIG><<<blocks, NTHREADS, Cfg<128>::SMEM, s>>>(tmx, tmA, ta);
