@@ -40,7 +40,12 @@ constexpr int NTHREADS = NCONS * 32;
 constexpr int BOX_STRIDED_BYTES = BK * 128;  // [BK rows][16 doubles]
 constexpr int BOX_CONTIG_BYTES = BM * 128;   // [BM rows][16 doubles]
 
-enum { TL_STRIDED = 0, TL_CONTIG = 1 };
+enum { TL_STRIDED = 0, TL_CONTIG = 1, TL_CPLX0 = 2 };
+// TL_CPLX0: pre == 2 (axis 0 of an interleaved complex field). X viewed as the 2-D tensor
+// (2 nk doubles per row, post rows); a box is [64 q][8 j x (re, im)] = 128 B rows, so one 128-bit
+// fragment load returns (re, im) of one (q, j): the re row and the im row of the pass are the two
+// DMMA tiles of a pair, exactly like the STRIDED pairing (rows r = c + 2q).
+constexpr int BOX_CPLX0_BYTES = (BM / 2) * 128;
 
 template <int BN>
 struct Cfg {
@@ -123,13 +128,13 @@ struct TArgs {
 template <int BN, int LOADER>
 __device__ __forceinline__ int row_map(int j, int g) {
   // row (within the warp tile) of MMA row g of row-tile j
-  if (LOADER == TL_STRIDED) return (j >> 1) * 16 + 2 * chS(g) + (j & 1);
+  if (LOADER == TL_STRIDED || LOADER == TL_CPLX0) return (j >> 1) * 16 + 2 * chS(g) + (j & 1);
   return j * 8 + chS(g);
 }
 template <int BN, int LOADER>
 __device__ __forceinline__ int col_map(int jc, int n) {
-  if (LOADER == TL_STRIDED) return (jc >> 1) * 16 + 2 * chS(n) + (jc & 1);
-  return (jc >> 1) * 16 + 2 * n + (jc & 1);
+  if (LOADER == TL_CONTIG) return (jc >> 1) * 16 + 2 * n + (jc & 1);
+  return (jc >> 1) * 16 + 2 * chS(n) + (jc & 1);
 }
 
 template <int BN, int LOADER>
@@ -146,12 +151,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int KT = (args.nk + BK - 1) / BK;
-  // Persistent CTAs: tile t = blockIdx.x + i * gridDim.x (N-tiles fastest, so the CTAs sharing an
-  // X panel are resident together). The k-stage counter `it` runs across tiles, so the producer
-  // streams the next tile's first stages while the consumers run the current tile's epilogue.
-  const long long ntiles = args.ntiles_m * args.ntiles_n;
-  const long long my_tiles =
-      blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // Persistent CTAs: CTA b owns the row panels b, b + gridDim.x, ... and walks all N-tiles of a
+  // panel back to back, so the panel's X rows are re-read from L2 (hot) and the per-axis matrix
+  // stays L2-resident. The k-stage counter `it` runs across tiles, so the producer streams the
+  // next tile's first stages while the consumers run the current tile's epilogue.
+  const long long my_panels =
+      blockIdx.x < args.ntiles_m ? (args.ntiles_m - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long my_tiles = my_panels * args.ntiles_n;
   const long long total_it = my_tiles * KT;
 
   if (tid == 0) {
@@ -173,9 +179,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int box_p[BM / 16], box_q[BM / 16];
   auto producer_tile = [&](long long lt) {
     p_tile = lt;
-    const long long tile = blockIdx.x + lt * gridDim.x;
-    p_row0 = (tile / args.ntiles_n) * BM;
-    p_col0 = static_cast<int>(tile % args.ntiles_n) * BN;
+    const long long panel = blockIdx.x + (lt / args.ntiles_n) * gridDim.x;
+    p_row0 = panel * BM;
+    p_col0 = static_cast<int>(lt % args.ntiles_n) * BN;
     if (LOADER == TL_STRIDED && !args.x2d) {
       // (p, q) of each 16-row box (pre % 16 == 0: a box never straddles two q)
       long long q = p_row0 / args.pre;
@@ -211,11 +217,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         else
           tma_load_3d(xs + b * BOX_STRIDED_BYTES, &tmx, box_p[b], k0, box_q[b], &full[s]);
       }
-    } else {
+    } else if (LOADER == TL_CONTIG) {
 #pragma unroll
       for (int h = 0; h < BK / 16; ++h)
         tma_load_2d(xs + h * BOX_CONTIG_BYTES, &tmx, k0 + 16 * h, static_cast<int>(p_row0),
                     &full[s]);
+    } else {
+#pragma unroll
+      for (int h = 0; h < BK / 8; ++h)
+        tma_load_2d(xs + h * BOX_CPLX0_BYTES, &tmx, 2 * (k0 + 8 * h),
+                    static_cast<int>(p_row0 >> 1), &full[s]);
     }
 #pragma unroll
     for (int c = 0; c < BN / 16; ++c)
@@ -238,9 +249,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       ep.kind == EPI_SPEC_MUL || ep.kind == EPI_SPEC_DIV || ep.kind == EPI_SPEC_PHASE;
   long long it = 0;
   for (long long lt = 0; lt < my_tiles; ++lt) {
-    const long long tile = blockIdx.x + lt * gridDim.x;
-    const long long row0 = (tile / args.ntiles_n) * BM;
-    const int col0 = static_cast<int>(tile % args.ntiles_n) * BN;
+    const long long row0 = (blockIdx.x + (lt / args.ntiles_n) * gridDim.x) * BM;
+    const int col0 = static_cast<int>(lt % args.ntiles_n) * BN;
     double acc[C::RT][C::CT][2];
 #pragma unroll
     for (int i = 0; i < C::RT; ++i)
@@ -253,7 +263,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&full[s], static_cast<uint32_t>((it / STAGES) & 1));
       const char* xs = reinterpret_cast<const char*>(smem + s * C::STAGE_BYTES);
       const char* as = xs + C::X_BYTES;
-      if (LOADER == TL_STRIDED) {
+      if (LOADER == TL_STRIDED || LOADER == TL_CPLX0) {
 #pragma unroll
         for (int k4 = 0; k4 < BK / 4; ++k4) {
           const int kk = k4 * 4 + t;
@@ -261,7 +271,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           double af[C::RT], bf[C::CT];
 #pragma unroll
           for (int bb = 0; bb < C::RT / 2; ++bb) {
-            const double2 v = lds128(xs, (wm * (C::RT / 2) + bb) * BOX_STRIDED_BYTES + rowoff);
+            double2 v;
+            if (LOADER == TL_STRIDED) {
+              v = lds128(xs, (wm * (C::RT / 2) + bb) * BOX_STRIDED_BYTES + rowoff);
+            } else {
+              const int ql = wm * (C::WTM / 2) + bb * 8 + cs;  // ql & 7 == chS(g)
+              v = lds128(xs, (kk >> 3) * BOX_CPLX0_BYTES + ql * 128 + (((kk & 7) ^ cs) << 4));
+            }
             af[2 * bb] = v.x;
             af[2 * bb + 1] = v.y;
           }
@@ -331,7 +347,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           double val = acc[j][jc][v];
           const long long yi = ybase + pre * static_cast<long long>(ok ? i : 0);
           if (spectral) {
-            // PHASE: the re/im partner (row r ^ 1) is this thread's tile j ^ 1 (STRIDED map)
+            // PHASE: the re/im partner (row r ^ 1) is this thread's tile j ^ 1 (paired maps)
             const double other = ep.kind == EPI_SPEC_PHASE ? acc[j ^ 1][jc][v] : 0.0;
             val = spectral_epilogue_ext(ep, val, other, lam_lo, ep.axis, ok ? i : -1, q, p);
           } else if (ep.kind == EPI_AXPY_DIAG && ok) {
@@ -378,6 +394,8 @@ void set_attr_tma() {
 }  // namespace
 
 void prime_mode_product_tma_kernels() {
+  set_attr_tma<128, TL_CPLX0>();
+  set_attr_tma<64, TL_CPLX0>();
   set_attr_tma<128, TL_STRIDED>();
   set_attr_tma<128, TL_CONTIG>();
   set_attr_tma<64, TL_STRIDED>();
@@ -388,6 +406,7 @@ bool mode_product_tma_eligible(const double* x, const PassShape& ps) {
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
   if (ps.pre * ps.post > 0x7fffffffLL) return false;  // TMA coordinates are 32-bit
   if (ps.pre == 1) return ps.nk % 2 == 0;             // row stride nk * 8 must be 16-B aligned
+  if (ps.pre == 2) return true;                       // complex axis 0 (TL_CPLX0), rows of 2nk
   if (ps.pre % 2 != 0) return false;                  // k stride pre * 8 must be 16-B aligned
   return ps.post == 1 || ps.pre % 16 == 0;            // a 16-row box never straddles two q
 }
@@ -415,7 +434,14 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
     encode(&tmA, a_pad, 2, dims, str, box);
   }
   const bool contig = ps.pre == 1;
-  if (contig) {
+  const bool cplx0 = ps.pre == 2;
+  if (cplx0) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * ps.nk),
+                                static_cast<cuuint64_t>(ps.post)};
+    const cuuint64_t str[1] = {static_cast<cuuint64_t>(2 * ps.nk) * 8};
+    const cuuint32_t box[2] = {16, BM / 2};
+    encode(&tmx, x, 2, dims, str, box);
+  } else if (contig) {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ps.nk), static_cast<cuuint64_t>(ta.R)};
     const cuuint64_t str[1] = {static_cast<cuuint64_t>(ps.nk) * 8};
     const cuuint32_t box[2] = {16, BM};
@@ -440,9 +466,13 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
-  const long long tiles = ta.ntiles_m * ta.ntiles_n;
-  const long long blocks = tiles < num_sms ? tiles : num_sms;  // one persistent CTA per SM
-  if (bn == 128) {
+  const long long blocks = ta.ntiles_m < num_sms ? ta.ntiles_m : num_sms;  // one CTA per SM
+  if (cplx0) {
+    if (bn == 128)
+      mode_product_tma_kernel<128, TL_CPLX0><<<blocks, NTHREADS, Cfg<128>::SMEM, s>>>(tmx, tmA, ta);
+    else
+      mode_product_tma_kernel<64, TL_CPLX0><<<blocks, NTHREADS, Cfg<64>::SMEM, s>>>(tmx, tmA, ta);
+  } else if (bn == 128) {
     if (contig)
       mode_product_tma_kernel<128, TL_CONTIG><<<blocks, NTHREADS, Cfg<128>::SMEM, s>>>(tmx, tmA, ta);
     else
