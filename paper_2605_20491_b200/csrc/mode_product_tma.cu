@@ -198,12 +198,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   };
-  auto issue = [&](long long it) {
-    const long long lt = it / KT;
-    const int kt = static_cast<int>(it - lt * KT);
-    if (lt != p_tile) producer_tile(lt);
-    const int s = static_cast<int>(it % STAGES);
-    mbar_wait(&empty[s], static_cast<uint32_t>(((it / STAGES) & 1) ^ 1));
+  // producer cursor: (local tile, k tile, ring slot, ring phase) advanced incrementally (no
+  // 64-bit divisions on the producer's critical path)
+  long long c_lt = 0;
+  int c_kt = 0, c_slot = 0;
+  uint32_t c_phase = 0;
+  auto issue = [&]() {
+    if (c_lt != p_tile) producer_tile(c_lt);
+    const int s = c_slot;
+    const int kt = c_kt;
+    mbar_wait(&empty[s], c_phase ^ 1);
+    if (++c_slot == STAGES) {
+      c_slot = 0;
+      c_phase ^= 1;
+    }
+    if (++c_kt == KT) {
+      c_kt = 0;
+      ++c_lt;
+    }
     unsigned char* xs = smem + s * C::STAGE_BYTES;
     unsigned char* as = xs + C::X_BYTES;
     mbar_expect_tx(&full[s], C::STAGE_BYTES);
@@ -235,7 +247,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (producer) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmx) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tma) : "memory");
-    for (long long it = 0; it < STAGES - 1 && it < total_it; ++it) issue(it);
+    for (long long it = 0; it < STAGES - 1 && it < total_it; ++it) issue();
   }
 
   // ---------------------------------------------------------------- DMMA consumers --
@@ -248,6 +260,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const bool spectral =
       ep.kind == EPI_SPEC_MUL || ep.kind == EPI_SPEC_DIV || ep.kind == EPI_SPEC_PHASE;
   long long it = 0;
+  int slot = 0;
+  uint32_t phase = 0;
   for (long long lt = 0; lt < my_tiles; ++lt) {
     const long long row0 = (blockIdx.x + (lt / args.ntiles_n) * gridDim.x) * BM;
     const int col0 = static_cast<int>(lt % args.ntiles_n) * BN;
@@ -258,9 +272,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int j = 0; j < C::CT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     for (int kt = 0; kt < KT; ++kt, ++it) {
-      if (producer && it + STAGES - 1 < total_it) issue(it + STAGES - 1);
-      const int s = static_cast<int>(it % STAGES);
-      mbar_wait(&full[s], static_cast<uint32_t>((it / STAGES) & 1));
+      if (producer && it + STAGES - 1 < total_it) issue();
+      const int s = slot;
+      mbar_wait(&full[s], phase);
+      if (++slot == STAGES) {
+        slot = 0;
+        phase ^= 1;
+      }
       const char* xs = reinterpret_cast<const char*>(smem + s * C::STAGE_BYTES);
       const char* as = xs + C::X_BYTES;
       if (LOADER == TL_STRIDED || LOADER == TL_CPLX0) {
