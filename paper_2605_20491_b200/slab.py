@@ -74,7 +74,9 @@ class KronopPassBackend:
         return out
 
     def dot(self, a, b):
-        return torch.dot(a, b) if not a.is_complex() else torch.vdot(a, b)
+        """Local dot product through kronop_inner (deterministic fixed-tree reduction)."""
+        from . import api
+        return api.inner(self.ctx, a, b, (a.numel(),))
 
 
 class SlabOperator:
@@ -180,7 +182,10 @@ class SlabOperator:
     def dot(self, a, b) -> float:
         """Global dot product: local dot + all-reduce (sum) of one scalar."""
         s = self.backend.dot(a, b)
-        t = s.reshape(1).to(torch.float64) if not s.is_complex() else torch.view_as_real(s).reshape(2)
+        if isinstance(s, torch.Tensor):
+            s = s.item()
+        vals = [s.real, s.imag] if isinstance(s, complex) else [float(s)]
+        t = torch.tensor(vals, dtype=torch.float64, device=a.device)
         if self.P > 1:
             dist.all_reduce(t, group=self.group)
         return float(t[0]) if t.numel() == 1 else complex(float(t[0]), float(t[1]))

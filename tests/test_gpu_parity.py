@@ -485,3 +485,27 @@ def test_high_dimensional_operators(ctx, spec):
     b = P.build_potential(kind, grid).nonseparable
     out = host(A.qhop_step(op, dev(b), dev(psi), 0.02, 3))
     assert rel(out, K.qhop_step(ko, b, psi, 0.02, 3)) < 1e-12
+
+
+def test_slab_operator_single_rank_on_gpu(ctx):
+    """slab.py with the libkronop pass backend (kronop_op_pass_ex) on one GPU (P = 1: the
+    all-to-alls degenerate to copies) equals the single-device operators."""
+    A = api()
+    from paper_2605_20491_b200 import slab as S
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, 13, 5, 3)
+    pot = P.build_potential("stirrer", grid)
+    op = grid.separable_operator(ctx, pot.separable, 0.0)
+    v2 = pot.v2_device()
+    sl = S.SlabOperator(op.axes, S.KronopPassBackend(ctx), shift=0.0, diag_slab=v2)
+    u = dev(K.uniform_pm1(5, grid.node_count()))
+    fo = A.FullOperator(op, v2)
+    assert rel(host(sl.apply(u, sigma=0.3)), host(fo.apply(u, sigma=0.3))) < 1e-13
+    assert rel(host(sl.solve(u)), host(op.solve(u))) < 1e-13
+    psi = dev(K.seeded_complex_field(grid.shape, 6))
+    assert rel(host(sl.propagate(psi, 0.02)), host(op.propagate(psi, 0.02))) < 1e-13
+    x = torch.zeros_like(u)
+    it, res, conv = S.slab_pcg(lambda v: sl.apply(v), sl.solve, u, x, sl.dot, rel_tol=1e-10)
+    rep = A.pcg(A.apply_map(op, v2), A.solve_map(op), u, torch.zeros_like(u),
+                A.PcgConfig(rel_tol=1e-10))
+    assert conv and it == rep.iterations

@@ -54,7 +54,7 @@ class NumpyPassBackend:
         return torch.from_numpy(np.ascontiguousarray(y))
 
     def dot(self, a, b):
-        return torch.vdot(a, b) if a.is_complex() else torch.dot(a, b)
+        return complex(torch.vdot(a, b)) if a.is_complex() else float(torch.dot(a, b))
 
 
 def _free_port():
