@@ -384,7 +384,7 @@ def run_kronop_slab(args):
     # end to end: this rank's slab from pinned host memory, solve, back to pinned host memory
     bh = torch.empty(op.local_size(), dtype=torch.float64, pin_memory=True)
     bh.copy_(b.cpu())
-    xh = torch.empty_like(bh)
+    xh = torch.empty(op.local_size(), dtype=torch.float64, pin_memory=True)
     barrier(world)
     t0 = time.perf_counter()
     for _ in range(max(1, min(args.steps, 3))):
