@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -80,8 +81,78 @@ void run_pass(kronop_ctx& ctx, const double* x, double* y, View& v, int raxis, c
   v.ext[raxis] = m;
 }
 
+// Small-extent path: consecutive axes fused per HBM round trip (fused_small.cu).
+static bool use_fused_small(const kronop_op& op) {
+  static const bool disabled = [] {
+    const char* e = getenv("KRONOP_DISABLE_FUSED_SMALL");  // A/B switch for profiling
+    return e && e[0] == '1';
+  }();
+  if (disabled) return false;
+  for (int a = 0; a < op.d; ++a)
+    if (op.n[a] > 32) return false;
+  return true;
+}
+
+static void sep_transform_fused_small(kronop_ctx& ctx, const kronop_op& op, const double* in,
+                                      double* out, int cplx, SepKind kind, double shift, double dt,
+                                      const double* diag, double sigma) {
+  View v = make_view(op.d, op.n, cplx);
+  ensure_scratch(ctx, static_cast<size_t>(v.total()));
+  // groups of consecutive spatial axes: up to 3 axes, fused extent <= 1024
+  std::vector<std::pair<int, int>> groups;  // (first spatial axis, count)
+  for (int a = 0; a < op.d;) {
+    int f = 1, F = op.n[a];
+    while (f < 3 && a + f < op.d && F * op.n[a + f] <= 1024) F *= op.n[a + f++];
+    groups.emplace_back(a, f);
+    a += f;
+  }
+  EpiParams spec;
+  spec.kind = kind == SEP_APPLY ? EPI_SPEC_MUL : kind == SEP_SOLVE ? EPI_SPEC_DIV : EPI_SPEC_PHASE;
+  spec.ndims = v.nd;
+  for (int i = 0; i < v.nd; ++i) spec.ext[i] = v.ext[i];
+  for (int a = 0; a < op.d; ++a) spec.lam[a + v.cplx] = op.lam[a];
+  spec.shift = shift;
+  spec.dt = dt;
+  spec.cplx = v.cplx;
+  double* w = ctx.scratch[0];
+  const int ng = static_cast<int>(groups.size());
+  for (int dir = 0; dir < 2; ++dir) {
+    for (int g = 0; g < ng; ++g) {
+      const int a0 = groups[g].first, f = groups[g].second;
+      const double* mats[3];
+      int lda[3];
+      for (int j = 0; j < f; ++j) {
+        mats[j] = dir == 0 ? op.fwd[a0 + j] : op.bwd[a0 + j];
+        lda[j] = op.lda[a0 + j];
+      }
+      const bool last = g == ng - 1;
+      const double* src = (dir == 0 && g == 0) ? in : w;
+      double* dst = (dir == 1 && last) ? out : w;
+      EpiParams ep;
+      bool spectral = false;
+      if (dir == 0 && last) {
+        ep = spec;
+        spectral = true;
+      } else if (dir == 1 && last && (diag != nullptr || sigma != 0.0)) {
+        ep.kind = EPI_AXPY_DIAG;
+        ep.diag = diag;
+        ep.u = in;
+        ep.sigma = sigma;
+        ep.cplx = v.cplx;
+      }
+      launch_fused_small(ctx.stream, src, dst, v.nd, v.ext, a0 + v.cplx, f, mats, lda, ep,
+                         spectral);
+      ctx.ws.launches += 1;
+    }
+  }
+}
+
 void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
                    SepKind kind, double shift, double dt, const double* diag, double sigma) {
+  if (use_fused_small(op)) {
+    sep_transform_fused_small(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
+    return;
+  }
   View v = make_view(op.d, op.n, cplx);
   ensure_scratch(ctx, static_cast<size_t>(v.total()));
   const int d = op.d;
@@ -277,6 +348,7 @@ int kronop_ctx_create(int device, void* stream, kronop_ctx** out) {
       KCUDA(cudaMallocHost(&c->hscal, kScalarSlots * sizeof(double)));
       prime_mode_product_kernels();
       prime_mode_product_tma_kernels();
+      prime_fused_small_kernels();
     } catch (...) {
       delete c;
       throw;

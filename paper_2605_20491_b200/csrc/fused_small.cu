@@ -1,0 +1,270 @@
+// Small-extent, high-dimensional transforms (SURVEY.md §7 hard part 5; BASELINE config 5: 6D
+// n = 29, 9D n = 9): several consecutive axes are contracted per HBM round trip.
+//
+// At n <= 32 a single mode-product pass has arithmetic intensity n/8 flop/B (<= 4): HBM-bound, and
+// the 8x8x4 DMMA tiles of the large-n kernels would be >= 50% padding. Here one CTA stages a tile
+// [Qt q][n_a x ... x n_{a+f-1}][P p] of the real view (p = the axes below the group, q = the axes
+// above it) in shared memory, applies the f per-axis matrices one after the other in place (each
+// thread owns whole fibers: it reads its n inputs, forms the n outputs with DFMA against the
+// matrix held in shared memory, and writes them back to the same fiber), runs the fused
+// epilogue, and stores the tile. f axes cost one read + one write of the field instead of f, so a
+// 6-axis propagate moves 2 x 3 (not 2 x 6) fields for n = 29 and 2 x 3 (not 2 x 9) for 9D n = 9.
+// Same contraction as proj/src/tensor.cpp:105-145 per axis, same epilogues as operators.cpp.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "epilogue.cuh"
+#include "kronop_internal.cuh"
+
+namespace kronop_dev {
+
+namespace {
+
+constexpr int FS_THREADS = 256;
+constexpr int FS_MAXF = 3;
+
+struct FSArgs {
+  const double* x;
+  double* y;
+  long long pre, post;  // real-view extents below / above the group
+  int f;                // number of fused axes
+  int n[FS_MAXF];       // their extents
+  int F;                // product of n
+  const double* a[FS_MAXF];
+  int lda[FS_MAXF];
+  int P, Qt;            // tile: P consecutive p, Qt consecutive q (Qt > 1 only if P == pre)
+  long long tiles_p;    // ceil(pre / P)
+  EpiParams ep;         // ep.axis = real-view axis of the group's FIRST axis
+  int spectral_last;    // apply the spectral epilogue (group ends at the last axis, forward)
+};
+
+// R fibers per thread share every matrix element loaded from shared memory (R DFMAs per LDS).
+template <int MAXN>
+struct FiberCfg {
+  static constexpr int R = MAXN >= 32 ? 2 : 4;
+};
+
+template <int MAXN>
+__device__ __forceinline__ void fiber_block(double* tile, const double* am, int m, int stride,
+                                            long long nfib, long long f0) {
+  constexpr int R = FiberCfg<MAXN>::R;
+  double xin[R][MAXN];
+  long long base[R];
+  bool ok[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const long long fib = f0 + static_cast<long long>(r) * FS_THREADS;
+    ok[r] = fib < nfib;
+    const long long inner = fib % stride;
+    const long long outer = fib / stride;
+    base[r] = inner + outer * static_cast<long long>(stride) * m;
+#pragma unroll
+    for (int k = 0; k < MAXN; ++k)
+      xin[r][k] = (ok[r] && k < m) ? tile[base[r] + static_cast<long long>(k) * stride] : 0.0;
+  }
+  for (int i = 0; i < m; ++i) {
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXN; ++k) {
+      if (k < m) {
+        const double a = am[i + MAXN * k];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = __fma_rn(a, xin[r][k], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (ok[r]) tile[base[r] + static_cast<long long>(i) * stride] = acc[r];
+  }
+}
+
+template <int MAXN>
+__global__ void __launch_bounds__(FS_THREADS) fused_small_kernel(const FSArgs args) {
+  extern __shared__ __align__(16) double sm[];
+  double* amat = sm;                               // FS_MAXF x MAXN x MAXN
+  double* tile = sm + FS_MAXF * MAXN * MAXN;       // [Qt][F][P]
+  const int tid = threadIdx.x;
+  const long long pre = args.pre;
+  const int P = args.P, F = args.F, Qt = args.Qt;
+  const long long tp = blockIdx.x % args.tiles_p;
+  const long long tq = blockIdx.x / args.tiles_p;
+  const long long p0 = tp * P;
+  const long long q0 = tq * Qt;
+  const int Pv = static_cast<int>(pre - p0 < P ? pre - p0 : P);                 // valid p
+  const int Qv = static_cast<int>(args.post - q0 < Qt ? args.post - q0 : Qt);  // valid q
+
+  // matrices (column-major, zero-padded to MAXN x MAXN)
+  for (int j = 0; j < args.f; ++j)
+    for (int e = tid; e < MAXN * MAXN; e += FS_THREADS) {
+      const int i = e % MAXN, k = e / MAXN;
+      amat[j * MAXN * MAXN + e] =
+          (i < args.n[j] && k < args.n[j]) ? args.a[j][i + static_cast<long long>(args.lda[j]) * k] : 0.0;
+    }
+  // tile load: element (p, f, q) at x[p0 + p + pre * (f + F * (q0 + q))]
+  const long long E = static_cast<long long>(P) * F * Qt;
+  const long long gbase = p0 + pre * static_cast<long long>(F) * q0;
+  if (P == pre) {  // the whole tile is one contiguous run
+    const long long Ev = static_cast<long long>(P) * F * Qv;
+    for (long long e = tid; e < E; e += FS_THREADS) tile[e] = e < Ev ? args.x[gbase + e] : 0.0;
+  } else {
+    for (long long e = tid; e < E; e += FS_THREADS) {
+      const int p = static_cast<int>(e % P);
+      const long long r = e / P;  // (f, q) with Qt == 1
+      tile[e] = p < Pv ? args.x[gbase + p + pre * r] : 0.0;
+    }
+  }
+  __syncthreads();
+
+  // the fused axes, one after the other, in place
+  int stride = P;
+  for (int j = 0; j < args.f; ++j) {
+    const int m = args.n[j];
+    const long long nfib = E / m;
+    for (long long f0 = tid; f0 < nfib; f0 += static_cast<long long>(FS_THREADS) * FiberCfg<MAXN>::R)
+      fiber_block<MAXN>(tile, amat + j * MAXN * MAXN, m, stride, nfib, f0);
+    stride *= m;
+    __syncthreads();
+  }
+
+  // epilogue + store
+  const EpiParams& ep = args.ep;
+  const bool spectral = args.spectral_last != 0;
+  for (long long e = tid; e < E; e += FS_THREADS) {
+    const int p = static_cast<int>(e % P);
+    const long long r = e / P;
+    const int fidx = static_cast<int>(r % F);
+    const int q = static_cast<int>(r / F);
+    if (p >= Pv || q >= Qv) continue;
+    const long long gi = gbase + p + pre * (fidx + static_cast<long long>(F) * q);
+    double val = tile[e];
+    if (spectral) {
+      // global lambda index: p over the axes below the group, fidx over the group, q above
+      const long long pp = p0 + p;
+      double lam = lambda_partial_low_ext(ep, pp, ep.axis);
+      int rem = fidx;
+      for (int j = 0; j < args.f; ++j) {
+        const int idx = rem % args.n[j];
+        rem /= args.n[j];
+        if (ep.lam[ep.axis + j]) lam = __dadd_rn(lam, ep.lam[ep.axis + j][idx]);
+      }
+      long long qq = q0 + q;
+      for (int ax = ep.axis + args.f; ax < ep.ndims; ++ax) {
+        const long long ex = ep.ext[ax];
+        const long long idx = qq % ex;
+        qq /= ex;
+        if (ep.lam[ax]) lam = __dadd_rn(lam, ep.lam[ax][idx]);
+      }
+      const double ls = __dsub_rn(lam, ep.shift);
+      if (ep.kind == EPI_SPEC_MUL) {
+        val = __dmul_rn(val, ls);
+      } else if (ep.kind == EPI_SPEC_DIV) {
+        val = __ddiv_rn(val, ls);
+      } else {  // phase: the re/im partner is the neighbouring p (leading re/im axis)
+        const bool is_im = (pp & 1) != 0;
+        const double other = tile[is_im ? e - 1 : e + 1];
+        const double phase = __dmul_rn(-ls, ep.dt);
+        double sn, cs;
+        sincos(phase, &sn, &cs);
+        const double re = is_im ? other : val;
+        const double im = is_im ? val : other;
+        val = is_im ? __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs))
+                    : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
+      }
+    } else if (ep.kind == EPI_AXPY_DIAG) {
+      const double uu = ep.u[gi];
+      if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (gi >> 1) : gi], uu));
+      if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+    }
+    args.y[gi] = val;
+  }
+}
+
+template <int MAXN>
+void launch_fs(cudaStream_t s, const FSArgs& a, size_t smem) {
+  static bool attr = false;
+  if (!attr) {
+    KCUDA(cudaFuncSetAttribute(fused_small_kernel<MAXN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               232448 - 1024));
+    attr = true;
+  }
+  const long long tiles = a.tiles_p * ((a.post + a.Qt - 1) / a.Qt);
+  fused_small_kernel<MAXN><<<static_cast<unsigned>(tiles), FS_THREADS, smem, s>>>(a);
+  KCUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void prime_fused_small_kernels() {
+  KCUDA(cudaFuncSetAttribute(fused_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             232448 - 1024));
+  KCUDA(cudaFuncSetAttribute(fused_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             232448 - 1024));
+  KCUDA(cudaFuncSetAttribute(fused_small_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             232448 - 1024));
+}
+
+int fused_small_max_extent() { return 32; }
+
+// Plan + launch one fused group of `f` consecutive real-view axes starting at `axis` of the view
+// (ext[] = current real-view extents). mats[j] / lda[j]: square n_j x n_j padded matrices.
+void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, const long long* ext,
+                        int axis, int f, const double* const* mats, const int* lda,
+                        const EpiParams& ep, bool spectral_last) {
+  param_check(f >= 1 && f <= FS_MAXF, "fused_small: group size");
+  FSArgs a{};
+  a.x = x;
+  a.y = y;
+  a.pre = 1;
+  for (int i = 0; i < axis; ++i) a.pre *= ext[i];
+  a.post = 1;
+  for (int i = axis + f; i < nd; ++i) a.post *= ext[i];
+  a.f = f;
+  a.F = 1;
+  int maxn = 1;
+  for (int j = 0; j < f; ++j) {
+    a.n[j] = static_cast<int>(ext[axis + j]);
+    a.F *= a.n[j];
+    a.a[j] = mats[j];
+    a.lda[j] = lda[j];
+    maxn = a.n[j] > maxn ? a.n[j] : maxn;
+  }
+  param_check(maxn <= 32, "fused_small: extent > 32");
+  const int MAXN = maxn <= 8 ? 8 : maxn <= 16 ? 16 : 32;
+  // tile: ~96 KB of doubles so two CTAs share an SM (one loads while the other computes); when
+  // that leaves runs of < 16 contiguous p (poor coalescing), use ~200 KB and one CTA per SM.
+  long long budget = 12288 - FS_MAXF * MAXN * MAXN;  // doubles
+  if (a.pre * a.F > budget && budget / a.F < 16) budget = 25600 - FS_MAXF * MAXN * MAXN;
+  if (a.pre * a.F <= budget) {
+    a.P = static_cast<int>(a.pre);
+    long long qt = budget / (a.pre * a.F);
+    if (qt > a.post) qt = a.post;
+    a.Qt = static_cast<int>(qt < 1 ? 1 : qt);
+  } else {
+    long long P = budget / a.F;
+    if (P > 64) P = 64;
+    if (a.pre % 2 == 0 && P > 1) P &= ~1LL;  // keep re/im pairs (leading re/im axis) together
+    param_check(P >= 1, "fused_small: tile does not fit");
+    a.P = static_cast<int>(P);
+    a.Qt = 1;
+  }
+  a.tiles_p = (a.pre + a.P - 1) / a.P;
+  a.ep = ep;
+  a.ep.axis = axis;
+  a.spectral_last = spectral_last ? 1 : 0;
+  if (spectral_last && ep.kind == EPI_SPEC_PHASE)
+    param_check(a.P % 2 == 0 || a.P == a.pre, "fused_small: phase needs re/im pairs in a tile");
+  const size_t smem =
+      (static_cast<size_t>(FS_MAXF) * MAXN * MAXN + static_cast<size_t>(a.P) * a.F * a.Qt) *
+      sizeof(double);
+  if (MAXN == 8)
+    launch_fs<8>(s, a, smem);
+  else if (MAXN == 16)
+    launch_fs<16>(s, a, smem);
+  else
+    launch_fs<32>(s, a, smem);
+}
+
+}  // namespace kronop_dev

@@ -79,6 +79,11 @@ void prime_mode_product_kernels();
 // TMA + mbarrier warp-specialised kernel (mode_product_tma.cu) for the STRIDED (pre % 128 == 0)
 // and CONTIG (pre == 1, even nk) geometries; launch_mode_product dispatches to it when eligible.
 void prime_mode_product_tma_kernels();
+// Fused small-extent multi-axis transform (fused_small.cu), used when every axis has n <= 32.
+void prime_fused_small_kernels();
+void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, const long long* ext,
+                        int axis, int f, const double* const* mats, const int* lda,
+                        const EpiParams& ep, bool spectral_last);
 bool mode_product_tma_eligible(const double* x, const PassShape& ps);
 void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const double* a_pad,
                              int lda, const PassShape& ps, const EpiParams& ep);
