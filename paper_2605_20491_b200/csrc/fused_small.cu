@@ -39,50 +39,46 @@ struct FSArgs {
   int spectral_last;    // apply the spectral epilogue (group ends at the last axis, forward)
 };
 
-// R fibers per thread share every matrix element loaded from shared memory (R DFMAs per LDS).
+// One fiber per thread: its m inputs live in registers (so the transform is in place), the m
+// outputs are formed 8 at a time (8 independent DFMA chains), and the 8 matrix entries of each
+// step are one pair of 128-bit shared loads broadcast to the whole warp (the warp walks the same
+// output block in lockstep).
 template <int MAXN>
-struct FiberCfg {
-  static constexpr int R = MAXN >= 32 ? 2 : 4;
-};
-
-template <int MAXN>
-__device__ __forceinline__ void fiber_block(double* tile, const double* am, int m, int stride,
-                                            long long nfib, long long f0) {
-  constexpr int R = FiberCfg<MAXN>::R;
-  double xin[R][MAXN];
-  long long base[R];
-  bool ok[R];
+__device__ __forceinline__ void fiber_one(double* tile, const double* am, int m, int stride,
+                                          int base) {
+  double xin[MAXN];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const long long fib = f0 + static_cast<long long>(r) * FS_THREADS;
-    ok[r] = fib < nfib;
-    const long long inner = fib % stride;
-    const long long outer = fib / stride;
-    base[r] = inner + outer * static_cast<long long>(stride) * m;
+  for (int k = 0; k < MAXN; ++k) xin[k] = k < m ? tile[base + k * stride] : 0.0;
 #pragma unroll
-    for (int k = 0; k < MAXN; ++k)
-      xin[r][k] = (ok[r] && k < m) ? tile[base[r] + static_cast<long long>(k) * stride] : 0.0;
-  }
-  for (int i = 0; i < m; ++i) {
-    double acc[R];
+  for (int i0 = 0; i0 < MAXN; i0 += 8) {
+    if (i0 < m) {
+      double acc[8];
 #pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+      for (int r = 0; r < 8; ++r) acc[r] = 0.0;
 #pragma unroll
-    for (int k = 0; k < MAXN; ++k) {
-      if (k < m) {
-        const double a = am[i + MAXN * k];
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] = __fma_rn(a, xin[r][k], acc[r]);
+      for (int k = 0; k < MAXN; ++k) {
+        if (k < m) {
+          const double2* col = reinterpret_cast<const double2*>(am + i0 + MAXN * k);
+          const double2 c0 = col[0], c1 = col[1], c2 = col[2], c3 = col[3];
+          acc[0] = __fma_rn(c0.x, xin[k], acc[0]);
+          acc[1] = __fma_rn(c0.y, xin[k], acc[1]);
+          acc[2] = __fma_rn(c1.x, xin[k], acc[2]);
+          acc[3] = __fma_rn(c1.y, xin[k], acc[3]);
+          acc[4] = __fma_rn(c2.x, xin[k], acc[4]);
+          acc[5] = __fma_rn(c2.y, xin[k], acc[5]);
+          acc[6] = __fma_rn(c3.x, xin[k], acc[6]);
+          acc[7] = __fma_rn(c3.y, xin[k], acc[7]);
+        }
       }
-    }
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (ok[r]) tile[base[r] + static_cast<long long>(i) * stride] = acc[r];
+      for (int r = 0; r < 8; ++r)
+        if (i0 + r < m) tile[base + (i0 + r) * stride] = acc[r];
+    }
   }
 }
 
 template <int MAXN>
-__global__ void __launch_bounds__(FS_THREADS) fused_small_kernel(const FSArgs args) {
+__global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs args) {
   extern __shared__ __align__(16) double sm[];
   double* amat = sm;                               // FS_MAXF x MAXN x MAXN
   double* tile = sm + FS_MAXF * MAXN * MAXN;       // [Qt][F][P]
@@ -110,9 +106,10 @@ __global__ void __launch_bounds__(FS_THREADS) fused_small_kernel(const FSArgs ar
     const long long Ev = static_cast<long long>(P) * F * Qv;
     for (long long e = tid; e < E; e += FS_THREADS) tile[e] = e < Ev ? args.x[gbase + e] : 0.0;
   } else {
-    for (long long e = tid; e < E; e += FS_THREADS) {
-      const int p = static_cast<int>(e % P);
-      const long long r = e / P;  // (f, q) with Qt == 1
+    const int Ei = static_cast<int>(E);
+    for (int e = tid; e < Ei; e += FS_THREADS) {
+      const int r = e / P;  // (f, q) with Qt == 1
+      const int p = e - r * P;
       tile[e] = p < Pv ? args.x[gbase + p + pre * r] : 0.0;
     }
   }
@@ -122,9 +119,12 @@ __global__ void __launch_bounds__(FS_THREADS) fused_small_kernel(const FSArgs ar
   int stride = P;
   for (int j = 0; j < args.f; ++j) {
     const int m = args.n[j];
-    const long long nfib = E / m;
-    for (long long f0 = tid; f0 < nfib; f0 += static_cast<long long>(FS_THREADS) * FiberCfg<MAXN>::R)
-      fiber_block<MAXN>(tile, amat + j * MAXN * MAXN, m, stride, nfib, f0);
+    const int nfib = static_cast<int>(E / m);
+    for (int fib = tid; fib < nfib; fib += FS_THREADS) {
+      const int inner = fib % stride;
+      const int outer = fib / stride;
+      fiber_one<MAXN>(tile, amat + j * MAXN * MAXN, m, stride, inner + outer * stride * m);
+    }
     stride *= m;
     __syncthreads();
   }
@@ -132,11 +132,12 @@ __global__ void __launch_bounds__(FS_THREADS) fused_small_kernel(const FSArgs ar
   // epilogue + store
   const EpiParams& ep = args.ep;
   const bool spectral = args.spectral_last != 0;
-  for (long long e = tid; e < E; e += FS_THREADS) {
-    const int p = static_cast<int>(e % P);
-    const long long r = e / P;
-    const int fidx = static_cast<int>(r % F);
-    const int q = static_cast<int>(r / F);
+  const int Ei = static_cast<int>(E);
+  for (int e = tid; e < Ei; e += FS_THREADS) {
+    const int r = e / P;
+    const int p = e - r * P;
+    const int q = r / F;
+    const int fidx = r - q * F;
     if (p >= Pv || q >= Qv) continue;
     const long long gi = gbase + p + pre * (fidx + static_cast<long long>(F) * q);
     double val = tile[e];
@@ -235,8 +236,8 @@ void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, cons
   const int MAXN = maxn <= 8 ? 8 : maxn <= 16 ? 16 : 32;
   // tile: ~96 KB of doubles so two CTAs share an SM (one loads while the other computes); when
   // that leaves runs of < 16 contiguous p (poor coalescing), use ~200 KB and one CTA per SM.
-  long long budget = 12288 - FS_MAXF * MAXN * MAXN;  // doubles
-  if (a.pre * a.F > budget && budget / a.F < 16) budget = 25600 - FS_MAXF * MAXN * MAXN;
+  long long budget = 14080 - FS_MAXF * MAXN * MAXN;  // doubles: <= 110 KB per CTA, 2 per SM
+  if (a.pre * a.F > budget && budget / a.F < 8) budget = 27648 - FS_MAXF * MAXN * MAXN;
   if (a.pre * a.F <= budget) {
     a.P = static_cast<int>(a.pre);
     long long qt = budget / (a.pre * a.F);
