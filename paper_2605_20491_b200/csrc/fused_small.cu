@@ -43,6 +43,17 @@ struct FSArgs {
 // outputs are formed 8 at a time (8 independent DFMA chains), and the 8 matrix entries of each
 // step are one pair of 128-bit shared loads broadcast to the whole warp (the warp walks the same
 // output block in lockstep).
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+
 template <int MAXN>
 __device__ __forceinline__ void fiber_one(double* tile, const double* am, int m, int stride,
                                           int base) {
@@ -102,17 +113,34 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
   // tile load: element (p, f, q) at x[p0 + p + pre * (f + F * (q0 + q))]
   const long long E = static_cast<long long>(P) * F * Qt;
   const long long gbase = p0 + pre * static_cast<long long>(F) * q0;
+  // asynchronous copies (LDGSTS): thousands of loads in flight per CTA, zero-fill outside
   if (P == pre) {  // the whole tile is one contiguous run
     const long long Ev = static_cast<long long>(P) * F * Qv;
-    for (long long e = tid; e < E; e += FS_THREADS) tile[e] = e < Ev ? args.x[gbase + e] : 0.0;
+    const int Ei = static_cast<int>(E);
+    const bool vec = ((gbase & 1) == 0) && ((reinterpret_cast<uintptr_t>(args.x) & 15) == 0);
+    if (vec) {
+      for (int e = 2 * tid; e < Ei; e += 2 * FS_THREADS) {
+        const bool ok = e < Ev;  // Ev is even when P*F is even; else fall back below
+        if (ok && e + 1 < Ev)
+          cp_async16(tile + e, args.x + gbase + e, true);
+        else {
+          cp_async8(tile + e, args.x + gbase + (ok ? e : 0), ok);
+          cp_async8(tile + e + 1, args.x + gbase + (e + 1 < Ev ? e + 1 : 0), e + 1 < Ev);
+        }
+      }
+    } else {
+      for (int e = tid; e < Ei; e += FS_THREADS)
+        cp_async8(tile + e, args.x + gbase + (e < Ev ? e : 0), e < Ev);
+    }
   } else {
     const int Ei = static_cast<int>(E);
     for (int e = tid; e < Ei; e += FS_THREADS) {
       const int r = e / P;  // (f, q) with Qt == 1
       const int p = e - r * P;
-      tile[e] = p < Pv ? args.x[gbase + p + pre * r] : 0.0;
+      cp_async8(tile + e, args.x + gbase + (p < Pv ? p + pre * r : 0), p < Pv);
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
 
   // the fused axes, one after the other, in place
@@ -133,6 +161,7 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
   const EpiParams& ep = args.ep;
   const bool spectral = args.spectral_last != 0;
   const int Ei = static_cast<int>(E);
+#pragma unroll 4
   for (int e = tid; e < Ei; e += FS_THREADS) {
     const int r = e / P;
     const int p = e - r * P;
