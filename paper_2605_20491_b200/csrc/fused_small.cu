@@ -91,8 +91,9 @@ __device__ __forceinline__ void fiber_one(double* tile, const double* am, int m,
 template <int MAXN>
 __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs args) {
   extern __shared__ __align__(16) double sm[];
-  double* amat = sm;                               // FS_MAXF x MAXN x MAXN
-  double* tile = sm + FS_MAXF * MAXN * MAXN;       // [Qt][F][P]
+  double* amat = sm;                                      // FS_MAXF x MAXN x MAXN
+  double* lam_low = sm + FS_MAXF * MAXN * MAXN;           // P (spectral epilogue), even-padded
+  double* tile = lam_low + ((args.P + 1) & ~1);           // [Qt][F][P]
   const int tid = threadIdx.x;
   const long long pre = args.pre;
   const int P = args.P, F = args.F, Qt = args.Qt;
@@ -157,11 +158,35 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
     __syncthreads();
   }
 
-  // epilogue + store
+  // epilogue + store. The spectral factor needs the global multi-index: the part from the axes
+  // below the group depends only on p (precomputed once per tile, in axis order from 0.0 exactly
+  // like direct_sum_grid), the group part is added axis by axis; the spectral group always
+  // contains the last axis, so nothing lies above it.
   const EpiParams& ep = args.ep;
   const bool spectral = args.spectral_last != 0;
+  const bool contiguous = P == pre;
   const int Ei = static_cast<int>(E);
+  if (spectral) {
+    for (int pl = tid; pl < P; pl += FS_THREADS)
+      lam_low[pl] = lambda_partial_low_ext(ep, p0 + pl, ep.axis);
+    __syncthreads();
+  }
+  if (!spectral && ep.kind != EPI_AXPY_DIAG) {
+    if (contiguous) {
+      const long long Ev = static_cast<long long>(P) * F * Qv;
 #pragma unroll 4
+      for (int e = tid; e < Ei; e += FS_THREADS)
+        if (e < Ev) args.y[gbase + e] = tile[e];
+    } else {
+#pragma unroll 4
+      for (int e = tid; e < Ei; e += FS_THREADS) {
+        const int r = e / P;
+        const int p = e - r * P;
+        if (p < Pv) args.y[gbase + p + pre * r] = tile[e];
+      }
+    }
+    return;
+  }
   for (int e = tid; e < Ei; e += FS_THREADS) {
     const int r = e / P;
     const int p = e - r * P;
@@ -171,21 +196,12 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
     const long long gi = gbase + p + pre * (fidx + static_cast<long long>(F) * q);
     double val = tile[e];
     if (spectral) {
-      // global lambda index: p over the axes below the group, fidx over the group, q above
-      const long long pp = p0 + p;
-      double lam = lambda_partial_low_ext(ep, pp, ep.axis);
+      double lam = lam_low[p];
       int rem = fidx;
       for (int j = 0; j < args.f; ++j) {
         const int idx = rem % args.n[j];
         rem /= args.n[j];
         if (ep.lam[ep.axis + j]) lam = __dadd_rn(lam, ep.lam[ep.axis + j][idx]);
-      }
-      long long qq = q0 + q;
-      for (int ax = ep.axis + args.f; ax < ep.ndims; ++ax) {
-        const long long ex = ep.ext[ax];
-        const long long idx = qq % ex;
-        qq /= ex;
-        if (ep.lam[ax]) lam = __dadd_rn(lam, ep.lam[ax][idx]);
       }
       const double ls = __dsub_rn(lam, ep.shift);
       if (ep.kind == EPI_SPEC_MUL) {
@@ -193,7 +209,7 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
       } else if (ep.kind == EPI_SPEC_DIV) {
         val = __ddiv_rn(val, ls);
       } else {  // phase: the re/im partner is the neighbouring p (leading re/im axis)
-        const bool is_im = (pp & 1) != 0;
+        const bool is_im = ((p0 + p) & 1) != 0;
         const double other = tile[is_im ? e - 1 : e + 1];
         const double phase = __dmul_rn(-ls, ep.dt);
         double sn, cs;
@@ -203,7 +219,7 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
         val = is_im ? __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs))
                     : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
       }
-    } else if (ep.kind == EPI_AXPY_DIAG) {
+    } else {  // EPI_AXPY_DIAG
       const double uu = ep.u[gi];
       if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (gi >> 1) : gi], uu));
       if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
@@ -286,9 +302,9 @@ void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, cons
   a.spectral_last = spectral_last ? 1 : 0;
   if (spectral_last && ep.kind == EPI_SPEC_PHASE)
     param_check(a.P % 2 == 0 || a.P == a.pre, "fused_small: phase needs re/im pairs in a tile");
-  const size_t smem =
-      (static_cast<size_t>(FS_MAXF) * MAXN * MAXN + static_cast<size_t>(a.P) * a.F * a.Qt) *
-      sizeof(double);
+  const size_t smem = (static_cast<size_t>(FS_MAXF) * MAXN * MAXN + ((a.P + 1) & ~1) +
+                       static_cast<size_t>(a.P) * a.F * a.Qt) *
+                      sizeof(double);
   if (MAXN == 8)
     launch_fs<8>(s, a, smem);
   else if (MAXN == 16)
