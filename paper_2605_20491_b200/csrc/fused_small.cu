@@ -34,127 +34,114 @@ struct FSArgs {
   const double* a[FS_MAXF];
   int lda[FS_MAXF];
   int P, Qt;            // tile: P consecutive p, Qt consecutive q (Qt > 1 only if P == pre)
+  int Pp;               // padded row length in shared memory (4 mod 16 doubles)
   long long tiles_p;    // ceil(pre / P)
   EpiParams ep;         // ep.axis = real-view axis of the group's FIRST axis
   int spectral_last;    // apply the spectral epilogue (group ends at the last axis, forward)
 };
 
-// One fiber per thread: its m inputs live in registers (so the transform is in place), the m
-// outputs are formed 8 at a time (8 independent DFMA chains), and the 8 matrix entries of each
-// step are one pair of 128-bit shared loads broadcast to the whole warp (the warp walks the same
-// output block in lockstep).
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem),
                "r"(valid ? 8 : 0));
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
-               "r"(valid ? 16 : 0));
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
 }
 
+// One axis of the group on the staged tile, in place, on the FP64 tensor cores: each warp takes 8
+// fibers at a time (the DMMA M dimension), k = the fiber index (K padded to 4), n = the output
+// index (N padded to 8). The matrix fragments live in registers for the whole tile, so shared
+// memory carries only the fiber reads and writes (strides are 4 mod 16 doubles: conflict free).
 template <int MAXN>
-__device__ __forceinline__ void fiber_one(double* tile, const double* am, int m, int stride,
-                                          int base) {
-  double xin[MAXN];
+__device__ __forceinline__ void axis_dmma(double* tile, const double* am, int m, int S, int nfib,
+                                          int warp, int lane) {
+  constexpr int K4 = MAXN / 4, NT = MAXN / 8;
+  const int g = lane >> 2, t = lane & 3;
+  double bf[K4][NT];
 #pragma unroll
-  for (int k = 0; k < MAXN; ++k) xin[k] = k < m ? tile[base + k * stride] : 0.0;
+  for (int kk = 0; kk < K4; ++kk)
 #pragma unroll
-  for (int i0 = 0; i0 < MAXN; i0 += 8) {
-    if (i0 < m) {
-      double acc[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) acc[r] = 0.0;
-#pragma unroll
-      for (int k = 0; k < MAXN; ++k) {
-        if (k < m) {
-          const double2* col = reinterpret_cast<const double2*>(am + i0 + MAXN * k);
-          const double2 c0 = col[0], c1 = col[1], c2 = col[2], c3 = col[3];
-          acc[0] = __fma_rn(c0.x, xin[k], acc[0]);
-          acc[1] = __fma_rn(c0.y, xin[k], acc[1]);
-          acc[2] = __fma_rn(c1.x, xin[k], acc[2]);
-          acc[3] = __fma_rn(c1.y, xin[k], acc[3]);
-          acc[4] = __fma_rn(c2.x, xin[k], acc[4]);
-          acc[5] = __fma_rn(c2.y, xin[k], acc[5]);
-          acc[6] = __fma_rn(c3.x, xin[k], acc[6]);
-          acc[7] = __fma_rn(c3.y, xin[k], acc[7]);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (i0 + r < m) tile[base + (i0 + r) * stride] = acc[r];
+    for (int nt = 0; nt < NT; ++nt) {
+      const int k = 4 * kk + t, n = 8 * nt + g;
+      bf[kk][nt] = (k < m && n < m) ? am[n + MAXN * k] : 0.0;
     }
+  const int k4m = (m + 3) >> 2, ntm = (m + 7) >> 3;
+  for (int f0 = warp * 8; f0 < nfib; f0 += 8 * (FS_THREADS / 32)) {
+    const int fib = f0 + g;
+    const bool fok = fib < nfib;
+    const int fb = fok ? fib : f0;
+    const int base = (fb % S) + (fb / S) * S * m;
+    double acc[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < K4; ++kk) {
+      if (kk < k4m) {
+        const int k = 4 * kk + t;
+        const double a = k < m ? tile[base + k * S] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          if (nt < ntm) dmma884(acc[nt], a, bf[kk][nt]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int n = 8 * nt + 2 * t + v;
+        if (fok && nt < ntm && n < m) tile[base + n * S] = acc[nt][v];
+      }
   }
 }
 
 template <int MAXN>
 __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs args) {
   extern __shared__ __align__(16) double sm[];
-  double* amat = sm;                                      // FS_MAXF x MAXN x MAXN
-  double* lam_low = sm + FS_MAXF * MAXN * MAXN;           // P (spectral epilogue), even-padded
-  double* tile = lam_low + ((args.P + 1) & ~1);           // [Qt][F][P]
+  const int P = args.P, F = args.F, Qt = args.Qt, Pp = args.Pp;
+  double* amat = sm;                                // FS_MAXF x MAXN x MAXN
+  double* lam_low = sm + FS_MAXF * MAXN * MAXN;     // P (spectral epilogue), even-padded
+  double* tile = lam_low + ((P + 1) & ~1);          // element (p, r) at p + Pp * r, r = (f, q)
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const long long pre = args.pre;
-  const int P = args.P, F = args.F, Qt = args.Qt;
   const long long tp = blockIdx.x % args.tiles_p;
   const long long tq = blockIdx.x / args.tiles_p;
   const long long p0 = tp * P;
   const long long q0 = tq * Qt;
   const int Pv = static_cast<int>(pre - p0 < P ? pre - p0 : P);                 // valid p
   const int Qv = static_cast<int>(args.post - q0 < Qt ? args.post - q0 : Qt);  // valid q
+  const int R = F * Qt;    // rows (f, q) of the tile
+  const int Rv = F * Qv;   // valid rows
+  const long long gbase = p0 + pre * static_cast<long long>(F) * q0;  // element (p, r) at gbase + p + pre * r
 
-  // matrices (column-major, zero-padded to MAXN x MAXN)
   for (int j = 0; j < args.f; ++j)
     for (int e = tid; e < MAXN * MAXN; e += FS_THREADS) {
       const int i = e % MAXN, k = e / MAXN;
-      amat[j * MAXN * MAXN + e] =
-          (i < args.n[j] && k < args.n[j]) ? args.a[j][i + static_cast<long long>(args.lda[j]) * k] : 0.0;
+      amat[j * MAXN * MAXN + e] = (i < args.n[j] && k < args.n[j])
+                                      ? args.a[j][i + static_cast<long long>(args.lda[j]) * k]
+                                      : 0.0;
     }
-  // tile load: element (p, f, q) at x[p0 + p + pre * (f + F * (q0 + q))]
-  const long long E = static_cast<long long>(P) * F * Qt;
-  const long long gbase = p0 + pre * static_cast<long long>(F) * q0;
-  // asynchronous copies (LDGSTS): thousands of loads in flight per CTA, zero-fill outside
-  if (P == pre) {  // the whole tile is one contiguous run
-    const long long Ev = static_cast<long long>(P) * F * Qv;
-    const int Ei = static_cast<int>(E);
-    const bool vec = ((gbase & 1) == 0) && ((reinterpret_cast<uintptr_t>(args.x) & 15) == 0);
-    if (vec) {
-      for (int e = 2 * tid; e < Ei; e += 2 * FS_THREADS) {
-        const bool ok = e < Ev;  // Ev is even when P*F is even; else fall back below
-        if (ok && e + 1 < Ev)
-          cp_async16(tile + e, args.x + gbase + e, true);
-        else {
-          cp_async8(tile + e, args.x + gbase + (ok ? e : 0), ok);
-          cp_async8(tile + e + 1, args.x + gbase + (e + 1 < Ev ? e + 1 : 0), e + 1 < Ev);
-        }
-      }
-    } else {
-      for (int e = tid; e < Ei; e += FS_THREADS)
-        cp_async8(tile + e, args.x + gbase + (e < Ev ? e : 0), e < Ev);
-    }
-  } else {
-    const int Ei = static_cast<int>(E);
-    for (int e = tid; e < Ei; e += FS_THREADS) {
-      const int r = e / P;  // (f, q) with Qt == 1
-      const int p = e - r * P;
-      cp_async8(tile + e, args.x + gbase + (p < Pv ? p + pre * r : 0), p < Pv);
-    }
+  // tile load (LDGSTS, zero-fill outside the field and in the padding columns)
+  const int PR = Pp * R;
+  for (int e = tid; e < PR; e += FS_THREADS) {
+    const int r = e / Pp;
+    const int p = e - r * Pp;
+    const bool ok = p < Pv && r < Rv;
+    cp_async8(tile + e, args.x + (ok ? gbase + p + pre * r : 0), ok);
   }
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
 
-  // the fused axes, one after the other, in place
-  int stride = P;
+  int S = Pp;
   for (int j = 0; j < args.f; ++j) {
     const int m = args.n[j];
-    const int nfib = static_cast<int>(E / m);
-    for (int fib = tid; fib < nfib; fib += FS_THREADS) {
-      const int inner = fib % stride;
-      const int outer = fib / stride;
-      fiber_one<MAXN>(tile, amat + j * MAXN * MAXN, m, stride, inner + outer * stride * m);
-    }
-    stride *= m;
+    axis_dmma<MAXN>(tile, amat + j * MAXN * MAXN, m, S, PR / m, warp, lane);
+    S *= m;
     __syncthreads();
   }
 
@@ -164,37 +151,29 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
   // contains the last axis, so nothing lies above it.
   const EpiParams& ep = args.ep;
   const bool spectral = args.spectral_last != 0;
-  const bool contiguous = P == pre;
-  const int Ei = static_cast<int>(E);
   if (spectral) {
     for (int pl = tid; pl < P; pl += FS_THREADS)
       lam_low[pl] = lambda_partial_low_ext(ep, p0 + pl, ep.axis);
     __syncthreads();
   }
+  const int PvR = P * Rv;
   if (!spectral && ep.kind != EPI_AXPY_DIAG) {
-    if (contiguous) {
-      const long long Ev = static_cast<long long>(P) * F * Qv;
 #pragma unroll 4
-      for (int e = tid; e < Ei; e += FS_THREADS)
-        if (e < Ev) args.y[gbase + e] = tile[e];
-    } else {
-#pragma unroll 4
-      for (int e = tid; e < Ei; e += FS_THREADS) {
-        const int r = e / P;
-        const int p = e - r * P;
-        if (p < Pv) args.y[gbase + p + pre * r] = tile[e];
-      }
+    for (int e = tid; e < PvR; e += FS_THREADS) {
+      const int r = e / P;
+      const int p = e - r * P;
+      if (p < Pv) args.y[gbase + p + pre * r] = tile[p + Pp * r];
     }
     return;
   }
-  for (int e = tid; e < Ei; e += FS_THREADS) {
+  for (int e = tid; e < PvR; e += FS_THREADS) {
     const int r = e / P;
     const int p = e - r * P;
-    const int q = r / F;
-    const int fidx = r - q * F;
-    if (p >= Pv || q >= Qv) continue;
-    const long long gi = gbase + p + pre * (fidx + static_cast<long long>(F) * q);
-    double val = tile[e];
+    if (p >= Pv) continue;
+    const int fidx = r % F;
+    const long long gi = gbase + p + pre * r;
+    const int si = p + Pp * r;
+    double val = tile[si];
     if (spectral) {
       double lam = lam_low[p];
       int rem = fidx;
@@ -210,7 +189,7 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
         val = __ddiv_rn(val, ls);
       } else {  // phase: the re/im partner is the neighbouring p (leading re/im axis)
         const bool is_im = ((p0 + p) & 1) != 0;
-        const double other = tile[is_im ? e - 1 : e + 1];
+        const double other = tile[is_im ? si - 1 : si + 1];
         const double phase = __dmul_rn(-ls, ep.dt);
         double sn, cs;
         sincos(phase, &sn, &cs);
@@ -279,23 +258,24 @@ void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, cons
   }
   param_check(maxn <= 32, "fused_small: extent > 32");
   const int MAXN = maxn <= 8 ? 8 : maxn <= 16 ? 16 : 32;
-  // tile: ~96 KB of doubles so two CTAs share an SM (one loads while the other computes); when
-  // that leaves runs of < 16 contiguous p (poor coalescing), use ~200 KB and one CTA per SM.
-  long long budget = 14080 - FS_MAXF * MAXN * MAXN;  // doubles: <= 110 KB per CTA, 2 per SM
-  if (a.pre * a.F > budget && budget / a.F < 8) budget = 27648 - FS_MAXF * MAXN * MAXN;
-  if (a.pre * a.F <= budget) {
+  // tile: <= ~110 KB of shared memory so two CTAs share an SM (one loads while the other
+  // computes); rows are padded to Pp = 4 mod 16 doubles (conflict-free fragment access).
+  auto padp = [](long long P) { return P + ((4 - P) % 16 + 16) % 16; };
+  const long long budget = 14080 - FS_MAXF * MAXN * MAXN - 64;  // doubles
+  if (padp(a.pre) * a.F <= budget) {
     a.P = static_cast<int>(a.pre);
-    long long qt = budget / (a.pre * a.F);
+    long long qt = budget / (padp(a.pre) * a.F);
     if (qt > a.post) qt = a.post;
     a.Qt = static_cast<int>(qt < 1 ? 1 : qt);
   } else {
-    long long P = budget / a.F;
-    if (P > 64) P = 64;
-    if (a.pre % 2 == 0 && P > 1) P &= ~1LL;  // keep re/im pairs (leading re/im axis) together
-    param_check(P >= 1, "fused_small: tile does not fit");
+    long long P = 16;
+    while (P + 16 <= 64 && padp(P + 16) * a.F <= budget) P += 16;
+    if (padp(P) * a.F > budget) P = 4;
+    param_check(padp(P) * a.F <= budget, "fused_small: tile does not fit");
     a.P = static_cast<int>(P);
     a.Qt = 1;
   }
+  a.Pp = static_cast<int>(padp(a.P));
   a.tiles_p = (a.pre + a.P - 1) / a.P;
   a.ep = ep;
   a.ep.axis = axis;
@@ -303,7 +283,7 @@ void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, cons
   if (spectral_last && ep.kind == EPI_SPEC_PHASE)
     param_check(a.P % 2 == 0 || a.P == a.pre, "fused_small: phase needs re/im pairs in a tile");
   const size_t smem = (static_cast<size_t>(FS_MAXF) * MAXN * MAXN + ((a.P + 1) & ~1) +
-                       static_cast<size_t>(a.P) * a.F * a.Qt) *
+                       static_cast<size_t>(a.Pp) * a.F * a.Qt) *
                       sizeof(double);
   if (MAXN == 8)
     launch_fs<8>(s, a, smem);
