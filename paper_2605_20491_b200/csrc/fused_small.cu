@@ -261,7 +261,10 @@ void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, cons
   // tile: <= ~110 KB of shared memory so two CTAs share an SM (one loads while the other
   // computes); rows are padded to Pp = 4 mod 16 doubles (conflict-free fragment access).
   auto padp = [](long long P) { return P + ((4 - P) % 16 + 16) % 16; };
-  const long long budget = 14080 - FS_MAXF * MAXN * MAXN - 64;  // doubles
+  long long budget = 14080 - FS_MAXF * MAXN * MAXN - 64;  // doubles
+  // fewer than 16 contiguous p per row would wreck coalescing: take ~215 KB, one CTA per SM
+  if (padp(a.pre) * a.F > budget && padp(16) * a.F > budget)
+    budget = 27600 - FS_MAXF * MAXN * MAXN - 64;
   if (padp(a.pre) * a.F <= budget) {
     a.P = static_cast<int>(a.pre);
     long long qt = budget / (padp(a.pre) * a.F);
