@@ -126,17 +126,25 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
                                       ? args.a[j][i + static_cast<long long>(args.lda[j]) * k]
                                       : 0.0;
     }
-  // tile load (LDGSTS, zero-fill outside the field and in the padding columns)
-  const int PR = Pp * R;
-  for (int e = tid; e < PR; e += FS_THREADS) {
-    const int r = e / Pp;
-    const int p = e - r * Pp;
-    const bool ok = p < Pv && r < Rv;
-    cp_async8(tile + e, args.x + (ok ? gbase + p + pre * r : 0), ok);
+  // tile load (LDGSTS, zero-fill outside the field and in the padding columns). Lanes walk
+  // (row, p) pairs with per-thread constant offsets: no per-element integer division.
+  const int RW = P <= 32 ? 32 / P : 1;                 // rows per warp iteration
+  const int lr = P <= 32 ? lane / P : 0;               // this lane's row within the iteration
+  const int lp = P <= 32 ? lane - lr * P : lane;       // this lane's p
+  const bool lane_on = P <= 32 ? lr < RW : true;
+  for (int r0 = warp * RW; r0 < R; r0 += RW * (FS_THREADS / 32)) {
+    const int r = r0 + lr;
+    if (!lane_on || r >= R) continue;
+    for (int p = lp; p < Pp; p += 32) {
+      const bool ok = p < Pv && r < Rv;
+      cp_async8(tile + p + Pp * r, args.x + (ok ? gbase + p + pre * r : 0), ok);
+      if (P <= 32 && p + 32 >= Pp) break;
+    }
   }
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
 
+  const int PR = Pp * R;
   int S = Pp;
   for (int j = 0; j < args.f; ++j) {
     const int m = args.n[j];
@@ -145,65 +153,74 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
     __syncthreads();
   }
 
-  // epilogue + store. The spectral factor needs the global multi-index: the part from the axes
-  // below the group depends only on p (precomputed once per tile, in axis order from 0.0 exactly
-  // like direct_sum_grid), the group part is added axis by axis; the spectral group always
-  // contains the last axis, so nothing lies above it.
+  // epilogue + store (same division-free (row, p) walk). The spectral factor needs the global
+  // multi-index: the axes below the group depend only on p (lam_low, computed once per tile in
+  // axis order from 0.0 exactly like direct_sum_grid), the group indices only on the row (packed
+  // per row once per tile); the spectral group always contains the last axis.
   const EpiParams& ep = args.ep;
   const bool spectral = args.spectral_last != 0;
+  int* rowidx = reinterpret_cast<int*>(amat);  // the matrices are no longer needed
   if (spectral) {
     for (int pl = tid; pl < P; pl += FS_THREADS)
       lam_low[pl] = lambda_partial_low_ext(ep, p0 + pl, ep.axis);
+    for (int fr = tid; fr < F; fr += FS_THREADS) {
+      int rem = fr, packed = 0;
+      for (int j = 0; j < args.f; ++j) {
+        packed |= (rem % args.n[j]) << (10 * j);
+        rem /= args.n[j];
+      }
+      rowidx[fr] = packed;
+    }
     __syncthreads();
   }
-  const int PvR = P * Rv;
-  if (!spectral && ep.kind != EPI_AXPY_DIAG) {
-#pragma unroll 4
-    for (int e = tid; e < PvR; e += FS_THREADS) {
-      const int r = e / P;
-      const int p = e - r * P;
-      if (p < Pv) args.y[gbase + p + pre * r] = tile[p + Pp * r];
-    }
-    return;
-  }
-  for (int e = tid; e < PvR; e += FS_THREADS) {
-    const int r = e / P;
-    const int p = e - r * P;
-    if (p >= Pv) continue;
-    const int fidx = r % F;
-    const long long gi = gbase + p + pre * r;
-    const int si = p + Pp * r;
-    double val = tile[si];
+  const bool plain = !spectral && ep.kind != EPI_AXPY_DIAG;
+  const double* l0 = spectral ? ep.lam[ep.axis] : nullptr;
+  const double* l1 = spectral && args.f > 1 ? ep.lam[ep.axis + 1] : nullptr;
+  const double* l2 = spectral && args.f > 2 ? ep.lam[ep.axis + 2] : nullptr;
+  for (int r0 = warp * RW; r0 < Rv; r0 += RW * (FS_THREADS / 32)) {
+    const int r = r0 + lr;
+    if (!lane_on || r >= Rv) continue;
+    int packed = 0;
     if (spectral) {
-      double lam = lam_low[p];
-      int rem = fidx;
-      for (int j = 0; j < args.f; ++j) {
-        const int idx = rem % args.n[j];
-        rem /= args.n[j];
-        if (ep.lam[ep.axis + j]) lam = __dadd_rn(lam, ep.lam[ep.axis + j][idx]);
-      }
-      const double ls = __dsub_rn(lam, ep.shift);
-      if (ep.kind == EPI_SPEC_MUL) {
-        val = __dmul_rn(val, ls);
-      } else if (ep.kind == EPI_SPEC_DIV) {
-        val = __ddiv_rn(val, ls);
-      } else {  // phase: the re/im partner is the neighbouring p (leading re/im axis)
-        const bool is_im = ((p0 + p) & 1) != 0;
-        const double other = tile[is_im ? si - 1 : si + 1];
-        const double phase = __dmul_rn(-ls, ep.dt);
-        double sn, cs;
-        sincos(phase, &sn, &cs);
-        const double re = is_im ? other : val;
-        const double im = is_im ? val : other;
-        val = is_im ? __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs))
-                    : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
-      }
-    } else {  // EPI_AXPY_DIAG
-      const double uu = ep.u[gi];
-      if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (gi >> 1) : gi], uu));
-      if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+      const int q = r / F;
+      packed = rowidx[r - q * F];
     }
-    args.y[gi] = val;
+    for (int p = lp; p < Pv; p += 32) {
+      const long long gi = gbase + p + pre * r;
+      const int si = p + Pp * r;
+      double val = tile[si];
+      if (plain) {
+        args.y[gi] = val;
+      } else if (spectral) {
+        double lam = lam_low[p];
+        if (l0) lam = __dadd_rn(lam, l0[packed & 1023]);
+        if (l1) lam = __dadd_rn(lam, l1[(packed >> 10) & 1023]);
+        if (l2) lam = __dadd_rn(lam, l2[(packed >> 20) & 1023]);
+        const double ls = __dsub_rn(lam, ep.shift);
+        if (ep.kind == EPI_SPEC_MUL) {
+          val = __dmul_rn(val, ls);
+        } else if (ep.kind == EPI_SPEC_DIV) {
+          val = __ddiv_rn(val, ls);
+        } else {  // phase: the re/im partner is the neighbouring p (leading re/im axis)
+          const bool is_im = ((p0 + p) & 1) != 0;
+          const double other = tile[is_im ? si - 1 : si + 1];
+          const double phase = __dmul_rn(-ls, ep.dt);
+          double sn, cs;
+          sincos(phase, &sn, &cs);
+          const double re = is_im ? other : val;
+          const double im = is_im ? val : other;
+          val = is_im ? __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs))
+                      : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
+        }
+        args.y[gi] = val;
+      } else {  // EPI_AXPY_DIAG
+        const double uu = ep.u[gi];
+        if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (gi >> 1) : gi], uu));
+        if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+        args.y[gi] = val;
+      }
+      if (P <= 32) break;
+    }
   }
 }
 
@@ -261,10 +278,7 @@ void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, cons
   // tile: <= ~110 KB of shared memory so two CTAs share an SM (one loads while the other
   // computes); rows are padded to Pp = 4 mod 16 doubles (conflict-free fragment access).
   auto padp = [](long long P) { return P + ((4 - P) % 16 + 16) % 16; };
-  long long budget = 14080 - FS_MAXF * MAXN * MAXN - 64;  // doubles
-  // fewer than 16 contiguous p per row would wreck coalescing: take ~215 KB, one CTA per SM
-  if (padp(a.pre) * a.F > budget && padp(16) * a.F > budget)
-    budget = 27600 - FS_MAXF * MAXN * MAXN - 64;
+  const long long budget = 14080 - FS_MAXF * MAXN * MAXN - 64 - 512;  // doubles
   if (padp(a.pre) * a.F <= budget) {
     a.P = static_cast<int>(a.pre);
     long long qt = budget / (padp(a.pre) * a.F);
