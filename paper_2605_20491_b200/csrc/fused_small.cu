@@ -70,32 +70,49 @@ __device__ __forceinline__ void axis_dmma(double* tile, const double* am, int m,
       bf[kk][nt] = (k < m && n < m) ? am[n + MAXN * k] : 0.0;
     }
   const int k4m = (m + 3) >> 2, ntm = (m + 7) >> 3;
-  for (int f0 = warp * 8; f0 < nfib; f0 += 8 * (FS_THREADS / 32)) {
-    const int fib = f0 + g;
-    const bool fok = fib < nfib;
-    const int fb = fok ? fib : f0;
-    const int base = (fb % S) + (fb / S) * S * m;
-    double acc[NT][2];
+  // G independent groups of 8 fibers per iteration: G * NT accumulator chains hide the DMMA
+  // latency (a single group has only NT chains of K4 dependent DMMAs).
+  constexpr int G = MAXN >= 32 ? 2 : 4;
+  for (int f0 = warp * 8 * G; f0 < nfib; f0 += 8 * G * (FS_THREADS / 32)) {
+    int base[G];
+    bool fok[G];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    for (int gg = 0; gg < G; ++gg) {
+      const int fib = f0 + 8 * gg + g;
+      fok[gg] = fib < nfib;
+      const int fb = fok[gg] ? fib : f0;
+      base[gg] = (fb % S) + (fb / S) * S * m;
+    }
+    double acc[G][NT][2];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[gg][nt][0] = acc[gg][nt][1] = 0.0;
 #pragma unroll
     for (int kk = 0; kk < K4; ++kk) {
       if (kk < k4m) {
         const int k = 4 * kk + t;
-        const double a = k < m ? tile[base + k * S] : 0.0;
+        double a[G];
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) a[gg] = k < m ? tile[base[gg] + k * S] : 0.0;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
-          if (nt < ntm) dmma884(acc[nt], a, bf[kk][nt]);
+          if (nt < ntm) {
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg) dmma884(acc[gg][nt], a[gg], bf[kk][nt]);
+          }
       }
     }
     __syncwarp();
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int gg = 0; gg < G; ++gg)
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int n = 8 * nt + 2 * t + v;
-        if (fok && nt < ntm && n < m) tile[base + n * S] = acc[nt][v];
-      }
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int n = 8 * nt + 2 * t + v;
+          if (fok[gg] && nt < ntm && n < m) tile[base[gg] + n * S] = acc[gg][nt][v];
+        }
   }
 }
 
