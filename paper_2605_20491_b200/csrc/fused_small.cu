@@ -52,14 +52,16 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// One axis of the group on the staged tile, in place, on the FP64 tensor cores: each warp takes 8
-// fibers at a time (the DMMA M dimension), k = the fiber index (K padded to 4), n = the output
-// index (N padded to 8). The matrix fragments live in registers for the whole tile, so shared
-// memory carries only the fiber reads and writes (strides are 4 mod 16 doubles: conflict free).
-template <int MAXN>
+// One axis of the group on the staged tile, in place, on the FP64 tensor cores: each warp takes
+// 8 x G fibers at a time (G DMMA M-blocks), k = the fiber index (K = 4*K4), n = the output index
+// (N = 8*NT). K4/NT are compile-time (chosen per axis from m) so the DMMA stream carries no
+// predicates; the matrix fragments live in registers for the whole tile, shared memory carries
+// only the fiber reads and writes (row strides are 4 mod 16 doubles: conflict free); the G * NT
+// accumulator chains hide the DMMA latency.
+template <int MAXN, int K4, int NT>
 __device__ __forceinline__ void axis_dmma(double* tile, const double* am, int m, int S, int nfib,
                                           int warp, int lane) {
-  constexpr int K4 = MAXN / 4, NT = MAXN / 8;
+  constexpr int G = NT >= 4 ? 2 : 4;
   const int g = lane >> 2, t = lane & 3;
   double bf[K4][NT];
 #pragma unroll
@@ -69,10 +71,6 @@ __device__ __forceinline__ void axis_dmma(double* tile, const double* am, int m,
       const int k = 4 * kk + t, n = 8 * nt + g;
       bf[kk][nt] = (k < m && n < m) ? am[n + MAXN * k] : 0.0;
     }
-  const int k4m = (m + 3) >> 2, ntm = (m + 7) >> 3;
-  // G independent groups of 8 fibers per iteration: G * NT accumulator chains hide the DMMA
-  // latency (a single group has only NT chains of K4 dependent DMMAs).
-  constexpr int G = MAXN >= 32 ? 2 : 4;
   for (int f0 = warp * 8 * G; f0 < nfib; f0 += 8 * G * (FS_THREADS / 32)) {
     int base[G];
     bool fok[G];
@@ -81,7 +79,8 @@ __device__ __forceinline__ void axis_dmma(double* tile, const double* am, int m,
       const int fib = f0 + 8 * gg + g;
       fok[gg] = fib < nfib;
       const int fb = fok[gg] ? fib : f0;
-      base[gg] = (fb % S) + (fb / S) * S * m;
+      const int o = fb / S;
+      base[gg] = (fb - o * S) + o * S * m;
     }
     double acc[G][NT][2];
 #pragma unroll
@@ -90,18 +89,14 @@ __device__ __forceinline__ void axis_dmma(double* tile, const double* am, int m,
       for (int nt = 0; nt < NT; ++nt) acc[gg][nt][0] = acc[gg][nt][1] = 0.0;
 #pragma unroll
     for (int kk = 0; kk < K4; ++kk) {
-      if (kk < k4m) {
-        const int k = 4 * kk + t;
-        double a[G];
+      const int k = 4 * kk + t;
+      double a[G];
 #pragma unroll
-        for (int gg = 0; gg < G; ++gg) a[gg] = k < m ? tile[base[gg] + k * S] : 0.0;
+      for (int gg = 0; gg < G; ++gg) a[gg] = k < m ? tile[base[gg] + k * S] : 0.0;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          if (nt < ntm) {
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-            for (int gg = 0; gg < G; ++gg) dmma884(acc[gg][nt], a[gg], bf[kk][nt]);
-          }
-      }
+        for (int gg = 0; gg < G; ++gg) dmma884(acc[gg][nt], a[gg], bf[kk][nt]);
     }
     __syncwarp();
 #pragma unroll
@@ -111,8 +106,23 @@ __device__ __forceinline__ void axis_dmma(double* tile, const double* am, int m,
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const int n = 8 * nt + 2 * t + v;
-          if (fok[gg] && nt < ntm && n < m) tile[base[gg] + n * S] = acc[gg][nt][v];
+          if (fok[gg] && n < m) tile[base[gg] + n * S] = acc[gg][nt][v];
         }
+  }
+}
+
+template <int MAXN>
+__device__ __forceinline__ void axis_dispatch(double* tile, const double* am, int m, int S,
+                                              int nfib, int warp, int lane) {
+  switch ((m + 3) >> 2) {
+    case 1: axis_dmma<MAXN, 1, 1>(tile, am, m, S, nfib, warp, lane); break;
+    case 2: axis_dmma<MAXN, 2, 1>(tile, am, m, S, nfib, warp, lane); break;
+    case 3: if (MAXN >= 16) axis_dmma<MAXN, (MAXN >= 16 ? 3 : 1), (MAXN >= 16 ? 2 : 1)>(tile, am, m, S, nfib, warp, lane); break;
+    case 4: if (MAXN >= 16) axis_dmma<MAXN, (MAXN >= 16 ? 4 : 1), (MAXN >= 16 ? 2 : 1)>(tile, am, m, S, nfib, warp, lane); break;
+    case 5: if (MAXN >= 32) axis_dmma<MAXN, (MAXN >= 32 ? 5 : 1), (MAXN >= 32 ? 3 : 1)>(tile, am, m, S, nfib, warp, lane); break;
+    case 6: if (MAXN >= 32) axis_dmma<MAXN, (MAXN >= 32 ? 6 : 1), (MAXN >= 32 ? 3 : 1)>(tile, am, m, S, nfib, warp, lane); break;
+    case 7: if (MAXN >= 32) axis_dmma<MAXN, (MAXN >= 32 ? 7 : 1), (MAXN >= 32 ? 4 : 1)>(tile, am, m, S, nfib, warp, lane); break;
+    default: if (MAXN >= 32) axis_dmma<MAXN, (MAXN >= 32 ? 8 : 1), (MAXN >= 32 ? 4 : 1)>(tile, am, m, S, nfib, warp, lane); break;
   }
 }
 
@@ -165,7 +175,7 @@ __global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const FSArgs
   int S = Pp;
   for (int j = 0; j < args.f; ++j) {
     const int m = args.n[j];
-    axis_dmma<MAXN>(tile, amat + j * MAXN * MAXN, m, S, PR / m, warp, lane);
+    axis_dispatch<MAXN>(tile, amat + j * MAXN * MAXN, m, S, PR / m, warp, lane);
     S *= m;
     __syncthreads();
   }
