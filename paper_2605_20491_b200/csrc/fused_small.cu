@@ -25,8 +25,8 @@ constexpr int FS_THREADS = 256;
 constexpr int FS_MAXF = 3;
 
 struct FSArgs {
-  const double* x;
-  double* y;
+  const double* __restrict__ x;
+  double* __restrict__ y;
   long long pre, post;  // real-view extents below / above the group
   int f;                // number of fused axes
   int n[FS_MAXF];       // their extents
@@ -71,6 +71,8 @@ __device__ __forceinline__ void axis_dmma(double* tile, const double* am, int m,
       const int k = 4 * kk + t, n = 8 * nt + g;
       bf[kk][nt] = (k < m && n < m) ? am[n + MAXN * k] : 0.0;
     }
+  const float invS = 1.0f / static_cast<float>(S);
+  const int Sm = S * m;
   for (int f0 = warp * 8 * G; f0 < nfib; f0 += 8 * G * (FS_THREADS / 32)) {
     int base[G];
     bool fok[G];
@@ -79,8 +81,11 @@ __device__ __forceinline__ void axis_dmma(double* tile, const double* am, int m,
       const int fib = f0 + 8 * gg + g;
       fok[gg] = fib < nfib;
       const int fb = fok[gg] ? fib : f0;
-      const int o = fb / S;
-      base[gg] = (fb - o * S) + o * S * m;
+      // fb / S through a float reciprocal, corrected to the exact quotient (fb < 2^22)
+      int o = __float2int_rz(static_cast<float>(fb) * invS);
+      o -= (o * S > fb);
+      o += ((o + 1) * S <= fb);
+      base[gg] = fb + o * (Sm - S);
     }
     double acc[G][NT][2];
 #pragma unroll
@@ -126,26 +131,25 @@ __device__ __forceinline__ void axis_dispatch(double* tile, const double* am, in
   }
 }
 
-// Persistent CTAs, double-buffered: while the tensor cores transform tile i in one buffer, the
-// LDGSTS copies of tile i + 1 stream into the other (the pass is HBM-bound; this keeps ~100 KB in
-// flight per SM instead of idling between a tile's load and its compute).
 template <int MAXN>
-__global__ void __launch_bounds__(FS_THREADS, 1) fused_small_kernel(const FSArgs args) {
+__global__ void __launch_bounds__(FS_THREADS, 2) fused_small_kernel(const __grid_constant__ FSArgs args) {
   extern __shared__ __align__(16) double sm[];
   const int P = args.P, F = args.F, Qt = args.Qt, Pp = args.Pp;
-  double* amat = sm;                                 // FS_MAXF x MAXN x MAXN
-  int* rowidx = reinterpret_cast<int*>(sm + FS_MAXF * MAXN * MAXN);  // F packed group indices
-  double* lam_low = sm + FS_MAXF * MAXN * MAXN + ((F + 1) / 2 + 1) / 2 * 2;  // P, even-padded
-  double* buf0 = lam_low + ((P + 1) & ~1);
-  const int R = F * Qt;  // rows (f, q) of a tile
-  const int PR = Pp * R;
-  double* bufs[2] = {buf0, buf0 + PR};
+  double* amat = sm;                                // FS_MAXF x MAXN x MAXN
+  double* lam_low = sm + FS_MAXF * MAXN * MAXN;     // P (spectral epilogue), even-padded
+  double* tile = lam_low + ((P + 1) & ~1);          // element (p, r) at p + Pp * r, r = (f, q)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const long long pre = args.pre;
-  const long long ntiles = args.tiles_p * ((args.post + Qt - 1) / Qt);
-  const EpiParams& ep = args.ep;
-  const bool spectral = args.spectral_last != 0;
+  const long long tp = blockIdx.x % args.tiles_p;
+  const long long tq = blockIdx.x / args.tiles_p;
+  const long long p0 = tp * P;
+  const long long q0 = tq * Qt;
+  const int Pv = static_cast<int>(pre - p0 < P ? pre - p0 : P);                 // valid p
+  const int Qv = static_cast<int>(args.post - q0 < Qt ? args.post - q0 : Qt);  // valid q
+  const int R = F * Qt;    // rows (f, q) of the tile
+  const int Rv = F * Qv;   // valid rows
+  const long long gbase = p0 + pre * static_cast<long long>(F) * q0;  // element (p, r) at gbase + p + pre * r
 
   for (int j = 0; j < args.f; ++j)
     for (int e = tid; e < MAXN * MAXN; e += FS_THREADS) {
@@ -154,7 +158,43 @@ __global__ void __launch_bounds__(FS_THREADS, 1) fused_small_kernel(const FSArgs
                                       ? args.a[j][i + static_cast<long long>(args.lda[j]) * k]
                                       : 0.0;
     }
-  if (spectral)
+  // tile load (LDGSTS, zero-fill outside the field and in the padding columns). Lanes walk
+  // (row, p) pairs with per-thread constant offsets: no per-element integer division.
+  const int RW = P <= 32 ? 32 / P : 1;                 // rows per warp iteration
+  const int lr = P <= 32 ? lane / P : 0;               // this lane's row within the iteration
+  const int lp = P <= 32 ? lane - lr * P : lane;       // this lane's p
+  const bool lane_on = P <= 32 ? lr < RW : true;
+  for (int r0 = warp * RW; r0 < R; r0 += RW * (FS_THREADS / 32)) {
+    const int r = r0 + lr;
+    if (!lane_on || r >= R) continue;
+    for (int p = lp; p < Pp; p += 32) {
+      const bool ok = p < Pv && r < Rv;
+      cp_async8(tile + p + Pp * r, args.x + (ok ? gbase + p + pre * r : 0), ok);
+      if (P <= 32 && p + 32 >= Pp) break;
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+
+  const int PR = Pp * R;
+  int S = Pp;
+  for (int j = 0; j < args.f; ++j) {
+    const int m = args.n[j];
+    axis_dispatch<MAXN>(tile, amat + j * MAXN * MAXN, m, S, PR / m, warp, lane);
+    S *= m;
+    __syncthreads();
+  }
+
+  // epilogue + store (same division-free (row, p) walk). The spectral factor needs the global
+  // multi-index: the axes below the group depend only on p (lam_low, computed once per tile in
+  // axis order from 0.0 exactly like direct_sum_grid), the group indices only on the row (packed
+  // per row once per tile); the spectral group always contains the last axis.
+  const EpiParams& ep = args.ep;
+  const bool spectral = args.spectral_last != 0;
+  int* rowidx = reinterpret_cast<int*>(amat);  // the matrices are no longer needed
+  if (spectral) {
+    for (int pl = tid; pl < P; pl += FS_THREADS)
+      lam_low[pl] = lambda_partial_low_ext(ep, p0 + pl, ep.axis);
     for (int fr = tid; fr < F; fr += FS_THREADS) {
       int rem = fr, packed = 0;
       for (int j = 0; j < args.f; ++j) {
@@ -163,122 +203,56 @@ __global__ void __launch_bounds__(FS_THREADS, 1) fused_small_kernel(const FSArgs
       }
       rowidx[fr] = packed;
     }
-
-  // lanes walk (row, p) pairs with per-thread constant offsets: no per-element division
-  const int RW = P <= 32 ? 32 / P : 1;
-  const int lr = P <= 32 ? lane / P : 0;
-  const int lp = P <= 32 ? lane - lr * P : lane;
-  const bool lane_on = P <= 32 ? lr < RW : true;
-
-  auto tile_geom = [&](long long tile, long long& p0, long long& q0, int& Pv, int& Rv,
-                       long long& gbase) {
-    const long long tp = tile % args.tiles_p;
-    const long long tq = tile / args.tiles_p;
-    p0 = tp * P;
-    q0 = tq * Qt;
-    Pv = static_cast<int>(pre - p0 < P ? pre - p0 : P);
-    const int Qv = static_cast<int>(args.post - q0 < Qt ? args.post - q0 : Qt);
-    Rv = F * Qv;
-    gbase = p0 + pre * static_cast<long long>(F) * q0;  // element (p, r) at gbase + p + pre * r
-  };
-  auto load = [&](long long tile, double* dst) {
-    long long p0, q0, gbase;
-    int Pv, Rv;
-    tile_geom(tile, p0, q0, Pv, Rv, gbase);
-    for (int r0 = warp * RW; r0 < R; r0 += RW * (FS_THREADS / 32)) {
-      const int r = r0 + lr;
-      if (!lane_on || r >= R) continue;
-      for (int p = lp; p < Pp; p += 32) {
-        const bool ok = p < Pv && r < Rv;
-        cp_async8(dst + p + Pp * r, args.x + (ok ? gbase + p + pre * r : 0), ok);
-        if (P <= 32 && p + 32 >= Pp) break;
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-
-  long long tile = blockIdx.x;
-  if (tile < ntiles) load(tile, bufs[0]);
-  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    double* cur = bufs[it & 1];
-    const long long next = tile + gridDim.x;
-    if (next < ntiles) {
-      load(next, bufs[(it + 1) & 1]);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
     __syncthreads();
-
-    int S = Pp;
-    for (int j = 0; j < args.f; ++j) {
-      const int m = args.n[j];
-      axis_dispatch<MAXN>(cur, amat + j * MAXN * MAXN, m, S, PR / m, warp, lane);
-      S *= m;
-      __syncthreads();
-    }
-
-    // epilogue + store. The spectral factor needs the global multi-index: the axes below the
-    // group depend only on p (lam_low, in axis order from 0.0 exactly like direct_sum_grid), the
-    // group indices only on the row; the spectral group always contains the last axis.
-    long long p0, q0, gbase;
-    int Pv, Rv;
-    tile_geom(tile, p0, q0, Pv, Rv, gbase);
+  }
+  const bool plain = !spectral && ep.kind != EPI_AXPY_DIAG;
+  const double* l0 = spectral ? ep.lam[ep.axis] : nullptr;
+  const double* l1 = spectral && args.f > 1 ? ep.lam[ep.axis + 1] : nullptr;
+  const double* l2 = spectral && args.f > 2 ? ep.lam[ep.axis + 2] : nullptr;
+  for (int r0 = warp * RW; r0 < Rv; r0 += RW * (FS_THREADS / 32)) {
+    const int r = r0 + lr;
+    if (!lane_on || r >= Rv) continue;
+    int packed = 0;
     if (spectral) {
-      for (int pl = tid; pl < P; pl += FS_THREADS)
-        lam_low[pl] = lambda_partial_low_ext(ep, p0 + pl, ep.axis);
-      __syncthreads();
+      const int q = r / F;
+      packed = rowidx[r - q * F];
     }
-    const bool plain = !spectral && ep.kind != EPI_AXPY_DIAG;
-    const double* l0 = spectral ? ep.lam[ep.axis] : nullptr;
-    const double* l1 = spectral && args.f > 1 ? ep.lam[ep.axis + 1] : nullptr;
-    const double* l2 = spectral && args.f > 2 ? ep.lam[ep.axis + 2] : nullptr;
-    for (int r0 = warp * RW; r0 < Rv; r0 += RW * (FS_THREADS / 32)) {
-      const int r = r0 + lr;
-      if (!lane_on || r >= Rv) continue;
-      int packed = 0;
-      if (spectral) {
-        const int q = r / F;
-        packed = rowidx[r - q * F];
-      }
-      for (int p = lp; p < Pv; p += 32) {
-        const long long gi = gbase + p + pre * r;
-        const int si = p + Pp * r;
-        double val = cur[si];
-        if (plain) {
-          args.y[gi] = val;
-        } else if (spectral) {
-          double lam = lam_low[p];
-          if (l0) lam = __dadd_rn(lam, l0[packed & 1023]);
-          if (l1) lam = __dadd_rn(lam, l1[(packed >> 10) & 1023]);
-          if (l2) lam = __dadd_rn(lam, l2[(packed >> 20) & 1023]);
-          const double ls = __dsub_rn(lam, ep.shift);
-          if (ep.kind == EPI_SPEC_MUL) {
-            val = __dmul_rn(val, ls);
-          } else if (ep.kind == EPI_SPEC_DIV) {
-            val = __ddiv_rn(val, ls);
-          } else {  // phase: the re/im partner is the neighbouring p (leading re/im axis)
-            const bool is_im = ((p0 + p) & 1) != 0;
-            const double other = cur[is_im ? si - 1 : si + 1];
-            const double phase = __dmul_rn(-ls, ep.dt);
-            double sn, cs;
-            sincos(phase, &sn, &cs);
-            const double re = is_im ? other : val;
-            const double im = is_im ? val : other;
-            val = is_im ? __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs))
-                        : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
-          }
-          args.y[gi] = val;
-        } else {  // EPI_AXPY_DIAG
-          const double uu = ep.u[gi];
-          if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (gi >> 1) : gi], uu));
-          if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
-          args.y[gi] = val;
+    for (int p = lp; p < Pv; p += 32) {
+      const long long gi = gbase + p + pre * r;
+      const int si = p + Pp * r;
+      double val = tile[si];
+      if (plain) {
+        args.y[gi] = val;
+      } else if (spectral) {
+        double lam = lam_low[p];
+        if (l0) lam = __dadd_rn(lam, l0[packed & 1023]);
+        if (l1) lam = __dadd_rn(lam, l1[(packed >> 10) & 1023]);
+        if (l2) lam = __dadd_rn(lam, l2[(packed >> 20) & 1023]);
+        const double ls = __dsub_rn(lam, ep.shift);
+        if (ep.kind == EPI_SPEC_MUL) {
+          val = __dmul_rn(val, ls);
+        } else if (ep.kind == EPI_SPEC_DIV) {
+          val = __ddiv_rn(val, ls);
+        } else {  // phase: the re/im partner is the neighbouring p (leading re/im axis)
+          const bool is_im = ((p0 + p) & 1) != 0;
+          const double other = tile[is_im ? si - 1 : si + 1];
+          const double phase = __dmul_rn(-ls, ep.dt);
+          double sn, cs;
+          sincos(phase, &sn, &cs);
+          const double re = is_im ? other : val;
+          const double im = is_im ? val : other;
+          val = is_im ? __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs))
+                      : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
         }
-        if (P <= 32) break;
+        args.y[gi] = val;
+      } else {  // EPI_AXPY_DIAG
+        const double uu = ep.u[gi];
+        if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (gi >> 1) : gi], uu));
+        if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+        args.y[gi] = val;
       }
+      if (P <= 32) break;
     }
-    __syncthreads();  // the buffer is refilled by the next iteration's prefetch
   }
 }
 
@@ -290,15 +264,8 @@ void launch_fs(cudaStream_t s, const FSArgs& a, size_t smem) {
                                232448 - 1024));
     attr = true;
   }
-  static int num_sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
   const long long tiles = a.tiles_p * ((a.post + a.Qt - 1) / a.Qt);
-  const long long grid = tiles < num_sms ? tiles : num_sms;
-  fused_small_kernel<MAXN><<<static_cast<unsigned>(grid), FS_THREADS, smem, s>>>(a);
+  fused_small_kernel<MAXN><<<static_cast<unsigned>(tiles), FS_THREADS, smem, s>>>(a);
   KCUDA(cudaGetLastError());
 }
 
@@ -340,23 +307,19 @@ void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, cons
   }
   param_check(maxn <= 32, "fused_small: extent > 32");
   const int MAXN = maxn <= 8 ? 8 : maxn <= 16 ? 16 : 32;
-  // two tile buffers of <= ~100 KB each (one CTA per SM, double-buffered); rows padded to
-  // Pp = 4 or 12 mod 16 doubles (conflict-free 64-bit fragment access)
-  auto padp = [](long long P) {
-    long long q = P;
-    while (q % 16 != 4 && q % 16 != 12) ++q;
-    return q;
-  };
-  const long long fixed = FS_MAXF * MAXN * MAXN + (a.F + 3) / 2 + 2 + 66;
-  const long long budget = (28000 - fixed) / 2;  // doubles per buffer (227 KB total)
+  // tile: <= ~110 KB of shared memory so two CTAs share an SM (one loads while the other
+  // computes); rows are padded to Pp = 4 mod 16 doubles (conflict-free fragment access).
+  auto padp = [](long long P) { return P + ((4 - P) % 16 + 16) % 16; };
+  const long long budget = 14080 - FS_MAXF * MAXN * MAXN - 64 - 512;  // doubles
   if (padp(a.pre) * a.F <= budget) {
     a.P = static_cast<int>(a.pre);
     long long qt = budget / (padp(a.pre) * a.F);
     if (qt > a.post) qt = a.post;
     a.Qt = static_cast<int>(qt < 1 ? 1 : qt);
   } else {
-    long long P = 64;
-    while (P > 2 && padp(P) * a.F > budget) P = P > 16 ? P - 16 : P / 2;
+    long long P = 16;
+    while (P + 16 <= 64 && padp(P + 16) * a.F <= budget) P += 16;
+    if (padp(P) * a.F > budget) P = 4;
     param_check(padp(P) * a.F <= budget, "fused_small: tile does not fit");
     a.P = static_cast<int>(P);
     a.Qt = 1;
@@ -368,9 +331,8 @@ void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, cons
   a.spectral_last = spectral_last ? 1 : 0;
   if (spectral_last && ep.kind == EPI_SPEC_PHASE)
     param_check(a.P % 2 == 0 || a.P == a.pre, "fused_small: phase needs re/im pairs in a tile");
-  const size_t smem = (static_cast<size_t>(FS_MAXF) * MAXN * MAXN +
-                       ((a.F + 1) / 2 + 1) / 2 * 2 + ((a.P + 1) & ~1) +
-                       2 * static_cast<size_t>(a.Pp) * a.F * a.Qt) *
+  const size_t smem = (static_cast<size_t>(FS_MAXF) * MAXN * MAXN + ((a.P + 1) & ~1) +
+                       static_cast<size_t>(a.Pp) * a.F * a.Qt) *
                       sizeof(double);
   if (MAXN == 8)
     launch_fs<8>(s, a, smem);
