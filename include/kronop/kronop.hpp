@@ -419,4 +419,106 @@ inline EigenpairResult inverse_iteration(const FullOperator& op,
   return out;
 }
 
+// ------------------------------------------------------------------- tensor.hpp:79-106 --
+template <typename S>
+void mode_product(Context& ctx, const DeviceField<S>& x, const std::vector<double>& a, int m,
+                  int axis, DeviceField<S>& out) {  // a: column-major m x shape[axis]
+  check(kronop_mode_product(ctx.get(), x.data(), static_cast<int>(x.shape().size()),
+                            x.shape().data(), is_complex_v<S>, a.data(), m, axis, out.data()));
+}
+template <typename S>
+void kron_apply(Context& ctx, const DeviceField<S>& x,
+                const std::vector<const std::vector<double>*>& mats, const std::vector<int>& rows,
+                DeviceField<S>& out) {  // null entries = identity
+  std::vector<const double*> p(mats.size(), nullptr);
+  for (std::size_t a = 0; a < mats.size(); ++a) p[a] = mats[a] ? mats[a]->data() : nullptr;
+  check(kronop_kron_apply(ctx.get(), x.data(), static_cast<int>(x.shape().size()),
+                          x.shape().data(), is_complex_v<S>, p.data(), rows.data(), out.data()));
+}
+inline double inner(Context& ctx, const DeviceField<double>& u, const DeviceField<double>& v,
+                    const MassWeights* mass = nullptr) {  // Weighting::Plain / Mass
+  double r[2] = {0, 0};
+  std::vector<const double*> m;
+  if (mass)
+    for (const auto& w : *mass) m.push_back(w.data());
+  check(kronop_inner(ctx.get(), u.data(), v.data(), static_cast<int>(u.shape().size()),
+                     u.shape().data(), 0, mass ? m.data() : nullptr, r));
+  return r[0];
+}
+
+// ------------------------------------------------------------- splitting.hpp:46-52 --
+inline void qhop_step(const SeparableOperator& a, const DeviceField<double>& b_diag,
+                      const DeviceField<std::complex<double>>& psi, double h, int quad_points,
+                      DeviceField<std::complex<double>>& out) {
+  check(kronop_qhop_step(a.context().get(), a.handle(), b_diag.data(), psi.data(), h, quad_points,
+                         out.data()));
+}
+inline void yoshida_step(const SeparableOperator& a, const DeviceField<double>& b_diag,
+                         const DeviceField<std::complex<double>>& psi, double h, int quad_points,
+                         DeviceField<std::complex<double>>& out) {
+  check(kronop_yoshida_step(a.context().get(), a.handle(), b_diag.data(), psi.data(), h,
+                            quad_points, out.data()));
+}
+
+// -------------------------------------------------------------------- gpe.hpp:17-74 --
+enum class GpeFlowKind { ModifiedH1, AdaptiveMetric };
+enum class GpeInit { Constant, Eigenfunction, Supplied };
+struct GpeFlowConfig {
+  GpeFlowKind kind = GpeFlowKind::ModifiedH1;
+  double step = 0.1, metric_shift = 20.0, energy_rel_tol = 1e-12;
+  int max_iterations = 20000;
+  PcgConfig inner{.stagnation_window = 100};
+  GpeInit init = GpeInit::Eigenfunction;
+  bool record_history = false;
+};
+struct GpeHistoryRow {
+  int iteration = 0;
+  double energy = 0.0, rel_change = 0.0;
+  long linear_solves = 0;
+  double seconds = 0.0;
+};
+struct GpeResult {
+  double energy = 0.0, eigenvalue = 0.0;
+  int iterations = 0;
+  long linear_solves = 0;
+  bool converged = false;
+  std::vector<GpeHistoryRow> history;
+};
+struct GpeProblem {  // gpe.hpp:17-22 (mass weights travel with the operator)
+  FullOperator hamiltonian;
+  const SeparableOperator* laplacian = nullptr;
+  double beta = 0.0;
+};
+inline double gpe_energy(const GpeProblem& p, const DeviceField<double>& u) {
+  double e = 0.0;
+  check(kronop_gpe_energy(p.hamiltonian.sep->context().get(), p.hamiltonian.sep->handle(),
+                          p.hamiltonian.diagonal ? p.hamiltonian.diagonal->data() : nullptr,
+                          p.beta, u.data(), &e));
+  return e;
+}
+inline GpeResult gpe_gradient_flow(const GpeProblem& p, const GpeFlowConfig& config,
+                                   DeviceField<double>& state,
+                                   const DeviceField<double>* initial = nullptr) {
+  kronop_gpe_config c{config.kind == GpeFlowKind::ModifiedH1 ? KRONOP_GPE_H1 : KRONOP_GPE_AU,
+                      config.step, config.metric_shift, config.energy_rel_tol,
+                      config.max_iterations, config.inner.c(),
+                      config.init == GpeInit::Constant        ? KRONOP_GPE_INIT_CONSTANT
+                      : config.init == GpeInit::Eigenfunction ? KRONOP_GPE_INIT_EIGENFUNCTION
+                                                              : KRONOP_GPE_INIT_SUPPLIED,
+                      config.record_history ? 1 : 0};
+  kronop_gpe_result r{};
+  std::vector<double> hist(config.record_history ? 5 * static_cast<size_t>(config.max_iterations) : 0);
+  check(kronop_gpe_gradient_flow(p.hamiltonian.sep->context().get(), p.hamiltonian.sep->handle(),
+                                 p.hamiltonian.diagonal ? p.hamiltonian.diagonal->data() : nullptr,
+                                 p.laplacian->handle(), p.beta, &c,
+                                 initial ? initial->data() : nullptr, state.data(), &r,
+                                 config.record_history ? hist.data() : nullptr));
+  GpeResult out{r.energy, r.eigenvalue, r.iterations, static_cast<long>(r.linear_solves),
+                r.converged != 0, {}};
+  for (int i = 0; i < r.history_len; ++i)
+    out.history.push_back({static_cast<int>(hist[5 * i]), hist[5 * i + 1], hist[5 * i + 2],
+                           static_cast<long>(hist[5 * i + 3]), hist[5 * i + 4]});
+  return out;
+}
+
 }  // namespace kronop

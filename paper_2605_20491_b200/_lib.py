@@ -89,6 +89,7 @@ PROTOTYPES = {
     "kronop_direct_sum_grid": (I, [P, I, IP, C.POINTER(DP), P]),
     "kronop_op_create": (I, [P, I, IP, C.POINTER(DP), C.POINTER(DP), C.POINTER(DP),
                              C.POINTER(DP), D, C.POINTER(P)]),
+    "kronop_op_create_folded": (I, [P, I, IP] + [C.POINTER(DP)] * 8 + [D, C.POINTER(P)]),
     "kronop_op_destroy": (I, [P]),
     "kronop_op_set_shift": (I, [P, D]),
     "kronop_op_info": (I, [P, DP, DP, DP, C.POINTER(C.c_size_t)]),
@@ -120,6 +121,7 @@ PROTOTYPES = {
     "kronop_host_interp_matrix": (I, [D, I, I, I, I, DP]),
     "kronop_host_sym_eig": (I, [I, DP, DP, DP]),
     "kronop_host_build_sem_axis": (I, [D, I, I, DP, DP, DP, DP]),
+    "kronop_host_build_sem_axis_folded": (I, [D, I, I] + [DP] * 8),
     "kronop_splitmix_uniform": (I, [P, C.c_uint64, C.c_uint64, C.c_size_t, P]),
 }
 

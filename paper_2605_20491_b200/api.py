@@ -180,6 +180,55 @@ def build_axis(basis: Basis1D, f: Optional[Callable] = None, fvals: Optional[np.
     return ax
 
 
+@dataclass
+class FoldedAxis:
+    """Even/odd factorisation of a mirror-symmetric axis (host_setup.hpp FoldedAxis): half-size
+    forward / backward blocks on u = x_i + x_{n-1-i} (+ middle node) and v = x_i - x_{n-1-i}."""
+    n: int
+    eigenvalues_even: np.ndarray
+    eigenvalues_odd: np.ndarray
+    fe: np.ndarray
+    fo: np.ndarray
+    be: np.ndarray
+    bo: np.ndarray
+    ground: np.ndarray
+
+    @property
+    def size(self):
+        return self.n
+
+    @property
+    def eigenvalues(self):
+        """All eigenvalues in folded order [even | odd] (the transformed layout)."""
+        return np.concatenate([self.eigenvalues_even, self.eigenvalues_odd])
+
+
+def build_axis_folded(basis: Basis1D, f: Optional[Callable] = None,
+                      fvals: Optional[np.ndarray] = None) -> FoldedAxis:
+    """Folded build_axis for a symmetric SEM axis and an even potential (ParameterError otherwise)."""
+    n = basis.size
+    if fvals is None:
+        fvals = np.array([f(float(x)) for x in basis.nodes]) if f is not None else np.zeros(n)
+    fvals = np.ascontiguousarray(fvals, dtype=np.float64)
+    key = ("folded", basis.half_width, basis.cell_count, basis.degree, fvals.tobytes())
+    if key in _AXIS_CACHE:
+        return _AXIS_CACHE[key]
+    no = n // 2
+    ne = n - no
+    le, lo = np.zeros(ne), np.zeros(max(no, 1))
+    fe, be = np.zeros(ne * ne), np.zeros(ne * ne)
+    fo, bo = np.zeros(max(no * no, 1)), np.zeros(max(no * no, 1))
+    g = np.zeros(n)
+    check(lib().kronop_host_build_sem_axis_folded(basis.half_width, basis.cell_count, basis.degree,
+                                                  _dptr(fvals), _dptr(le), _dptr(lo), _dptr(fe),
+                                                  _dptr(fo), _dptr(be), _dptr(bo), _dptr(g)))
+    ax = FoldedAxis(n, le, lo[:no].copy(), fe.reshape(ne, ne, order="F"),
+                    fo[:no * no].reshape(no, no, order="F"), be.reshape(ne, ne, order="F"),
+                    bo[:no * no].reshape(no, no, order="F"), g)
+    _AXIS_CACHE[key] = ax
+    return ax
+
+
 # ---------------------------------------------------------------------------- operators --
 class SeparableOperator:
     """proj/include/kronop/operators.hpp:15-53, resident on the device."""
@@ -202,6 +251,32 @@ class SeparableOperator:
         h = C.c_void_p()
         check(lib().kronop_op_create(ctx.h, d, n, T, Ti, lam, mp, shift, C.byref(h)))
         self.h = h
+
+    @classmethod
+    def folded(cls, ctx: Context, axes: Sequence[FoldedAxis], shift: float = 0.0,
+               mass: Optional[Sequence[np.ndarray]] = None) -> "SeparableOperator":
+        """Even/odd folded variant (kronop_op_create_folded): same operator, half-size blocks per
+        axis. Per-pass entry points (transform_pass, the slab backend) are not available."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.axes = list(axes)
+        d = len(axes)
+        self.shape = tuple(a.n for a in axes)
+        n = (C.c_int * d)(*self.shape)
+        groups = [[np.asfortranarray(getattr(a, k)) if getattr(a, k).size else np.zeros(1)
+                   for a in axes] for k in ("fe", "fo", "be", "bo")]
+        groups += [[np.ascontiguousarray(a.eigenvalues_even) for a in axes],
+                   [np.ascontiguousarray(a.eigenvalues_odd) if a.n > 1 else np.zeros(1)
+                    for a in axes],
+                   [np.ascontiguousarray(a.ground) for a in axes]]
+        self._keep = groups
+        ptrs = [_arr_of_ptrs(g) for g in groups]
+        self.mass = [np.ascontiguousarray(m, dtype=np.float64) for m in mass] if mass else None
+        mp = _arr_of_ptrs(self.mass) if self.mass else None
+        h = C.c_void_p()
+        check(lib().kronop_op_create_folded(ctx.h, d, n, *ptrs, mp, shift, C.byref(h)))
+        self.h = h
+        return self
 
     def __del__(self):
         try:
@@ -442,17 +517,22 @@ class Grid:
         return np.ascontiguousarray(np.broadcast_to(v, tuple(reversed(self.shape))).reshape(-1),
                                     dtype=np.float64)
 
-    def separable_operator(self, ctx: Context, per_axis=None, shift: float = 0.0):
-        """grid.cpp:71-83: per_axis = list of scalar functions (or None = 0)."""
+    def separable_operator(self, ctx: Context, per_axis=None, shift: float = 0.0,
+                           folded: bool = False):
+        """grid.cpp:71-83: per_axis = list of scalar functions (or None = 0). folded=True builds
+        the even/odd folded variant (symmetric axes and even per-axis potentials only)."""
         axes = []
         for a in range(self.dim):
             f = per_axis[a] if per_axis else None
             fv = np.array([f(float(x)) for x in self.axes[a].nodes]) if f else None
-            axes.append(build_axis(self.axes[a], f=None, fvals=fv))
+            build = build_axis_folded if folded else build_axis
+            axes.append(build(self.axes[a], f=None, fvals=fv))
+        if folded:
+            return SeparableOperator.folded(ctx, axes, shift, mass=self.mass)
         return SeparableOperator(ctx, axes, shift, mass=self.mass)
 
-    def laplacian(self, ctx: Context, shift: float = 0.0):
-        return self.separable_operator(ctx, None, shift)
+    def laplacian(self, ctx: Context, shift: float = 0.0, folded: bool = False):
+        return self.separable_operator(ctx, None, shift, folded=folded)
 
 
 # ----------------------------------------------------------------------------- drivers --

@@ -147,8 +147,83 @@ static void sep_transform_fused_small(kronop_ctx& ctx, const kronop_op& op, cons
   }
 }
 
+// Even/odd folded operator (kronop_op_create_folded): per axis, fold into [u | v] halves, two
+// half-size DMMA passes on the sub-ranges (PassShape ldx/ldy = the full axis stride), and on the
+// way back two half-size passes then unfold. Half the flops of the dense pass per axis at the
+// cost of one extra HBM round trip (fold/unfold) per axis and direction.
+static void sep_transform_folded(kronop_ctx& ctx, const kronop_op& op, const double* in,
+                                 double* out, int cplx, SepKind kind, double shift, double dt,
+                                 const double* diag, double sigma) {
+  View v = make_view(op.d, op.n, cplx);
+  ensure_scratch(ctx, static_cast<size_t>(v.total()));
+  double* s0 = ctx.scratch[0];
+  double* s1 = ctx.scratch[1];
+  const int d = op.d;
+  auto geom = [&](int a, long long& pre, long long& post) {
+    const int ra = a + v.cplx;
+    pre = 1;
+    post = 1;
+    for (int i = 0; i < ra; ++i) pre *= v.ext[i];
+    for (int i = ra + 1; i < v.nd; ++i) post *= v.ext[i];
+  };
+  auto halves = [&](int a, const double* x, double* y, bool forward, const EpiParams& ep0) {
+    long long pre, post;
+    geom(a, pre, post);
+    const int n = op.n[a];
+    for (int h = 0; h < 2; ++h) {
+      const int m = h == 0 ? op.ne[a] : op.no[a];
+      if (m == 0) continue;
+      const long long off = h == 0 ? 0 : pre * op.ne[a];
+      PassShape ps;
+      ps.pre = pre;
+      ps.post = post;
+      ps.nk = m;
+      ps.m = m;
+      ps.ldx = pre * n;
+      ps.ldy = pre * n;
+      EpiParams ep = ep0;
+      if (ep.kind != EPI_STORE) ep.lam[a + v.cplx] = op.lam[a] + (h == 0 ? 0 : op.ne[a]);
+      const double* mat = forward ? (h == 0 ? op.fe[a] : op.fo[a]) : (h == 0 ? op.be[a] : op.bo[a]);
+      const int lda = h == 0 ? op.lda_e[a] : op.lda_o[a];
+      launch_mode_product(ctx.stream, x + off, y + off, mat, lda, ps, ep);
+      ctx.ws.launches += 1;
+    }
+  };
+  const double* cur = in;
+  for (int a = 0; a < d; ++a) {
+    long long pre, post;
+    geom(a, pre, post);
+    launch_fold(ctx.stream, ctx.ws, cur, s0, pre, op.n[a], post);
+    EpiParams ep;
+    if (a == d - 1) {
+      ep.kind = kind == SEP_APPLY ? EPI_SPEC_MUL : kind == SEP_SOLVE ? EPI_SPEC_DIV : EPI_SPEC_PHASE;
+      ep.axis = a + v.cplx;
+      ep.ndims = v.nd;
+      for (int i = 0; i < v.nd; ++i) ep.ext[i] = v.ext[i];
+      for (int b = 0; b < d; ++b) ep.lam[b + v.cplx] = op.lam[b];
+      ep.shift = shift;
+      ep.dt = dt;
+      ep.cplx = v.cplx;
+    }
+    halves(a, s0, s1, true, ep);
+    cur = s1;
+  }
+  for (int a = 0; a < d; ++a) {
+    long long pre, post;
+    geom(a, pre, post);
+    halves(a, s1, s0, false, EpiParams{});
+    const bool last = a == d - 1;
+    launch_unfold(ctx.stream, ctx.ws, s0, last ? out : s1, pre, op.n[a], post,
+                  last ? diag : nullptr, last ? in : nullptr, last ? sigma : 0.0, v.cplx);
+  }
+}
+
 void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
                    SepKind kind, double shift, double dt, const double* diag, double sigma) {
+  if (op.folded) {
+    sep_transform_folded(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
+    return;
+  }
   if (use_fused_small(op)) {
     sep_transform_fused_small(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
     return;
@@ -554,11 +629,73 @@ int kronop_op_create(kronop_ctx* ctx, int d, const int* n, const double* const* 
   });
 }
 
+int kronop_op_create_folded(kronop_ctx* ctx, int d, const int* n, const double* const* fe,
+                            const double* const* fo, const double* const* be,
+                            const double* const* bo, const double* const* lambda_even,
+                            const double* const* lambda_odd, const double* const* ground,
+                            const double* const* mass, double shift, kronop_op** out) {
+  return guard([&] {
+    param_check(ctx && n && fe && fo && be && bo && lambda_even && lambda_odd && ground && out,
+                "SeparableOperator(folded): null argument");
+    param_check(d >= 1 && d <= KRONOP_MAX_DIM, "SeparableOperator: need at least one axis");
+    auto* op = new kronop_op();
+    try {
+      op->ctx = ctx;
+      op->d = d;
+      op->N = 1;
+      op->shift = shift;
+      op->has_mass = mass != nullptr;
+      op->folded = true;
+      double lmin = 0.0, lmax = 0.0;
+      for (int a = 0; a < d; ++a) {
+        const int na = n[a], ne = na - na / 2, no = na / 2;
+        param_check(na >= 1 && fe[a] && be[a] && lambda_even[a] && lambda_odd[a] && ground[a] &&
+                        (no == 0 || (fo[a] && bo[a])),
+                    "SeparableOperator(folded): bad axis");
+        op->n[a] = na;
+        op->ne[a] = ne;
+        op->no[a] = no;
+        op->N *= na;
+        // eigenvalues in folded order [even | odd], matching the transformed layout
+        op->hlam[a].assign(lambda_even[a], lambda_even[a] + ne);
+        op->hlam[a].insert(op->hlam[a].end(), lambda_odd[a], lambda_odd[a] + no);
+        op->lda_e[a] = upload_padded(*ctx, fe[a], ne, ne, &op->fe[a], true);
+        upload_padded(*ctx, be[a], ne, ne, &op->be[a], true);
+        if (no) {
+          op->lda_o[a] = upload_padded(*ctx, fo[a], no, no, &op->fo[a], true);
+          upload_padded(*ctx, bo[a], no, no, &op->bo[a], true);
+        }
+        KCUDA(cudaMalloc(&op->lam[a], na * sizeof(double)));
+        KCUDA(cudaMemcpy(op->lam[a], op->hlam[a].data(), na * sizeof(double),
+                         cudaMemcpyHostToDevice));
+        KCUDA(cudaMalloc(&op->bwd[a], na * sizeof(double)));  // ground-state column only
+        KCUDA(cudaMemcpy(op->bwd[a], ground[a], na * sizeof(double), cudaMemcpyHostToDevice));
+        lmin += *std::min_element(op->hlam[a].begin(), op->hlam[a].end());
+        lmax += *std::max_element(op->hlam[a].begin(), op->hlam[a].end());
+        if (mass) {
+          param_check(mass[a] != nullptr, "SeparableOperator: mass vector missing");
+          op->hmass[a].assign(mass[a], mass[a] + na);
+          KCUDA(cudaMalloc(&op->mass[a], na * sizeof(double)));
+          KCUDA(cudaMemcpy(op->mass[a], mass[a], na * sizeof(double), cudaMemcpyHostToDevice));
+        }
+      }
+      op->lmin = lmin;
+      op->lmax = lmax;
+    } catch (...) {
+      kronop_op_destroy(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
 int kronop_op_destroy(kronop_op* op) {
   return guard([&] {
     if (!op) return;
     if (op->ctx) cudaStreamSynchronize(op->ctx->stream);
     for (int a = 0; a < KRONOP_MAX_DIM; ++a) {
+      for (double* p : {op->fe[a], op->fo[a], op->be[a], op->bo[a]})
+        if (p) cudaFree(p);
       if (op->fwd[a]) cudaFree(op->fwd[a]);
       if (op->bwd[a]) cudaFree(op->bwd[a]);
       if (op->lam[a]) cudaFree(op->lam[a]);
@@ -645,6 +782,7 @@ int kronop_op_pass(kronop_ctx* ctx, const kronop_op* op, int axis, int forward, 
   return guard([&] {
     param_check(ctx && op && in && out && in != out, "op_pass: bad argument");
     param_check(axis >= 0 && axis < op->d, "op_pass: axis out of range");
+    param_check(!op->folded, "op_pass: not available on a folded operator");
     View v = make_view(op->d, op->n, is_complex);
     EpiParams ep;
     run_pass(*ctx, in, out, v, axis + v.cplx, forward ? op->fwd[axis] : op->bwd[axis],
@@ -658,6 +796,7 @@ int kronop_op_pass_ex(kronop_ctx* ctx, const kronop_op* op, int axis, int forwar
   return guard([&] {
     param_check(ctx && op && in && out && in != out, "op_pass: bad argument");
     param_check(axis >= 0 && axis < op->d, "op_pass: axis out of range");
+    param_check(!op->folded, "op_pass: not available on a folded operator");
     param_check(epilogue >= KRONOP_EPI_STORE && epilogue <= KRONOP_EPI_AXPY_DIAG,
                 "op_pass: bad epilogue");
     View v = make_view(op->d, op->n, is_complex);
@@ -714,7 +853,7 @@ static void host_roundtrip(kronop_ctx* ctx, const kronop_op* op, const double* i
   if (kind == SEP_SOLVE) check_solve_shift(*ctx, *op, op->shift);
   const int d = op->d;
   const int nz = op->n[d - 1];
-  if (d < 2 || nz < 2) {
+  if (d < 2 || nz < 2 || op->folded) {
     KCUDA(cudaMemcpyAsync(ctx->io[0], in_host, nd * sizeof(double), cudaMemcpyHostToDevice,
                           ctx->stream));
     sep_transform(*ctx, *op, ctx->io[0], ctx->io[1], cplx, kind, op->shift, dt, nullptr, 0.0);
@@ -877,6 +1016,23 @@ int kronop_host_sym_eig(int n, const double* a, double* eigenvalues, double* q) 
     kronop_host::sym_eig(n, a, lam, qq);
     std::copy(lam.begin(), lam.end(), eigenvalues);
     std::copy(qq.begin(), qq.end(), q);
+  });
+}
+
+int kronop_host_build_sem_axis_folded(double half_width, int cell_count, int degree,
+                                      const double* fvals, double* lambda_even,
+                                      double* lambda_odd, double* fe, double* fo, double* be,
+                                      double* bo, double* ground) {
+  return guard([&] {
+    const auto b = kronop_host::assemble_sem(half_width, cell_count, degree);
+    const auto f = kronop_host::build_sem_axis_folded(b, fvals);
+    std::copy(f.lam_e.begin(), f.lam_e.end(), lambda_even);
+    std::copy(f.lam_o.begin(), f.lam_o.end(), lambda_odd);
+    std::copy(f.fe.begin(), f.fe.end(), fe);
+    std::copy(f.be.begin(), f.be.end(), be);
+    if (fo) std::copy(f.fo.begin(), f.fo.end(), fo);
+    if (bo) std::copy(f.bo.begin(), f.bo.end(), bo);
+    std::copy(f.g0.begin(), f.g0.end(), ground);
   });
 }
 

@@ -45,6 +45,15 @@ struct kronop_op {
   std::vector<double> hlam[KRONOP_MAX_DIM];
   std::vector<double> hmass[KRONOP_MAX_DIM];
   double shift = 0.0, lmin = 0.0, lmax = 0.0;
+  // even/odd folded operator (kronop_op_create_folded): per axis the half-size blocks; lam[a] is
+  // in folded order [even modes | odd modes]; bwd[a] holds the ground-state column only.
+  bool folded = false;
+  int ne[KRONOP_MAX_DIM] = {}, no[KRONOP_MAX_DIM] = {};
+  double* fe[KRONOP_MAX_DIM] = {};
+  double* fo[KRONOP_MAX_DIM] = {};
+  double* be[KRONOP_MAX_DIM] = {};
+  double* bo[KRONOP_MAX_DIM] = {};
+  int lda_e[KRONOP_MAX_DIM] = {}, lda_o[KRONOP_MAX_DIM] = {};
 };
 
 namespace kronop_dev {

@@ -464,4 +464,121 @@ AxisFactor build_sem_axis(const SemBasis& basis, const double* fvals) {  // axis
   return out;
 }
 
+// ---------------------------------------------------------------- even/odd folding --
+FoldedAxis build_sem_axis_folded(const SemBasis& basis, const double* fvals) {
+  const int n = basis.size();
+  const double L = basis.half_width;
+  auto S = [&](int i, int j) { return basis.stiffness[i + static_cast<size_t>(n) * j]; };
+  double smax = 0.0, fmax = 0.0, mmax = 0.0;
+  for (int i = 0; i < n; ++i) {
+    fmax = std::max(fmax, std::abs(fvals[i]));
+    mmax = std::max(mmax, basis.mass[i]);
+    for (int j = 0; j < n; ++j) smax = std::max(smax, std::abs(S(i, j)));
+  }
+  for (int i = 0; i < n; ++i) {
+    const int r = n - 1 - i;
+    if (std::abs(basis.nodes[i] + basis.nodes[r]) > 1e-12 * L ||
+        std::abs(basis.mass[i] - basis.mass[r]) > 1e-12 * mmax ||
+        std::abs(fvals[i] - fvals[r]) > 1e-12 * std::max(fmax, 1e-300))
+      throw Error(KRONOP_EPARAM, "build_sem_axis_folded: axis is not mirror symmetric");
+    for (int j = 0; j < n; ++j)
+      if (std::abs(S(i, j) - S(r, n - 1 - j)) > 1e-12 * smax)
+        throw Error(KRONOP_EPARAM, "build_sem_axis_folded: stiffness is not persymmetric");
+  }
+  // symmetrised axis operator A = M^{-1/2} S M^{-1/2} + diag(f) (axis.cpp:55-66)
+  std::vector<double> sq(n), isq(n);
+  for (int i = 0; i < n; ++i) {
+    sq[i] = std::sqrt(basis.mass[i]);
+    isq[i] = 1.0 / sq[i];
+  }
+  auto A = [&](int i, int j) {
+    double a = isq[i] * S(i, j) * isq[j];
+    if (i == j) a += fvals[i];
+    return a;
+  };
+  FoldedAxis fa;
+  fa.n = n;
+  fa.no = n / 2;
+  fa.ne = n - fa.no;
+  const int no = fa.no, ne = fa.ne;
+  const bool odd_n = (n % 2) == 1;
+  const int mid = no;  // index of the middle node when n is odd
+  const double r2 = std::sqrt(2.0), ir2 = 1.0 / std::sqrt(2.0);
+  // blocks in the orthonormal bases (e_i +- e_{n-1-i})/sqrt2 (+ e_mid)
+  std::vector<double> ae(static_cast<size_t>(ne) * ne), ao(static_cast<size_t>(no) * no);
+  for (int j = 0; j < no; ++j)
+    for (int i = 0; i < no; ++i) {
+      const double a = A(i, j), b = A(i, n - 1 - j);
+      ae[i + static_cast<size_t>(ne) * j] = a + b;
+      ao[i + static_cast<size_t>(no) * j] = a - b;
+    }
+  if (odd_n) {
+    for (int i = 0; i < no; ++i) {
+      ae[i + static_cast<size_t>(ne) * (ne - 1)] = r2 * A(i, mid);
+      ae[(ne - 1) + static_cast<size_t>(ne) * i] = r2 * A(mid, i);
+    }
+    ae[(ne - 1) + static_cast<size_t>(ne) * (ne - 1)] = A(mid, mid);
+  }
+  // symmetrise exactly (rounding of a + b vs b + a is already symmetric; guard anyway)
+  for (int j = 0; j < ne; ++j)
+    for (int i = 0; i < j; ++i) {
+      const double v = 0.5 * (ae[i + static_cast<size_t>(ne) * j] + ae[j + static_cast<size_t>(ne) * i]);
+      ae[i + static_cast<size_t>(ne) * j] = ae[j + static_cast<size_t>(ne) * i] = v;
+    }
+  std::vector<double> y, z;
+  sym_eig(ne, ae.data(), fa.lam_e, y);
+  if (no > 0) sym_eig(no, ao.data(), fa.lam_o, z);
+  // full-length eigenvector components of block row i (i < no: mirrored pair, i == mid)
+  auto ye = [&](int i, int k) { return y[i + static_cast<size_t>(ne) * k]; };
+  auto zo = [&](int i, int k) { return z[i + static_cast<size_t>(no) * k]; };
+  // sign rule on the full vector (axis.cpp:44-52): first |q_i| >= (1-1e-8) max|q| is positive.
+  // For an even/odd vector the first such index lies in the first half (or is the middle node).
+  for (int k = 0; k < ne; ++k) {
+    double mx = 0.0;
+    for (int i = 0; i < no; ++i) mx = std::max(mx, std::abs(ye(i, k)) * ir2);
+    if (odd_n) mx = std::max(mx, std::abs(ye(mid, k)));
+    double first = 0.0;
+    for (int i = 0; i < no && first == 0.0; ++i)
+      if (std::abs(ye(i, k)) * ir2 >= (1.0 - 1e-8) * mx) first = ye(i, k);
+    if (first == 0.0 && odd_n) first = ye(mid, k);
+    if (first < 0.0)
+      for (int i = 0; i < ne; ++i) y[i + static_cast<size_t>(ne) * k] = -y[i + static_cast<size_t>(ne) * k];
+  }
+  for (int k = 0; k < no; ++k) {
+    double mx = 0.0;
+    for (int i = 0; i < no; ++i) mx = std::max(mx, std::abs(zo(i, k)));
+    for (int i = 0; i < no; ++i)
+      if (std::abs(zo(i, k)) >= (1.0 - 1e-8) * mx) {
+        if (zo(i, k) < 0.0)
+          for (int t = 0; t < no; ++t) z[t + static_cast<size_t>(no) * k] = -z[t + static_cast<size_t>(no) * k];
+        break;
+      }
+  }
+  // forward: w_k = sum_i q_k(i) sqrt(m_i) x_i  ->  Fe[k][i] (on u), Fo[k][i] (on v), column-major
+  fa.fe.assign(static_cast<size_t>(ne) * ne, 0.0);
+  fa.be.assign(static_cast<size_t>(ne) * ne, 0.0);
+  for (int k = 0; k < ne; ++k) {
+    for (int i = 0; i < no; ++i) {
+      fa.fe[k + static_cast<size_t>(ne) * i] = ye(i, k) * ir2 * sq[i];
+      fa.be[i + static_cast<size_t>(ne) * k] = ye(i, k) * ir2 * isq[i];
+    }
+    if (odd_n) {
+      fa.fe[k + static_cast<size_t>(ne) * mid] = ye(mid, k) * sq[mid];
+      fa.be[mid + static_cast<size_t>(ne) * k] = ye(mid, k) * isq[mid];
+    }
+  }
+  fa.fo.assign(static_cast<size_t>(no) * no, 0.0);
+  fa.bo.assign(static_cast<size_t>(no) * no, 0.0);
+  for (int k = 0; k < no; ++k)
+    for (int i = 0; i < no; ++i) {
+      fa.fo[k + static_cast<size_t>(no) * i] = zo(i, k) * ir2 * sq[i];
+      fa.bo[i + static_cast<size_t>(no) * k] = zo(i, k) * ir2 * isq[i];
+    }
+  // ground state column of T: the lowest even mode (the global minimum of a symmetric problem)
+  fa.g0.assign(n, 0.0);
+  for (int i = 0; i < no; ++i) fa.g0[i] = fa.g0[n - 1 - i] = ye(i, 0) * ir2 * isq[i];
+  if (odd_n) fa.g0[mid] = ye(mid, 0) * isq[mid];
+  return fa;
+}
+
 }  // namespace kronop_host

@@ -37,6 +37,21 @@ struct AxisFactor {  // axis.hpp:23-29 (AxisEigens)
   std::vector<double> inverse_transform;  // T^{-1}
 };
 
+// Even/odd folding of a mirror-symmetric axis (symmetric nodes and mass, persymmetric stiffness,
+// even potential): the axis operator commutes with the reversal J, so its eigenvectors are even
+// or odd and each transform splits into two half-size blocks acting on
+//   u_i = x_i + x_{n-1-i} (i < no), u_mid = x_mid (n odd)   and   v_i = x_i - x_{n-1-i}.
+// Folded layout along the axis: [u (ne entries) | v (no entries)], ne = ceil(n/2), no = floor(n/2).
+struct FoldedAxis {
+  int n = 0, ne = 0, no = 0;
+  std::vector<double> lam_e, lam_o;  // eigenvalues of the even / odd modes (ascending each)
+  std::vector<double> fe, fo;        // forward blocks: w_e = Fe u (ne x ne), w_o = Fo v (no x no)
+  std::vector<double> be, bo;        // backward blocks: e = Be w_e, o = Bo w_o; x = unfold(e, o)
+  std::vector<double> g0;            // full-length lowest eigenvector column of T (ground state)
+};
+// Throws KRONOP_EPARAM when the axis is not mirror symmetric to 1e-12 (relative).
+FoldedAxis build_sem_axis_folded(const SemBasis& basis, const double* fvals);
+
 void legendre_pair(int k, double x, double& p, double& dp);
 void gauss_legendre(int m, std::vector<double>& nodes, std::vector<double>& weights);
 GllRule gll_rule(int degree);

@@ -71,6 +71,11 @@ struct EpiParams {
 struct PassShape {
   long long pre = 1, post = 1;
   int nk = 0, m = 0;
+  // q-strides of X and Y (doubles). 0 = dense (pre * nk, pre * m); larger values address a
+  // sub-range of a longer axis (the even/odd halves of a folded axis).
+  long long ldx = 0, ldy = 0;
+  long long ldx_eff() const { return ldx ? ldx : pre * nk; }
+  long long ldy_eff() const { return ldy ? ldy : pre * m; }
 };
 
 // Launch one pass. a_pad: device matrix, column-major with leading dimension lda >= pad_up(m,128),

@@ -99,16 +99,17 @@ struct KArgs {
   const double* a;
   int lda;
   long long pre, post, R;  // R = pre * post rows
+  long long ldx, ldy;      // q-strides of X and Y
   int nk, m;
   int ntiles_n;
   long long ntiles_m;
   EpiParams ep;
 };
 
-__device__ __forceinline__ long long x_row_base(long long r, long long pre, int nk) {
-  // X(r, j) lives at x_row_base(r) + pre * j (r = p + pre * q flattened).
+__device__ __forceinline__ long long x_row_base(long long r, long long pre, long long ldx) {
+  // X(r, j) lives at x_row_base(r) + pre * j (r = p + pre * q flattened; ldx = q-stride).
   const long long q = r / pre;
-  return (r - q * pre) + q * pre * nk;
+  return (r - q * pre) + q * ldx;
 }
 
 template <int BN, int LOADER, int VEC>
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) mode_product_kernel(const KArgs a
     const long long grow = row0 + r;
     xrow_ok[s] = grow < R;
     const long long gr = xrow_ok[s] ? grow : 0;
-    xoff[s] = LOADER == LD_CONTIG ? gr * nk : x_row_base(gr, pre, nk);
+    xoff[s] = LOADER == LD_CONTIG ? gr * args.ldx : x_row_base(gr, pre, args.ldx);
     xk[s] = k;
     xsm[s] = LOADER == LD_CONTIG ? r * XL::STRIDE + k : k * XL::STRIDE + r;
   }
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) mode_product_kernel(const KArgs a
   // ---------------------------------------------------------------- epilogue --
   const EpiParams& ep = args.ep;
   const int m = args.m;
-  const long long mstride = pre * m;  // output row base: (r % pre) + pre*m*(r / pre)
+  const long long mstride = args.ldy;  // output row base: (r % pre) + ldy*(r / pre)
 #pragma unroll
   for (int rb = 0; rb < TC::RB; ++rb) {
     const long long r = row0 + wm * TC::WTM + rb * 8 + g;
@@ -364,6 +365,8 @@ void launch_mode_product(cudaStream_t s, const double* x, double* y, const doubl
   ka.R = ps.pre * ps.post;
   ka.nk = ps.nk;
   ka.m = ps.m;
+  ka.ldx = ps.ldx_eff();
+  ka.ldy = ps.ldy_eff();
   ka.ep = ep;
   const int bn = ps.m > 64 ? 128 : 64;
   ka.ntiles_n = (ps.m + bn - 1) / bn;
@@ -372,10 +375,10 @@ void launch_mode_product(cudaStream_t s, const double* x, double* y, const doubl
   int loader, vec;
   if (ps.pre == 1) {
     loader = LD_CONTIG;
-    vec = (x16 && ps.nk % 2 == 0) ? 2 : 1;
+    vec = (x16 && ps.ldx_eff() % 2 == 0) ? 2 : 1;
   } else {
     loader = ps.pre >= 32 ? LD_STRIDED_R : LD_STRIDED_K;
-    vec = (x16 && ps.pre % 2 == 0) ? 2 : 1;
+    vec = (x16 && ps.pre % 2 == 0 && ps.ldx_eff() % 2 == 0) ? 2 : 1;
   }
   if (ep.kind == EPI_SPEC_PHASE)
     param_check(ep.cplx && ps.pre % 2 == 0, "mode_product: phase epilogue needs complex data");

@@ -119,6 +119,7 @@ struct TArgs {
   double* y;
   int x2d;  // STRIDED with post == 1: X is the 2-D (pre x nk) tensor map
   long long pre, post, R;
+  long long ldy;  // q-stride of Y
   int nk, m;
   int ntiles_n;
   long long ntiles_m;
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const long long rr = rok ? r : 0;
       const long long q = rr / pre;
       const long long p = rr - q * pre;
-      const long long ybase = p + q * pre * m;
+      const long long ybase = p + q * args.ldy;
       const double lam_lo = spectral ? lambda_partial_low_ext(ep, p, ep.axis) : 0.0;
 #pragma unroll
       for (int jc = 0; jc < C::CT; ++jc) {
@@ -423,8 +424,9 @@ void prime_mode_product_tma_kernels() {
 bool mode_product_tma_eligible(const double* x, const PassShape& ps) {
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
   if (ps.pre * ps.post > 0x7fffffffLL) return false;  // TMA coordinates are 32-bit
-  if (ps.pre == 1) return ps.nk % 2 == 0;             // row stride nk * 8 must be 16-B aligned
-  if (ps.pre == 2) return true;                       // complex axis 0 (TL_CPLX0), rows of 2nk
+  if (ps.ldx_eff() % 2 != 0) return false;           // q-stride * 8 must be 16-B aligned
+  if (ps.pre == 1) return true;                       // CONTIG: row stride ldx
+  if (ps.pre == 2) return true;                       // complex axis 0 (TL_CPLX0), rows of ldx
   if (ps.pre % 2 != 0) return false;                  // k stride pre * 8 must be 16-B aligned
   return ps.post == 1 || ps.pre % 16 == 0;            // a 16-row box never straddles two q
 }
@@ -437,6 +439,7 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
   ta.pre = ps.pre;
   ta.post = ps.post;
   ta.R = ps.pre * ps.post;
+  ta.ldy = ps.ldy_eff();
   ta.nk = ps.nk;
   ta.m = ps.m;
   ta.ep = ep;
@@ -456,12 +459,12 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
   if (cplx0) {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * ps.nk),
                                 static_cast<cuuint64_t>(ps.post)};
-    const cuuint64_t str[1] = {static_cast<cuuint64_t>(2 * ps.nk) * 8};
+    const cuuint64_t str[1] = {static_cast<cuuint64_t>(ps.ldx_eff()) * 8};
     const cuuint32_t box[2] = {16, BM / 2};
     encode(&tmx, x, 2, dims, str, box);
   } else if (contig) {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ps.nk), static_cast<cuuint64_t>(ta.R)};
-    const cuuint64_t str[1] = {static_cast<cuuint64_t>(ps.nk) * 8};
+    const cuuint64_t str[1] = {static_cast<cuuint64_t>(ps.ldx_eff()) * 8};
     const cuuint32_t box[2] = {16, BM};
     encode(&tmx, x, 2, dims, str, box);
   } else if (ps.post == 1) {
@@ -474,7 +477,7 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(ps.pre), static_cast<cuuint64_t>(ps.nk),
                                 static_cast<cuuint64_t>(ps.post)};
     const cuuint64_t str[2] = {static_cast<cuuint64_t>(ps.pre) * 8,
-                               static_cast<cuuint64_t>(ps.pre) * ps.nk * 8};
+                               static_cast<cuuint64_t>(ps.ldx_eff()) * 8};
     const cuuint32_t box[3] = {16, BK, 1};
     encode(&tmx, x, 3, dims, str, box);
   }

@@ -364,4 +364,103 @@ void launch_sub(cudaStream_t s, Workspace& ws, double* y, const double* x, const
   KCUDA(cudaGetLastError());
 }
 
+// --------------------------------------------------------------- even/odd folding --
+// Element (p, i, q) at p + pre * (i + n * q). Rows (i, q) are walked by blocks when pre is wide
+// (threads over p, coalesced); for pre < 32 a block walks whole q-slabs of pre * n contiguous
+// doubles (i = e / pre with a small divisor).
+__device__ __forceinline__ double fold_value(const double* x, long long base, long long pre, int n,
+                                             int i) {
+  const int no = n / 2, ne = n - no;
+  if (i < no) return __dadd_rn(x[base + pre * i], x[base + pre * (n - 1 - i)]);
+  if (i < ne) return x[base + pre * i];  // middle node (n odd)
+  const int j = i - ne;
+  return __dsub_rn(x[base + pre * j], x[base + pre * (n - 1 - j)]);
+}
+__device__ __forceinline__ double unfold_value(const double* z, long long base, long long pre,
+                                               int n, int i) {
+  const int no = n / 2, ne = n - no;
+  if (i < no) return __dadd_rn(z[base + pre * i], z[base + pre * (ne + i)]);
+  const int j = n - 1 - i;
+  if (j < no) return __dsub_rn(z[base + pre * j], z[base + pre * (ne + j)]);
+  return z[base + pre * no];  // middle node
+}
+
+template <bool UNFOLD>
+__global__ void k_fold_wide(const double* __restrict__ x, double* __restrict__ y, long long pre,
+                            int n, long long post, const double* diag, const double* u,
+                            double sigma, int cplx) {
+  const long long rows = static_cast<long long>(n) * post;
+  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+    const long long q = row / n;
+    const int i = static_cast<int>(row - q * n);
+    const long long base = pre * n * q;
+    for (long long p = threadIdx.x; p < pre; p += blockDim.x) {
+      double v = UNFOLD ? unfold_value(x, base + p, pre, n, i) : fold_value(x, base + p, pre, n, i);
+      const long long yi = base + p + pre * i;
+      if (UNFOLD && (diag || sigma != 0.0)) {
+        const double uu = u[yi];
+        if (diag) v = __dadd_rn(v, __dmul_rn(diag[cplx ? (yi >> 1) : yi], uu));
+        if (sigma != 0.0) v = __dsub_rn(v, __dmul_rn(sigma, uu));
+      }
+      y[yi] = v;
+    }
+  }
+}
+
+template <bool UNFOLD>
+__global__ void k_fold_narrow(const double* __restrict__ x, double* __restrict__ y, int pre, int n,
+                              long long post, const double* diag, const double* u, double sigma,
+                              int cplx) {
+  const int span = pre * n;
+  for (long long q = blockIdx.x; q < post; q += gridDim.x) {
+    const long long base = static_cast<long long>(span) * q;
+    for (int e = threadIdx.x; e < span; e += blockDim.x) {
+      const int i = pre == 1 ? e : pre == 2 ? (e >> 1) : e / pre;
+      const int p = e - i * pre;
+      double v = UNFOLD ? unfold_value(x, base + p, pre, n, i) : fold_value(x, base + p, pre, n, i);
+      const long long yi = base + e;
+      if (UNFOLD && (diag || sigma != 0.0)) {
+        const double uu = u[yi];
+        if (diag) v = __dadd_rn(v, __dmul_rn(diag[cplx ? (yi >> 1) : yi], uu));
+        if (sigma != 0.0) v = __dsub_rn(v, __dmul_rn(sigma, uu));
+      }
+      y[yi] = v;
+    }
+  }
+}
+
+static void launch_fold_impl(cudaStream_t s, Workspace& ws, const double* x, double* y,
+                             long long pre, int n, long long post, const double* diag,
+                             const double* u, double sigma, int cplx, bool unfold) {
+  if (pre >= 32) {
+    const long long rows = static_cast<long long>(n) * post;
+    const unsigned grid = static_cast<unsigned>(rows < 1184 * 4 ? rows : 1184 * 4);
+    const int thr = pre >= 256 ? 256 : 128;
+    if (unfold)
+      k_fold_wide<true><<<grid, thr, 0, s>>>(x, y, pre, n, post, diag, u, sigma, cplx);
+    else
+      k_fold_wide<false><<<grid, thr, 0, s>>>(x, y, pre, n, post, diag, u, sigma, cplx);
+  } else {
+    const unsigned grid = static_cast<unsigned>(post < 1184 * 4 ? post : 1184 * 4);
+    if (unfold)
+      k_fold_narrow<true><<<grid, 256, 0, s>>>(x, y, static_cast<int>(pre), n, post, diag, u,
+                                               sigma, cplx);
+    else
+      k_fold_narrow<false><<<grid, 256, 0, s>>>(x, y, static_cast<int>(pre), n, post, diag, u,
+                                                sigma, cplx);
+  }
+  ws.launches += 1;
+  KCUDA(cudaGetLastError());
+}
+
+void launch_fold(cudaStream_t s, Workspace& ws, const double* x, double* y, long long pre, int n,
+                 long long post) {
+  launch_fold_impl(s, ws, x, y, pre, n, post, nullptr, nullptr, 0.0, 0, false);
+}
+
+void launch_unfold(cudaStream_t s, Workspace& ws, const double* z, double* y, long long pre, int n,
+                   long long post, const double* diag, const double* u, double sigma, int cplx) {
+  launch_fold_impl(s, ws, z, y, pre, n, post, diag, u, sigma, cplx, true);
+}
+
 }  // namespace kronop_dev

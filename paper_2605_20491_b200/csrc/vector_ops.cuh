@@ -51,5 +51,13 @@ void launch_axpby(cudaStream_t s, Workspace& ws, double* y, const double* x, dou
                   long long n);
 void launch_sub(cudaStream_t s, Workspace& ws, double* y, const double* x, const double* b,
                 long long n);
+// Even/odd fold / unfold along one real-view axis of extent n (pre below, post above):
+// fold: [u_i = x_i + x_{n-1-i}, u_mid = x_mid | v_i = x_i - x_{n-1-i}];
+// unfold: x_i = e_i + o_i, x_{n-1-i} = e_i - o_i, x_mid = e_mid, then optionally
+// y = (y + diag .* u) - sigma u (FullOperator / shifted map epilogue).
+void launch_fold(cudaStream_t s, Workspace& ws, const double* x, double* y, long long pre, int n,
+                 long long post);
+void launch_unfold(cudaStream_t s, Workspace& ws, const double* z, double* y, long long pre, int n,
+                   long long post, const double* diag, const double* u, double sigma, int cplx);
 
 }  // namespace kronop_dev

@@ -159,6 +159,30 @@ int main() {
                 exact, r.outer_iterations);
   }
 
+  // test_gpe.cpp — H1 and a_u flows agree (acceptance.cpp:397-401 criterion 8c, small grid)
+  {
+    const Basis1D b = assemble_sem(8.0, 2, 12);
+    auto mass = std::make_shared<MassWeights>(MassWeights{b.mass, b.mass, b.mass});
+    const auto f = [](double x) { return x * x + 100.0 * std::pow(std::sin(M_PI * x / 4.0), 2); };
+    std::vector<AxisEigens> axes(3, build_axis(b, f));
+    std::vector<AxisEigens> lap_axes(3, build_axis(b, [](double) { return 0.0; }));
+    SeparableOperator sep(ctx, axes, 0.0, mass), lap(ctx, lap_axes, 0.0, mass);
+    const int n = b.size();
+    GpeProblem prob{FullOperator{&sep, nullptr}, &lap, 10.0};
+    GpeFlowConfig cfg;
+    cfg.energy_rel_tol = 1e-13;
+    DeviceField<double> s1(ctx, Shape{n, n, n}), s2(ctx, Shape{n, n, n});
+    const GpeResult h1 = gpe_gradient_flow(prob, cfg, s1);
+    cfg.kind = GpeFlowKind::AdaptiveMetric;
+    cfg.step = 1.0;
+    const GpeResult au = gpe_gradient_flow(prob, cfg, s2);
+    CHECK(h1.converged && au.converged);
+    CHECK(std::abs(h1.energy - au.energy) <= 1e-10 * std::abs(h1.energy));
+    CHECK(std::abs(gpe_energy(prob, s1) - h1.energy) <= 1e-12 * std::abs(h1.energy));
+    std::printf("ok gpe h1 E=%.12f (%d its), a_u E=%.12f (%d its)\n", h1.energy, h1.iterations,
+                au.energy, au.iterations);
+  }
+
   // errors.hpp: ParameterError on bad input through the C-ABI
   {
     bool threw = false;

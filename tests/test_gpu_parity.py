@@ -509,3 +509,79 @@ def test_slab_operator_single_rank_on_gpu(ctx):
     rep = A.pcg(A.apply_map(op, v2), A.solve_map(op), u, torch.zeros_like(u),
                 A.PcgConfig(rel_tol=1e-10))
     assert conv and it == rep.iterations
+
+
+# ------------------------------------------------------------------ even/odd folding --
+@pytest.mark.parametrize("spec", [(8.0, 4, 7, 3), (8.0, 3, 5, 3), (2.0, 3, 4, 2), (1.5, 5, 6, 1),
+                                  (8.0, 13, 5, 3), (8.0, 37, 7, 3), (1.0, 1, 3, 4), (8.0, 3, 3, 6)])
+def test_folded_operator_matches_unfolded(ctx, spec):
+    """The even/odd folded operator (kronop_op_create_folded) is the same operator as the dense
+    one: apply / solve / propagate / FullOperator apply agree to 1e-12 on real and complex
+    fields (odd and even extents, the n = 2 and 1-D edge cases, the fused-small regime)."""
+    A = api()
+    grid = A.Grid.sem(*spec)
+    f = [lambda t: t * t] * grid.dim
+    op = grid.separable_operator(ctx, f, 0.5)
+    fo = grid.separable_operator(ctx, f, 0.5, folded=True)
+    n = grid.node_count()
+    u = dev(K.uniform_pm1(31, n))
+    psi = dev(K.seeded_complex_field(grid.shape, 32))
+    for a, b in ((fo.apply(u), op.apply(u)), (fo.solve(u), op.solve(u)),
+                 (fo.apply(psi), op.apply(psi)), (fo.solve(psi), op.solve(psi)),
+                 (fo.propagate(psi, 0.11), op.propagate(psi, 0.11)),
+                 (fo.propagate(psi, -1.3), op.propagate(psi, -1.3))):
+        assert rel(host(a), host(b)) < 1e-12
+    v2 = grid.sample(lambda c: 2.0 * np.exp(-sum((ci - 0.3) ** 2 for ci in c)))
+    fa, fb = A.FullOperator(fo, dev(v2)), A.FullOperator(op, dev(v2))
+    assert rel(host(fa.apply(u, sigma=0.7)), host(fb.apply(u, sigma=0.7))) < 1e-12
+    inplace = psi.clone()
+    fo.propagate(inplace, 0.2, out=inplace)
+    assert rel(host(inplace), host(op.propagate(psi, 0.2))) < 1e-12
+    s0, lo0, hi0 = op.info()
+    s1, lo1, hi1 = fo.info()
+    assert s0 == s1 and abs(lo0 - lo1) <= 1e-12 * abs(hi0) and abs(hi0 - hi1) <= 1e-12 * abs(hi0)
+    assert rel(host(fo.ground_state()), host(op.ground_state())) < 1e-10
+    assert rel(host(fo.solve_host(host(u), np.empty(n))), host(op.solve(u))) < 1e-12
+
+
+def test_folded_operator_pcg_and_inverse_iteration(ctx):
+    """Folded preconditioner inside PCG (stirrer, acceptance.cpp:202-236 instance) and inside
+    inverse iteration (criterion 5): the oracle's iteration counts and values."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, 8, 6, 3)
+    pot = P.build_potential("stirrer", grid)
+    op = grid.separable_operator(ctx, pot.separable, folded=True)
+    b = A.splitmix_uniform(ctx, 1, grid.node_count())
+    x = torch.zeros_like(b)
+    cfg = A.PcgConfig(rel_tol=1e-8, record_history=True)
+    rep = A.pcg(A.apply_map(op, pot.v2_device()), A.solve_map(op), b, x, cfg)
+    kg = K.Grid.sem(8.0, 8, 6, 3)
+    kop = K.build_full_operator(kg, K.build_potential("stirrer", kg))
+    xr = np.zeros(kg.node_count())
+    krep = K.pcg(kop.apply, kop.sep.solve, K.seeded_field(kg.shape, 1), xr,
+                 K.PcgConfig(rel_tol=1e-8, record_history=True))
+    assert rep.converged and rep.iterations == krep.iterations
+    assert np.allclose(rep.history, krep.history, rtol=1e-7, atol=0)
+    assert rel(host(x), xr) < 1e-10
+    grid = A.Grid.sem(8.0, 8, 10, 3)
+    pot = P.build_potential("sep-osc", grid, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    op = grid.separable_operator(ctx, pot.separable, folded=True)
+    init = torch.ones(grid.node_count(), dtype=torch.float64, device="cuda")
+    r = A.inverse_iteration(A.FullOperator(op), A.InverseIterationConfig(), init)
+    assert r.converged
+    kg = K.Grid.sem(8.0, 8, 10, 3)
+    kp = K.build_potential("sep-osc", kg, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
+    kr = K.inverse_iteration(K.FullOperator(kg.separable_operator(kp.separable)),
+                             K.InverseIterationConfig(), np.ones(kg.node_count()), kg.mass)
+    assert abs(r.eigenvalue - kr.eigenvalue) <= 1e-12 * kr.eigenvalue
+
+
+def test_folded_operator_refuses_per_pass_api(ctx):
+    from paper_2605_20491_b200 import ParameterError
+    A = api()
+    grid = A.Grid.sem(2.0, 3, 4, 3)
+    fo = grid.laplacian(ctx, folded=True)
+    u = dev(K.uniform_pm1(3, grid.node_count()))
+    with pytest.raises(ParameterError):
+        fo.transform_pass(u, 0, True)

@@ -142,3 +142,62 @@ def test_host_error_codes():
         A.gauss_legendre(17)
     with pytest.raises(ParameterError):
         A.assemble_sem(-1.0, 3, 2)
+
+
+def _unfold_rows(fa):
+    """Full-length T^-1 (rows = modes in folded order) and T (columns) from the folded blocks."""
+    n, ne, no = fa.n, len(fa.eigenvalues_even), len(fa.eigenvalues_odd)
+    ti = np.zeros((n, n))
+    t = np.zeros((n, n))
+    for i in range(no):
+        ti[:ne, i] = fa.fe[:, i]
+        ti[:ne, n - 1 - i] = fa.fe[:, i]
+        ti[ne:, i] = fa.fo[:, i]
+        ti[ne:, n - 1 - i] = -fa.fo[:, i]
+        t[i, :ne] = fa.be[i, :]
+        t[n - 1 - i, :ne] = fa.be[i, :]
+        t[i, ne:] = fa.bo[i, :]
+        t[n - 1 - i, ne:] = -fa.bo[i, :]
+    if n % 2:
+        ti[:ne, no] = fa.fe[:, no]
+        t[no, :ne] = fa.be[no, :]
+    return t, ti
+
+
+@pytest.mark.parametrize("spec,f", [((8.0, 4, 7), lambda t: t * t),          # n = 29 (odd)
+                                    ((8.0, 3, 5), lambda t: t * t),          # n = 16 (even)
+                                    ((1.0, 8, 10), lambda t: 1600 * np.sin(np.pi * t / 4) ** 2 + 2 * t * t),
+                                    ((2.0, 1, 3), None),                     # n = 2
+                                    ((2.0, 1, 2), lambda t: 3.0)])           # n = 1
+def test_build_axis_folded_reassembles_full_factorisation(spec, f):
+    """The even/odd blocks reassemble a factorisation T diag(L) T^-1 of the same axis operator;
+    the eigenvalues (sorted) equal the unfolded ones and the mode vectors agree with build_axis's
+    (same sign rule) wherever the eigenvalue is simple."""
+    A = api()
+    b = A.assemble_sem(*spec)
+    fa = A.build_axis_folded(b, f)
+    ax = A.build_axis(b, f)
+    n = b.size
+    lam = fa.eigenvalues
+    scale = max(np.abs(ax.eigenvalues).max(), 1.0)
+    assert np.abs(np.sort(lam) - ax.eigenvalues).max() < 1e-12 * scale
+    t, ti = _unfold_rows(fa)
+    assert np.abs(t @ ti - np.eye(n)).max() < 1e-11
+    dense = K.dense_axis_operator(K.assemble_sem(*spec), f or (lambda x: 0.0))
+    assert np.abs(t @ np.diag(lam) @ ti - dense).max() < 1e-11 * scale
+    order = np.argsort(lam, kind="stable")
+    gaps = np.diff(ax.eigenvalues)
+    for r, k in enumerate(order):
+        lo = gaps[r - 1] if r > 0 else np.inf
+        hi = gaps[r] if r < n - 1 else np.inf
+        if min(lo, hi) > 1e-6 * scale:
+            assert np.abs(ti[k] - ax.inverse_transform[r]).max() < 1e-9 * np.abs(ti[k]).max()
+    assert np.abs(fa.ground - ax.transform[:, 0]).max() < 1e-10 * np.abs(fa.ground).max()
+
+
+def test_build_axis_folded_rejects_asymmetric_potential():
+    from paper_2605_20491_b200 import ParameterError
+    A = api()
+    b = A.assemble_sem(2.0, 3, 4)
+    with pytest.raises(ParameterError):
+        A.build_axis_folded(b, lambda t: t * t + 0.1 * t)
