@@ -195,6 +195,37 @@ AxisEigens build_axis(const Basis1D& basis, F&& f) {  // axis.hpp:37
   return a;
 }
 
+struct HermiteBasis {  // hermite.hpp:13-19
+  int size = 0;
+  std::vector<double> nodes, psi_last, mass;
+  std::vector<double> diff;  // n x n column-major
+};
+inline HermiteBasis hermite_basis(int n) {  // hermite.hpp:29
+  if (n < 2) throw ParameterError("hermite_basis: need n >= 2");
+  HermiteBasis b;
+  b.size = n;
+  b.nodes.resize(n);
+  b.psi_last.resize(n);
+  b.mass.resize(n);
+  b.diff.resize(static_cast<std::size_t>(n) * n);
+  check(kronop_host_hermite_basis(n, b.nodes.data(), b.psi_last.data(), b.mass.data(),
+                                  b.diff.data()));
+  return b;
+}
+template <class F>
+AxisEigens build_axis(const HermiteBasis& basis, F&& f) {  // axis.hpp:39
+  const int n = basis.size;
+  std::vector<double> fv(n);
+  for (int i = 0; i < n; ++i) fv[i] = f(basis.nodes[i]);
+  AxisEigens a;
+  a.eigenvalues.resize(n);
+  a.transform.resize(static_cast<std::size_t>(n) * n);
+  a.inverse_transform.resize(static_cast<std::size_t>(n) * n);
+  check(kronop_host_build_hermite_axis(n, fv.data(), a.eigenvalues.data(), a.transform.data(),
+                                       a.inverse_transform.data()));
+  return a;
+}
+
 // ------------------------------------------------------------- operators.hpp:15-62 --
 class SeparableOperator {
  public:

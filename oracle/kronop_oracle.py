@@ -363,6 +363,78 @@ def build_axis(basis: Basis1D, f: Callable[[float], float]) -> AxisEigens:
     return AxisEigens(lam, inv_sqrt_m[:, None] * q, q.T * sqrt_m[None, :])
 
 
+# ------------------------------------------------------------------------ hermite.cpp
+
+@dataclass
+class HermiteBasis:
+    size: int
+    nodes: np.ndarray
+    psi_last: np.ndarray
+    diff: np.ndarray
+    mass: np.ndarray
+
+
+def hermite_basis(n: int) -> HermiteBasis:
+    """Hermite-Gauss collocation (proj/src/hermite.cpp:10-66): Jacobi-matrix nodes (zero diagonal,
+    off-diagonal sqrt(k/2)) symmetrised exactly, psi_{n-1} by the normalised three-term
+    recurrence, D(i,j) = psi_i / (psi_j (x_i - x_j)), mass 1 / (n psi_j^2)."""
+    if n < 2:
+        raise ParameterError("hermite_basis: need n >= 2")
+    if n > 745:
+        raise CapabilityError("hermite_basis: n > 745 underflows the Hermite recurrence in FP64")
+    from scipy.linalg import eigh_tridiagonal
+    sub = np.sqrt(np.arange(1, n) / 2.0)
+    nodes = np.sort(eigh_tridiagonal(np.zeros(n), sub, eigvals_only=True))
+    for i in range(n // 2):
+        j = n - 1 - i
+        xm = 0.5 * (nodes[j] - nodes[i])
+        nodes[i], nodes[j] = -xm, xm
+    if n % 2:
+        nodes[n // 2] = 0.0
+    psi = np.empty(n)
+    for j in range(n):
+        x = float(nodes[j])
+        pk, pkm1 = math.pow(math.pi, -0.25) * math.exp(-x * x / 2.0), 0.0
+        for k in range(n - 1):
+            pk1 = x * math.sqrt(2.0 / (k + 1)) * pk - math.sqrt(k / (k + 1.0)) * pkm1
+            pkm1, pk = pk, pk1
+        if pk == 0.0:
+            raise CapabilityError("hermite_basis: psi_{n-1} underflowed at a node")
+        psi[j] = pk
+    diff = np.zeros((n, n))
+    for i in range(n):
+        for j in range(n):
+            if i != j:
+                diff[i, j] = psi[i] / (psi[j] * (nodes[i] - nodes[j]))
+    mass = 1.0 / (n * psi * psi)
+    return HermiteBasis(n, nodes, psi, diff, mass)
+
+
+def hermite_operator(basis: HermiteBasis, f: Callable[[float], float]):
+    """Symmetrised -D^2 + diag(f) (proj/src/hermite.cpp:68-95): returns (sym, scale = psi)."""
+    n = basis.size
+    x = basis.nodes
+    with np.errstate(divide="ignore"):
+        w = 1.0 / (x[:, None] - x[None, :])
+    np.fill_diagonal(w, 0.0)
+    a = -(w @ w)
+    for j in range(n):
+        fx = f(float(x[j]))
+        if not math.isfinite(fx):
+            raise ParameterError("hermite_operator: f not finite at a node")
+        a[j, j] += fx
+    if np.abs(a - a.T).max() > 1e-8 * np.abs(a).max():
+        raise NumericalError("hermite_operator: symmetrization degraded at n = %d" % n)
+    return 0.5 * (a + a.T), basis.psi_last.copy()
+
+
+def build_hermite_axis(basis: HermiteBasis, f: Callable[[float], float]) -> AxisEigens:
+    """proj/src/axis.cpp:76-84: T = diag(psi) Q, T^{-1} = Q^T diag(1/psi)."""
+    sym, scale = hermite_operator(basis, f)
+    lam, q = sym_eig(sym)
+    return AxisEigens(lam, scale[:, None] * q, q.T * (1.0 / scale)[None, :])
+
+
 # --------------------------------------------------------------------------- grid.cpp
 
 @dataclass
@@ -376,6 +448,13 @@ class Grid:
             raise ParameterError("Grid: dimension must be in [1, 9]")
         b = assemble_sem(half_width, cell_count, degree)
         return Grid([b] * dimension)
+
+    @staticmethod
+    def hermite(n: int, dimension: int) -> "Grid":
+        """Isotropic Hermite grid on R^d (proj/src/grid.cpp:24-32)."""
+        if dimension < 1 or dimension > 9:
+            raise ParameterError("Grid: dimension must be in [1, 9]")
+        return Grid([hermite_basis(n)] * dimension)
 
     @property
     def dim(self) -> int:
@@ -418,7 +497,8 @@ class Grid:
             f = per_axis[a] if per_axis and per_axis[a] is not None else (lambda t: 0.0)
             key = (id(self.axes[a]), tuple(f(float(x)) for x in self.axes[a].nodes))
             if key not in cache:
-                cache[key] = build_axis(self.axes[a], f)
+                build = build_hermite_axis if isinstance(self.axes[a], HermiteBasis) else build_axis
+                cache[key] = build(self.axes[a], f)
             eig.append(cache[key])
         return SeparableOperator(eig, shift)
 
@@ -1144,6 +1224,29 @@ def dense_axis_operator(basis: Basis1D, f) -> np.ndarray:
     h = basis.stiffness / basis.mass[:, None]
     h = h + np.diag([f(float(x)) for x in basis.nodes])
     return h
+
+
+def dense_hermite_axis_operator(basis: HermiteBasis, f) -> np.ndarray:
+    """-D^2 + diag(f) from the Hermite differentiation matrix, unsymmetrised
+    (proj/src/dense_ref.cpp:19-23)."""
+    return -(basis.diff @ basis.diff) + np.diag([f(float(x)) for x in basis.nodes])
+
+
+def clustering_report(sym_axis_ops: Sequence[np.ndarray], v2: np.ndarray, epsilon: float):
+    """Spectrum of I + A^{-1/2} diag(v2) A^{-1/2} (proj/src/dense_ref.cpp:114-147): returns
+    (ascending spectrum, outliers outside (1-eps, 1+eps), mu_max / mu_min)."""
+    total = int(np.prod([op.shape[0] for op in sym_axis_ops]))
+    if total > 5000:
+        raise CapabilityError("clustering_report: N > 5000")
+    a = dense_assemble(sym_axis_ops, None, 0.0)
+    lam, q = np.linalg.eigh(a)
+    if lam[0] <= 0.0:
+        raise ParameterError("clustering_report: A is not positive definite")
+    a_inv_half = (q * (1.0 / np.sqrt(lam))[None, :]) @ q.T
+    b = a_inv_half @ np.diag(v2) @ a_inv_half
+    mu = np.linalg.eigvalsh(0.5 * (b + b.T)) + 1.0
+    outliers = int(np.sum((mu < 1.0 - epsilon) | (mu > 1.0 + epsilon)))
+    return mu, outliers, float(mu[-1] / mu[0])
 
 
 def dense_sym_axis_operator(basis: Basis1D, f) -> np.ndarray:

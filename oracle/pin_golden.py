@@ -147,6 +147,46 @@ def c5():
                       " 2.1e-5, on refinement the oracle reaches it (239^3: see 5_refined_rel_239)"}
 
 
+def c4():
+    """acceptance.cpp:262-289: preconditioned-spectrum clustering for the bump V2 over
+    n in {49, 99} x L in {8, 16}: identical outlier counts, condition numbers within 5%."""
+    trap_f = lambda x: x * x
+    bump = lambda x: 8.0 * np.exp(-(x - 1.0) * (x - 1.0))
+    counts, kappas = [], []
+    for half in (8.0, 16.0):
+        for cells in (2, 4):
+            b = K.assemble_sem(half, cells, 25)
+            v2 = np.array([bump(float(x)) for x in b.nodes])
+            _, out, kappa = K.clustering_report([K.dense_sym_axis_operator(b, trap_f)], v2, 0.1)
+            counts.append(out)
+            kappas.append(kappa)
+    kmin, kmax = min(kappas), max(kappas)
+    return {"4_outliers": counts, "4a_pass": len(set(counts)) == 1, "4_kappa": kappas,
+            "4b_pass": (kmax - kmin) <= 0.05 * kmin}
+
+
+def c6():
+    """acceptance.cpp:310-345: Hermite axes. 1-D oscillator levels {1,3,5,7}; 3-D lambda_1 = 3 by
+    inverse iteration on Grid::hermite(40, 3); 99^3 solve residual with the accuracy potential."""
+    b40 = K.hermite_basis(40)
+    ax = K.build_hermite_axis(b40, lambda x: x * x)
+    worst = float(np.max(np.abs(ax.eigenvalues[:4] - np.array([1.0, 3.0, 5.0, 7.0]))))
+    g = K.Grid.hermite(40, 3)
+    op = K.FullOperator(g.separable_operator([lambda x: x * x] * 3))
+    r = K.inverse_iteration(op, K.InverseIterationConfig(), np.ones(g.node_count()), g.mass)
+    g99 = K.Grid.hermite(99, 3)
+    pot = K.build_potential("sep-osc", g99, osc_amplitude=1600.0, quad_coeffs=[1.0, 2.0, 3.0])
+    h = g99.separable_operator(pot.separable)
+    f = g99.sample(lambda c: np.sin(np.pi / 2 * (c[0] + 1.0)) * np.sin(np.pi * (c[1] + 1.0))
+                   * np.sin(1.5 * np.pi * (c[2] + 1.0))
+                   * np.exp(-(c[0] ** 2 + c[1] ** 2 + c[2] ** 2) / 4.0))
+    u = h.solve(f)
+    res = float(np.linalg.norm(h.apply(u) - f) / np.linalg.norm(f))
+    return {"6_levels_err": worst, "6a_pass": worst <= 1e-9, "6_lambda": r.eigenvalue,
+            "6b_pass": abs(r.eigenvalue - 3.0) <= 1e-9, "6_outer": r.outer_iterations,
+            "6_residual_99": res, "6c_pass": res <= 1e-10}
+
+
 def c7():
     cfg = K.InverseIterationConfig()
     grids = [K.Grid.sem(8.0, 2, 20, 3), K.Grid.sem(8.0, 4, 20, 3)]
@@ -312,7 +352,7 @@ def c13():
     return {"13a_drift": drift, "13a_pass": drift <= 1e-8}
 
 
-CRITERIA = {"1": c1, "2": c2, "3": c3, "5": c5, "7": c7, "8": c8, "9": c9, "10": c10, "11": c11,
+CRITERIA = {"1": c1, "2": c2, "3": c3, "4": c4, "5": c5, "6": c6, "7": c7, "8": c8, "9": c9, "10": c10, "11": c11,
             "12": c12, "13": c13}
 
 

@@ -121,6 +121,8 @@ PROTOTYPES = {
     "kronop_host_interp_matrix": (I, [D, I, I, I, I, DP]),
     "kronop_host_sym_eig": (I, [I, DP, DP, DP]),
     "kronop_host_build_sem_axis": (I, [D, I, I, DP, DP, DP, DP]),
+    "kronop_host_hermite_basis": (I, [I, DP, DP, DP, DP]),
+    "kronop_host_build_hermite_axis": (I, [I, DP, DP, DP, DP]),
     "kronop_host_build_sem_axis_folded": (I, [D, I, I] + [DP] * 8),
     "kronop_splitmix_uniform": (I, [P, C.c_uint64, C.c_uint64, C.c_size_t, P]),
 }

@@ -163,12 +163,39 @@ class AxisEigens:
 _AXIS_CACHE = {}
 
 
-def build_axis(basis: Basis1D, f: Optional[Callable] = None, fvals: Optional[np.ndarray] = None):
-    """build_axis for an SEM basis (axis.cpp:55-74) via the C++ Householder+QL eigensolver."""
+@dataclass
+class HermiteBasis:
+    """Hermite-function collocation axis (hermite.hpp:13-19)."""
+    size: int
+    nodes: np.ndarray
+    psi_last: np.ndarray
+    diff: np.ndarray
+    mass: np.ndarray
+
+
+def hermite_basis(n: int) -> HermiteBasis:
+    """hermite_basis(n) (hermite.cpp:10-66) through the C++ host setup."""
+    nodes, psi, mass, diff = np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(max(n, 1) ** 2)
+    check(lib().kronop_host_hermite_basis(n, _dptr(nodes), _dptr(psi), _dptr(mass), _dptr(diff)))
+    return HermiteBasis(n, nodes, psi, diff.reshape(n, n, order="F"), mass)
+
+
+def build_axis(basis, f: Optional[Callable] = None, fvals: Optional[np.ndarray] = None):
+    """build_axis for an SEM basis (axis.cpp:55-74) or a Hermite basis (axis.cpp:76-84) via the
+    C++ Householder+QL eigensolver."""
     n = basis.size
     if fvals is None:
         fvals = np.array([f(float(x)) for x in basis.nodes]) if f is not None else np.zeros(n)
     fvals = np.ascontiguousarray(fvals, dtype=np.float64)
+    if isinstance(basis, HermiteBasis):
+        key = ("hermite", n, fvals.tobytes())
+        if key not in _AXIS_CACHE:
+            lam, t, ti = np.zeros(n), np.zeros(n * n), np.zeros(n * n)
+            check(lib().kronop_host_build_hermite_axis(n, _dptr(fvals), _dptr(lam), _dptr(t),
+                                                       _dptr(ti)))
+            _AXIS_CACHE[key] = AxisEigens(lam, t.reshape(n, n, order="F"),
+                                          ti.reshape(n, n, order="F"))
+        return _AXIS_CACHE[key]
     key = (basis.half_width, basis.cell_count, basis.degree, fvals.tobytes())
     if key in _AXIS_CACHE:
         return _AXIS_CACHE[key]
@@ -206,6 +233,8 @@ class FoldedAxis:
 def build_axis_folded(basis: Basis1D, f: Optional[Callable] = None,
                       fvals: Optional[np.ndarray] = None) -> FoldedAxis:
     """Folded build_axis for a symmetric SEM axis and an even potential (ParameterError otherwise)."""
+    if not isinstance(basis, Basis1D):
+        raise L.ParameterError(L.KRONOP_EPARAM, "build_axis_folded: SEM axes only")
     n = basis.size
     if fvals is None:
         fvals = np.array([f(float(x)) for x in basis.nodes]) if f is not None else np.zeros(n)
@@ -486,6 +515,13 @@ class Grid:
             raise L.ParameterError(L.KRONOP_EPARAM, "Grid: dimension must be in [1, 9]")
         b = assemble_sem(half_width, cell_count, degree)
         return Grid([b] * dimension)
+
+    @staticmethod
+    def hermite(n: int, dimension: int) -> "Grid":
+        """Isotropic Hermite collocation grid on R^d (grid.cpp:24-32)."""
+        if dimension < 1 or dimension > 9:
+            raise L.ParameterError(L.KRONOP_EPARAM, "Grid: dimension must be in [1, 9]")
+        return Grid([hermite_basis(n)] * dimension)
 
     @property
     def dim(self):

@@ -1019,6 +1019,27 @@ int kronop_host_sym_eig(int n, const double* a, double* eigenvalues, double* q) 
   });
 }
 
+int kronop_host_hermite_basis(int n, double* nodes, double* psi_last, double* mass, double* diff) {
+  return guard([&] {
+    const auto b = kronop_host::hermite_basis(n);
+    std::copy(b.nodes.begin(), b.nodes.end(), nodes);
+    std::copy(b.psi_last.begin(), b.psi_last.end(), psi_last);
+    std::copy(b.mass.begin(), b.mass.end(), mass);
+    if (diff) std::copy(b.diff.begin(), b.diff.end(), diff);
+  });
+}
+
+int kronop_host_build_hermite_axis(int n, const double* fvals, double* lambda, double* T,
+                                   double* Tinv) {
+  return guard([&] {
+    const auto b = kronop_host::hermite_basis(n);
+    const auto f = kronop_host::build_hermite_axis(b, fvals);
+    std::copy(f.eigenvalues.begin(), f.eigenvalues.end(), lambda);
+    std::copy(f.transform.begin(), f.transform.end(), T);
+    std::copy(f.inverse_transform.begin(), f.inverse_transform.end(), Tinv);
+  });
+}
+
 int kronop_host_build_sem_axis_folded(double half_width, int cell_count, int degree,
                                       const double* fvals, double* lambda_even,
                                       double* lambda_odd, double* fe, double* fo, double* be,

@@ -581,4 +581,95 @@ FoldedAxis build_sem_axis_folded(const SemBasis& basis, const double* fvals) {
   return fa;
 }
 
+// ------------------------------------------------------------------ Hermite axes --
+HermiteAxis hermite_basis(int n) {  // hermite.cpp:10-66
+  if (n < 2) throw Error(KRONOP_EPARAM, "hermite_basis: need n >= 2");
+  if (n > 745)
+    throw Error(KRONOP_ECAPABILITY,
+                "hermite_basis: n > 745 underflows the Hermite recurrence in FP64");
+  HermiteAxis b;
+  b.n = n;
+  // nodes = eigenvalues of the Jacobi matrix (zero diagonal, off-diagonal sqrt(k/2))
+  std::vector<double> v(static_cast<size_t>(n) * n, 0.0), d(n, 0.0), e(n, 0.0);
+  for (int i = 0; i < n; ++i) v[i + static_cast<size_t>(n) * i] = 1.0;
+  for (int k = 1; k < n; ++k) e[k] = std::sqrt(k / 2.0);  // e[i]: coupling of rows i-1 and i
+  tridiagonal_ql(n, v, d, e);
+  std::sort(d.begin(), d.end());
+  b.nodes = d;
+  for (int i = 0; i < n / 2; ++i) {  // symmetrise exactly
+    const int j = n - 1 - i;
+    const double xm = 0.5 * (b.nodes[j] - b.nodes[i]);
+    b.nodes[i] = -xm;
+    b.nodes[j] = xm;
+  }
+  if (n % 2 == 1) b.nodes[n / 2] = 0.0;
+  b.psi_last.resize(n);
+  const double c0 = std::pow(M_PI, -0.25);
+  for (int j = 0; j < n; ++j) {
+    const double x = b.nodes[j];
+    double pk = c0 * std::exp(-x * x / 2.0), pkm1 = 0.0;
+    for (int k = 0; k < n - 1; ++k) {
+      const double pk1 = x * std::sqrt(2.0 / (k + 1)) * pk - std::sqrt(k / (k + 1.0)) * pkm1;
+      pkm1 = pk;
+      pk = pk1;
+    }
+    if (pk == 0.0) throw Error(KRONOP_ECAPABILITY, "hermite_basis: psi_{n-1} underflowed at a node");
+    b.psi_last[j] = pk;
+  }
+  b.diff.assign(static_cast<size_t>(n) * n, 0.0);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i)
+      if (i != j)
+        b.diff[i + static_cast<size_t>(n) * j] =
+            b.psi_last[i] / (b.psi_last[j] * (b.nodes[i] - b.nodes[j]));
+  b.mass.resize(n);
+  for (int j = 0; j < n; ++j) b.mass[j] = 1.0 / (n * b.psi_last[j] * b.psi_last[j]);
+  return b;
+}
+
+AxisFactor build_hermite_axis(const HermiteAxis& basis, const double* fvals) {
+  const int n = basis.n;
+  // a = -(W D W^-1)^2 + diag(f), W D W^-1 = [1 / (x_i - x_j)] (hermite.cpp:75-86)
+  std::vector<double> w(static_cast<size_t>(n) * n, 0.0), a(static_cast<size_t>(n) * n, 0.0);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i)
+      if (i != j) w[i + static_cast<size_t>(n) * j] = 1.0 / (basis.nodes[i] - basis.nodes[j]);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      double acc = 0.0;
+      for (int k = 0; k < n; ++k)
+        acc += w[i + static_cast<size_t>(n) * k] * w[k + static_cast<size_t>(n) * j];
+      a[i + static_cast<size_t>(n) * j] = -acc;
+    }
+  for (int j = 0; j < n; ++j) {
+    if (!std::isfinite(fvals[j]))
+      throw Error(KRONOP_EPARAM, "hermite_operator: f not finite at a node");
+    a[j + static_cast<size_t>(n) * j] += fvals[j];
+  }
+  double amax = 0.0, asym = 0.0;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      amax = std::max(amax, std::abs(a[i + static_cast<size_t>(n) * j]));
+      asym = std::max(asym, std::abs(a[i + static_cast<size_t>(n) * j] -
+                                     a[j + static_cast<size_t>(n) * i]));
+    }
+  if (asym > 1e-8 * amax)
+    throw Error(KRONOP_ENUMERICAL,
+                "hermite_operator: symmetrization degraded at n = " + std::to_string(n));
+  AxisFactor out;
+  std::vector<double> q;
+  sym_eig(n, a.data(), out.eigenvalues, q);  // symmetrises 0.5 (a + a^T) itself
+  out.transform.resize(static_cast<size_t>(n) * n);
+  out.inverse_transform.resize(static_cast<size_t>(n) * n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      // T = diag(psi) Q, T^{-1} = Q^T diag(1/psi) (axis.cpp:80-81)
+      out.transform[i + static_cast<size_t>(n) * j] =
+          basis.psi_last[i] * q[i + static_cast<size_t>(n) * j];
+      out.inverse_transform[i + static_cast<size_t>(n) * j] =
+          q[j + static_cast<size_t>(n) * i] * (1.0 / basis.psi_last[j]);
+    }
+  return out;
+}
+
 }  // namespace kronop_host

@@ -52,6 +52,18 @@ struct FoldedAxis {
 // Throws KRONOP_EPARAM when the axis is not mirror symmetric to 1e-12 (relative).
 FoldedAxis build_sem_axis_folded(const SemBasis& basis, const double* fvals);
 
+// Hermite-function collocation axis on the real line (hermite.hpp:13-19, hermite.cpp:10-66).
+struct HermiteAxis {
+  int n = 0;
+  std::vector<double> nodes;     // ascending, exactly symmetric about 0
+  std::vector<double> psi_last;  // psi_{n-1}(x_j)
+  std::vector<double> mass;      // 1 / (n psi_{n-1}(x_j)^2)
+  std::vector<double> diff;      // n x n column-major, D(i,j) = psi_i / (psi_j (x_i - x_j))
+};
+HermiteAxis hermite_basis(int n);
+// build_axis(HermiteBasis, f) (axis.cpp:76-84 over hermite_operator, hermite.cpp:68-95).
+AxisFactor build_hermite_axis(const HermiteAxis& basis, const double* fvals);
+
 void legendre_pair(int k, double x, double& p, double& dp);
 void gauss_legendre(int m, std::vector<double>& nodes, std::vector<double>& weights);
 GllRule gll_rule(int degree);

@@ -183,6 +183,14 @@ int main() {
                 au.energy, au.iterations);
   }
 
+  // test_axis_eigen.cpp:130-140 — Hermite axis oscillator levels
+  {
+    const HermiteBasis hb = hermite_basis(60);
+    const AxisEigens ax = build_axis(hb, osc);
+    for (int j = 0; j < 4; ++j) CHECK(std::abs(ax.eigenvalues[j] - (2.0 * j + 1.0)) < 1e-9);
+    std::printf("ok hermite levels %.12f %.12f\n", ax.eigenvalues[0], ax.eigenvalues[3]);
+  }
+
   // errors.hpp: ParameterError on bad input through the C-ABI
   {
     bool threw = false;

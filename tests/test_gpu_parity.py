@@ -585,3 +585,31 @@ def test_folded_operator_refuses_per_pass_api(ctx):
     u = dev(K.uniform_pm1(3, grid.node_count()))
     with pytest.raises(ParameterError):
         fo.transform_pass(u, 0, True)
+
+
+# ---------------------------------------------------------------------- Hermite axes --
+def test_hermite_grid_criterion6(ctx):
+    """acceptance.cpp:320-344 on the device: 3-D oscillator lambda_1 = 3 (Grid::hermite(40, 3),
+    inverse iteration from the constant field) and the 99^3 solve residual with the accuracy
+    potential; plus kernel parity of apply / solve / propagate on a Hermite grid."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    g = A.Grid.hermite(40, 3)
+    op = g.separable_operator(ctx, [lambda x: x * x] * 3)
+    init = torch.ones(g.node_count(), dtype=torch.float64, device="cuda")
+    r = A.inverse_iteration(A.FullOperator(op), A.InverseIterationConfig(), init)
+    assert r.converged and abs(r.eigenvalue - 3.0) <= 1e-9
+    g99 = A.Grid.hermite(99, 3)
+    pot = P.build_potential("sep-osc", g99, osc_amplitude=1600.0, quad_coeffs=[1.0, 2.0, 3.0])
+    h = g99.separable_operator(ctx, pot.separable)
+    f = g99.sample(lambda c: np.sin(np.pi / 2 * (c[0] + 1.0)) * np.sin(np.pi * (c[1] + 1.0))
+                   * np.sin(1.5 * np.pi * (c[2] + 1.0))
+                   * np.exp(-(c[0] ** 2 + c[1] ** 2 + c[2] ** 2) / 4.0))
+    fd = dev(f)
+    u = h.solve(fd)
+    res = rel(host(h.apply(u)), f)
+    assert res <= 1e-10
+    ko = oracle_op_from(h)
+    assert rel(host(u), ko.solve(f)) < 1e-13
+    psi = K.seeded_complex_field(g99.shape, 7)
+    assert rel(host(h.propagate(dev(psi), 0.01)), ko.propagate(psi, 0.01)) < 1e-13

@@ -201,3 +201,39 @@ def test_build_axis_folded_rejects_asymmetric_potential():
     b = A.assemble_sem(2.0, 3, 4)
     with pytest.raises(ParameterError):
         A.build_axis_folded(b, lambda t: t * t + 0.1 * t)
+
+
+
+@pytest.mark.parametrize("n", [2, 3, 20, 40, 99, 200])
+def test_hermite_basis_and_axis_against_oracle(n):
+    """hermite_basis / build_axis(HermiteBasis) (hermite.cpp:10-95, axis.cpp:76-84) in the C++
+    host setup against the oracle: nodes, psi_{n-1}, mass and D to rounding; eigenvalues to
+    1e-12; the factorisation reproduces the dense operator."""
+    A = api()
+    b = A.hermite_basis(n)
+    ob = K.hermite_basis(n)
+    assert np.abs(b.nodes - ob.nodes).max() <= 1e-13 * max(1.0, np.abs(ob.nodes).max())
+    assert np.array_equal(b.nodes, -b.nodes[::-1])
+    assert np.abs(b.psi_last - ob.psi_last).max() <= 1e-10 * np.abs(ob.psi_last).max()
+    assert np.abs(b.mass / ob.mass - 1.0).max() <= 1e-10
+    assert np.abs(b.diff - ob.diff).max() <= 1e-10 * np.abs(ob.diff).max()
+    f = lambda x: x * x + 0.5 * np.cos(x)
+    ax = A.build_axis(b, f)
+    oax = K.build_hermite_axis(ob, f)
+    scale = np.abs(oax.eigenvalues).max()
+    assert np.abs(ax.eigenvalues - oax.eigenvalues).max() <= 1e-12 * scale
+    assert np.abs(ax.transform @ ax.inverse_transform - np.eye(n)).max() < 1e-10
+    dense = K.dense_hermite_axis_operator(ob, f)
+    rec = ax.transform @ np.diag(ax.eigenvalues) @ ax.inverse_transform
+    assert np.abs(rec - dense).max() < 1e-9 * np.abs(dense).max()
+
+
+def test_hermite_error_codes():
+    from paper_2605_20491_b200 import ParameterError, CapabilityError
+    A = api()
+    with pytest.raises(ParameterError):
+        A.hermite_basis(1)
+    with pytest.raises(CapabilityError):
+        A.hermite_basis(746)
+    with pytest.raises(ParameterError):
+        A.build_axis(A.hermite_basis(5), lambda x: float("inf"))

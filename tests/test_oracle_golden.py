@@ -169,7 +169,9 @@ def test_pinned_acceptance_results():
     assert g["2"]["2_pass"]
     assert g["3"]["3a_pass"] and g["3"]["3b_pass"] and g["3"]["3d_pass"]
     # criterion 5: golden lambda is the converged (599^3) value; refined oracle grids reach it
+    assert g["4"]["4a_pass"] and g["4"]["4b_pass"]
     assert g["5"]["5b_pass"] and g["5"]["5c_pass"]
+    assert g["6"]["6a_pass"] and g["6"]["6b_pass"] and g["6"]["6c_pass"]
     assert g["5"]["5_refined_rel_239"] < 1e-10
     # criterion 7: stirrer multilevel ground state at the reference's own desk grid
     assert g["7"]["7a_pass"] and g["7"]["7_rel"] < 1e-9 and g["7"]["7b_pass"]
@@ -186,3 +188,19 @@ def test_pinned_acceptance_results():
     assert g["11"]["11a_pass"]
     assert g["12"]["12b_pass"]
     assert g["13"]["13a_pass"]
+
+
+def test_hermite_oracle_criterion6a_and_dense_cross_check():
+    """Hermite axis (hermite.cpp): 1-D oscillator levels (acceptance.cpp:310-318) and the factored
+    axis against the unsymmetrised dense -D^2 + diag(f) (dense_ref.cpp:19-23)."""
+    b = K.hermite_basis(40)
+    ax = K.build_hermite_axis(b, lambda x: x * x)
+    assert np.abs(ax.eigenvalues[:4] - np.array([1.0, 3.0, 5.0, 7.0])).max() <= 1e-9
+    dense = K.dense_hermite_axis_operator(b, lambda x: x * x)
+    rec = ax.transform @ np.diag(ax.eigenvalues) @ ax.inverse_transform
+    assert np.abs(rec - dense).max() < 1e-9 * np.abs(dense).max()
+    assert np.array_equal(b.nodes, -b.nodes[::-1])
+    with pytest.raises(K.ParameterError):
+        K.hermite_basis(1)
+    with pytest.raises(K.CapabilityError):
+        K.hermite_basis(746)
