@@ -91,6 +91,7 @@ PROTOTYPES = {
                              C.POINTER(DP), D, C.POINTER(P)]),
     "kronop_op_create_folded": (I, [P, I, IP] + [C.POINTER(DP)] * 8 + [D, C.POINTER(P)]),
     "kronop_op_destroy": (I, [P]),
+    "kronop_ctx_trim": (I, [P]),
     "kronop_op_set_shift": (I, [P, D]),
     "kronop_op_info": (I, [P, DP, DP, DP, C.POINTER(C.c_size_t)]),
     "kronop_op_eigenvalue_grid": (I, [P, P, P]),

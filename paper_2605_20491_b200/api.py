@@ -9,6 +9,7 @@ stream come from torch; all arithmetic runs in libkronop.so (there is no CPU pat
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import math
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional, Sequence
@@ -56,6 +57,9 @@ class Context:
         h = C.c_void_p()
         check(lib().kronop_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h)))
         self.h = h
+        # operators bound to this context: released before it (garbage-collected reference
+        # cycles, e.g. a failed test's traceback, may finalise the context first)
+        self._ops = weakref.WeakSet()
 
     def enter(self):
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
@@ -66,6 +70,10 @@ class Context:
     def synchronize(self):
         check(lib().kronop_ctx_synchronize(self.h))
 
+    def trim(self):
+        """Return the idle driver work buffers (kronop_ctx_trim) to the device."""
+        check(lib().kronop_ctx_trim(self.h))
+
     def launch_count(self) -> int:
         v = C.c_uint64()
         check(lib().kronop_ctx_launch_count(self.h, C.byref(v)))
@@ -73,6 +81,8 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None):
+            for op in list(getattr(self, "_ops", ())):
+                op.release()
             lib().kronop_ctx_destroy(self.h)
             self.h = None
 
@@ -280,6 +290,7 @@ class SeparableOperator:
         h = C.c_void_p()
         check(lib().kronop_op_create(ctx.h, d, n, T, Ti, lam, mp, shift, C.byref(h)))
         self.h = h
+        ctx._ops.add(self)
 
     @classmethod
     def folded(cls, ctx: Context, axes: Sequence[FoldedAxis], shift: float = 0.0,
@@ -305,12 +316,17 @@ class SeparableOperator:
         h = C.c_void_p()
         check(lib().kronop_op_create_folded(ctx.h, d, n, *ptrs, mp, shift, C.byref(h)))
         self.h = h
+        ctx._ops.add(self)
         return self
+
+    def release(self):
+        if getattr(self, "h", None):
+            lib().kronop_op_destroy(self.h)
+            self.h = None
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
-                lib().kronop_op_destroy(self.h)
+            self.release()
         except Exception:
             pass
 

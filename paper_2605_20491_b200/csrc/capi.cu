@@ -59,6 +59,44 @@ void ensure_scratch(kronop_ctx& ctx, size_t doubles) {
   ctx.scratch_cap = doubles;
 }
 
+double* pool_get(kronop_ctx& ctx, size_t n) {
+  kronop_ctx::Block* best = nullptr;
+  for (auto& b : ctx.pool)
+    if (!b.used && b.cap >= n && (!best || b.cap < best->cap)) best = &b;
+  if (best) {
+    best->used = true;
+    return best->p;
+  }
+  double* p = nullptr;
+  if (cudaMalloc(&p, n * sizeof(double)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    pool_trim(ctx);  // give the idle blocks back and retry once
+    KCUDA(cudaMalloc(&p, n * sizeof(double)));
+  }
+  ctx.pool.push_back({p, n, true});
+  return p;
+}
+
+void pool_trim(kronop_ctx& ctx) {
+  KCUDA(cudaStreamSynchronize(ctx.stream));
+  std::vector<kronop_ctx::Block> keep;
+  for (auto& b : ctx.pool) {
+    if (b.used)
+      keep.push_back(b);
+    else
+      KCUDA(cudaFree(b.p));
+  }
+  ctx.pool.swap(keep);
+}
+
+void pool_put(kronop_ctx& ctx, double* p) {
+  for (auto& b : ctx.pool)
+    if (b.p == p) {
+      b.used = false;
+      return;
+    }
+}
+
 double* ensure_tmp(kronop_ctx& ctx, size_t doubles) {
   if (doubles > ctx.tmp_cap) {
     if (ctx.tmp) KCUDA(cudaFreeAsync(ctx.tmp, ctx.stream));
@@ -438,6 +476,7 @@ int kronop_ctx_destroy(kronop_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto p : ctx->scratch) if (p) cudaFree(p);
     for (auto p : ctx->io) if (p) cudaFree(p);
+    for (auto& b : ctx->pool) cudaFree(b.p);
     if (ctx->tmp) cudaFree(ctx->tmp);
     if (ctx->ws.partials) cudaFree(ctx->ws.partials);
     if (ctx->dscal) cudaFree(ctx->dscal);
@@ -450,6 +489,13 @@ int kronop_ctx_destroy(kronop_ctx* ctx) {
     if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
+  });
+}
+
+int kronop_ctx_trim(kronop_ctx* ctx) {
+  return guard([&] {
+    param_check(ctx != nullptr, "ctx_trim: null context");
+    pool_trim(*ctx);
   });
 }
 

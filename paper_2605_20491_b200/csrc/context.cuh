@@ -27,7 +27,15 @@ struct kronop_ctx {
   cudaEvent_t ev_in[kMaxChunks] = {};
   cudaEvent_t ev_out[kMaxChunks] = {};
   cudaEvent_t ev_ready = nullptr;
+  // device block pool for driver vectors (stream-ordered reuse on `stream`; freed at destroy)
+  struct Block {
+    double* p;
+    size_t cap;
+    bool used;
+  };
+  std::vector<Block> pool;
 };
+
 
 constexpr int kScalarSlots = 256;
 
@@ -57,6 +65,11 @@ struct kronop_op {
 };
 
 namespace kronop_dev {
+// Smallest free pool block with capacity >= n doubles, else a new cudaMalloc'd block.
+double* pool_get(kronop_ctx& ctx, size_t n);
+void pool_put(kronop_ctx& ctx, double* p);
+void pool_trim(kronop_ctx& ctx);  // cudaFree every idle block
+
 
 // Real view of a field: an optional leading re/im axis of extent 2, then the spatial axes.
 struct View {

@@ -38,13 +38,16 @@ int guard2(F&& f) {
   }
 }
 
-// RAII device buffer
+// RAII device buffer from the context's block pool (pool_get / pool_put, capi.cu): drivers that
+// are called repeatedly (PCG, inverse iteration, GPE, evolve) reuse their vectors instead of a
+// cudaMalloc / cudaFree pair (which synchronises the device) per call.
 struct DBuf {
+  kronop_ctx* c = nullptr;
   double* p = nullptr;
   DBuf() = default;
-  explicit DBuf(size_t n) { KCUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(double))); }
+  DBuf(kronop_ctx& ctx, size_t n) : c(&ctx), p(pool_get(ctx, std::max<size_t>(n, 1))) {}
   ~DBuf() {
-    if (p) cudaFree(p);
+    if (p) pool_put(*c, p);
   }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
@@ -142,8 +145,9 @@ __global__ void k_pcg_finish(PcgScalars* sc, double* history, cudaGraphCondition
 struct PcgWork {
   DBuf r, z, p, q, best, tmp, hist;
   DBuf scal;  // PcgScalars + slots
-  PcgWork(long long n, int max_iter)
-      : r(n), z(n), p(n), q(n), best(n), tmp(n), hist(max_iter + 2), scal(64) {}
+  PcgWork(kronop_ctx& c, long long n, int max_iter)
+      : r(c, n), z(c, n), p(c, n), q(c, n), best(c, n), tmp(c, n), hist(c, max_iter + 2),
+        scal(c, 64) {}
   PcgScalars* sc() { return reinterpret_cast<PcgScalars*>(scal.p); }
   double* slot(int i) { return scal.p + 32 + i; }
 };
@@ -322,7 +326,7 @@ __global__ void k_argmax_abs_partial(const double* u, long long n, double* pv, l
 }
 
 static void fix_sign(kronop_ctx& ctx, double* u, long long n) {  // ground_state.cpp:23-27
-  DBuf pv(kRedBlocks), pi(kRedBlocks);
+  DBuf pv(ctx, kRedBlocks), pi(ctx, kRedBlocks);
   k_argmax_abs_partial<<<kRedBlocks, 256, 0, ctx.stream>>>(u, n, pv.p,
                                                            reinterpret_cast<long long*>(pi.p));
   KCUDA(cudaGetLastError());
@@ -359,7 +363,7 @@ int kronop_pcg(kronop_ctx* ctx, const kronop_linear_map* apply_a, const kronop_l
     const long long n = apply_a->op ? apply_a->op->N : 0;
     check_map(*ctx, apply_a, n);
     check_map(*ctx, precond, n);
-    PcgWork w(n, config->max_iter);
+    PcgWork w(*ctx, n, config->max_iter);
     pcg_run(*ctx, *apply_a, *precond, b, x, n, *config, *report, history, w);
   });
 }
@@ -382,7 +386,7 @@ int kronop_inverse_iteration(kronop_ctx* ctx, const kronop_op* op, const double*
     if (cfg->shift_mode == KRONOP_SHIFT_FRACTION) sigma = cfg->shift_fraction * op->lmin;
     else if (cfg->shift_mode == KRONOP_SHIFT_OFFSET) sigma = op->lmin - cfg->shift_offset;
     ensure_scratch(c, static_cast<size_t>(n));
-    DBuf u(n), hu(n), w(n), slots(8);
+    DBuf u(c, n), hu(c, n), w(c, n), slots(c, 8);
     auto rayleigh = [&](const double* v) {  // ground_state.cpp:46-49
       sep_transform(c, *op, v, hu.p, 0, SEP_APPLY, op->shift, 0.0, diag, 0.0);
       const double num = wdot(c, *op, v, hu.p, slots.p);
@@ -403,7 +407,7 @@ int kronop_inverse_iteration(kronop_ctx* ctx, const kronop_op* op, const double*
     kronop_linear_map M{op, KRONOP_MAP_SOLVE, nullptr, 0.0, nullptr};
     if (!separable) check_solve_shift(c, *op, op->shift);
     std::unique_ptr<PcgWork> pw;
-    if (!separable) pw.reset(new PcgWork(n, cfg->inner.max_iter));
+    if (!separable) pw.reset(new PcgWork(c, n, cfg->inner.max_iter));
     for (int outer = 0; outer < cfg->max_outer; ++outer) {
       if (separable) {
         sep_transform(c, *op, u.p, w.p, 0, SEP_SOLVE, sigma, 0.0, nullptr, 0.0);
@@ -494,7 +498,7 @@ int kronop_gpe_energy(kronop_ctx* ctx, const kronop_op* hamiltonian, const doubl
   return guard2([&] {
     param_check(ctx && hamiltonian && u && energy, "gpe_energy: null argument");
     param_check(hamiltonian->has_mass, "gpe_energy: field needs mass weights");
-    DBuf hu(hamiltonian->N), sq(hamiltonian->N), slots(4);
+    DBuf hu(*ctx, hamiltonian->N), sq(*ctx, hamiltonian->N), slots(*ctx, 4);
     *energy = gpe_energy_dev(*ctx, *hamiltonian, diag, beta, u, hu.p, sq.p, slots.p);
   });
 }
@@ -516,7 +520,8 @@ int kronop_gpe_gradient_flow(kronop_ctx* ctx, const kronop_op* ham, const double
     const long long n = ham->N;
     const auto t0 = std::chrono::steady_clock::now();
     ensure_scratch(c, static_cast<size_t>(n));
-    DBuf u(n), w(n), grad(n), r(n), rt(n), ut(n), dg(n), sq(n), slots(8);
+    DBuf u(c, n), w(c, n), grad(c, n), r(c, n), rt(c, n), ut(c, n), dg(c, n), sq(c, n),
+        slots(c, 8);
     // initial state (gpe.cpp:76-92)
     if (cfg->init == KRONOP_GPE_INIT_SUPPLIED) {
       KCUDA(cudaMemcpyAsync(u.p, initial, n * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
@@ -554,7 +559,7 @@ int kronop_gpe_gradient_flow(kronop_ctx* ctx, const kronop_op* ham, const double
     if (cfg->kind == KRONOP_GPE_H1) check_solve_shift(c, *lap, alpha);
     else check_solve_shift(c, *ham, ham->shift);
     std::unique_ptr<PcgWork> pw;
-    if (cfg->kind == KRONOP_GPE_AU) pw.reset(new PcgWork(n, cfg->inner.max_iter));
+    if (cfg->kind == KRONOP_GPE_AU) pw.reset(new PcgWork(c, n, cfg->inner.max_iter));
     for (int it = 0; it < cfg->max_iterations; ++it) {
       if (cfg->kind == KRONOP_GPE_H1) {  // gpe.cpp:108-117
         sep_transform(c, *ham, u.p, r.p, 0, SEP_APPLY, ham->shift, 0.0, diag, 0.0);
@@ -753,7 +758,7 @@ int kronop_evolve(kronop_ctx* ctx, const kronop_split_spec* spec, const kronop_o
     kronop_ctx& c = *ctx;
     const long long n = a->N;
     ensure_scratch(c, static_cast<size_t>(2 * n));
-    DBuf start(2 * n), ref(2 * n), slots(4);
+    DBuf start(c, 2 * n), ref(c, 2 * n), slots(c, 4);
     // psi = psi0 / ||psi0||_2 (splitting.cpp:118-119)
     launch_dot(c.stream, c.ws, psi0, psi0, n, 1, nullptr, slots.p);
     launch_div_by(c.stream, c.ws, state, psi0, 2 * n, slots.p, 1);
@@ -769,14 +774,14 @@ int kronop_evolve(kronop_ctx* ctx, const kronop_split_spec* spec, const kronop_o
       KCUDA(cudaMemcpyAsync(ref.p, start.p, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice,
                             c.stream));
       // ref *= complex(cos, sin): reuse the B-phase kernel with b = 1, factor = -phase
-      DBuf one(n);
+      DBuf one(c, n);
       std::vector<double> ones(static_cast<size_t>(n), 1.0);
       KCUDA(cudaMemcpyAsync(one.p, ones.data(), n * sizeof(double), cudaMemcpyHostToDevice,
                             c.stream));
       launch_phase(c.stream, c.ws, ref.p, one.p, -phase, n);
       KCUDA(cudaStreamSynchronize(c.stream));
     }
-    DBuf diff(2 * n);
+    DBuf diff(c, 2 * n);
     launch_sub(c.stream, c.ws, diff.p, state, ref.p, 2 * n);
     if (spec->mass_weighted_error) {
       const IndexGeomHost g = mass_geom(*a);
