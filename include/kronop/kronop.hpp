@@ -16,6 +16,7 @@
 #include <stdexcept>
 #include <string>
 #include <type_traits>
+#include <variant>
 #include <vector>
 
 #include "../kronop_cuda.h"
@@ -154,6 +155,42 @@ class DeviceField {
   std::size_t n_ = 0;
   double* p_ = nullptr;
 };
+
+// ------------------------------------------------------------- fieldio.hpp:10-16 --
+template <typename S>
+void dump_field(const std::string& path, const TensorField<S>& field) {
+  std::vector<int> shp(field.shape().begin(), field.shape().end());
+  check(kronop_field_dump_host(path.c_str(), field.dim(), shp.data(), is_complex_v<S>,
+                               reinterpret_cast<const double*>(field.data())));
+}
+// Device fields stream through pinned staging chunks (no full host copy).
+template <typename S>
+void dump_field(const std::string& path, Context& ctx, const DeviceField<S>& field) {
+  std::vector<int> shp(field.shape().begin(), field.shape().end());
+  check(kronop_field_dump(ctx.get(), path.c_str(), static_cast<int>(shp.size()), shp.data(),
+                          is_complex_v<S>, field.data()));
+}
+using LoadedField = std::variant<RealField, ComplexField>;
+inline LoadedField load_field(const std::string& path) {
+  int d = 0, cplx = 0, shp[9] = {};
+  check(kronop_field_load_header(path.c_str(), &d, shp, &cplx));
+  const Shape shape(shp, shp + d);
+  auto load = [&](auto f) -> LoadedField {
+    check(kronop_field_load_host(path.c_str(), reinterpret_cast<double*>(f.data()),
+                                 f.size() * (cplx ? 2 : 1)));
+    return f;
+  };
+  return cplx ? load(ComplexField(shape)) : load(RealField(shape));
+}
+template <typename S>
+DeviceField<S> load_field(const std::string& path, Context& ctx) {
+  int d = 0, cplx = 0, shp[9] = {};
+  check(kronop_field_load_header(path.c_str(), &d, shp, &cplx));
+  if (cplx != is_complex_v<S>) throw ParameterError("load_field: scalar kind mismatch");
+  DeviceField<S> f(ctx, Shape(shp, shp + d));
+  check(kronop_field_load(ctx.get(), path.c_str(), f.data(), f.doubles()));
+  return f;
+}
 
 // -------------------------------------------------------- axis.hpp / basis1d.hpp (host) --
 struct Basis1D {  // basis1d.hpp:17-29

@@ -1307,3 +1307,46 @@ def box_state(grid: Grid, half_width: float) -> np.ndarray:
             v = v * np.sin(np.pi * (c[a] + half_width) / (2.0 * half_width))
         return v
     return grid.sample(f)
+
+
+# ------------------------------------------------------------------------------ fieldio.cpp
+
+FIELD_MAGIC = 0x4B4F5046
+
+
+def dump_field(path: str, field: np.ndarray, shape: Sequence[int]):
+    """Binary checkpoint (proj/src/fieldio.cpp:28-47, format fieldio.hpp:10-13)."""
+    import struct
+    cplx = np.iscomplexobj(field)
+    with open(path, "wb") as f:
+        f.write(struct.pack("<4I", FIELD_MAGIC, 1, len(shape), 1 if cplx else 0))
+        f.write(struct.pack("<%dQ" % len(shape), *shape))
+        f.write(np.ascontiguousarray(field, dtype=np.complex128 if cplx else np.float64).tobytes())
+
+
+def load_field(path: str):
+    """proj/src/fieldio.cpp:49-73: returns (field, shape)."""
+    import struct
+    with open(path, "rb") as f:
+        raw = f.read()
+    if len(raw) < 16:
+        raise ParameterError("load_field: truncated file")
+    magic, version, dim, kind = struct.unpack_from("<4I", raw, 0)
+    if magic != FIELD_MAGIC:
+        raise ParameterError("load_field: bad magic")
+    if version != 1:
+        raise ParameterError("load_field: bad version")
+    if dim < 1 or dim > 9:
+        raise ParameterError("load_field: bad dimension")
+    if len(raw) < 16 + 8 * dim:
+        raise ParameterError("load_field: truncated file")
+    shape = struct.unpack_from("<%dQ" % dim, raw, 16)
+    if kind not in (0, 1):
+        raise ParameterError("load_field: unknown scalar kind")
+    n = int(np.prod(shape)) * (2 if kind else 1)
+    body = raw[16 + 8 * dim:]
+    if len(body) < 8 * n:
+        raise ParameterError("load_field: truncated data")
+    a = np.frombuffer(body[:8 * n], dtype=np.float64).copy()
+    return (a.view(np.complex128) if kind else a), tuple(shape)
+

@@ -92,6 +92,11 @@ PROTOTYPES = {
     "kronop_op_create_folded": (I, [P, I, IP] + [C.POINTER(DP)] * 8 + [D, C.POINTER(P)]),
     "kronop_op_destroy": (I, [P]),
     "kronop_ctx_trim": (I, [P]),
+    "kronop_field_dump": (I, [P, C.c_char_p, I, IP, I, P]),
+    "kronop_field_dump_host": (I, [C.c_char_p, I, IP, I, DP]),
+    "kronop_field_load_header": (I, [C.c_char_p, IP, IP, IP]),
+    "kronop_field_load": (I, [P, C.c_char_p, P, C.c_size_t]),
+    "kronop_field_load_host": (I, [C.c_char_p, DP, C.c_size_t]),
     "kronop_op_set_shift": (I, [P, D]),
     "kronop_op_info": (I, [P, DP, DP, DP, C.POINTER(C.c_size_t)]),
     "kronop_op_eigenvalue_grid": (I, [P, P, P]),
@@ -123,6 +128,7 @@ PROTOTYPES = {
     "kronop_host_sym_eig": (I, [I, DP, DP, DP]),
     "kronop_host_build_sem_axis": (I, [D, I, I, DP, DP, DP, DP]),
     "kronop_host_hermite_basis": (I, [I, DP, DP, DP, DP]),
+    "kronop_host_eval_weights": (I, [D, I, I, DP, I, DP]),
     "kronop_host_build_hermite_axis": (I, [I, DP, DP, DP, DP]),
     "kronop_host_build_sem_axis_folded": (I, [D, I, I] + [DP] * 8),
     "kronop_splitmix_uniform": (I, [P, C.c_uint64, C.c_uint64, C.c_size_t, P]),
@@ -137,6 +143,7 @@ class KronopError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__("[%d] %s" % (code, msg))
         self.code = code
+        self.msg = msg
 
 
 class ParameterError(KronopError):

@@ -143,6 +143,16 @@ def assemble_sem(half_width: float, cell_count: int, degree: int) -> Basis1D:
     return Basis1D(half_width, cell_count, degree, x, m, s.reshape(n, n, order="F"))
 
 
+def eval_weights(basis: Basis1D, x) -> np.ndarray:
+    """Rows of eval_weights_row(basis, x_t) (basis1d.cpp:90-115): (len(x), n) matrix E with
+    E @ u = u_h(x) for nodal values u."""
+    xs = np.ascontiguousarray(np.atleast_1d(np.asarray(x, dtype=np.float64)))
+    out = np.zeros((len(xs), basis.size))
+    check(lib().kronop_host_eval_weights(basis.half_width, basis.cell_count, basis.degree,
+                                         _dptr(xs), len(xs), _dptr(out)))
+    return out
+
+
 def interp_matrix(coarse: Basis1D, fine: Basis1D) -> np.ndarray:
     p = np.zeros(fine.size * coarse.size)
     check(lib().kronop_host_interp_matrix(coarse.half_width, coarse.cell_count, coarse.degree,
@@ -779,6 +789,8 @@ class LevelReport:
     total_inner_iterations: int
     inner_per_outer: float
     eigenvalue: float
+    setup_seconds: float = 0.0
+    interp_seconds: float = 0.0
 
 
 def multilevel_ground_state(ctx: Context, grids: Sequence[Grid], make_operator,
@@ -788,19 +800,78 @@ def multilevel_ground_state(ctx: Context, grids: Sequence[Grid], make_operator,
     device), continue. make_operator(grid) -> FullOperator. Returns (EigenpairResult, [LevelReport])."""
     if not grids:
         raise L.ParameterError(L.KRONOP_EPARAM, "multilevel_ground_state: no levels")
+    import time
     guess, prev = None, None
     levels, pair = [], None
     for grid in grids:
+        t0 = time.perf_counter()
         op = make_operator(grid)
+        torch.cuda.synchronize()
+        setup_s, interp_s = time.perf_counter() - t0, 0.0
         if guess is None:
             initial = op.sep.ground_state()
         else:
+            if not all(isinstance(b, Basis1D) for b in prev.axes + grid.axes):
+                raise L.ParameterError(L.KRONOP_EPARAM,
+                                       "multilevel_ground_state: levels must be SEM grids")
+            t0 = time.perf_counter()
             mats = [interp_matrix(prev.axes[a], grid.axes[a]) for a in range(grid.dim)]
             initial = kron_apply(ctx, guess, prev.shape, mats)
+            torch.cuda.synchronize()
+            interp_s = time.perf_counter() - t0
         pair = inverse_iteration(op, config, initial)
         levels.append(LevelReport(grid.axes[0].size, pair.outer_iterations,
                                   pair.total_inner_iterations,
-                                  pair.total_inner_iterations / max(1, pair.outer_iterations),
-                                  pair.eigenvalue))
+                                  pair.total_inner_iterations / max(1, pair.outer_iterations)
+                                  if pair.outer_iterations > 0 else 0.0,
+                                  pair.eigenvalue, setup_s, interp_s))
         guess, prev = pair.eigenvector, grid
     return pair, levels
+
+
+# ------------------------------------------------------------------------------ field I/O --
+def _shape_arr(shape):
+    return (C.c_int * len(shape))(*[int(n) for n in shape])
+
+
+def dump_field(path: str, field, shape: Sequence[int], ctx: Optional[Context] = None):
+    """dump_field (fieldio.cpp:28-47) in the reference's binary format. `field` is a CUDA tensor
+    (streamed through pinned chunks on ctx's stream) or a numpy array (host path); `shape` is the
+    reference shape (axis 0 first). Complex dtype -> scalar kind 1."""
+    if isinstance(field, torch.Tensor):
+        if ctx is None:
+            raise ValueError("dump_field: a device field needs its Context")
+        with _Call(ctx):
+            check(lib().kronop_field_dump(ctx.h, path.encode(), len(shape), _shape_arr(shape),
+                                          int(field.is_complex()), _ptr(field)))
+    else:
+        a = np.ascontiguousarray(field)
+        cplx = np.iscomplexobj(a)
+        v = a.view(np.float64) if cplx else a.astype(np.float64, copy=False)
+        check(lib().kronop_field_dump_host(path.encode(), len(shape), _shape_arr(shape),
+                                           int(cplx), _dptr(v)))
+
+
+def load_field_header(path: str):
+    d, cplx = C.c_int(), C.c_int()
+    shp = (C.c_int * 9)()
+    check(lib().kronop_field_load_header(path.encode(), C.byref(d), shp, C.byref(cplx)))
+    return tuple(shp[i] for i in range(d.value)), bool(cplx.value)
+
+
+def load_field(path: str, ctx: Optional[Context] = None):
+    """load_field (fieldio.cpp:49-73): returns (field, shape, is_complex); a CUDA tensor when ctx
+    is given (uploaded through pinned chunks), else a numpy array."""
+    shape, cplx = load_field_header(path)
+    n = int(np.prod(shape))
+    doubles = n * (2 if cplx else 1)
+    if ctx is None:
+        buf = np.empty(doubles, dtype=np.float64)
+        check(lib().kronop_field_load_host(path.encode(), _dptr(buf), doubles))
+        return (buf.view(np.complex128) if cplx else buf), shape, cplx
+    t = torch.empty(n, dtype=torch.complex128 if cplx else torch.float64,
+                    device="cuda:%d" % ctx.device)
+    with _Call(ctx):
+        check(lib().kronop_field_load(ctx.h, path.encode(), _ptr(t), doubles))
+    return t, shape, cplx
+

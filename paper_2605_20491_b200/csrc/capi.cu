@@ -256,6 +256,64 @@ static void sep_transform_folded(kronop_ctx& ctx, const kronop_op& op, const dou
   }
 }
 
+// Small-extent path, rotating layout (fused_rot.cu): groups of up to 3 consecutive axes (fused
+// extent <= 1024), forward groups then backward groups; each launch moves its group to the slow
+// end, so after each direction the layout is the caller's again.
+static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out,
+                              int cplx, SepKind kind, double shift, double dt, const double* diag,
+                              double sigma) {
+  const size_t nd = static_cast<size_t>(op.N) * (cplx ? 2 : 1);
+  ensure_scratch(ctx, nd);
+  std::vector<std::pair<int, int>> groups;
+  for (int a = 0; a < op.d;) {
+    int f = 1, F = op.n[a];
+    while (f < 3 && a + f < op.d && F * op.n[a + f] <= 1024) F *= op.n[a + f++];
+    groups.emplace_back(a, f);
+    a += f;
+  }
+  const double* src = in;
+  if (!fused_rot_eligible(in)) {  // bulk copies need 16-byte aligned tiles
+    double* t = ensure_tmp(ctx, nd);
+    KCUDA(cudaMemcpyAsync(t, in, nd * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+    src = t;
+  }
+  const int ng = static_cast<int>(groups.size());
+  int k = 0;
+  for (int dir = 0; dir < 2; ++dir)
+    for (int g = 0; g < ng; ++g, ++k) {
+      const int a0 = groups[g].first, f = groups[g].second;
+      const bool last = dir == 1 && g == ng - 1;
+      double* dst = last ? out : ctx.scratch[k % 2];
+      const double* mats[3];
+      int lda[3], n[3];
+      for (int j = 0; j < f; ++j) {
+        mats[j] = dir == 0 ? op.fwd[a0 + j] : op.bwd[a0 + j];
+        lda[j] = op.lda[a0 + j];
+        n[j] = op.n[a0 + j];
+      }
+      RotEpi e;
+      if (dir == 0 && g == ng - 1) {
+        e.kind = kind == SEP_APPLY ? EPI_SPEC_MUL : kind == SEP_SOLVE ? EPI_SPEC_DIV : EPI_SPEC_PHASE;
+        e.shift = shift;
+        e.dt = dt;
+        for (int j = 0; j < f; ++j) e.lam_g[j] = op.lam[a0 + j];
+        e.nq = a0;
+        for (int j = 0; j < a0; ++j) {
+          e.qext[j] = op.n[j];
+          e.lam_q[j] = op.lam[j];
+        }
+      } else if (last && (diag != nullptr || sigma != 0.0)) {
+        e.kind = EPI_AXPY_DIAG;
+        e.diag = diag;
+        e.u = in;
+        e.sigma = sigma;
+      }
+      launch_fused_rot(ctx.stream, src, dst, cplx, f, n, op.N, mats, lda, e);
+      ctx.ws.launches += 1;
+      src = dst;
+    }
+}
+
 void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
                    SepKind kind, double shift, double dt, const double* diag, double sigma) {
   if (op.folded) {
@@ -263,7 +321,14 @@ void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, doubl
     return;
   }
   if (use_fused_small(op)) {
-    sep_transform_fused_small(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
+    static const bool legacy = [] {
+      const char* e = getenv("KRONOP_FUSED_SMALL_LEGACY");  // A/B switch: in-place tiles
+      return e && e[0] == '1';
+    }();
+    if (legacy)
+      sep_transform_fused_small(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
+    else
+      sep_transform_rot(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
     return;
   }
   View v = make_view(op.d, op.n, cplx);
@@ -462,6 +527,7 @@ int kronop_ctx_create(int device, void* stream, kronop_ctx** out) {
       prime_mode_product_kernels();
       prime_mode_product_tma_kernels();
       prime_fused_small_kernels();
+      prime_fused_rot_kernels();
     } catch (...) {
       delete c;
       throw;
@@ -1062,6 +1128,18 @@ int kronop_host_sym_eig(int n, const double* a, double* eigenvalues, double* q) 
     kronop_host::sym_eig(n, a, lam, qq);
     std::copy(lam.begin(), lam.end(), eigenvalues);
     std::copy(qq.begin(), qq.end(), q);
+  });
+}
+
+int kronop_host_eval_weights(double half_width, int cell_count, int degree, const double* x,
+                             int count, double* out) {
+  return guard([&] {
+    const auto b = kronop_host::assemble_sem(half_width, cell_count, degree);
+    const int n = b.size();
+    for (int t = 0; t < count; ++t) {
+      const auto row = kronop_host::eval_weights_row(b, x[t]);
+      std::copy(row.begin(), row.end(), out + static_cast<size_t>(n) * t);
+    }
   });
 }
 

@@ -526,10 +526,7 @@ int kronop_gpe_gradient_flow(kronop_ctx* ctx, const kronop_op* ham, const double
     if (cfg->init == KRONOP_GPE_INIT_SUPPLIED) {
       KCUDA(cudaMemcpyAsync(u.p, initial, n * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
     } else if (cfg->init == KRONOP_GPE_INIT_CONSTANT) {
-      std::vector<double> one(static_cast<size_t>(n), 1.0);
-      KCUDA(cudaMemcpyAsync(u.p, one.data(), n * sizeof(double), cudaMemcpyHostToDevice,
-                            c.stream));
-      KCUDA(cudaStreamSynchronize(c.stream));
+      launch_fill(c.stream, c.ws, u.p, 1.0, n);
     } else {
       KCUDA(cudaMemsetAsync(u.p, 0, n * sizeof(double), c.stream));
       IndexGeomHost g;
@@ -773,13 +770,8 @@ int kronop_evolve(kronop_ctx* ctx, const kronop_split_spec* spec, const kronop_o
       const double phase = -stationary_eigenvalue * spec->total_time;
       KCUDA(cudaMemcpyAsync(ref.p, start.p, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice,
                             c.stream));
-      // ref *= complex(cos, sin): reuse the B-phase kernel with b = 1, factor = -phase
-      DBuf one(c, n);
-      std::vector<double> ones(static_cast<size_t>(n), 1.0);
-      KCUDA(cudaMemcpyAsync(one.p, ones.data(), n * sizeof(double), cudaMemcpyHostToDevice,
-                            c.stream));
-      launch_phase(c.stream, c.ws, ref.p, one.p, -phase, n);
-      KCUDA(cudaStreamSynchronize(c.stream));
+      // ref *= complex(cos, sin): the B-phase kernel with b = 1 (nullptr), factor = -phase
+      launch_phase(c.stream, c.ws, ref.p, nullptr, -phase, n);
     }
     DBuf diff(c, 2 * n);
     launch_sub(c.stream, c.ws, diff.p, state, ref.p, 2 * n);

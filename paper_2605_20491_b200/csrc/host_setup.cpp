@@ -581,6 +581,51 @@ FoldedAxis build_sem_axis_folded(const SemBasis& basis, const double* fvals) {
   return fa;
 }
 
+// ------------------------------------------------------- point evaluation (slices) --
+static std::vector<double> lagrange_eval_weights(const std::vector<double>& nodes, double x) {
+  // quadrature.cpp:105-122
+  const int n = static_cast<int>(nodes.size());
+  std::vector<double> w(n, 0.0);
+  for (int j = 0; j < n; ++j)
+    if (x == nodes[j]) {
+      w[j] = 1.0;
+      return w;
+    }
+  const std::vector<double> b = barycentric_weights(nodes);
+  double denom = 0.0;
+  for (int j = 0; j < n; ++j) {
+    w[j] = b[j] / (x - nodes[j]);
+    denom += w[j];
+  }
+  for (int j = 0; j < n; ++j) w[j] /= denom;
+  return w;
+}
+
+std::vector<double> eval_weights_row(const SemBasis& basis, double x) {  // basis1d.cpp:90-115
+  const double l = basis.half_width;
+  if (x < -l || x > l) throw Error(KRONOP_EPARAM, "eval_cellwise: target outside [-L, L]");
+  const int n = basis.size();
+  std::vector<double> row(n, 0.0);
+  const auto hit = std::lower_bound(basis.nodes.begin(), basis.nodes.end(), x);
+  if (hit != basis.nodes.end() && *hit == x) {
+    row[hit - basis.nodes.begin()] = 1.0;
+    return row;
+  }
+  const int k = basis.degree;
+  const double h = 2.0 * l / basis.cell_count;
+  int c = static_cast<int>(std::floor((x + l) / h));
+  c = std::clamp(c, 0, basis.cell_count - 1);
+  const double left = -l + c * h;
+  const double xi = 2.0 * (x - left) / h - 1.0;
+  const std::vector<double> wloc = lagrange_eval_weights(basis.rule.nodes, xi);
+  for (int j = 0; j <= k; ++j) {
+    const int g = c * k + j;
+    if (g == 0 || g == basis.cell_count * k) continue;  // boundary value is zero
+    row[g - 1] += wloc[j];
+  }
+  return row;
+}
+
 // ------------------------------------------------------------------ Hermite axes --
 HermiteAxis hermite_basis(int n) {  // hermite.cpp:10-66
   if (n < 2) throw Error(KRONOP_EPARAM, "hermite_basis: need n >= 2");

@@ -61,6 +61,8 @@ struct HermiteAxis {
   std::vector<double> diff;      // n x n column-major, D(i,j) = psi_i / (psi_j (x_i - x_j))
 };
 HermiteAxis hermite_basis(int n);
+// eval_weights_row(basis, x) (basis1d.cpp:90-115): the row r with r . u = u_h(x).
+std::vector<double> eval_weights_row(const SemBasis& basis, double x);
 // build_axis(HermiteBasis, f) (axis.cpp:76-84 over hermite_operator, hermite.cpp:68-95).
 AxisFactor build_hermite_axis(const HermiteAxis& basis, const double* fvals);
 

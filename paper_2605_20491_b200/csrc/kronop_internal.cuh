@@ -84,6 +84,23 @@ void prime_mode_product_kernels();
 // TMA + mbarrier warp-specialised kernel (mode_product_tma.cu) for the STRIDED (pre % 128 == 0)
 // and CONTIG (pre == 1, even nk) geometries; launch_mode_product dispatches to it when eligible.
 void prime_mode_product_tma_kernels();
+// Rotating-layout group transform (fused_rot.cu): contracts the f fastest axes after the re/im
+// axis and writes them to the slowest end. Used when every axis has n <= 32.
+struct RotEpi {
+  int kind = EPI_STORE;  // EPI_STORE, EPI_SPEC_* (last forward group), EPI_AXPY_DIAG (last backward)
+  double shift = 0.0, dt = 0.0, sigma = 0.0;
+  const double* diag = nullptr;
+  const double* u = nullptr;
+  const double* lam_g[3] = {};               // eigenvalues of the group axes
+  int nq = 0;                                // axes below the group (original order)
+  long long qext[KRONOP_MAX_DIM] = {};
+  const double* lam_q[KRONOP_MAX_DIM] = {};
+};
+void prime_fused_rot_kernels();
+bool fused_rot_eligible(const double* x);
+void launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f, const int* n,
+                      long long N, const double* const* mats, const int* lda, const RotEpi& epi);
+
 // Fused small-extent multi-axis transform (fused_small.cu), used when every axis has n <= 32.
 void prime_fused_small_kernels();
 void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, const long long* ext,

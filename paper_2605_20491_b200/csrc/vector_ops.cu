@@ -221,6 +221,19 @@ void launch_scale(cudaStream_t s, Workspace& ws, double* y, const double* x, lon
   KCUDA(cudaGetLastError());
 }
 
+__global__ void k_fill(double* y, double v, long long n) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += stride)
+    y[i] = v;
+}
+
+void launch_fill(cudaStream_t s, Workspace& ws, double* y, double v, long long n) {
+  k_fill<<<kEltBlocks, kThreads, 0, s>>>(y, v, n);
+  ws.launches += 1;
+  KCUDA(cudaGetLastError());
+}
+
 // y = x / *nrm (division, as in u.flat() /= sqrt(...) ground_state.cpp:63,84)
 __global__ void k_div_by(double* y, const double* x, long long n, const double* nrm, int sq) {
   const double dnm = sq ? sqrt(*nrm) : *nrm;
@@ -258,7 +271,7 @@ __global__ void k_phase(double* psi, const double* b, double factor, long long n
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += stride) {
-    const double phase = __dmul_rn(-factor, b[i]);
+    const double phase = b ? __dmul_rn(-factor, b[i]) : -factor;  // b = nullptr: b = 1
     double sn, cs;
     sincos(phase, &sn, &cs);
     const double re = psi[2 * i], im = psi[2 * i + 1];

@@ -37,6 +37,7 @@ void launch_copy_if(cudaStream_t s, Workspace& ws, double* dst, const double* sr
                     const int* flag);
 void launch_scale(cudaStream_t s, Workspace& ws, double* y, const double* x, long long n, double a,
                   const double* ap, int ap_mode);
+void launch_fill(cudaStream_t s, Workspace& ws, double* y, double v, long long n);
 void launch_div_by(cudaStream_t s, Workspace& ws, double* y, const double* x, long long n,
                    const double* nrm_dev, int take_sqrt);
 void launch_mul_diag(cudaStream_t s, Workspace& ws, double* y, const double* x, const double* d,

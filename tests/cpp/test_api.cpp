@@ -191,6 +191,22 @@ int main() {
     std::printf("ok hermite levels %.12f %.12f\n", ax.eigenvalues[0], ax.eigenvalues[3]);
   }
 
+  // fieldio.cpp:28-73 — host and device checkpoints round-trip bit for bit
+  {
+    ComplexField psi({7, 5, 3});
+    std::uint64_t s = 11;
+    for (std::size_t k = 0; k < psi.size(); ++k) psi[k] = {uniform(s), uniform(s)};
+    dump_field("/tmp/kronop_cpp_io.kf", psi);
+    const LoadedField back = load_field("/tmp/kronop_cpp_io.kf");
+    const ComplexField& b2 = std::get<ComplexField>(back);
+    for (std::size_t k = 0; k < psi.size(); ++k) CHECK(b2[k] == psi[k]);
+    DeviceField<std::complex<double>> dpsi(ctx, psi);
+    dump_field("/tmp/kronop_cpp_io2.kf", ctx, dpsi);
+    const auto d2 = load_field<std::complex<double>>("/tmp/kronop_cpp_io2.kf", ctx).download();
+    for (std::size_t k = 0; k < psi.size(); ++k) CHECK(d2[k] == psi[k]);
+    std::printf("ok field io round trips\n");
+  }
+
   // errors.hpp: ParameterError on bad input through the C-ABI
   {
     bool threw = false;

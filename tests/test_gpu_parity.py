@@ -527,16 +527,20 @@ def test_folded_operator_matches_unfolded(ctx, spec):
     u = dev(K.uniform_pm1(31, n))
     psi = dev(K.seeded_complex_field(grid.shape, 32))
     for a, b in ((fo.apply(u), op.apply(u)), (fo.solve(u), op.solve(u)),
-                 (fo.apply(psi), op.apply(psi)), (fo.solve(psi), op.solve(psi)),
-                 (fo.propagate(psi, 0.11), op.propagate(psi, 0.11)),
-                 (fo.propagate(psi, -1.3), op.propagate(psi, -1.3))):
+                 (fo.apply(psi), op.apply(psi)), (fo.solve(psi), op.solve(psi))):
         assert rel(host(a), host(b)) < 1e-12
+    # the two factorisations' eigenvalues differ by rounding (~eps lambda_max), which the phase
+    # multiplies by dt: bound the propagate difference by that, not by a fixed 1e-12
+    lmax = max(abs(fo.info()[2]), 1.0)
+    for dt in (0.11, -1.3):
+        bound = max(1e-12, 64 * 2.2e-16 * lmax * abs(dt))
+        assert rel(host(fo.propagate(psi, dt)), host(op.propagate(psi, dt))) < bound
     v2 = grid.sample(lambda c: 2.0 * np.exp(-sum((ci - 0.3) ** 2 for ci in c)))
     fa, fb = A.FullOperator(fo, dev(v2)), A.FullOperator(op, dev(v2))
     assert rel(host(fa.apply(u, sigma=0.7)), host(fb.apply(u, sigma=0.7))) < 1e-12
     inplace = psi.clone()
     fo.propagate(inplace, 0.2, out=inplace)
-    assert rel(host(inplace), host(op.propagate(psi, 0.2))) < 1e-12
+    assert rel(host(inplace), host(op.propagate(psi, 0.2))) < max(1e-12, 64 * 2.2e-16 * lmax * 0.2)
     s0, lo0, hi0 = op.info()
     s1, lo1, hi1 = fo.info()
     assert s0 == s1 and abs(lo0 - lo1) <= 1e-12 * abs(hi0) and abs(hi0 - hi1) <= 1e-12 * abs(hi0)
@@ -613,3 +617,21 @@ def test_hermite_grid_criterion6(ctx):
     assert rel(host(u), ko.solve(f)) < 1e-13
     psi = K.seeded_complex_field(g99.shape, 7)
     assert rel(host(h.propagate(dev(psi), 0.01)), ko.propagate(psi, 0.01)) < 1e-13
+
+
+def test_field_io_device_streaming(ctx, tmp_path):
+    """Device dump/load (pinned double-buffered streaming) against the oracle's reader/writer,
+    on a field larger than one 32 MiB staging chunk (real) and a complex field."""
+    A = api()
+    shape = (160, 160, 200)  # 5.1 M doubles = 41 MB: two chunks
+    x = A.splitmix_uniform(ctx, 9, int(np.prod(shape)))
+    p = str(tmp_path / "x.kf")
+    A.dump_field(p, x, shape, ctx=ctx)
+    got, shp = K.load_field(p)
+    assert shp == shape and np.array_equal(got, host(x))
+    y, shp2, cplx = A.load_field(p, ctx=ctx)
+    assert shp2 == shape and not cplx and torch.equal(y, x)
+    z = K.seeded_complex_field((31, 17, 9), 4)
+    K.dump_field(p, z, (31, 17, 9))
+    zt, _, cplx = A.load_field(p, ctx=ctx)
+    assert cplx and np.array_equal(host(zt), z)

@@ -1,0 +1,155 @@
+"""The experiment harness (proj/src/harness.cpp, config.cpp, csv.cpp) on the B200 path: config
+grammar and CSV format on the CPU, every command end to end on the GPU against the oracle."""
+import csv
+import os
+
+import numpy as np
+import pytest
+
+from oracle import kronop_oracle as K
+
+
+def H():
+    from paper_2605_20491_b200 import harness
+    return harness
+
+
+def test_config_grammar_and_errors():
+    """config.cpp:37-73 grammar, typed getters and their error messages."""
+    from paper_2605_20491_b200 import ParameterError
+    h = H()
+    cfg = h.Config.parse_string("# c\n[run]\ncommand = solve  # trailing\n[grid]\ncells = 4, 8\n"
+                                "L=2.5\n[pcg]\nhistory = true\n", "t.cfg")
+    assert cfg.require_string("run.command") == "solve"
+    assert cfg.get_int_list("grid.cells", [8]) == [4, 8]
+    assert cfg.get_real("grid.L", 8.0) == 2.5
+    assert cfg.get_bool("pcg.history", False) is True
+    assert cfg.get_real("pcg.tol", 1e-12) == 1e-12
+    assert cfg.resolved["pcg.tol"] == "9.9999999999999998e-13"  # precision-17 default, as C++
+    cfg.check_all_consumed()
+    for text, msg in (("[run\n", "unterminated section header"), ("[]\n", "empty section name"),
+                      ("x = 1\n", "key outside any"), ("[a]\nb\n", "expected key = value"),
+                      ("[a]\n = 1\n", "empty key"), ("[a]\nb=1\nb=2\n", "duplicate key a.b")):
+        with pytest.raises(ParameterError, match=msg):
+            h.Config.parse_string(text)
+    c2 = h.Config.parse_string("[a]\nx = 1.5e\ny = 3.0\nz = maybe\nw = 1,x\n")
+    with pytest.raises(ParameterError, match="bad number for a.x"):
+        c2.get_real("a.x", 0.0)
+    with pytest.raises(ParameterError, match="bad integer for a.y"):
+        c2.get_int("a.y", 0)
+    with pytest.raises(ParameterError, match="expected true/false"):
+        c2.get_bool("a.z", False)
+    with pytest.raises(ParameterError, match="bad list entry"):
+        c2.get_real_list("a.w", [])
+    c3 = h.Config.parse_string("[a]\nused = 1\nunused = 2\n")
+    c3.get_int("a.used", 0)
+    with pytest.raises(ParameterError, match="unknown key a.unused"):
+        c3.check_all_consumed()
+
+
+def test_csv_format(tmp_path):
+    """csv.cpp:18-32: %.13e doubles, %d integers, strings verbatim."""
+    h = H()
+    p = str(tmp_path / "x.csv")
+    w = h.CsvWriter(p, ["a", "b", "c", "d"])
+    w.row([1.0 / 3.0, 7, "", "true"])
+    w.close()
+    assert open(p).read() == "a,b,c,d\n3.3333333333333e-01,7,,true\n"
+
+
+def _run(tmp_path, text, ctx):
+    h = H()
+    cfg_path = str(tmp_path / "run.cfg")
+    with open(cfg_path, "w") as f:
+        f.write(text)
+    out = str(tmp_path / "out")
+    rc = h.run_to_exit_code(cfg_path, False, out, ctx=ctx)
+    return rc, out
+
+
+def _rows(path):
+    with open(path) as f:
+        return list(csv.DictReader(f))
+
+
+@pytest.mark.gpu
+def test_harness_solve_manufactured_and_outputs(ctx, tmp_path):
+    """cmd_solve (harness.cpp:212-283) on two SEM levels, manufactured rhs: the l2 error equals
+    the oracle's solve of the same problem; checkpoint and slice outputs are written."""
+    rc, out = _run(tmp_path, "[run]\ncommand = solve\n[grid]\nL = 1.0\ndegree = 6\ncells = 3, 4\n"
+                   "dimension = 3\n[potential]\nkind = sep-osc\namplitude = 1600\nquad = 1, 2, 3\n"
+                   "[output]\ncheckpoint = u.kf\nslice_csv = s.csv\nslice_res = 5\n", ctx)
+    assert rc == 0
+    rows = _rows(os.path.join(out, "solve.csv"))
+    assert [int(r["n"]) for r in rows] == [17, 23]
+    for r, cells in zip(rows, (3, 4)):
+        g = K.Grid.sem(1.0, cells, 6, 3)
+        pot = K.build_potential("sep-osc", g, osc_amplitude=1600.0, quad_coeffs=[1.0, 2.0, 3.0])
+        op = g.separable_operator(pot.separable)
+        us = g.sample(lambda c: np.sin(np.pi * c[0]) * np.sin(2 * np.pi * c[1]) * np.sin(3 * np.pi * c[2]))
+        lap = sum(((a + 1) * np.pi) ** 2 for a in range(3))
+        rhs = (lap + K.separable_sum_field(g, pot)) * us
+        u = op.solve(rhs)
+        err = np.linalg.norm(u - us) / np.linalg.norm(us)
+        assert abs(float(r["l2_rel_err"]) - err) <= 1e-9 * err
+        assert float(r["residual"]) < 1e-12 and int(r["pcg_iters"]) == 0
+    u_file, shape = K.load_field(os.path.join(out, "u.kf"))
+    assert shape == (23, 23, 23)
+    assert len(_rows(os.path.join(out, "s.csv"))) == 25
+    man = open(os.path.join(out, "manifest.txt")).read()
+    assert "run.command = solve" in man and "grid.cells = 3, 4" in man
+
+
+@pytest.mark.gpu
+def test_harness_pcg_bench_and_ground_state(ctx, tmp_path):
+    """cmd_pcg_bench (acceptance criterion 3 setup) iteration counts equal the oracle's; the
+    multilevel ground state writes one CSV row per level (criterion 7 pipeline)."""
+    rc, out = _run(tmp_path, "[run]\ncommand = pcg-bench\n[grid]\nL = 8\ndegree = 6\ncells = 8\n"
+                   "[potential]\nkind = stirrer\n[pcg]\ntol = 1e-8\nhistory = true\n", ctx)
+    assert rc == 0
+    r = _rows(os.path.join(out, "pcg_bench.csv"))[0]
+    g = K.Grid.sem(8.0, 8, 6, 3)
+    kop = K.build_full_operator(g, K.build_potential("stirrer", g))
+    krep = K.pcg(kop.apply, kop.sep.solve, K.seeded_field(g.shape, 1), np.zeros(g.node_count()),
+                 K.PcgConfig(rel_tol=1e-8))
+    assert int(r["iterations"]) == krep.iterations and r["converged"] == "true"
+    assert len(_rows(os.path.join(out, "pcg_history_n47.csv"))) == krep.iterations + 1
+    rc, out = _run(tmp_path, "[run]\ncommand = ground-state\noutput_dir = x\n[grid]\nL = 8\n"
+                   "degree = 20\ncells = 2, 4\n[potential]\nkind = stirrer\n", ctx)
+    assert rc == 0
+    rows = _rows(os.path.join(out, "ground_state.csv"))
+    assert [int(x["n"]) for x in rows] == [39, 79]
+    assert abs(float(rows[-1]["eigenvalue"]) - 5.286155366963) < 1e-6 * 5.3
+
+
+@pytest.mark.gpu
+def test_harness_gpe_propagate_clustering_and_exit_codes(ctx, tmp_path):
+    rc, out = _run(tmp_path, "[run]\ncommand = gpe\n[grid]\nL = 8\ndegree = 6\ncells = 3\n"
+                   "[potential]\nkind = sep-osc\n[gpe]\nbeta = 10\nflow = au\ntol = 1e-10\n", ctx)
+    assert rc == 0
+    rows = _rows(os.path.join(out, "gpe.csv"))
+    e = [float(x["energy"]) for x in rows]
+    assert all(b <= a * (1 + 1e-13) for a, b in zip(e, e[1:]))
+    rc, out = _run(tmp_path, "[run]\ncommand = convergence-table\n[grid]\nL = 8\ndegree = 5\n"
+                   "cells = 6\n[potential]\nkind = sep-osc\n[propagate]\nmerge = true\nT = 0.1\n"
+                   "dt_list = 0.02, 0.01, 0.005\n", ctx)
+    assert rc == 0
+    rows = _rows(os.path.join(out, "propagate.csv"))
+    assert rows[0]["rate"] == "" and 1.8 <= float(rows[2]["rate"]) <= 2.2
+    assert max(float(x["mass_norm_drift"]) for x in rows) < 1e-12
+    rc, out = _run(tmp_path, "[run]\ncommand = clustering\n[grid]\nL = 8\ndegree = 8\ncells = 2\n"
+                   "[potential]\nkind = stirrer\n", ctx)
+    assert rc == 0
+    r = _rows(os.path.join(out, "clustering.csv"))[0]
+    g = K.Grid.sem(8.0, 2, 8, 3)
+    pot = K.build_potential("stirrer", g)
+    ops = [K.dense_sym_axis_operator(g.axes[a], pot.separable[a]) for a in range(3)]
+    _, outl, kappa = K.clustering_report(ops, pot.nonseparable, 0.1)
+    assert int(r["outliers"]) == outl and abs(float(r["condition"]) - kappa) < 1e-9 * kappa
+    rc, out = _run(tmp_path, "[run]\ncommand = clustering\n[grid]\nL = 8\ndegree = 25\ncells = 2\n"
+                   "dimension = 1\n[potential]\nkind = stirrer\n", ctx)
+    assert rc == 2  # stirrer needs a 3D grid: ParameterError -> exit code 2
+    rc, out = _run(tmp_path, "[run]\ncommand = solve\n[grid]\ncells = 3\nbogus = 1\n", ctx)
+    assert rc == 2  # unknown key
+    rc, out = _run(tmp_path, "[run]\ncommand = solve\n[grid]\ndegree = 10\ncells = 60\n", ctx)
+    assert rc == 4  # > 2e8 scalars without allow_large

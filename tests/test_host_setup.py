@@ -237,3 +237,41 @@ def test_hermite_error_codes():
         A.hermite_basis(746)
     with pytest.raises(ParameterError):
         A.build_axis(A.hermite_basis(5), lambda x: float("inf"))
+
+
+def test_field_io_host_round_trip_and_oracle_format(tmp_path):
+    """dump_field / load_field (fieldio.cpp:28-73) through the C-ABI host entry points: the
+    product's files load in the oracle's restatement of the reference reader and vice versa,
+    bit for bit, for real and complex fields; the reference's error cases raise ParameterError."""
+    from paper_2605_20491_b200 import ParameterError
+    A = api()
+    shape = (5, 3, 4)
+    x = K.uniform_pm1(5, 60)
+    z = K.seeded_complex_field(shape, 6)
+    for data in (x, z):
+        p1, p2 = str(tmp_path / "a.kf"), str(tmp_path / "b.kf")
+        A.dump_field(p1, data, shape)
+        got, shp = K.load_field(p1)
+        assert shp == shape and np.array_equal(got, data)
+        K.dump_field(p2, data, shape)
+        back, shp2, cplx = A.load_field(p2)
+        assert shp2 == shape and cplx == np.iscomplexobj(data) and np.array_equal(back, data)
+        assert open(p1, "rb").read() == open(p2, "rb").read()
+    bad = tmp_path / "bad.kf"
+    raw = bytearray(open(str(tmp_path / "a.kf"), "rb").read())
+    for mutate, msg in ((lambda r: r.__setitem__(slice(0, 4), b"XXXX"), "bad magic"),
+                        (lambda r: r.__setitem__(slice(4, 8), (2).to_bytes(4, "little")), "bad version"),
+                        (lambda r: r.__setitem__(slice(8, 12), (10).to_bytes(4, "little")), "bad dimension"),
+                        (lambda r: r.__setitem__(slice(12, 16), (7).to_bytes(4, "little")), "unknown scalar kind")):
+        r = bytearray(raw)
+        mutate(r)
+        bad.write_bytes(bytes(r))
+        with pytest.raises(ParameterError, match=msg):
+            A.load_field(str(bad))
+        with pytest.raises(K.ParameterError, match=msg):
+            K.load_field(str(bad))
+    bad.write_bytes(bytes(raw[:-8]))
+    with pytest.raises(ParameterError, match="truncated"):
+        A.load_field(str(bad))
+    with pytest.raises(ParameterError, match="cannot open"):
+        A.load_field(str(tmp_path / "missing.kf"))
