@@ -47,6 +47,17 @@ def load_peaks():
     return peaks
 
 
+def load_pass_traffic():
+    """DRAM bytes per 1024^3 pass of the dominant kernel from the committed `ncu --set full`
+    capture (dram__bytes_read.sum + dram__bytes_write.sum), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_full_pass1024.json")) as f:
+            m = json.load(f)
+        return m["traffic_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 class ClockSampler:
     def __init__(self, gpu_index=0):
         self.proc = None
@@ -223,6 +234,33 @@ def secondary_metrics(A, P, ctx, device):
                   "L=8), A=-Delta, B=sep-osc V, box psi0, dt=5e-3, T=0.1 (PAPER.md:1381 setup)"}
     del lap, bdiag, psi0, state
     torch.cuda.empty_cache()
+    # BASELINE config 5 kernels: one complex propagate of the kinetic split (the A-step of
+    # qHOP/Strang) on the 6D n = 29 and 9D n = 9 grids (fused_rot kernel)
+    for name, (L_, cells, k, d) in {"6d_n29": (5.0, 3, 10, 6), "9d_n9": (3.0, 2, 5, 9)}.items():
+        g = A.Grid.sem(L_, cells, k, d)
+        lap = g.laplacian(ctx)
+        N = g.node_count()
+        psi = torch.view_as_complex(A.splitmix_uniform(ctx, 3, 2 * N).view(-1, 2))
+        o = torch.empty_like(psi)
+        lap.propagate(psi, 0.005, out=o)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        for _ in range(3):
+            lap.propagate(psi, 0.005, out=o)
+        e1.record(ctx.stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 3e3
+        n = g.shape[0]
+        out["config5_propagate_" + name] = {
+            "value": t * 1e3, "unit": "ms", "dof": N, "d": d, "n": n,
+            "hbm_gbs_equiv": 2 * 3 * 2 * 16 * N / t / 1e9,
+            "tflops": 8.0 * d * n * N / t / 1e12,
+            "config": "exp(-i dt (-Delta)) on %dD SEM n=%d complex128 (BASELINE configs[5] "
+                      "kinetic step; fused_rot kernel, 2 x 3 field round trips)" % (d, n)}
+        del lap, psi, o
+        torch.cuda.empty_cache()
     return out
 
 
@@ -363,7 +401,9 @@ def run_kronop(args):
             "tflops": 12.0 * n ** 4 / t_step / 1e12,
             "roofline": {"bound": "tensor", "achieved": achieved,
                          "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                         "frac": achieved / peaks["fp64_tflops"], "traffic": None,
+                         "frac": achieved / peaks["fp64_tflops"],
+                         "traffic": load_pass_traffic(),
+                         "traffic_algorithmic": 16 * N,
                          "kernel": "mode_product_kernel (FP64 DMMA), 1024^3 pass = 2 n^4 flops",
                          "per_axis_ms": [t * 1e3 for t in per_axis],
                          "peak_src": peaks["fp64_src"]},

@@ -716,8 +716,23 @@ int kronop_op_create(kronop_ctx* ctx, int d, const int* n, const double* const* 
         op->n[a] = n[a];
         op->N *= n[a];
         op->hlam[a].assign(lambda[a], lambda[a] + n[a]);
-        op->lda[a] = upload_padded(*ctx, Tinv[a], n[a], n[a], &op->fwd[a], true);
-        upload_padded(*ctx, T[a], n[a], n[a], &op->bwd[a], true);
+        // an axis identical to an earlier one (isotropic grids) shares its device transforms:
+        // less memory, and the small-extent kernel can keep one matrix in registers for a group
+        int same = -1;
+        const size_t nn = static_cast<size_t>(n[a]) * n[a];
+        for (int b = 0; b < a && same < 0; ++b)
+          if (n[b] == n[a] && !std::memcmp(T[a], T[b], nn * sizeof(double)) &&
+              !std::memcmp(Tinv[a], Tinv[b], nn * sizeof(double)))
+            same = b;
+        if (same >= 0) {
+          op->fwd[a] = op->fwd[same];
+          op->bwd[a] = op->bwd[same];
+          op->lda[a] = op->lda[same];
+          op->shared_axis[a] = true;
+        } else {
+          op->lda[a] = upload_padded(*ctx, Tinv[a], n[a], n[a], &op->fwd[a], true);
+          upload_padded(*ctx, T[a], n[a], n[a], &op->bwd[a], true);
+        }
         KCUDA(cudaMalloc(&op->lam[a], n[a] * sizeof(double)));
         KCUDA(cudaMemcpy(op->lam[a], lambda[a], n[a] * sizeof(double), cudaMemcpyHostToDevice));
         // direct-sum extremes in axis order from 0.0 (operators.cpp:13-15; rounding is
@@ -808,8 +823,10 @@ int kronop_op_destroy(kronop_op* op) {
     for (int a = 0; a < KRONOP_MAX_DIM; ++a) {
       for (double* p : {op->fe[a], op->fo[a], op->be[a], op->bo[a]})
         if (p) cudaFree(p);
-      if (op->fwd[a]) cudaFree(op->fwd[a]);
-      if (op->bwd[a]) cudaFree(op->bwd[a]);
+      if (!op->shared_axis[a]) {
+        if (op->fwd[a]) cudaFree(op->fwd[a]);
+        if (op->bwd[a]) cudaFree(op->bwd[a]);
+      }
       if (op->lam[a]) cudaFree(op->lam[a]);
       if (op->mass[a]) cudaFree(op->mass[a]);
     }

@@ -55,6 +55,7 @@ struct kronop_op {
   double shift = 0.0, lmin = 0.0, lmax = 0.0;
   // even/odd folded operator (kronop_op_create_folded): per axis the half-size blocks; lam[a] is
   // in folded order [even modes | odd modes]; bwd[a] holds the ground-state column only.
+  bool shared_axis[KRONOP_MAX_DIM] = {};  // fwd/bwd alias an earlier identical axis
   bool folded = false;
   int ne[KRONOP_MAX_DIM] = {}, no[KRONOP_MAX_DIM] = {};
   double* fe[KRONOP_MAX_DIM] = {};

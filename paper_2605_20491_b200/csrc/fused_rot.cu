@@ -34,8 +34,10 @@ namespace kronop_dev {
 
 namespace {
 
-constexpr int RT_THREADS = 512;
-constexpr int RT_WARPS = RT_THREADS / 32;
+// threads per CTA: 16 warps for the DMMA path (latency hiding), 8 for the DFMA path (the n x n
+// matrix lives in registers: 2 n^2 + O(n) registers per thread)
+template <int DN>
+__host__ __device__ constexpr int rt_threads() { return DN > 0 ? 256 : 512; }
 constexpr int RT_MAXF = 3;
 constexpr int RT_STAGES = 3;
 constexpr int RT_TILE = 8192;  // doubles per stage (64 KB)
@@ -54,6 +56,7 @@ struct RotArgs {
   const double* a[RT_MAXF];
   int lda[RT_MAXF];
   int kpat[RT_MAXF];     // k permutation per axis (kidx)
+  int uniform;           // every group axis has the same matrix
   float inv_n[RT_MAXF];  // 1 / n_j (fast_div)
   int epi;               // EPI_STORE / EPI_SPEC_* / EPI_AXPY_DIAG
   double shift, dt, sigma;
@@ -135,14 +138,14 @@ __device__ __forceinline__ int kidx(int pat, int t, int kk) {
 // axis at stride S; each warp takes 8 x G fibers per step on DMMA (k = fiber element, n = output
 // index). The axis' B fragments come from shared memory (fragment order, conflict free) once per
 // tile, so only one axis' matrix occupies registers.
-template <int K4, int NT, int G>
+template <int K4, int NT, int G, int THREADS>
 __device__ __forceinline__ void axis_inplace(double* tile, const double* frag, const int (&koff)[K4],
                                              int m, int S, int nfib, int warp, int lane) {
   const int t = lane & 3, g = lane >> 2;
   const double* fl = frag + lane;
   const float invS = 1.0f / static_cast<float>(S);
   const int Sm = S * m;
-  for (int f0 = warp * 8 * G; f0 < nfib; f0 += 8 * G * RT_WARPS) {
+  for (int f0 = warp * 8 * G; f0 < nfib; f0 += 8 * G * (THREADS / 32)) {
     const double* src[G];
     bool fok[G];
 #pragma unroll
@@ -184,35 +187,36 @@ __device__ __forceinline__ void axis_inplace(double* tile, const double* frag, c
   }
 }
 
-// Small extents (n <= 12): the DMMA tiles would be mostly padding (n = 9 fills 42% of a K12 x N16
+// Small extents (n <= 10): the DMMA tiles would be mostly padding (n = 9 fills 42% of a K12 x N16
 // tile), so each thread contracts whole fibers with DFMA: it reads its n inputs, forms the n
 // outputs against the matrix (shared memory, row-major with an even row pitch, read as 16-byte
 // broadcasts) and writes them back in place.
 template <int N>
-__device__ __forceinline__ void axis_dfma(double* tile, const double* mat, int S, int nfib,
-                                          int tid) {
+__device__ __forceinline__ void load_matrix(double (&M)[N][N], const double* mat) {
   constexpr int NP = (N + 1) & ~1;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int k = 0; k < N; ++k) M[i][k] = mat[i * NP + k];
+}
+
+template <int N, int THREADS>
+__device__ __forceinline__ void axis_dfma(double* tile, const double (&M)[N][N], int S, int nfib,
+                                          int tid) {
   const float invS = 1.0f / static_cast<float>(S);
   const int Sm = S * N;
-  for (int f = tid; f < nfib; f += RT_THREADS) {
+  for (int f = tid; f < nfib; f += THREADS) {
     double* p = tile + f + fast_div(f, S, invS) * (Sm - S);
     double x[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) x[k] = p[k * S];
-    double y[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int k = 0; k < NP; k += 2) {
-        const double2 mk = *reinterpret_cast<const double2*>(mat + i * NP + k);
-        acc = fma(mk.x, x[k], acc);
-        if (k + 1 < N) acc = fma(mk.y, x[k + 1], acc);
-      }
-      y[i] = acc;
+      for (int k = 0; k < N; ++k) acc = fma(M[i][k], x[k], acc);
+      p[i * S] = acc;  // in place: the fiber's inputs are all in registers
     }
-#pragma unroll
-    for (int i = 0; i < N; ++i) p[i * S] = y[i];
   }
 }
 
@@ -239,7 +243,7 @@ __device__ __forceinline__ double group_lambda(const RotArgs& A, double lam_low,
 // writes one run of C * Qt contiguous doubles; complex fields move (re, im) pairs as 16-byte
 // units (one sincos per pair for the phase). Epilogues: spectral (last forward group) or the
 // V2 / sigma AXPY (last backward group).
-template <int NF>
+template <int NF, int THREADS>
 __device__ __forceinline__ void store_tile(const RotArgs& A, const double* tile, long long q0,
                                            int qv, const double* lam_low, int tid) {
   const int C = A.C, F = A.F, Qt = A.Qt;
@@ -247,11 +251,11 @@ __device__ __forceinline__ void store_tile(const RotArgs& A, const double* tile,
   const int units = Qt * F;  // (re, im) pairs or real scalars
   const bool spectral = A.epi == EPI_SPEC_MUL || A.epi == EPI_SPEC_DIV || A.epi == EPI_SPEC_PHASE;
   const float invQt = 1.0f / static_cast<float>(Qt);
-#pragma unroll 2
-  for (int u = tid; u < units; u += RT_THREADS) {
+#pragma unroll 4
+  for (int u = tid; u < units; u += THREADS) {
     const int g = fast_div(u, Qt, invQt);
     const int qi = u - g * Qt;
-    if (qi >= qv) continue;
+    if (qi >= qv) continue;  // partial last tile only
     const long long gi = static_cast<long long>(C) * (q0 + qi) + CQ * g;
     const double* sp = tile + C * (g + F * qi);
     if (C == 2) {
@@ -302,7 +306,8 @@ __device__ __forceinline__ void store_tile(const RotArgs& A, const double* tile,
 }
 
 template <int NF, int K4, int NT, int DN>
-__global__ void __launch_bounds__(RT_THREADS, 1) fused_rot_kernel(const __grid_constant__ RotArgs A) {
+__global__ void __launch_bounds__(rt_threads<DN>(), 1) fused_rot_kernel(const __grid_constant__ RotArgs A) {
+  constexpr int THREADS = rt_threads<DN>();
   constexpr int G = NT >= 3 ? 2 : (NT == 2 ? 2 : 4);  // 8 G NT independent DMMA chains per warp
   // DN > 0: DFMA path with n = DN on every group axis (matrices row-major, pitch DNP);
   // DN == 0: DMMA path (B fragments in fragment order)
@@ -311,8 +316,9 @@ __global__ void __launch_bounds__(RT_THREADS, 1) fused_rot_kernel(const __grid_c
   extern __shared__ __align__(128) double sm[];
   double* stages = sm;                                   // RT_STAGES x RT_TILE
   double* frags = stages + RT_STAGES * RT_TILE;          // NF x FRAG
-  double* lam_low = frags + NF * FRAG;                   // <= 64 (Qt)
-  uint64_t* full = reinterpret_cast<uint64_t*>(lam_low + 64);
+  double* lam_low2 = frags + NF * FRAG;                  // 2 x 64 (Qt), double-buffered per tile
+  uint64_t* full = reinterpret_cast<uint64_t*>(lam_low2 + 128);
+  int* done = reinterpret_cast<int*>(full + RT_STAGES);  // per-stage count of warps finished
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = lane & 3;
   const bool spectral = A.epi == EPI_SPEC_MUL || A.epi == EPI_SPEC_DIV || A.epi == EPI_SPEC_PHASE;
@@ -320,7 +326,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) fused_rot_kernel(const __grid_c
   // B fragments of every group axis in fragment order: frag[j][(kk NT + nt) 32 + lane] =
   // M_j(8 nt + lane/4, k(lane%4, kk)); zero outside the n x n matrix.
   for (int j = 0; j < NF; ++j)
-    for (int e = tid; e < FRAG; e += RT_THREADS) {
+    for (int e = tid; e < FRAG; e += THREADS) {
       int i, k;
       if (DN > 0) {
         i = e / DNP;
@@ -348,9 +354,12 @@ __global__ void __launch_bounds__(RT_THREADS, 1) fused_rot_kernel(const __grid_c
       S *= A.n[j];
     }
   }
-  for (int e = tid; e < RT_STAGES * RT_TILE; e += RT_THREADS) stages[e] = 0.0;  // finite padding
+  for (int e = tid; e < RT_STAGES * RT_TILE; e += THREADS) stages[e] = 0.0;  // finite padding
   if (tid == 0) {
-    for (int s = 0; s < RT_STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < RT_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      done[s] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
@@ -362,12 +371,15 @@ __global__ void __launch_bounds__(RT_THREADS, 1) fused_rot_kernel(const __grid_c
     }
 
   const int tile_elems = A.Qt * A.C * A.F;
+  double Mreg[DN > 0 ? DN : 1][DN > 0 ? DN : 1];  // DFMA path: the axis matrix in registers
+  bool mloaded = false;
   int it = 0;
   for (long long tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++it) {
     const int s = it % RT_STAGES;
     double* buf = stages + s * RT_TILE;
     const long long q0 = tile * A.Qt;
     const int qv = static_cast<int>(A.Q - q0 < A.Qt ? A.Q - q0 : A.Qt);
+    double* lam_low = lam_low2 + 64 * (it & 1);  // warps may still store the previous tile
     if (spectral && tid < A.Qt) {  // lambda of the axes below the group, axis order from 0.0
       long long q = q0 + tid;
       double lam = 0.0;
@@ -384,20 +396,32 @@ __global__ void __launch_bounds__(RT_THREADS, 1) fused_rot_kernel(const __grid_c
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
       const int m = A.n[j];
-      if constexpr (DN > 0)
-        axis_dfma<DN>(buf, frags + j * FRAG, S, tile_elems / DN, tid);
-      else
-        axis_inplace<K4, NT, G>(buf, frags + j * FRAG, koff[j], m, S, tile_elems / m, warp, lane);
+      if constexpr (DN > 0) {
+        // one matrix for the whole group (isotropic grid): loaded once per CTA, below
+        if (!A.uniform || !mloaded) load_matrix<DN>(Mreg, frags + j * FRAG);
+        mloaded = true;
+        axis_dfma<DN, THREADS>(buf, Mreg, S, tile_elems / DN, tid);
+      } else
+        axis_inplace<K4, NT, G, THREADS>(buf, frags + j * FRAG, koff[j], m, S, tile_elems / m,
+                                         warp, lane);
       S *= m;
       __syncthreads();
     }
-    store_tile<NF>(A, buf, q0, qv, lam_low, tid);
-    __syncthreads();  // stage s fully consumed
-    if (tid == 0) {
-      const long long next = tile + static_cast<long long>(RT_STAGES) * gridDim.x;
-      if (next < A.ntiles) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        issue_tile(A, next, buf, &full[s]);
+    store_tile<NF, THREADS>(A, buf, q0, qv, lam_low, tid);
+    // No CTA barrier here: a warp that has stored its share moves on to the next tile's first
+    // axis (another stage) while the others finish storing. The last warp to finish with stage
+    // s refills it.
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&done[s], 1) == THREADS / 32 - 1) {
+        done[s] = 0;
+        __threadfence_block();
+        const long long next = tile + static_cast<long long>(RT_STAGES) * gridDim.x;
+        if (next < A.ntiles) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          issue_tile(A, next, buf, &full[s]);
+        }
       }
     }
   }
@@ -406,8 +430,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1) fused_rot_kernel(const __grid_c
 template <int NF, int K4, int NT, int DN>
 constexpr size_t rot_smem_bytes() {
   constexpr int FRAG = DN > 0 ? DN * ((DN + 1) & ~1) : K4 * NT * 32;
-  return (static_cast<size_t>(RT_STAGES) * RT_TILE + NF * FRAG + 64) * sizeof(double) +
-         RT_STAGES * sizeof(uint64_t);
+  return (static_cast<size_t>(RT_STAGES) * RT_TILE + NF * FRAG + 128) * sizeof(double) +
+         RT_STAGES * (sizeof(uint64_t) + sizeof(int));
 }
 
 template <int NF, int K4, int NT, int DN = 0>
@@ -423,7 +447,7 @@ void launch_rot(cudaStream_t s, const RotArgs& a) {
   }();
   const long long grid = a.ntiles < grid_cap ? a.ntiles : grid_cap;
   fused_rot_kernel<NF, K4, NT, DN>
-      <<<static_cast<unsigned>(grid), RT_THREADS, rot_smem_bytes<NF, K4, NT, DN>(), s>>>(a);
+      <<<static_cast<unsigned>(grid), rt_threads<DN>(), rot_smem_bytes<NF, K4, NT, DN>(), s>>>(a);
   KCUDA(cudaGetLastError());
 }
 
@@ -515,6 +539,8 @@ void launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int 
     S *= n[j];
   }
   for (int j = 0; j < f; ++j) a.inv_n[j] = 1.0f / static_cast<float>(n[j]);
+  a.uniform = 1;
+  for (int j = 1; j < f; ++j) a.uniform &= (mats[j] == mats[0] && lda[j] == lda[0]) ? 1 : 0;
   a.epi = epi.kind;
   a.shift = epi.shift;
   a.dt = epi.dt;
@@ -533,14 +559,14 @@ void launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int 
     const char* e = getenv("KRONOP_ROT_NO_DFMA");  // A/B switch: DMMA for every extent
     return e && e[0] == '1';
   }();
-  if (same && maxn >= 2 && maxn <= 12 && !no_dfma) {
+  if (same && maxn >= 2 && maxn <= 10 && !no_dfma) {
     switch (f * 16 + maxn) {
 #define RT_DF(F, N) \
   case F * 16 + N: launch_rot<F, 1, 1, N>(s, a); return;
       RT_DF(1, 2) RT_DF(1, 3) RT_DF(1, 4) RT_DF(1, 5) RT_DF(1, 6) RT_DF(1, 7) RT_DF(1, 8)
-      RT_DF(1, 9) RT_DF(1, 10) RT_DF(1, 11) RT_DF(1, 12)
+      RT_DF(1, 9) RT_DF(1, 10)
       RT_DF(2, 2) RT_DF(2, 3) RT_DF(2, 4) RT_DF(2, 5) RT_DF(2, 6) RT_DF(2, 7) RT_DF(2, 8)
-      RT_DF(2, 9) RT_DF(2, 10) RT_DF(2, 11) RT_DF(2, 12)
+      RT_DF(2, 9) RT_DF(2, 10)
       RT_DF(3, 2) RT_DF(3, 3) RT_DF(3, 4) RT_DF(3, 5) RT_DF(3, 6) RT_DF(3, 7) RT_DF(3, 8)
       RT_DF(3, 9) RT_DF(3, 10)
 #undef RT_DF

@@ -152,13 +152,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int KT = (args.nk + BK - 1) / BK;
-  // Persistent CTAs: CTA b owns the row panels b, b + gridDim.x, ... and walks all N-tiles of a
-  // panel back to back, so the panel's X rows are re-read from L2 (hot) and the per-axis matrix
-  // stays L2-resident. The k-stage counter `it` runs across tiles, so the producer streams the
-  // next tile's first stages while the consumers run the current tile's epilogue.
-  const long long my_panels =
-      blockIdx.x < args.ntiles_m ? (args.ntiles_m - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const long long my_tiles = my_panels * args.ntiles_n;
+  // Persistent CTAs over the tile sequence T = blockIdx.x + lt * gridDim.x with the N-tiles of
+  // a row panel consecutive in T: the ~148 tiles in flight cover ~148 / ntiles_n panels, whose X
+  // rows (1 MB each at n = 1024) stay L2-resident while all N-tiles of the panel consume them, so
+  // X is read from HBM once (a CTA walking all N-tiles of its own panel keeps 148 panels live,
+  // more than L2, and re-reads X ntiles_n times). The per-axis matrix stays L2-resident. The
+  // k-stage counter `it` runs across tiles, so the producer streams the next tile's first stages
+  // while the consumers run the current tile's epilogue.
+  const long long total_tiles = args.ntiles_m * args.ntiles_n;
+  const long long my_tiles =
+      blockIdx.x < total_tiles ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const long long total_it = my_tiles * KT;
 
   if (tid == 0) {
@@ -180,9 +183,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int box_p[BM / 16], box_q[BM / 16];
   auto producer_tile = [&](long long lt) {
     p_tile = lt;
-    const long long panel = blockIdx.x + (lt / args.ntiles_n) * gridDim.x;
+    const long long T = blockIdx.x + lt * gridDim.x;
+    const long long panel = T / args.ntiles_n;
     p_row0 = panel * BM;
-    p_col0 = static_cast<int>(lt % args.ntiles_n) * BN;
+    p_col0 = static_cast<int>(T - panel * args.ntiles_n) * BN;
     if (LOADER == TL_STRIDED && !args.x2d) {
       // (p, q) of each 16-row box (pre % 16 == 0: a box never straddles two q)
       long long q = p_row0 / args.pre;
@@ -264,8 +268,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int slot = 0;
   uint32_t phase = 0;
   for (long long lt = 0; lt < my_tiles; ++lt) {
-    const long long row0 = (blockIdx.x + (lt / args.ntiles_n) * gridDim.x) * BM;
-    const int col0 = static_cast<int>(lt % args.ntiles_n) * BN;
+    const long long T = blockIdx.x + lt * gridDim.x;
+    const long long panel = T / args.ntiles_n;
+    const long long row0 = panel * BM;
+    const int col0 = static_cast<int>(T - panel * args.ntiles_n) * BN;
     double acc[C::RT][C::CT][2];
 #pragma unroll
     for (int i = 0; i < C::RT; ++i)
@@ -487,7 +493,8 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
-  const long long blocks = ta.ntiles_m < num_sms ? ta.ntiles_m : num_sms;  // one CTA per SM
+  const long long tiles = ta.ntiles_m * ta.ntiles_n;
+  const long long blocks = tiles < num_sms ? tiles : num_sms;  // one CTA per SM
   if (cplx0) {
     if (bn == 128)
       mode_product_tma_kernel<128, TL_CPLX0><<<blocks, NTHREADS, Cfg<128>::SMEM, s>>>(tmx, tmA, ta);
