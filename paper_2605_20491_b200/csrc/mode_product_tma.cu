@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "epilogue.cuh"
 #include "kronop_internal.cuh"
@@ -100,6 +101,44 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+// multicast variants (thread-block clusters of CL CTAs along N share the X tile)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1,
+                                               uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
+      "cluster [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, int c0, int c1,
+                                               int c2, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
+      "cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// arrive on the mbarrier at the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ double2 lds128(const char* base, uint32_t byte_off) {
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n"
@@ -138,7 +177,7 @@ __device__ __forceinline__ int col_map(int jc, int n) {
   return (jc >> 1) * 16 + 2 * chS(n) + (jc & 1);
 }
 
-template <int BN, int LOADER>
+template <int BN, int LOADER, int CL>
 __global__ void __launch_bounds__(NTHREADS, 1)
     mode_product_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                             const __grid_constant__ CUtensorMap tma, const TArgs args) {
@@ -159,19 +198,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // more than L2, and re-reads X ntiles_n times). The per-axis matrix stays L2-resident. The
   // k-stage counter `it` runs across tiles, so the producer streams the next tile's first stages
   // while the consumers run the current tile's epilogue.
-  const long long total_tiles = args.ntiles_m * args.ntiles_n;
-  const long long my_tiles =
-      blockIdx.x < total_tiles ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  //
+  // Clusters (CL > 1): the CL CTAs of a cluster take CL consecutive N-tiles of the same row
+  // panel in lockstep; each CTA issues 1/CL of the X boxes of a stage as a TMA multicast to the
+  // whole cluster, so X crosses L2 -> SM once per cluster, and a stage is refilled only after
+  // all CL x 8 consumer warps of the cluster released it (remote mbarrier arrivals).
+  const uint32_t crank = CL > 1 ? cluster_rank() : 0;
+  const long long cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  const int ngroups = args.ntiles_n / CL;
+  const long long total_tiles = args.ntiles_m * ngroups;
+  const long long my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / ncl + 1 : 0;
   const long long total_it = my_tiles * KT;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCONS);
+      mbar_init(&empty[s], NCONS * CL);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync();  // peers' barriers are initialised before any remote arrive / multicast
+  else
+    __syncthreads();
 
   // ------------------------------------------------------------------ producer state --
   // Lane 0 of warp 0 is the TMA producer (a dedicated producer warp would cap the DMMA warps at
@@ -183,10 +232,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int box_p[BM / 16], box_q[BM / 16];
   auto producer_tile = [&](long long lt) {
     p_tile = lt;
-    const long long T = blockIdx.x + lt * gridDim.x;
-    const long long panel = T / args.ntiles_n;
+    const long long T = cid + lt * ncl;
+    const long long panel = T / ngroups;
     p_row0 = panel * BM;
-    p_col0 = static_cast<int>(T - panel * args.ntiles_n) * BN;
+    p_col0 = (static_cast<int>(T - panel * ngroups) * CL + static_cast<int>(crank)) * BN;
     if (LOADER == TL_STRIDED && !args.x2d) {
       // (p, q) of each 16-row box (pre % 16 == 0: a box never straddles two q)
       long long q = p_row0 / args.pre;
@@ -225,25 +274,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     unsigned char* as = xs + C::X_BYTES;
     mbar_expect_tx(&full[s], C::STAGE_BYTES);
     const int k0 = kt * BK;
+    constexpr uint16_t mask = static_cast<uint16_t>((1u << CL) - 1u);
+    auto x2 = [&](void* dst, int c0, int c1, int b) {
+      if (CL == 1)
+        tma_load_2d(dst, &tmx, c0, c1, &full[s]);
+      else if (b % CL == static_cast<int>(crank))
+        tma_load_2d_mc(dst, &tmx, c0, c1, &full[s], mask);
+    };
     if (LOADER == TL_STRIDED) {
 #pragma unroll
       for (int b = 0; b < BM / 16; ++b) {
-        if (args.x2d)
-          tma_load_2d(xs + b * BOX_STRIDED_BYTES, &tmx, static_cast<int>(p_row0) + 16 * b, k0,
-                      &full[s]);
-        else
+        if (args.x2d) {
+          x2(xs + b * BOX_STRIDED_BYTES, static_cast<int>(p_row0) + 16 * b, k0, b);
+        } else if (CL == 1) {
           tma_load_3d(xs + b * BOX_STRIDED_BYTES, &tmx, box_p[b], k0, box_q[b], &full[s]);
+        } else if (b % CL == static_cast<int>(crank)) {
+          tma_load_3d_mc(xs + b * BOX_STRIDED_BYTES, &tmx, box_p[b], k0, box_q[b], &full[s],
+                         mask);
+        }
       }
     } else if (LOADER == TL_CONTIG) {
 #pragma unroll
       for (int h = 0; h < BK / 16; ++h)
-        tma_load_2d(xs + h * BOX_CONTIG_BYTES, &tmx, k0 + 16 * h, static_cast<int>(p_row0),
-                    &full[s]);
+        x2(xs + h * BOX_CONTIG_BYTES, k0 + 16 * h, static_cast<int>(p_row0), h);
     } else {
 #pragma unroll
       for (int h = 0; h < BK / 8; ++h)
-        tma_load_2d(xs + h * BOX_CPLX0_BYTES, &tmx, 2 * (k0 + 8 * h),
-                    static_cast<int>(p_row0 >> 1), &full[s]);
+        x2(xs + h * BOX_CPLX0_BYTES, 2 * (k0 + 8 * h), static_cast<int>(p_row0 >> 1), h);
     }
 #pragma unroll
     for (int c = 0; c < BN / 16; ++c)
@@ -268,10 +325,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int slot = 0;
   uint32_t phase = 0;
   for (long long lt = 0; lt < my_tiles; ++lt) {
-    const long long T = blockIdx.x + lt * gridDim.x;
-    const long long panel = T / args.ntiles_n;
+    const long long T = cid + lt * ncl;
+    const long long panel = T / ngroups;
     const long long row0 = panel * BM;
-    const int col0 = static_cast<int>(T - panel * args.ntiles_n) * BN;
+    const int col0 = (static_cast<int>(T - panel * ngroups) * CL + static_cast<int>(crank)) * BN;
     double acc[C::RT][C::CT][2];
 #pragma unroll
     for (int i = 0; i < C::RT; ++i)
@@ -350,7 +407,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) {
+        if (CL == 1) {
+          mbar_arrive(&empty[s]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < CL; ++q) mbar_arrive_cluster(&empty[s], q);
+        }
+      }
     }
 
     // --------------------------------------------------------------------- epilogue --
@@ -385,6 +449,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   }
+  if (CL > 1) cluster_sync();  // no CTA leaves while peers may still arrive on its barriers
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -412,8 +477,90 @@ void encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims
 
 template <int BN, int LOADER>
 void set_attr_tma() {
-  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER>,
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 4>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+}
+
+// Largest grid (multiple of CL, <= #SMs) of co-resident CL-CTA clusters, 0 if none fit.
+template <int BN, int LOADER, int CL>
+int cluster_grid(int num_sms) {
+  static int grid = [num_sms] {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(num_sms / CL * CL));
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = Cfg<BN>::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, mode_product_tma_kernel<BN, LOADER, CL>, &cfg) !=
+        cudaSuccess) {
+      (void)cudaGetLastError();
+      return 0;
+    }
+    return n * CL < num_sms ? n * CL : num_sms / CL * CL;
+  }();
+  return grid;
+}
+
+template <int BN, int LOADER, int CL>
+void launch_cl(cudaStream_t s, int blocks, const CUtensorMap& tmx, const CUtensorMap& tmA,
+               const TArgs& ta) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = Cfg<BN>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KCUDA(cudaLaunchKernelEx(&cfg, mode_product_tma_kernel<BN, LOADER, CL>, tmx, tmA, ta));
+}
+
+// Cluster size. Default 1: measured on B200 (profiles/r01_tma_cluster_experiment.json), 2-CTA
+// clusters with X multicast cut the 1024^3 pass's DRAM reads from 33-43 GB to 14-19 GB (8.6 GB
+// algorithmic) but run 5% slower (a stage is refilled only when both CTAs released it, and 3
+// stages of 64 KB leave no slack), 4-CTA clusters reach 10 GB but lose 20-40% (fewer co-resident
+// CTAs). The pass is DMMA-bound, so time wins: KRONOP_TMA_CLUSTER=2|4 selects the cluster path.
+template <int BN, int LOADER>
+void launch_tma(cudaStream_t s, int num_sms, long long ntiles_m, int ntiles_n,
+                const CUtensorMap& tmx, const CUtensorMap& tmA, const TArgs& ta) {
+  static const int forced = [] {
+    const char* e = getenv("KRONOP_TMA_CLUSTER");
+    return e ? atoi(e) : 0;
+  }();
+  const long long tiles = ntiles_m * ntiles_n;
+  int cl = 1;
+  for (int c : {4, 2}) {
+    if (c != forced) continue;
+    if (ntiles_n % c != 0 || tiles < 4LL * num_sms) continue;
+    const int g = c == 4 ? cluster_grid<BN, LOADER, 4>(num_sms) : cluster_grid<BN, LOADER, 2>(num_sms);
+    if (g >= num_sms - (forced ? num_sms : 0) && g > 0) {
+      cl = c;
+      break;
+    }
+  }
+  if (cl == 4) {
+    launch_cl<BN, LOADER, 4>(s, cluster_grid<BN, LOADER, 4>(num_sms), tmx, tmA, ta);
+  } else if (cl == 2) {
+    launch_cl<BN, LOADER, 2>(s, cluster_grid<BN, LOADER, 2>(num_sms), tmx, tmA, ta);
+  } else {
+    const long long blocks = tiles < num_sms ? tiles : num_sms;  // one CTA per SM
+    mode_product_tma_kernel<BN, LOADER, 1>
+        <<<static_cast<unsigned>(blocks), NTHREADS, Cfg<BN>::SMEM, s>>>(tmx, tmA, ta);
+  }
 }
 
 }  // namespace
@@ -493,23 +640,21 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
-  const long long tiles = ta.ntiles_m * ta.ntiles_n;
-  const long long blocks = tiles < num_sms ? tiles : num_sms;  // one CTA per SM
   if (cplx0) {
     if (bn == 128)
-      mode_product_tma_kernel<128, TL_CPLX0><<<blocks, NTHREADS, Cfg<128>::SMEM, s>>>(tmx, tmA, ta);
+      launch_tma<128, TL_CPLX0>(s, num_sms, ta.ntiles_m, ta.ntiles_n, tmx, tmA, ta);
     else
-      mode_product_tma_kernel<64, TL_CPLX0><<<blocks, NTHREADS, Cfg<64>::SMEM, s>>>(tmx, tmA, ta);
+      launch_tma<64, TL_CPLX0>(s, num_sms, ta.ntiles_m, ta.ntiles_n, tmx, tmA, ta);
   } else if (bn == 128) {
     if (contig)
-      mode_product_tma_kernel<128, TL_CONTIG><<<blocks, NTHREADS, Cfg<128>::SMEM, s>>>(tmx, tmA, ta);
+      launch_tma<128, TL_CONTIG>(s, num_sms, ta.ntiles_m, ta.ntiles_n, tmx, tmA, ta);
     else
-      mode_product_tma_kernel<128, TL_STRIDED><<<blocks, NTHREADS, Cfg<128>::SMEM, s>>>(tmx, tmA, ta);
+      launch_tma<128, TL_STRIDED>(s, num_sms, ta.ntiles_m, ta.ntiles_n, tmx, tmA, ta);
   } else {
     if (contig)
-      mode_product_tma_kernel<64, TL_CONTIG><<<blocks, NTHREADS, Cfg<64>::SMEM, s>>>(tmx, tmA, ta);
+      launch_tma<64, TL_CONTIG>(s, num_sms, ta.ntiles_m, ta.ntiles_n, tmx, tmA, ta);
     else
-      mode_product_tma_kernel<64, TL_STRIDED><<<blocks, NTHREADS, Cfg<64>::SMEM, s>>>(tmx, tmA, ta);
+      launch_tma<64, TL_STRIDED>(s, num_sms, ta.ntiles_m, ta.ntiles_n, tmx, tmA, ta);
   }
   KCUDA(cudaGetLastError());
 }
