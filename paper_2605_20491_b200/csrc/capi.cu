@@ -140,7 +140,10 @@ static void sep_transform_fused_small(kronop_ctx& ctx, const kronop_op& op, cons
   std::vector<std::pair<int, int>> groups;  // (first spatial axis, count)
   for (int a = 0; a < op.d;) {
     int f = 1, F = op.n[a];
-    while (f < 3 && a + f < op.d && F * op.n[a + f] <= 1024) F *= op.n[a + f++];
+    // three-axis groups only for extents <= 12 (the kernels' K/N instantiations for f = 3)
+    while (a + f < op.d && F * op.n[a + f] <= 1024 &&
+           (f < 2 || (f == 2 && op.n[a] <= 12 && op.n[a + 1] <= 12 && op.n[a + 2] <= 12)))
+      F *= op.n[a + f++];
     groups.emplace_back(a, f);
     a += f;
   }
@@ -267,7 +270,10 @@ static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double
   std::vector<std::pair<int, int>> groups;
   for (int a = 0; a < op.d;) {
     int f = 1, F = op.n[a];
-    while (f < 3 && a + f < op.d && F * op.n[a + f] <= 1024) F *= op.n[a + f++];
+    // three-axis groups only for extents <= 12 (the kernels' K/N instantiations for f = 3)
+    while (a + f < op.d && F * op.n[a + f] <= 1024 &&
+           (f < 2 || (f == 2 && op.n[a] <= 12 && op.n[a + 1] <= 12 && op.n[a + 2] <= 12)))
+      F *= op.n[a + f++];
     groups.emplace_back(a, f);
     a += f;
   }
@@ -994,7 +1000,7 @@ static void host_roundtrip(kronop_ctx* ctx, const kronop_op* op, const double* i
   ensure_copy_engines(ctx);
   ensure_scratch(*ctx, nd);
   cudaStream_t sc = ctx->stream, sin = ctx->copy_stream[0], sout = ctx->copy_stream[1];
-  const int chunks = std::min(nz, 8);
+  const int chunks = std::min(nz, kronop_ctx::kMaxChunks);
   const size_t plane = nd / nz;  // doubles per plane of the slowest axis
   std::vector<int> zc(chunks), z0(chunks);
   for (int c = 0, acc = 0; c < chunks; ++c) {

@@ -210,13 +210,17 @@ __device__ __forceinline__ void axis_dfma(double* tile, const double (&M)[N][N],
     double x[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) x[k] = p[k * S];
+    // k-outer: N independent accumulation chains advance together (ILP N); each output is still
+    // fma(M[i][N-1], x[N-1], ... fma(M[i][0], x[0], 0)) in k order
+    double acc[N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double acc = 0.0;
+    for (int i = 0; i < N; ++i) acc[i] = 0.0;
 #pragma unroll
-      for (int k = 0; k < N; ++k) acc = fma(M[i][k], x[k], acc);
-      p[i * S] = acc;  // in place: the fiber's inputs are all in registers
-    }
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fma(M[i][k], x[k], acc[i]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) p[i * S] = acc[i];  // in place: the inputs are in registers
   }
 }
 
@@ -250,11 +254,11 @@ __device__ __forceinline__ void store_tile(const RotArgs& A, const double* tile,
   const long long CQ = static_cast<long long>(C) * A.Q;
   const int units = Qt * F;  // (re, im) pairs or real scalars
   const bool spectral = A.epi == EPI_SPEC_MUL || A.epi == EPI_SPEC_DIV || A.epi == EPI_SPEC_PHASE;
-  const float invQt = 1.0f / static_cast<float>(Qt);
+  const int lq = __ffs(Qt) - 1;  // Qt is a power of two
 #pragma unroll 4
   for (int u = tid; u < units; u += THREADS) {
-    const int g = fast_div(u, Qt, invQt);
-    const int qi = u - g * Qt;
+    const int g = u >> lq;
+    const int qi = u & (Qt - 1);
     if (qi >= qv) continue;  // partial last tile only
     const long long gi = static_cast<long long>(C) * (q0 + qi) + CQ * g;
     const double* sp = tile + C * (g + F * qi);
@@ -431,7 +435,7 @@ template <int NF, int K4, int NT, int DN>
 constexpr size_t rot_smem_bytes() {
   constexpr int FRAG = DN > 0 ? DN * ((DN + 1) & ~1) : K4 * NT * 32;
   return (static_cast<size_t>(RT_STAGES) * RT_TILE + NF * FRAG + 128) * sizeof(double) +
-         RT_STAGES * (sizeof(uint64_t) + sizeof(int));
+         RT_STAGES * (2 * sizeof(uint64_t) + sizeof(int)) + 16;
 }
 
 template <int NF, int K4, int NT, int DN = 0>
@@ -523,7 +527,7 @@ void launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int 
     a.lda[j] = lda[j];
     maxn = n[j] > maxn ? n[j] : maxn;
   }
-  param_check(maxn <= 32 && a.F <= 1024, "fused_rot: group too large");
+  param_check(maxn <= 32 && a.F <= 1024 && (f < 3 || maxn <= 12), "fused_rot: group too large");
   a.Q = N / a.F;
   // C * Qt: the largest power of two >= 8 with C * Qt * F <= RT_TILE
   int cqt = 8;
@@ -559,7 +563,11 @@ void launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int 
     const char* e = getenv("KRONOP_ROT_NO_DFMA");  // A/B switch: DMMA for every extent
     return e && e[0] == '1';
   }();
-  if (same && maxn >= 2 && maxn <= 10 && !no_dfma) {
+  // the spectral launch keeps the 16-warp DMMA kernel: its store pass (one sincos per pair) is
+  // latency bound and needs the warps more than the contraction needs DFMA's efficiency
+  const bool spectral = epi.kind == EPI_SPEC_MUL || epi.kind == EPI_SPEC_DIV ||
+                        epi.kind == EPI_SPEC_PHASE;
+  if (same && maxn >= 2 && maxn <= 10 && !no_dfma && !spectral) {
     switch (f * 16 + maxn) {
 #define RT_DF(F, N) \
   case F * 16 + N: launch_rot<F, 1, 1, N>(s, a); return;
