@@ -381,6 +381,14 @@ class SeparableOperator:
             check(lib().kronop_sep_solve(self.ctx.h, self.h, _ptr(b), int(b.is_complex()), _ptr(out)))
         return out
 
+    def solve_bf16(self, b: torch.Tensor, out=None) -> torch.Tensor:
+        """Reduced-precision solve (kronop_sep_solve_lowp, BF16 storage / FP32 accumulation on
+        the tcgen05 tensor cores): the paper's BF16 mode, ~1e-2 relative accuracy."""
+        out = self._out(b, out)
+        with _Call(self.ctx):
+            check(lib().kronop_sep_solve_lowp(self.ctx.h, self.h, _ptr(b), 1, _ptr(out)))
+        return out
+
     def propagate(self, psi: torch.Tensor, dt: float, out=None) -> torch.Tensor:
         if not psi.is_complex():
             raise ValueError("propagate needs a complex128 field")

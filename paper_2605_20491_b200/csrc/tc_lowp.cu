@@ -1,0 +1,387 @@
+// Reduced-precision transforms on the 5th-generation tensor cores (tcgen05 + TMEM): the BF16
+// variant of the separable solve (the paper's FP32 / TF32 / BF16 rows), as a
+// separately reported alternative path. FP64 has no tcgen05 kind, so the
+// north-star path stays on DMMA (mode_product_tma.cu); this file is the Blackwell tensor-core
+// path for the precisions that have one.
+//
+// One pass contracts the FASTEST axis of a BF16 field viewed as X[R rows][K] (K contiguous) with
+// the axis matrix B[m][K] (K contiguous): D[r][i] = sum_k X[r][k] B[i][k], FP32 accumulation in
+// TMEM, and writes Y[i * R + r] (the contracted axis moves to the slow end: after d passes the
+// layout is the original again, as in fused_rot.cu). Both operands are K-major, the canonical
+// UMMA layout, loaded by TMA with 128-byte swizzle.
+//
+// Per CTA (persistent, one per SM, 6 warps): warp 0 lane 0 = TMA producer (4-stage ring of
+// 48 KB: A 128 x 64, B 256 x 64 bf16); warp 1 = TMEM allocator + single-thread tcgen05.mma
+// issuer (M = 128, N = 256, K = 16 per instruction, 4 per stage) with tcgen05.commit releasing
+// smem stages and publishing finished accumulators; warps 2-5 = epilogue (tcgen05.ld 32x32b, the
+// fused spectral divide / multiply, BF16 or FP64 stores of the rotated output). Two TMEM
+// accumulator buffers (2 x 256 columns) let the epilogue of tile i overlap the MMAs of tile i+1.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "context.cuh"
+#include "kronop_internal.cuh"
+
+namespace kronop_dev {
+
+namespace {
+
+constexpr int TC_BM = 128, TC_BN = 256, TC_BK = 64, TC_STAGES = 4;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
+constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;  // 32 KB
+constexpr int TC_STAGE = TC_A_BYTES + TC_B_BYTES;
+constexpr int TC_THREADS = 192;
+constexpr int TC_SMEM = TC_STAGES * TC_STAGE + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TC_TMEM_COLS = 512;  // two 128 x 256 FP32 accumulators
+
+struct TcArgs {
+  void* y;
+  long long R;  // rows (product of the other axes)
+  int K;        // contracted extent
+  int m;        // output extent
+  int ntn;      // N tiles
+  long long ntm;
+  int epi;      // 0 store, 1 divide by (lambda - shift), 2 multiply
+  double shift;
+  int nlow;                              // axes below (row decomposition) for lambda
+  int lowext[KRONOP_MAX_DIM];
+  const double* lowlam[KRONOP_MAX_DIM];
+  const double* lamlast;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(uint64_t* b, int c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                      uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(su32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+// K-major, 128-byte-swizzled UMMA shared-memory descriptor (cute/arch/mma_sm100_desc.hpp layout):
+// start >> 4 | LBO 1 | SBO 1024 B (8-row groups) | version 1 (Blackwell) | SWIZZLE_128B.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor: BF16 x BF16 -> FP32, K-major A and B, M = 128, N = 256
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((TC_BN >> 3) << 17) |
+                            ((TC_BM >> 4) << 24);
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+template <int OUT_F64>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_pass_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tb,
+                   const TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + TC_STAGES * TC_STAGE);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* tfull = empty + TC_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mb_init(&tfull[b], 1);
+      mb_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     su32(tmem_slot)),
+                 "n"(TC_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const long long tiles = a.ntm * a.ntn;
+  const int KB = (a.K + TC_BK - 1) / TC_BK;
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tx) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tb) : "memory");
+      long long it = 0;
+      for (long long T = blockIdx.x; T < tiles; T += gridDim.x) {
+        const long long tm = T / a.ntn;
+        const int row0 = static_cast<int>(tm * TC_BM);
+        const int col0 = static_cast<int>(T - tm * a.ntn) * TC_BN;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % TC_STAGES);
+          const uint32_t ph = static_cast<uint32_t>((it / TC_STAGES) & 1);
+          mb_wait(&empty[s], ph ^ 1);
+          unsigned char* st = sm + s * TC_STAGE;
+          mb_expect_tx(&full[s], TC_STAGE);
+          tma2d(st, &tx, kb * TC_BK, row0, &full[s]);
+          tma2d(st + TC_A_BYTES, &tb, kb * TC_BK, col0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      long long it = 0, lt = 0;
+      for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
+        const int b = static_cast<int>(lt & 1);
+        const uint32_t tph = static_cast<uint32_t>((lt >> 1) & 1);
+        mb_wait(&tempty[b], tph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + b * TC_BN;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % TC_STAGES);
+          const uint32_t ph = static_cast<uint32_t>((it / TC_STAGES) & 1);
+          mb_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sa = su32(sm + s * TC_STAGE), sb = sa + TC_A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 16; ++kk)  // K = 16 bf16 = 32 bytes per instruction
+            umma_bf16(d, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
+          umma_commit(&empty[s]);  // smem stage free once these MMAs have read it
+        }
+        umma_commit(&tfull[b]);  // accumulator b complete
+      }
+    }
+  } else {  // epilogue warps 2..5: TMEM lane quadrant = warp % 4
+    const int q = warp & 3;
+    long long lt = 0;
+    for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
+      const int b = static_cast<int>(lt & 1);
+      const uint32_t tph = static_cast<uint32_t>((lt >> 1) & 1);
+      const long long tm = T / a.ntn;
+      const long long r = tm * TC_BM + 32 * q + lane;
+      const int col0 = static_cast<int>(T - tm * a.ntn) * TC_BN;
+      double lam_low = 0.0;
+      if (a.epi != 0 && r < a.R) {  // axes below the contracted one, in axis order from 0.0
+        long long rr = r;
+        for (int j = 0; j < a.nlow; ++j) {
+          const long long idx = rr % a.lowext[j];
+          rr /= a.lowext[j];
+          lam_low = __dadd_rn(lam_low, a.lowlam[j][idx]);
+        }
+      }
+      mb_wait(&tfull[b], tph);
+      tc_fence_after();
+      for (int c = 0; c < TC_BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + b * TC_BN + c * 32 + (static_cast<uint32_t>(32 * q) << 16), v);
+        if (r < a.R) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = col0 + c * 32 + j;
+            if (col >= a.m) break;
+            float val = __uint_as_float(v[j]);
+            if (a.epi != 0) {
+              const float ls = static_cast<float>(__dsub_rn(__dadd_rn(lam_low, a.lamlast[col]),
+                                                            a.shift));
+              val = a.epi == 1 ? val / ls : val * ls;
+            }
+            const long long gi = static_cast<long long>(col) * a.R + r;
+            if (OUT_F64)
+              static_cast<double*>(a.y)[gi] = static_cast<double>(val);
+            else
+              static_cast<__nv_bfloat16*>(a.y)[gi] = __float2bfloat16_rn(val);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mb_arrive(&tempty[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "n"(TC_TMEM_COLS));
+  }
+}
+
+__global__ void k_f64_to_bf16(const double* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                              long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    y[i] = __double2bfloat16(x[i]);
+}
+
+// padded column-major f64 matrix (lda) -> row-major bf16 [m][k]
+__global__ void k_mat_to_bf16(const double* __restrict__ a, int lda, int m, int k,
+                              __nv_bfloat16* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * k; e += gridDim.x * blockDim.x) {
+    const int i = e / k, kk = e - i * k;
+    out[e] = __double2bfloat16(a[i + static_cast<long long>(lda) * kk]);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    KCUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr));
+    if (qr != cudaDriverEntryPointSuccess || !p) fail(KRONOP_ERUNTIME, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+void encode_bf16_2d(CUtensorMap* map, const void* base, long long inner, long long outer,
+                    int box_inner, int box_outer) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  const cuuint64_t str[1] = {static_cast<cuuint64_t>(inner) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tc_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                                    dims, str, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(KRONOP_ERUNTIME, "cuTensorMapEncodeTiled (bf16) failed");
+}
+
+void tc_pass(cudaStream_t s, const __nv_bfloat16* x, const __nv_bfloat16* bmat, void* y,
+             long long R, int K, int m, bool out_f64, TcArgs a) {
+  CUtensorMap tx, tb;
+  encode_bf16_2d(&tx, x, K, R, TC_BK, TC_BM);
+  encode_bf16_2d(&tb, bmat, K, m, TC_BK, TC_BN);
+  a.y = y;
+  a.R = R;
+  a.K = K;
+  a.m = m;
+  a.ntn = (m + TC_BN - 1) / TC_BN;
+  a.ntm = (R + TC_BM - 1) / TC_BM;
+  static int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    return v;
+  }();
+  const long long tiles = a.ntm * a.ntn;
+  const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
+  if (out_f64)
+    tc_pass_kernel<1><<<grid, TC_THREADS, TC_SMEM, s>>>(tx, tb, a);
+  else
+    tc_pass_kernel<0><<<grid, TC_THREADS, TC_SMEM, s>>>(tx, tb, a);
+  KCUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+// (-Delta + V1 - shift)^{-1} b in BF16 storage / FP32 accumulation on tcgen05 (real field, every
+// extent a multiple of 8 for the 16-byte TMA row pitch). b, x: FP64 device fields.
+void sep_solve_bf16(kronop_ctx& ctx, kronop_op& op, const double* b, double* x) {
+  param_check(!op.folded, "solve_bf16: dense operators only");
+  for (int a = 0; a < op.d; ++a)
+    param_check(op.n[a] % 8 == 0 && op.n[a] >= 16, "solve_bf16: extents must be multiples of 8");
+  const long long N = op.N;
+  cudaStream_t s = ctx.stream;
+  // bf16 copies of the transforms (row-major [out][k]), made once per operator
+  if (!op.lp_ready) {
+    for (int a = 0; a < op.d; ++a) {
+      const int n = op.n[a];
+      for (int dir = 0; dir < 2; ++dir) {
+        void* p = nullptr;
+        KCUDA(cudaMalloc(&p, static_cast<size_t>(n) * n * 2));
+        k_mat_to_bf16<<<256, 256, 0, s>>>(dir == 0 ? op.fwd[a] : op.bwd[a], op.lda[a], n, n,
+                                         static_cast<__nv_bfloat16*>(p));
+        KCUDA(cudaGetLastError());
+        (dir == 0 ? op.lp_fwd[a] : op.lp_bwd[a]) = p;
+      }
+    }
+    op.lp_ready = true;
+  }
+  ensure_scratch(ctx, static_cast<size_t>((N + 3) / 4 + 16));  // two bf16 fields in doubles
+  __nv_bfloat16* f0 = reinterpret_cast<__nv_bfloat16*>(ctx.scratch[0]);
+  __nv_bfloat16* f1 = reinterpret_cast<__nv_bfloat16*>(ctx.scratch[1]);
+  k_f64_to_bf16<<<kEltBlocks, 256, 0, s>>>(b, f0, N);
+  KCUDA(cudaGetLastError());
+  ctx.ws.launches += 1;
+  const __nv_bfloat16* cur = f0;
+  int k = 0;
+  for (int dir = 0; dir < 2; ++dir)
+    for (int a = 0; a < op.d; ++a, ++k) {
+      const bool last = dir == 1 && a == op.d - 1;
+      __nv_bfloat16* dst = (k % 2 == 0) ? f1 : f0;
+      TcArgs ta{};
+      if (dir == 0 && a == op.d - 1) {
+        ta.epi = 1;
+        ta.shift = op.shift;
+        ta.nlow = op.d - 1;
+        for (int j = 0; j < op.d - 1; ++j) {
+          ta.lowext[j] = op.n[j];
+          ta.lowlam[j] = op.lam[j];
+        }
+        ta.lamlast = op.lam[a];
+      }
+      const int n = op.n[a];
+      tc_pass(s, cur, static_cast<const __nv_bfloat16*>(dir == 0 ? op.lp_fwd[a] : op.lp_bwd[a]),
+              last ? static_cast<void*>(x) : static_cast<void*>(dst), N / n, n, n, last, ta);
+      ctx.ws.launches += 1;
+      cur = dst;
+    }
+}
+
+}  // namespace kronop_dev

@@ -663,3 +663,51 @@ def test_small_extent_path_anisotropic(ctx, axes):
     kf = K.FullOperator(ko, v2)
     assert rel(host(fo.apply(dev(u), sigma=0.3)), kf.apply(u) - 0.3 * u) < 1e-13
     assert rel(host(fo.apply(dev(psi))), kf.apply(psi)) < 1e-13
+
+
+# ----------------------------------------------------- reduced precision (tcgen05 BF16) --
+@pytest.mark.parametrize("axes", [[(8.0, 13, 5)] * 3, [(8.0, 5, 5), (8.0, 41, 1), (8.0, 17, 1)],
+                                  [(8.0, 61, 5)] * 2 + [(8.0, 5, 5)]])
+def test_bf16_tcgen05_solve(ctx, axes):
+    """The paper's BF16 mode on the tcgen05 tensor cores (BF16 storage, FP32 accumulation in
+    TMEM): agrees with the FP64 solve to BF16 accuracy, and with a host emulation of the same
+    rounding chain (BF16 operands, FP32 accumulate, BF16 intermediates) far more closely; edge
+    tiles (R % 128, m % 256, K % 64 != 0) included."""
+    A = api()
+    grid = A.Grid([A.assemble_sem(*a) for a in axes])
+    op = grid.separable_operator(ctx, [lambda t: t * t] * grid.dim, 0.0)
+    n = grid.node_count()
+    b_np = K.uniform_pm1(5, n)
+    b = dev(b_np)
+    x64 = host(op.solve(b))
+    x16 = host(op.solve_bf16(b))
+    assert rel(x16, x64) < 3e-2
+
+    def bf16(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(torch.float64).numpy()
+
+    # emulation: contract the fastest axis, move it to the slow end, BF16 between passes
+    d = grid.dim
+    cur = bf16(b_np)
+    shape = list(grid.shape)  # current layout, fastest first
+    order = list(range(d))
+    for direction in (0, 1):
+        for a in range(d):
+            ax = op.axes[a]
+            mat = bf16(ax.inverse_transform if direction == 0 else ax.transform)
+            R = cur.size // shape[0]
+            X = cur.reshape(R, shape[0])
+            Y = (X @ mat.T).astype(np.float32).astype(np.float64)  # [R][m]
+            if direction == 0 and a == d - 1:
+                lam = np.zeros(R)
+                idx = np.arange(R)
+                for j in range(d - 1):
+                    lam = lam + op.axes[j].eigenvalues[idx % grid.shape[j]]
+                    idx //= grid.shape[j]
+                lam = lam[:, None] + ax.eigenvalues[None, :]
+                Y = (Y.astype(np.float32) / lam.astype(np.float32)).astype(np.float64)
+            cur = Y.T.reshape(-1)  # output [m][R]: the contracted axis is now the slowest
+            shape = shape[1:] + [shape[0]]
+            if not (direction == 1 and a == d - 1):
+                cur = bf16(cur)
+    assert rel(x16, cur) < 2e-3
