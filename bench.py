@@ -320,6 +320,25 @@ def folded_variant(A, grid, pot, ctx, b, x, bn, xn, op_dense, steps, world, loca
                       "FP64 in/out"}}
         del xb
         torch.cuda.empty_cache()
+        xt = torch.empty_like(x)
+        op_dense.solve_lowp(b, "tf32", out=xt)
+        ref = op_dense.solve(b)
+        tf_err = float(torch.linalg.norm(xt - ref) / torch.linalg.norm(ref))
+        del ref
+        torch.cuda.synchronize()
+        e0.record(ctx.stream)
+        for _ in range(k):
+            op_dense.solve_lowp(b, "tf32", out=xt)
+        e1.record(ctx.stream)
+        torch.cuda.synchronize()
+        tt = max_over_ranks(world, e0.elapsed_time(e1) / 1e3 / k, "cuda:%d" % local)
+        bf["tf32_solve"] = {
+            "value": world * N / tt / 1e9, "unit": "GDoF/s", "ms_per_step": tt * 1e3,
+            "rel_diff_vs_fp64": tf_err,
+            "config": "same workload; FP32 storage / TF32 products / FP32 accumulation, "
+                      "tcgen05.mma kind::tf32 (M128 N256 K8), TMEM accumulators; FP64 in/out"}
+        del xt
+        torch.cuda.empty_cache()
     except Exception as e:  # reported, never silently replaced
         bf = {"bf16_solve": {"error": str(e)[:200]}}
     return {**bf, "folded_solve": {

@@ -381,13 +381,18 @@ class SeparableOperator:
             check(lib().kronop_sep_solve(self.ctx.h, self.h, _ptr(b), int(b.is_complex()), _ptr(out)))
         return out
 
-    def solve_bf16(self, b: torch.Tensor, out=None) -> torch.Tensor:
-        """Reduced-precision solve (kronop_sep_solve_lowp, BF16 storage / FP32 accumulation on
-        the tcgen05 tensor cores): the paper's BF16 mode, ~1e-2 relative accuracy."""
+    def solve_lowp(self, b: torch.Tensor, precision: str = "bf16", out=None) -> torch.Tensor:
+        """Reduced-precision solve on the tcgen05 tensor cores (kronop_sep_solve_lowp, FP32
+        accumulation in TMEM): "bf16" (BF16 storage, the paper's BF16 mode, ~1e-2 relative) or
+        "tf32" (FP32 storage, TF32 products, ~1e-3)."""
         out = self._out(b, out)
+        prec = {"bf16": 1, "tf32": 2}[precision]
         with _Call(self.ctx):
-            check(lib().kronop_sep_solve_lowp(self.ctx.h, self.h, _ptr(b), 1, _ptr(out)))
+            check(lib().kronop_sep_solve_lowp(self.ctx.h, self.h, _ptr(b), prec, _ptr(out)))
         return out
+
+    def solve_bf16(self, b: torch.Tensor, out=None) -> torch.Tensor:
+        return self.solve_lowp(b, "bf16", out)
 
     def propagate(self, psi: torch.Tensor, dt: float, out=None) -> torch.Tensor:
         if not psi.is_complex():

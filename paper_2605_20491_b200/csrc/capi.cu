@@ -829,8 +829,8 @@ int kronop_op_destroy(kronop_op* op) {
     for (int a = 0; a < KRONOP_MAX_DIM; ++a) {
       for (double* p : {op->fe[a], op->fo[a], op->be[a], op->bo[a]})
         if (p) cudaFree(p);
-      if (op->lp_fwd[a]) cudaFree(op->lp_fwd[a]);
-      if (op->lp_bwd[a]) cudaFree(op->lp_bwd[a]);
+      for (void* p : {op->lp_fwd[a], op->lp_bwd[a], op->tf_fwd[a], op->tf_bwd[a]})
+        if (p) cudaFree(p);
       if (!op->shared_axis[a]) {
         if (op->fwd[a]) cudaFree(op->fwd[a]);
         if (op->bwd[a]) cudaFree(op->bwd[a]);
@@ -910,9 +910,10 @@ int kronop_sep_solve_lowp(kronop_ctx* ctx, kronop_op* op, const double* b, int p
                           double* out) {
   return guard([&] {
     param_check(ctx && op && b && out && b != out, "solve_lowp: bad argument");
-    param_check(precision == KRONOP_PREC_BF16, "solve_lowp: unsupported precision");
+    param_check(precision == KRONOP_PREC_BF16 || precision == KRONOP_PREC_TF32,
+                "solve_lowp: unsupported precision");
     check_solve_shift(*ctx, *op, op->shift);
-    sep_solve_bf16(*ctx, *op, b, out);
+    sep_solve_lowp(*ctx, *op, b, out, precision);
   });
 }
 

@@ -57,9 +57,10 @@ struct kronop_op {
   // in folded order [even modes | odd modes]; bwd[a] holds the ground-state column only.
   bool shared_axis[KRONOP_MAX_DIM] = {};  // fwd/bwd alias an earlier identical axis
   // reduced-precision copies of the transforms (tc_lowp.cu), made on first use
-  bool lp_ready = false;
-  void* lp_fwd[KRONOP_MAX_DIM] = {};
+  void* lp_fwd[KRONOP_MAX_DIM] = {};  // BF16
   void* lp_bwd[KRONOP_MAX_DIM] = {};
+  void* tf_fwd[KRONOP_MAX_DIM] = {};  // FP32 storage for TF32
+  void* tf_bwd[KRONOP_MAX_DIM] = {};
   bool folded = false;
   int ne[KRONOP_MAX_DIM] = {}, no[KRONOP_MAX_DIM] = {};
   double* fe[KRONOP_MAX_DIM] = {};
@@ -70,7 +71,7 @@ struct kronop_op {
 };
 
 namespace kronop_dev {
-void sep_solve_bf16(kronop_ctx& ctx, kronop_op& op, const double* b, double* x);
+void sep_solve_lowp(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int precision);
 // Smallest free pool block with capacity >= n doubles, else a new cudaMalloc'd block.
 double* pool_get(kronop_ctx& ctx, size_t n);
 void pool_put(kronop_ctx& ctx, double* p);

@@ -34,8 +34,14 @@ namespace kronop_dev {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 32;
-constexpr int STAGES = 3;
+#ifndef KRONOP_TMA_BK
+#define KRONOP_TMA_BK 32  // k per stage (A/B experiments: -DKRONOP_TMA_BK=16 -DKRONOP_TMA_STAGES=6)
+#endif
+#ifndef KRONOP_TMA_STAGES
+#define KRONOP_TMA_STAGES 3
+#endif
+constexpr int BK = KRONOP_TMA_BK;
+constexpr int STAGES = KRONOP_TMA_STAGES;
 constexpr int NCONS = 8;                 // DMMA warps; warp 0 lane 0 also drives TMA
 constexpr int NTHREADS = NCONS * 32;
 constexpr int BOX_STRIDED_BYTES = BK * 128;  // [BK rows][16 doubles]

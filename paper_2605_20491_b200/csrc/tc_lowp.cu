@@ -30,10 +30,30 @@ namespace kronop_dev {
 
 namespace {
 
-constexpr int TC_BM = 128, TC_BN = 256, TC_BK = 64, TC_STAGES = 4;
-constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
-constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;  // 32 KB
+constexpr int TC_BM = 128, TC_BN = 256, TC_STAGES = 4;
+// a stage holds 128-byte rows of K: 64 BF16 or 32 TF32 (FP32 storage) values
+constexpr int TC_ROW = 128;
+constexpr int TC_A_BYTES = TC_BM * TC_ROW;  // 16 KB
+constexpr int TC_B_BYTES = TC_BN * TC_ROW;  // 32 KB
 constexpr int TC_STAGE = TC_A_BYTES + TC_B_BYTES;
+
+enum { PREC_BF16 = 1, PREC_TF32 = 2 };
+template <int PREC>
+struct TcTraits;
+template <>
+struct TcTraits<PREC_BF16> {
+  using T = __nv_bfloat16;
+  static constexpr int BK = 64;      // elements per 128-byte row
+  static constexpr int UK = 16;      // K per tcgen05.mma (32 bytes)
+  static constexpr uint32_t FMT = 1; // BF16 in the instruction descriptor
+};
+template <>
+struct TcTraits<PREC_TF32> {
+  using T = float;
+  static constexpr int BK = 32;
+  static constexpr int UK = 8;
+  static constexpr uint32_t FMT = 2; // TF32
+};
 constexpr int TC_THREADS = 192;
 constexpr int TC_SMEM = TC_STAGES * TC_STAGE + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int TC_TMEM_COLS = 512;  // two 128 x 256 FP32 accumulators
@@ -94,14 +114,24 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) |
          (1ull << 46) | (2ull << 61);
 }
-// instruction descriptor: BF16 x BF16 -> FP32, K-major A and B, M = 128, N = 256
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((TC_BN >> 3) << 17) |
-                            ((TC_BM >> 4) << 24);
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+// instruction descriptor: FMT x FMT -> FP32, K-major A and B, M = 128, N = 256
+template <int PREC>
+__host__ __device__ constexpr uint32_t idesc() {
+  return (1u << 4) | (TcTraits<PREC>::FMT << 7) | (TcTraits<PREC>::FMT << 10) |
+         ((TC_BN >> 3) << 17) | ((TC_BM >> 4) << 24);
+}
+template <int PREC>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  if constexpr (PREC == PREC_BF16)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc<PREC>()), "r"(acc));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc<PREC>()), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -122,7 +152,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-template <int OUT_F64>
+// TF32 operands are stored pre-rounded (round to nearest): the tensor core drops the low 13
+// mantissa bits, which would otherwise truncate (a systematic bias that compounds over passes)
+__device__ __forceinline__ float round_tf32(float v) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(v));
+  return __uint_as_float(r);
+}
+template <int PREC, int OUT_F64>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_pass_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tb,
                    const TcArgs a) {
@@ -159,7 +196,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   const long long tiles = a.ntm * a.ntn;
-  const int KB = (a.K + TC_BK - 1) / TC_BK;
+  constexpr int BK = TcTraits<PREC>::BK;
+  const int KB = (a.K + BK - 1) / BK;
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tx) : "memory");
@@ -175,8 +213,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mb_wait(&empty[s], ph ^ 1);
           unsigned char* st = sm + s * TC_STAGE;
           mb_expect_tx(&full[s], TC_STAGE);
-          tma2d(st, &tx, kb * TC_BK, row0, &full[s]);
-          tma2d(st + TC_A_BYTES, &tb, kb * TC_BK, col0, &full[s]);
+          tma2d(st, &tx, kb * BK, row0, &full[s]);
+          tma2d(st + TC_A_BYTES, &tb, kb * BK, col0, &full[s]);
         }
       }
     }
@@ -196,8 +234,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc_fence_after();
           const uint32_t sa = su32(sm + s * TC_STAGE), sb = sa + TC_A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; ++kk)  // K = 16 bf16 = 32 bytes per instruction
-            umma_bf16(d, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
+          for (int kk = 0; kk < BK / TcTraits<PREC>::UK; ++kk)  // 32 bytes of K per instruction
+            umma<PREC>(d, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
           umma_commit(&empty[s]);  // smem stage free once these MMAs have read it
         }
         umma_commit(&tfull[b]);  // accumulator b complete
@@ -240,8 +278,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const long long gi = static_cast<long long>(col) * a.R + r;
             if (OUT_F64)
               static_cast<double*>(a.y)[gi] = static_cast<double>(val);
-            else
+            else if (PREC == PREC_BF16)
               static_cast<__nv_bfloat16*>(a.y)[gi] = __float2bfloat16_rn(val);
+            else
+              static_cast<float*>(a.y)[gi] = round_tf32(val);
           }
         }
       }
@@ -259,19 +299,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-__global__ void k_f64_to_bf16(const double* __restrict__ x, __nv_bfloat16* __restrict__ y,
-                              long long n) {
+__device__ __forceinline__ void cvt(double v, __nv_bfloat16& o) { o = __double2bfloat16(v); }
+__device__ __forceinline__ void cvt(double v, float& o) { o = round_tf32(static_cast<float>(v)); }
+
+template <class T>
+__global__ void k_f64_to_lowp(const double* __restrict__ x, T* __restrict__ y, long long n) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
-    y[i] = __double2bfloat16(x[i]);
+    cvt(x[i], y[i]);
 }
 
-// padded column-major f64 matrix (lda) -> row-major bf16 [m][k]
-__global__ void k_mat_to_bf16(const double* __restrict__ a, int lda, int m, int k,
-                              __nv_bfloat16* __restrict__ out) {
+// padded column-major f64 matrix (lda) -> row-major low-precision [m][k]
+template <class T>
+__global__ void k_mat_to_lowp(const double* __restrict__ a, int lda, int m, int k,
+                              T* __restrict__ out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * k; e += gridDim.x * blockDim.x) {
     const int i = e / k, kk = e - i * k;
-    out[e] = __double2bfloat16(a[i + static_cast<long long>(lda) * kk]);
+    cvt(a[i + static_cast<long long>(lda) * kk], out[e]);
   }
 }
 
@@ -287,24 +331,28 @@ PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
   return fn;
 }
 
-void encode_bf16_2d(CUtensorMap* map, const void* base, long long inner, long long outer,
-                    int box_inner, int box_outer) {
+void encode_lowp_2d(CUtensorMap* map, const void* base, long long inner, long long outer,
+                    int box_inner, int box_outer, int esize) {
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-  const cuuint64_t str[1] = {static_cast<cuuint64_t>(inner) * 2};
+  const cuuint64_t str[1] = {static_cast<cuuint64_t>(inner) * esize};
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = tc_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+  const CUresult r = tc_encode_fn()(map, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                    2, const_cast<void*>(base),
                                     dims, str, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) fail(KRONOP_ERUNTIME, "cuTensorMapEncodeTiled (bf16) failed");
+  if (r != CUDA_SUCCESS) fail(KRONOP_ERUNTIME, "cuTensorMapEncodeTiled (low precision) failed");
 }
 
-void tc_pass(cudaStream_t s, const __nv_bfloat16* x, const __nv_bfloat16* bmat, void* y,
-             long long R, int K, int m, bool out_f64, TcArgs a) {
+template <int PREC>
+void tc_pass(cudaStream_t s, const void* x, const void* bmat, void* y, long long R, int K, int m,
+             bool out_f64, TcArgs a) {
+  using T = typename TcTraits<PREC>::T;
   CUtensorMap tx, tb;
-  encode_bf16_2d(&tx, x, K, R, TC_BK, TC_BM);
-  encode_bf16_2d(&tb, bmat, K, m, TC_BK, TC_BN);
+  encode_lowp_2d(&tx, x, K, R, TcTraits<PREC>::BK, TC_BM, sizeof(T));
+  encode_lowp_2d(&tb, bmat, K, m, TcTraits<PREC>::BK, TC_BN, sizeof(T));
   a.y = y;
   a.R = R;
   a.K = K;
@@ -315,56 +363,56 @@ void tc_pass(cudaStream_t s, const __nv_bfloat16* x, const __nv_bfloat16* bmat, 
     int dev = 0, v = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
-    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<PREC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               TC_SMEM));
+    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<PREC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               TC_SMEM));
     return v;
   }();
   const long long tiles = a.ntm * a.ntn;
   const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
   if (out_f64)
-    tc_pass_kernel<1><<<grid, TC_THREADS, TC_SMEM, s>>>(tx, tb, a);
+    tc_pass_kernel<PREC, 1><<<grid, TC_THREADS, TC_SMEM, s>>>(tx, tb, a);
   else
-    tc_pass_kernel<0><<<grid, TC_THREADS, TC_SMEM, s>>>(tx, tb, a);
+    tc_pass_kernel<PREC, 0><<<grid, TC_THREADS, TC_SMEM, s>>>(tx, tb, a);
   KCUDA(cudaGetLastError());
 }
 
-}  // namespace
-
-// (-Delta + V1 - shift)^{-1} b in BF16 storage / FP32 accumulation on tcgen05 (real field, every
-// extent a multiple of 8 for the 16-byte TMA row pitch). b, x: FP64 device fields.
-void sep_solve_bf16(kronop_ctx& ctx, kronop_op& op, const double* b, double* x) {
-  param_check(!op.folded, "solve_bf16: dense operators only");
+template <int PREC>
+void sep_solve_lowp_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double* x) {
+  using T = typename TcTraits<PREC>::T;
+  param_check(!op.folded, "solve_lowp: dense operators only");
   for (int a = 0; a < op.d; ++a)
-    param_check(op.n[a] % 8 == 0 && op.n[a] >= 16, "solve_bf16: extents must be multiples of 8");
+    param_check(op.n[a] % 8 == 0 && op.n[a] >= 16, "solve_lowp: extents must be multiples of 8");
   const long long N = op.N;
   cudaStream_t s = ctx.stream;
-  // bf16 copies of the transforms (row-major [out][k]), made once per operator
-  if (!op.lp_ready) {
+  void** lf = PREC == PREC_BF16 ? op.lp_fwd : op.tf_fwd;
+  void** lb = PREC == PREC_BF16 ? op.lp_bwd : op.tf_bwd;
+  if (!lf[0]) {  // low-precision copies of the transforms (row-major [out][k]), made once
     for (int a = 0; a < op.d; ++a) {
       const int n = op.n[a];
       for (int dir = 0; dir < 2; ++dir) {
         void* p = nullptr;
-        KCUDA(cudaMalloc(&p, static_cast<size_t>(n) * n * 2));
-        k_mat_to_bf16<<<256, 256, 0, s>>>(dir == 0 ? op.fwd[a] : op.bwd[a], op.lda[a], n, n,
-                                         static_cast<__nv_bfloat16*>(p));
+        KCUDA(cudaMalloc(&p, static_cast<size_t>(n) * n * sizeof(T)));
+        k_mat_to_lowp<T><<<256, 256, 0, s>>>(dir == 0 ? op.fwd[a] : op.bwd[a], op.lda[a], n, n,
+                                             static_cast<T*>(p));
         KCUDA(cudaGetLastError());
-        (dir == 0 ? op.lp_fwd[a] : op.lp_bwd[a]) = p;
+        (dir == 0 ? lf : lb)[a] = p;
       }
     }
-    op.lp_ready = true;
   }
-  ensure_scratch(ctx, static_cast<size_t>((N + 3) / 4 + 16));  // two bf16 fields in doubles
-  __nv_bfloat16* f0 = reinterpret_cast<__nv_bfloat16*>(ctx.scratch[0]);
-  __nv_bfloat16* f1 = reinterpret_cast<__nv_bfloat16*>(ctx.scratch[1]);
-  k_f64_to_bf16<<<kEltBlocks, 256, 0, s>>>(b, f0, N);
+  ensure_scratch(ctx, static_cast<size_t>(N * sizeof(T) / 8 + 16));  // two low-precision fields
+  T* f0 = reinterpret_cast<T*>(ctx.scratch[0]);
+  T* f1 = reinterpret_cast<T*>(ctx.scratch[1]);
+  k_f64_to_lowp<T><<<kEltBlocks, 256, 0, s>>>(b, f0, N);
   KCUDA(cudaGetLastError());
   ctx.ws.launches += 1;
-  const __nv_bfloat16* cur = f0;
+  const T* cur = f0;
   int k = 0;
   for (int dir = 0; dir < 2; ++dir)
     for (int a = 0; a < op.d; ++a, ++k) {
       const bool last = dir == 1 && a == op.d - 1;
-      __nv_bfloat16* dst = (k % 2 == 0) ? f1 : f0;
+      T* dst = (k % 2 == 0) ? f1 : f0;
       TcArgs ta{};
       if (dir == 0 && a == op.d - 1) {
         ta.epi = 1;
@@ -377,11 +425,22 @@ void sep_solve_bf16(kronop_ctx& ctx, kronop_op& op, const double* b, double* x) 
         ta.lamlast = op.lam[a];
       }
       const int n = op.n[a];
-      tc_pass(s, cur, static_cast<const __nv_bfloat16*>(dir == 0 ? op.lp_fwd[a] : op.lp_bwd[a]),
-              last ? static_cast<void*>(x) : static_cast<void*>(dst), N / n, n, n, last, ta);
+      tc_pass<PREC>(s, cur, dir == 0 ? lf[a] : lb[a],
+                    last ? static_cast<void*>(x) : static_cast<void*>(dst), N / n, n, n, last, ta);
       ctx.ws.launches += 1;
       cur = dst;
     }
+}
+
+}  // namespace
+
+// (-Delta + V1 - shift)^{-1} b in BF16 or TF32 (FP32 storage) on tcgen05, FP32 accumulation
+// (real field, every extent a multiple of 8 for the 16-byte TMA row pitch). b, x: FP64 device.
+void sep_solve_lowp(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int precision) {
+  if (precision == PREC_BF16)
+    sep_solve_lowp_impl<PREC_BF16>(ctx, op, b, x);
+  else
+    sep_solve_lowp_impl<PREC_TF32>(ctx, op, b, x);
 }
 
 }  // namespace kronop_dev
