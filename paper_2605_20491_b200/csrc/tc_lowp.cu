@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "context.cuh"
 #include "kronop_internal.cuh"
@@ -102,6 +103,23 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0,
       "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma2d_mc(void* dst, const CUtensorMap* map, int c0, int c1,
+                                         uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
+      "cluster [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(su32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(su32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
 }
@@ -138,6 +156,14 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                    su32(bar))
                : "memory");
 }
+// arrive on the barrier at this offset in every CTA of `mask` once the issued MMAs completed
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;\n" ::"r"(su32(bar)),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
@@ -159,7 +185,11 @@ __device__ __forceinline__ float round_tf32(float v) {
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(v));
   return __uint_as_float(r);
 }
-template <int PREC, int OUT_F64>
+// CL = 2: the two CTAs of a cluster take vertically adjacent 128-row panels with the same
+// 256-column tile; each loads one 128-row half of the B tile as a TMA multicast into both, so the
+// matrix crosses L2 -> SM once per pair (B traffic halves); a stage is refilled only when both
+// CTAs' MMAs have read it (multicast tcgen05.commit into both empty barriers).
+template <int PREC, int OUT_F64, int CL>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_pass_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tb,
                    const TcArgs a) {
@@ -176,7 +206,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (tid == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mb_init(&full[s], 1);
-      mb_init(&empty[s], 1);
+      mb_init(&empty[s], CL);
     }
     for (int b = 0; b < 2; ++b) {
       mb_init(&tfull[b], 1);
@@ -184,6 +214,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if (CL > 1) cl_sync();  // the peer's barriers exist before any multicast / remote commit
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      su32(tmem_slot)),
@@ -195,7 +226,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const long long tiles = a.ntm * a.ntn;
+  // tile sequence: T over (row-panel group, column tile); a CL-cluster shares one T
+  const uint32_t crank = CL > 1 ? cl_rank() : 0;
+  const long long tiles = ((a.ntm + CL - 1) / CL) * a.ntn;
+  const long long t0 = blockIdx.x / CL, tstep = gridDim.x / CL;
   constexpr int BK = TcTraits<PREC>::BK;
   const int KB = (a.K + BK - 1) / BK;
   if (warp == 0) {
@@ -203,10 +237,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tx) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tb) : "memory");
       long long it = 0;
-      for (long long T = blockIdx.x; T < tiles; T += gridDim.x) {
-        const long long tm = T / a.ntn;
-        const int row0 = static_cast<int>(tm * TC_BM);
-        const int col0 = static_cast<int>(T - tm * a.ntn) * TC_BN;
+      for (long long T = t0; T < tiles; T += tstep) {
+        const long long tg = T / a.ntn;
+        const int row0 = static_cast<int>((tg * CL + crank) * TC_BM);
+        const int col0 = static_cast<int>(T - tg * a.ntn) * TC_BN;
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = static_cast<int>(it % TC_STAGES);
           const uint32_t ph = static_cast<uint32_t>((it / TC_STAGES) & 1);
@@ -214,14 +248,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           unsigned char* st = sm + s * TC_STAGE;
           mb_expect_tx(&full[s], TC_STAGE);
           tma2d(st, &tx, kb * BK, row0, &full[s]);
-          tma2d(st + TC_A_BYTES, &tb, kb * BK, col0, &full[s]);
+          if (CL == 1)
+            tma2d(st + TC_A_BYTES, &tb, kb * BK, col0, &full[s]);
+          else  // this CTA's 128-row half of the B tile, into both CTAs
+            tma2d_mc(st + TC_A_BYTES + crank * (TC_B_BYTES / 2), &tb, kb * BK,
+                     col0 + static_cast<int>(crank) * (TC_BN / 2), &full[s], 0x3);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       long long it = 0, lt = 0;
-      for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
+      for (long long T = t0; T < tiles; T += tstep, ++lt) {
         const int b = static_cast<int>(lt & 1);
         const uint32_t tph = static_cast<uint32_t>((lt >> 1) & 1);
         mb_wait(&tempty[b], tph ^ 1);
@@ -236,7 +274,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < BK / TcTraits<PREC>::UK; ++kk)  // 32 bytes of K per instruction
             umma<PREC>(d, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
-          umma_commit(&empty[s]);  // smem stage free once these MMAs have read it
+          if (CL == 1)
+            umma_commit(&empty[s]);  // smem stage free once these MMAs have read it
+          else
+            umma_commit_mc(&empty[s], 0x3);  // ... in both CTAs (the peer multicasts into it)
         }
         umma_commit(&tfull[b]);  // accumulator b complete
       }
@@ -244,12 +285,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {  // epilogue warps 2..5: TMEM lane quadrant = warp % 4
     const int q = warp & 3;
     long long lt = 0;
-    for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
+    for (long long T = t0; T < tiles; T += tstep, ++lt) {
       const int b = static_cast<int>(lt & 1);
       const uint32_t tph = static_cast<uint32_t>((lt >> 1) & 1);
-      const long long tm = T / a.ntn;
-      const long long r = tm * TC_BM + 32 * q + lane;
-      const int col0 = static_cast<int>(T - tm * a.ntn) * TC_BN;
+      const long long tg = T / a.ntn;
+      const long long r = (tg * CL + crank) * TC_BM + 32 * q + lane;
+      const int col0 = static_cast<int>(T - tg * a.ntn) * TC_BN;
       double lam_low = 0.0;
       if (a.epi != 0 && r < a.R) {  // axes below the contracted one, in axis order from 0.0
         long long rr = r;
@@ -292,6 +333,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cl_sync();  // the peer may still multicast / commit into this CTA until it is done
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
@@ -346,13 +388,44 @@ void encode_lowp_2d(CUtensorMap* map, const void* base, long long inner, long lo
   if (r != CUDA_SUCCESS) fail(KRONOP_ERUNTIME, "cuTensorMapEncodeTiled (low precision) failed");
 }
 
+template <int PREC, int OUT_F64, int CL>
+void tc_launch(cudaStream_t s, unsigned grid, const CUtensorMap& tx, const CUtensorMap& tb,
+               const TcArgs& a) {
+  static bool attr = [] {
+    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<PREC, OUT_F64, CL>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    return true;
+  }();
+  (void)attr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = TC_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KCUDA(cudaLaunchKernelEx(&cfg, tc_pass_kernel<PREC, OUT_F64, CL>, tx, tb, a));
+}
+
 template <int PREC>
 void tc_pass(cudaStream_t s, const void* x, const void* bmat, void* y, long long R, int K, int m,
              bool out_f64, TcArgs a) {
   using T = typename TcTraits<PREC>::T;
+  // KRONOP_TC_CLUSTER=2: B tile multicast across a CTA pair. Measured at 1024^3: no change
+  // (BF16 solve 19.8 -> 20.4 ms, TF32 30.1 -> 29.9 ms): each SM still receives its full 48 KB
+  // stage, which is what bounds the pass, so the default stays 1.
+  static const int cl = [] {
+    const char* e = getenv("KRONOP_TC_CLUSTER");
+    return e && e[0] == '2' ? 2 : 1;
+  }();
   CUtensorMap tx, tb;
   encode_lowp_2d(&tx, x, K, R, TcTraits<PREC>::BK, TC_BM, sizeof(T));
-  encode_lowp_2d(&tb, bmat, K, m, TcTraits<PREC>::BK, TC_BN, sizeof(T));
+  encode_lowp_2d(&tb, bmat, K, m, TcTraits<PREC>::BK, cl == 2 ? TC_BN / 2 : TC_BN, sizeof(T));
   a.y = y;
   a.R = R;
   a.K = K;
@@ -363,19 +436,24 @@ void tc_pass(cudaStream_t s, const void* x, const void* bmat, void* y, long long
     int dev = 0, v = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<PREC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               TC_SMEM));
-    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<PREC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               TC_SMEM));
     return v;
   }();
-  const long long tiles = a.ntm * a.ntn;
-  const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
-  if (out_f64)
-    tc_pass_kernel<PREC, 1><<<grid, TC_THREADS, TC_SMEM, s>>>(tx, tb, a);
-  else
-    tc_pass_kernel<PREC, 0><<<grid, TC_THREADS, TC_SMEM, s>>>(tx, tb, a);
-  KCUDA(cudaGetLastError());
+  const long long tiles = ((a.ntm + cl - 1) / cl) * a.ntn * cl;  // CTAs worth of work
+  long long g = tiles < sms ? tiles : sms;
+  g = g / cl * cl;
+  if (g < cl) g = cl;
+  const unsigned grid = static_cast<unsigned>(g);
+  if (cl == 2) {
+    if (out_f64)
+      tc_launch<PREC, 1, 2>(s, grid, tx, tb, a);
+    else
+      tc_launch<PREC, 0, 2>(s, grid, tx, tb, a);
+  } else {
+    if (out_f64)
+      tc_launch<PREC, 1, 1>(s, grid, tx, tb, a);
+    else
+      tc_launch<PREC, 0, 1>(s, grid, tx, tb, a);
+  }
 }
 
 template <int PREC>
