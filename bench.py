@@ -339,6 +339,25 @@ def folded_variant(A, grid, pot, ctx, b, x, bn, xn, op_dense, steps, world, loca
                       "tcgen05.mma kind::tf32 (M128 N256 K8), TMEM accumulators; FP64 in/out"}
         del xt
         torch.cuda.empty_cache()
+        xf = torch.empty_like(x)
+        op_dense.solve_lowp(b, "fp32", out=xf)
+        ref = op_dense.solve(b)
+        f3_err = float(torch.linalg.norm(xf - ref) / torch.linalg.norm(ref))
+        del ref
+        torch.cuda.synchronize()
+        e0.record(ctx.stream)
+        for _ in range(k):
+            op_dense.solve_lowp(b, "fp32", out=xf)
+        e1.record(ctx.stream)
+        torch.cuda.synchronize()
+        tf = max_over_ranks(world, e0.elapsed_time(e1) / 1e3 / k, "cuda:%d" % local)
+        bf["fp32_solve"] = {
+            "value": world * N / tf / 1e9, "unit": "GDoF/s", "ms_per_step": tf * 1e3,
+            "rel_diff_vs_fp64": f3_err,
+            "config": "same workload; FP32-level via 3xTF32: (hi, lo) TF32 pairs, three "
+                      "tcgen05.mma kind::tf32 (M128 N128 K8) per term into an FP32 TMEM accumulator"}
+        del xf
+        torch.cuda.empty_cache()
     except Exception as e:  # reported, never silently replaced
         bf = {"bf16_solve": {"error": str(e)[:200]}}
     return {**bf, "folded_solve": {

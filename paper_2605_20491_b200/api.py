@@ -383,10 +383,11 @@ class SeparableOperator:
 
     def solve_lowp(self, b: torch.Tensor, precision: str = "bf16", out=None) -> torch.Tensor:
         """Reduced-precision solve on the tcgen05 tensor cores (kronop_sep_solve_lowp, FP32
-        accumulation in TMEM): "bf16" (BF16 storage, the paper's BF16 mode, ~1e-2 relative) or
-        "tf32" (FP32 storage, TF32 products, ~1e-3)."""
+        accumulation in TMEM): "bf16" (BF16 storage, the paper's BF16 mode, ~1e-2 relative),
+        "tf32" (FP32 storage, TF32 products, ~1e-3) or "fp32" (3xTF32 on (hi, lo) pairs, the
+        paper's FP32 mode, ~1e-6)."""
         out = self._out(b, out)
-        prec = {"bf16": 1, "tf32": 2}[precision]
+        prec = {"bf16": 1, "tf32": 2, "fp32": 3}[precision]
         with _Call(self.ctx):
             check(lib().kronop_sep_solve_lowp(self.ctx.h, self.h, _ptr(b), prec, _ptr(out)))
         return out

@@ -61,6 +61,8 @@ struct kronop_op {
   void* lp_bwd[KRONOP_MAX_DIM] = {};
   void* tf_fwd[KRONOP_MAX_DIM] = {};  // FP32 storage for TF32
   void* tf_bwd[KRONOP_MAX_DIM] = {};
+  void* f3_fwd[KRONOP_MAX_DIM] = {};  // (hi, lo) TF32 pairs for the 3xTF32 FP32 mode
+  void* f3_bwd[KRONOP_MAX_DIM] = {};
   bool folded = false;
   int ne[KRONOP_MAX_DIM] = {}, no[KRONOP_MAX_DIM] = {};
   double* fe[KRONOP_MAX_DIM] = {};

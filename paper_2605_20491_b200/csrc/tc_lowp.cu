@@ -510,6 +510,279 @@ void sep_solve_lowp_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double
     }
 }
 
+// ---------------------------------------------------------------- FP32 via 3xTF32 --
+// The paper's FP32 row on tensor cores: every field value is carried as a pair (hi, lo) of
+// TF32-rounded floats (x ~ hi + lo, ~22 significant bits), every matrix likewise, and each
+// product is formed as hi*hi + hi*lo + lo*hi (the lo*lo term is below FP32 rounding) by three
+// tcgen05.mma kind::tf32 into one FP32 TMEM accumulator. Stage = A_hi, A_lo (128 x 32) and
+// B_hi, B_lo (128 x 32) = 64 KB, 3 stages; N = 128 per tile, two 128-column accumulators.
+constexpr int T3_BN = 128;
+constexpr int T3_A = TC_BM * TC_ROW;   // 16 KB per A half
+constexpr int T3_B = T3_BN * TC_ROW;   // 16 KB per B half
+constexpr int T3_STAGE = 2 * T3_A + 2 * T3_B;
+constexpr int T3_STAGES = 3;
+constexpr int T3_SMEM = T3_STAGES * T3_STAGE + 1024 + 256;
+constexpr int T3_TMEM_COLS = 256;
+constexpr uint32_t kIdesc3 =
+    (1u << 4) | (2u << 7) | (2u << 10) | ((T3_BN >> 3) << 17) | ((TC_BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32_n128(uint32_t d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(da), "l"(db), "r"(kIdesc3), "r"(acc));
+}
+
+template <int OUT_F64>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    t3_pass_kernel(const __grid_constant__ CUtensorMap txh, const __grid_constant__ CUtensorMap txl,
+                   const __grid_constant__ CUtensorMap tbh, const __grid_constant__ CUtensorMap tbl,
+                   const TcArgs a, float* __restrict__ ylo) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + T3_STAGES * T3_STAGE);
+  uint64_t* empty = full + T3_STAGES;
+  uint64_t* tfull = empty + T3_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < T3_STAGES; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mb_init(&tfull[b], 1);
+      mb_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     su32(tmem_slot)),
+                 "n"(T3_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const long long tiles = a.ntm * a.ntn;
+  constexpr int BK = 32;
+  const int KB = (a.K + BK - 1) / BK;
+  if (warp == 0) {
+    if (lane == 0) {
+      long long it = 0;
+      for (long long T = blockIdx.x; T < tiles; T += gridDim.x) {
+        const long long tm = T / a.ntn;
+        const int row0 = static_cast<int>(tm * TC_BM);
+        const int col0 = static_cast<int>(T - tm * a.ntn) * T3_BN;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % T3_STAGES);
+          const uint32_t ph = static_cast<uint32_t>((it / T3_STAGES) & 1);
+          mb_wait(&empty[s], ph ^ 1);
+          unsigned char* st = sm + s * T3_STAGE;
+          mb_expect_tx(&full[s], T3_STAGE);
+          tma2d(st, &txh, kb * BK, row0, &full[s]);
+          tma2d(st + T3_A, &txl, kb * BK, row0, &full[s]);
+          tma2d(st + 2 * T3_A, &tbh, kb * BK, col0, &full[s]);
+          tma2d(st + 2 * T3_A + T3_B, &tbl, kb * BK, col0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      long long it = 0, lt = 0;
+      for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
+        const int b = static_cast<int>(lt & 1);
+        mb_wait(&tempty[b], static_cast<uint32_t>((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + b * T3_BN;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % T3_STAGES);
+          mb_wait(&full[s], static_cast<uint32_t>((it / T3_STAGES) & 1));
+          tc_fence_after();
+          const uint32_t ah = su32(sm + s * T3_STAGE), al = ah + T3_A, bh = ah + 2 * T3_A,
+                         bl = bh + T3_B;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t o = kk * 32;
+            umma_tf32_n128(d, umma_desc(al + o), umma_desc(bh + o), (kb | kk) != 0);  // lo*hi
+            umma_tf32_n128(d, umma_desc(ah + o), umma_desc(bl + o), 1);               // hi*lo
+            umma_tf32_n128(d, umma_desc(ah + o), umma_desc(bh + o), 1);               // hi*hi
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[b]);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    long long lt = 0;
+    for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
+      const int b = static_cast<int>(lt & 1);
+      const long long tm = T / a.ntn;
+      const long long r = tm * TC_BM + 32 * q + lane;
+      const int col0 = static_cast<int>(T - tm * a.ntn) * T3_BN;
+      double lam_low = 0.0;
+      if (a.epi != 0 && r < a.R) {
+        long long rr = r;
+        for (int j = 0; j < a.nlow; ++j) {
+          const long long idx = rr % a.lowext[j];
+          rr /= a.lowext[j];
+          lam_low = __dadd_rn(lam_low, a.lowlam[j][idx]);
+        }
+      }
+      mb_wait(&tfull[b], static_cast<uint32_t>((lt >> 1) & 1));
+      tc_fence_after();
+      for (int c = 0; c < T3_BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + b * T3_BN + c * 32 + (static_cast<uint32_t>(32 * q) << 16), v);
+        if (r < a.R) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = col0 + c * 32 + j;
+            if (col >= a.m) break;
+            float val = __uint_as_float(v[j]);
+            if (a.epi != 0) {
+              const float ls = static_cast<float>(__dsub_rn(__dadd_rn(lam_low, a.lamlast[col]),
+                                                            a.shift));
+              val = val / ls;
+            }
+            const long long gi = static_cast<long long>(col) * a.R + r;
+            if (OUT_F64) {
+              static_cast<double*>(a.y)[gi] = static_cast<double>(val);
+            } else {
+              const float hi = round_tf32(val);
+              static_cast<float*>(a.y)[gi] = hi;
+              ylo[gi] = round_tf32(val - hi);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mb_arrive(&tempty[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "n"(T3_TMEM_COLS));
+  }
+}
+
+__global__ void k_f64_to_split(const double* __restrict__ x, float* __restrict__ hi,
+                               float* __restrict__ lo, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double v = x[i];
+    const float h = round_tf32(static_cast<float>(v));
+    hi[i] = h;
+    lo[i] = round_tf32(static_cast<float>(v - static_cast<double>(h)));
+  }
+}
+
+__global__ void k_mat_to_split(const double* __restrict__ a, int lda, int m, int k,
+                               float* __restrict__ hi, float* __restrict__ lo) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * k; e += gridDim.x * blockDim.x) {
+    const int i = e / k, kk = e - i * k;
+    const double v = a[i + static_cast<long long>(lda) * kk];
+    const float h = round_tf32(static_cast<float>(v));
+    hi[e] = h;
+    lo[e] = round_tf32(static_cast<float>(v - static_cast<double>(h)));
+  }
+}
+
+void t3_pass(cudaStream_t s, const float* xh, const float* xl, const float* bh, const float* bl,
+             void* y, float* ylo, long long R, int K, int m, bool out_f64, TcArgs a) {
+  CUtensorMap txh, txl, tbh, tbl;
+  encode_lowp_2d(&txh, xh, K, R, 32, TC_BM, 4);
+  encode_lowp_2d(&txl, xl, K, R, 32, TC_BM, 4);
+  encode_lowp_2d(&tbh, bh, K, m, 32, T3_BN, 4);
+  encode_lowp_2d(&tbl, bl, K, m, 32, T3_BN, 4);
+  a.y = y;
+  a.R = R;
+  a.K = K;
+  a.m = m;
+  a.ntn = (m + T3_BN - 1) / T3_BN;
+  a.ntm = (R + TC_BM - 1) / TC_BM;
+  static int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    KCUDA(cudaFuncSetAttribute(t3_pass_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, T3_SMEM));
+    KCUDA(cudaFuncSetAttribute(t3_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, T3_SMEM));
+    return v;
+  }();
+  const long long tiles = a.ntm * a.ntn;
+  const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
+  if (out_f64)
+    t3_pass_kernel<1><<<grid, TC_THREADS, T3_SMEM, s>>>(txh, txl, tbh, tbl, a, ylo);
+  else
+    t3_pass_kernel<0><<<grid, TC_THREADS, T3_SMEM, s>>>(txh, txl, tbh, tbl, a, ylo);
+  KCUDA(cudaGetLastError());
+}
+
+void sep_solve_3xtf32(kronop_ctx& ctx, kronop_op& op, const double* b, double* x) {
+  param_check(!op.folded, "solve_lowp: dense operators only");
+  for (int a = 0; a < op.d; ++a)
+    param_check(op.n[a] % 8 == 0 && op.n[a] >= 16, "solve_lowp: extents must be multiples of 8");
+  const long long N = op.N;
+  cudaStream_t s = ctx.stream;
+  if (!op.f3_fwd[0]) {  // (hi, lo) pairs of the transforms, row-major [out][k], made once
+    for (int a = 0; a < op.d; ++a) {
+      const int n = op.n[a];
+      for (int dir = 0; dir < 2; ++dir) {
+        void* p = nullptr;
+        KCUDA(cudaMalloc(&p, static_cast<size_t>(n) * n * 2 * sizeof(float)));
+        float* hp = static_cast<float*>(p);
+        k_mat_to_split<<<256, 256, 0, s>>>(dir == 0 ? op.fwd[a] : op.bwd[a], op.lda[a], n, n, hp,
+                                           hp + static_cast<size_t>(n) * n);
+        KCUDA(cudaGetLastError());
+        (dir == 0 ? op.f3_fwd : op.f3_bwd)[a] = p;
+      }
+    }
+  }
+  ensure_scratch(ctx, static_cast<size_t>(N + 16));  // (hi, lo) FP32 pairs = one double each
+  float* h0 = reinterpret_cast<float*>(ctx.scratch[0]);
+  float* l0 = h0 + N;
+  float* h1 = reinterpret_cast<float*>(ctx.scratch[1]);
+  float* l1 = h1 + N;
+  k_f64_to_split<<<kEltBlocks, 256, 0, s>>>(b, h0, l0, N);
+  KCUDA(cudaGetLastError());
+  ctx.ws.launches += 1;
+  const float *ch = h0, *cl = l0;
+  int k = 0;
+  for (int dir = 0; dir < 2; ++dir)
+    for (int a = 0; a < op.d; ++a, ++k) {
+      const bool last = dir == 1 && a == op.d - 1;
+      float* dh = (k % 2 == 0) ? h1 : h0;
+      float* dl = (k % 2 == 0) ? l1 : l0;
+      TcArgs ta{};
+      if (dir == 0 && a == op.d - 1) {
+        ta.epi = 1;
+        ta.shift = op.shift;
+        ta.nlow = op.d - 1;
+        for (int j = 0; j < op.d - 1; ++j) {
+          ta.lowext[j] = op.n[j];
+          ta.lowlam[j] = op.lam[j];
+        }
+        ta.lamlast = op.lam[a];
+      }
+      const int n = op.n[a];
+      const float* mh = static_cast<const float*>(dir == 0 ? op.f3_fwd[a] : op.f3_bwd[a]);
+      t3_pass(s, ch, cl, mh, mh + static_cast<size_t>(n) * n,
+              last ? static_cast<void*>(x) : static_cast<void*>(dh), dl, N / n, n, n, last, ta);
+      ctx.ws.launches += 1;
+      ch = dh;
+      cl = dl;
+    }
+}
+
 }  // namespace
 
 // (-Delta + V1 - shift)^{-1} b in BF16 or TF32 (FP32 storage) on tcgen05, FP32 accumulation
@@ -517,8 +790,10 @@ void sep_solve_lowp_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double
 void sep_solve_lowp(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int precision) {
   if (precision == PREC_BF16)
     sep_solve_lowp_impl<PREC_BF16>(ctx, op, b, x);
-  else
+  else if (precision == PREC_TF32)
     sep_solve_lowp_impl<PREC_TF32>(ctx, op, b, x);
+  else
+    sep_solve_3xtf32(ctx, op, b, x);
 }
 
 }  // namespace kronop_dev
