@@ -234,6 +234,29 @@ def secondary_metrics(A, P, ctx, device):
                   "L=8), A=-Delta, B=sep-osc V, box psi0, dt=5e-3, T=0.1 (PAPER.md:1381 setup)"}
     del lap, bdiag, psi0, state
     torch.cuda.empty_cache()
+    # BASELINE configs[1] second half: exp(-i dt (-Delta+V1)) on the 1024^3 grid, complex128
+    g = A.Grid.sem(8.0, 205, 5, 3)
+    op = g.separable_operator(ctx, [lambda t: t * t] * 3)
+    N = g.node_count()
+    psi = torch.view_as_complex(A.splitmix_uniform(ctx, 7, 2 * N).view(-1, 2))
+    o = torch.empty_like(psi)
+    op.propagate(psi, 0.01, out=o)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    for _ in range(2):
+        op.propagate(psi, 0.01, out=o)
+    e1.record(ctx.stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 2e3
+    out["propagate_1024"] = {
+        "value": N / t / 1e9, "unit": "GDoF/s", "ms_per_step": t * 1e3,
+        "tflops": 24.0 * 1024 ** 4 / t / 1e12,
+        "config": "exp(-i dt (-Delta+V1)), harmonic V1, 1024^3 complex128 (BASELINE configs[1]), "
+                  "dt = 0.01, phase fused into the last forward pass"}
+    del op, psi, o
+    torch.cuda.empty_cache()
     # BASELINE config 5 kernels: one complex propagate of the kinetic split (the A-step of
     # qHOP/Strang) on the 6D n = 29 and 9D n = 9 grids (fused_rot kernel)
     for name, (L_, cells, k, d) in {"6d_n29": (5.0, 3, 10, 6), "9d_n9": (3.0, 2, 5, 9)}.items():

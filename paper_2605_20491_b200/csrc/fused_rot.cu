@@ -37,7 +37,8 @@ namespace {
 // threads per CTA: 16 warps for the DMMA path (latency hiding), 8 for the DFMA path (the n x n
 // matrix lives in registers: 2 n^2 + O(n) registers per thread)
 template <int DN>
-__host__ __device__ constexpr int rt_threads() { return DN > 0 ? 256 : 512; }
+// (n = 9: 7 warps, so the 648 fibers an axis of a 9D tile holds split into 3 nearly full rounds)
+__host__ __device__ constexpr int rt_threads() { return DN == 9 ? 224 : DN > 0 ? 256 : 512; }
 constexpr int RT_MAXF = 3;
 constexpr int RT_STAGES = 3;
 constexpr int RT_TILE = 8192;  // doubles per stage (64 KB)
