@@ -99,8 +99,10 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(300)
-def test_slab_operators_world2_match_full_grid_oracle():
-    world = 2
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_slab_operators_match_full_grid_oracle(world):
+    """World sizes 2, 3, 4 on a 5 x 7 x 9 grid: uneven z-slabs and y-slabs (4 ranks: 3,2,2,2 and
+    2,2,2,1), every rank's piece of apply / solve / propagate / dot / PCG equal to the oracle."""
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
