@@ -335,9 +335,18 @@ def folded_variant(A, grid, pot, ctx, b, x, bn, xn, op_dense, steps, world, loca
         e1.record(ctx.stream)
         torch.cuda.synchronize()
         tb = max_over_ranks(world, e0.elapsed_time(e1) / 1e3 / k, "cuda:%d" % local)
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                bf16_peak = json.load(f).get("bf16_tflops_sustained")
+        except (OSError, ValueError):
+            bf16_peak = None
+        n1 = grid.shape[0]
         bf = {"bf16_solve": {
             "value": world * N / tb / 1e9, "unit": "GDoF/s", "ms_per_step": tb * 1e3,
             "rel_diff_vs_fp64": bf_err,
+            "tflops": 12.0 * n1 ** 4 / tb / 1e12,
+            "frac_of_bf16_peak": (12.0 * n1 ** 4 / tb / 1e12 / bf16_peak) if bf16_peak else None,
+            "bf16_peak_src": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS)",
             "config": "same workload; BF16 storage / FP32 accumulation, tcgen05.mma kind::f16 "
                       "(M128 N256 K16) with TMEM accumulators, TMA 128B-swizzled operands; "
                       "FP64 in/out"}}
