@@ -23,7 +23,7 @@ struct kronop_ctx {
   size_t io_cap = 0;
   // copy engines for the pipelined host path (H2D / D2H overlap the slab-local passes)
   cudaStream_t copy_stream[2] = {nullptr, nullptr};
-  static constexpr int kMaxChunks = 16;
+  static constexpr int kMaxChunks = 32;
   cudaEvent_t ev_in[kMaxChunks] = {};
   cudaEvent_t ev_out[kMaxChunks] = {};
   cudaEvent_t ev_ready = nullptr;
