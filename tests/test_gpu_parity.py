@@ -725,3 +725,30 @@ def test_lowp_tcgen05_solve(ctx, axes, prec):
     # is not IEEE-sequential, which the solve's cancellation amplifies to ~3e-4 (TF32 storage);
     # a layout / descriptor error would be O(1)
     assert rel(x16, cur) < (2e-3 if prec == "bf16" else 1e-3)
+
+
+# ------------------------------------------------------------------------- edge cases --
+@pytest.mark.parametrize("axes", [[(1.0, 1, 2), (2.0, 3, 4), (1.0, 1, 2)],       # n = 1, 11, 1
+                                  [(1.0, 1, 2)] * 9,                             # 9-D of n = 1
+                                  [(2.0, 2, 2), (1.0, 1, 2), (3.0, 5, 7), (1.0, 2, 2)],
+                                  [(8.0, 40, 5), (1.0, 1, 2)],                   # n = 199 (TMA) x 1
+                                  [(1.0, 1, 2), (8.0, 13, 5), (8.0, 13, 5)]])
+def test_degenerate_and_mixed_extents(ctx, axes):
+    """Axes of extent 1, mixed small / large extents and d up to 9 (tensor.hpp:33-34): every
+    operator path (small-extent kernel, TMA / cp.async passes) against the oracle, real and
+    complex, in place and out of place."""
+    A = api()
+    grid = A.Grid([A.assemble_sem(*a) for a in axes])
+    op = grid.separable_operator(ctx, [lambda t: t * t + 1.0] * grid.dim, 0.25)
+    ko = oracle_op_from(op, 0.25)
+    n = grid.node_count()
+    u = K.uniform_pm1(61, n)
+    psi = K.seeded_complex_field(grid.shape, 62)
+    for x in (u, psi):
+        assert rel(host(op.apply(dev(x))), ko.apply(x)) < 1e-13
+        xs = dev(x)
+        op.solve(xs, out=xs)  # in place
+        assert rel(host(xs), ko.solve(x)) < 1e-13
+    p = dev(psi)
+    op.propagate(p, 0.3, out=p)
+    assert rel(host(p), ko.propagate(psi, 0.3)) < 1e-13
