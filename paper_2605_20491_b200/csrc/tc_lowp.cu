@@ -423,6 +423,31 @@ void tc_pass(cudaStream_t s, const void* x, const void* bmat, void* y, long long
     const char* e = getenv("KRONOP_TC_CLUSTER");
     return e && e[0] == '2' ? 2 : 1;
   }();
+  static const bool two_sm = [] {
+    const char* e = getenv("KRONOP_TC_2SM");  // experimental: cta_group::2 pairs
+    return e && e[0] == '1';
+  }();
+  if (two_sm) {
+    CUtensorMap tx2, tb2;
+    encode_lowp_2d(&tx2, x, K, R, TcTraits<PREC>::BK, TC_BM, sizeof(T));
+    encode_lowp_2d(&tb2, bmat, K, m, TcTraits<PREC>::BK, TC_BN / 2, sizeof(T));
+    a.y = y;
+    a.R = R;
+    a.K = K;
+    a.m = m;
+    a.ntn = (m + TC_BN - 1) / TC_BN;
+    a.ntm = (R + TC_BM - 1) / TC_BM;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long pairs = ((a.ntm + 1) / 2) * a.ntn;
+    const long long g = 2 * (pairs < sms / 2 ? pairs : sms / 2);
+    if (out_f64)
+      tc2_launch<PREC, 1>(s, static_cast<unsigned>(g), tx2, tb2, a);
+    else
+      tc2_launch<PREC, 0>(s, static_cast<unsigned>(g), tx2, tb2, a);
+    return;
+  }
   CUtensorMap tx, tb;
   encode_lowp_2d(&tx, x, K, R, TcTraits<PREC>::BK, TC_BM, sizeof(T));
   encode_lowp_2d(&tb, bmat, K, m, TcTraits<PREC>::BK, cl == 2 ? TC_BN / 2 : TC_BN, sizeof(T));
@@ -508,6 +533,224 @@ void sep_solve_lowp_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double
       ctx.ws.launches += 1;
       cur = dst;
     }
+}
+
+// ------------------------------------------------------------- 2-SM (cta_group::2) --
+// A CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 issued by the leader (rank
+// 0): each CTA stages its own 128 rows of A and 128 of the 256 B rows (N split), so per SM a
+// stage is 32 KB for twice the FLOPs of the 1-SM kernel's 48 KB stage (6 stages fit). Both CTAs'
+// TMA loads complete on the leader's full barrier; the leader's commits multicast to both CTAs'
+// empty / accumulator-full barriers; both CTAs' epilogue warps release the leader's
+// accumulator-empty barrier. Protocol as in cute/arch/copy_sm100_tma.hpp (SM100_TMA_2SM_LOAD),
+// cute/arch/mma_sm100_umma.hpp (SM100_MMA_*_2x1SM_SS), cute/arch/tmem_allocator_sm100.hpp.
+constexpr int T2_STAGES = 6;
+constexpr int T2_A = TC_BM * TC_ROW;         // 16 KB
+constexpr int T2_B = (TC_BN / 2) * TC_ROW;   // 16 KB (this CTA's half of N)
+constexpr int T2_STAGE = T2_A + T2_B;
+constexpr int T2_SMEM = T2_STAGES * T2_STAGE + 1024 + 256;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the leader's barrier
+
+template <int PREC>
+__host__ __device__ constexpr uint32_t idesc2() {  // M = 256 (pair), N = 256
+  return (1u << 4) | (TcTraits<PREC>::FMT << 7) | (TcTraits<PREC>::FMT << 10) |
+         ((TC_BN >> 3) << 17) | ((256 >> 4) << 24);
+}
+__device__ __forceinline__ void tma2d_2sm(void* dst, const CUtensorMap* map, int c0, int c1,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(su32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(su32(bar) & kPeerMask)
+      : "memory");
+}
+template <int PREC>
+__device__ __forceinline__ void umma2(uint32_t d, uint64_t da, uint64_t db, uint32_t acc) {
+  if constexpr (PREC == PREC_BF16)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}\n" ::"r"(d),
+        "l"(da), "l"(db), "r"(idesc2<PREC>()), "r"(acc), "r"(0u));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}\n" ::"r"(d),
+        "l"(da), "l"(db), "r"(idesc2<PREC>()), "r"(acc), "r"(0u));
+}
+__device__ __forceinline__ void umma2_commit_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;\n" ::"r"(su32(bar)),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
+__device__ __forceinline__ void mb_arrive_rank(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(su32(bar)),
+      "r"(rank)
+      : "memory");
+}
+
+template <int PREC, int OUT_F64>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc2_pass_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tb,
+                    const TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + T2_STAGES * T2_STAGE);
+  uint64_t* empty = full + T2_STAGES;
+  uint64_t* tfull = empty + T2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t crank = cl_rank();
+  const bool leader = crank == 0;
+  if (tid == 0) {
+    for (int s = 0; s < T2_STAGES; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mb_init(&tfull[b], 1);
+      mb_init(&tempty[b], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     su32(tmem_slot)),
+                 "n"(TC_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cl_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const long long pair_tm = (a.ntm + 1) / 2;  // 256-row panels
+  const long long tiles = pair_tm * a.ntn;
+  const long long t0 = blockIdx.x / 2, tstep = gridDim.x / 2;
+  constexpr int BK = TcTraits<PREC>::BK;
+  const int KB = (a.K + BK - 1) / BK;
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs)
+      long long it = 0;
+      for (long long T = t0; T < tiles; T += tstep) {
+        const long long tg = T / a.ntn;
+        const int row0 = static_cast<int>((tg * 2 + crank) * TC_BM);
+        const int col0 = static_cast<int>(T - tg * a.ntn) * TC_BN + static_cast<int>(crank) * (TC_BN / 2);
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % T2_STAGES);
+          mb_wait(&empty[s], static_cast<uint32_t>((it / T2_STAGES) & 1) ^ 1);
+          unsigned char* st = sm + s * T2_STAGE;
+          if (leader) mb_expect_tx(&full[s], 2 * T2_STAGE);  // both CTAs' bytes land on it
+          tma2d_2sm(st, &tx, kb * BK, row0, &full[s]);
+          tma2d_2sm(st + T2_A, &tb, kb * BK, col0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // MMA issuer: the leader only
+      long long it = 0, lt = 0;
+      for (long long T = t0; T < tiles; T += tstep, ++lt) {
+        const int b = static_cast<int>(lt & 1);
+        mb_wait(&tempty[b], static_cast<uint32_t>((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + b * TC_BN;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % T2_STAGES);
+          mb_wait(&full[s], static_cast<uint32_t>((it / T2_STAGES) & 1));
+          tc_fence_after();
+          const uint32_t sa = su32(sm + s * T2_STAGE), sb = sa + T2_A;
+#pragma unroll
+          for (int kk = 0; kk < BK / TcTraits<PREC>::UK; ++kk)
+            umma2<PREC>(d, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
+          umma2_commit_mc(&empty[s]);
+        }
+        umma2_commit_mc(&tfull[b]);
+      }
+    }
+  } else {  // epilogue warps, both CTAs: this CTA's 128 rows x 256 columns
+    const int q = warp & 3;
+    long long lt = 0;
+    for (long long T = t0; T < tiles; T += tstep, ++lt) {
+      const int b = static_cast<int>(lt & 1);
+      const long long tg = T / a.ntn;
+      const long long r = (tg * 2 + crank) * TC_BM + 32 * q + lane;
+      const int col0 = static_cast<int>(T - tg * a.ntn) * TC_BN;
+      double lam_low = 0.0;
+      if (a.epi != 0 && r < a.R) {
+        long long rr = r;
+        for (int j = 0; j < a.nlow; ++j) {
+          const long long idx = rr % a.lowext[j];
+          rr /= a.lowext[j];
+          lam_low = __dadd_rn(lam_low, a.lowlam[j][idx]);
+        }
+      }
+      mb_wait(&tfull[b], static_cast<uint32_t>((lt >> 1) & 1));
+      tc_fence_after();
+      for (int c = 0; c < TC_BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + b * TC_BN + c * 32 + (static_cast<uint32_t>(32 * q) << 16), v);
+        if (r < a.R) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = col0 + c * 32 + j;
+            if (col >= a.m) break;
+            float val = __uint_as_float(v[j]);
+            if (a.epi != 0) {
+              const float ls = static_cast<float>(__dsub_rn(__dadd_rn(lam_low, a.lamlast[col]),
+                                                            a.shift));
+              val = val / ls;
+            }
+            const long long gi = static_cast<long long>(col) * a.R + r;
+            if (OUT_F64)
+              static_cast<double*>(a.y)[gi] = static_cast<double>(val);
+            else if (PREC == PREC_BF16)
+              static_cast<__nv_bfloat16*>(a.y)[gi] = __float2bfloat16_rn(val);
+            else
+              static_cast<float*>(a.y)[gi] = round_tf32(val);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mb_arrive_rank(&tempty[b], 0);  // the leader's barrier
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cl_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "n"(TC_TMEM_COLS));
+  }
+}
+
+template <int PREC, int OUT_F64>
+void tc2_launch(cudaStream_t s, unsigned grid, const CUtensorMap& tx, const CUtensorMap& tb,
+                const TcArgs& a) {
+  static bool attr = [] {
+    KCUDA(cudaFuncSetAttribute(tc2_pass_kernel<PREC, OUT_F64>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM));
+    return true;
+  }();
+  (void)attr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = T2_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KCUDA(cudaLaunchKernelEx(&cfg, tc2_pass_kernel<PREC, OUT_F64>, tx, tb, a));
 }
 
 // ---------------------------------------------------------------- FP32 via 3xTF32 --
