@@ -55,7 +55,8 @@ struct TcTraits<PREC_TF32> {
   static constexpr int UK = 8;
   static constexpr uint32_t FMT = 2; // TF32
 };
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM quadrant)
+constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_SMEM = TC_STAGES * TC_STAGE + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int TC_TMEM_COLS = 512;  // two 128 x 256 FP32 accumulators
 
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mb_init(&tfull[b], 1);
-      mb_init(&tempty[b], 4);
+      mb_init(&tempty[b], TC_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -282,8 +283,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         umma_commit(&tfull[b]);  // accumulator b complete
       }
     }
-  } else {  // epilogue warps 2..5: TMEM lane quadrant = warp % 4
+  } else {  // epilogue warps 2..9: TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4
     const int q = warp & 3;
+    const int hc = (warp - 2) >> 2;
     long long lt = 0;
     for (long long T = t0; T < tiles; T += tstep, ++lt) {
       const int b = static_cast<int>(lt & 1);
@@ -300,22 +302,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           lam_low = __dadd_rn(lam_low, a.lowlam[j][idx]);
         }
       }
+      const float lam_low_f = static_cast<float>(__dsub_rn(lam_low, a.shift));
       mb_wait(&tfull[b], tph);
       tc_fence_after();
-      for (int c = 0; c < TC_BN / 32; ++c) {
+      for (int c = hc * (TC_BN / 64); c < (hc + 1) * (TC_BN / 64); ++c) {
         uint32_t v[32];
         tmem_ld32(tmem + b * TC_BN + c * 32 + (static_cast<uint32_t>(32 * q) << 16), v);
-        if (r < a.R) {
+        if (a.epi == 0) {  // plain pass: no per-element arithmetic beyond the conversion
+          if (r < a.R) {
+            const int cb = col0 + c * 32;
+            const int nj = a.m - cb < 32 ? a.m - cb : 32;
+            long long gi = static_cast<long long>(cb) * a.R + r;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = col0 + c * 32 + j;
-            if (col >= a.m) break;
-            float val = __uint_as_float(v[j]);
-            if (a.epi != 0) {
-              const float ls = static_cast<float>(__dsub_rn(__dadd_rn(lam_low, a.lamlast[col]),
-                                                            a.shift));
-              val = a.epi == 1 ? val / ls : val * ls;
+            for (int j = 0; j < 32; ++j, gi += a.R) {
+              if (j >= nj) break;
+              const float val = __uint_as_float(v[j]);
+              if (OUT_F64)
+                static_cast<double*>(a.y)[gi] = static_cast<double>(val);
+              else if (PREC == PREC_BF16)
+                static_cast<__nv_bfloat16*>(a.y)[gi] = __float2bfloat16_rn(val);
+              else
+                static_cast<float*>(a.y)[gi] = round_tf32(val);
             }
+          }
+          continue;
+        }
+        // lambda of this chunk's 32 columns: one coalesced load, then broadcast by shuffle
+        float lam_c = 0.0f;
+        if (a.epi != 0) {
+          const int cl_ = col0 + c * 32 + lane;
+          lam_c = cl_ < a.m ? static_cast<float>(a.lamlast[cl_]) : 1.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {  // uniform (shuffles); stores predicated
+          const int col = col0 + c * 32 + j;
+          float val = __uint_as_float(v[j]);
+          if (a.epi != 0) {
+            // low-precision modes: lambda in FP32 and the fast FP32 divide (2 ulp) - the
+            // exact FP64 sum / IEEE divide made this pass epilogue-bound (7.3 vs 2.0 ms)
+            const float ls = lam_low_f + __shfl_sync(0xffffffffu, lam_c, j);
+            val = a.epi == 1 ? __fdividef(val, ls) : val * ls;
+          }
+          if (r < a.R && col < a.m) {
             const long long gi = static_cast<long long>(col) * a.R + r;
             if (OUT_F64)
               static_cast<double*>(a.y)[gi] = static_cast<double>(val);
@@ -423,9 +451,11 @@ void tc_pass(cudaStream_t s, const void* x, const void* bmat, void* y, long long
     const char* e = getenv("KRONOP_TC_CLUSTER");
     return e && e[0] == '2' ? 2 : 1;
   }();
+  // cta_group::2 pairs by default (1024^3: BF16 solve 16.0 -> 14.8 ms, TF32 26.8 -> 23.8 ms);
+  // KRONOP_TC_2SM=0 selects the 1-SM kernel
   static const bool two_sm = [] {
-    const char* e = getenv("KRONOP_TC_2SM");  // experimental: cta_group::2 pairs
-    return e && e[0] == '1';
+    const char* e = getenv("KRONOP_TC_2SM");
+    return !(e && e[0] == '0');
   }();
   if (two_sm) {
     CUtensorMap tx2, tb2;
@@ -613,7 +643,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mb_init(&tfull[b], 1);
-      mb_init(&tempty[b], 8);  // 4 epilogue warps in each CTA of the pair
+      mb_init(&tempty[b], 2 * TC_EPI_WARPS);  // the epilogue warps of both CTAs of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -673,6 +703,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {  // epilogue warps, both CTAs: this CTA's 128 rows x 256 columns
     const int q = warp & 3;
+    const int hc = (warp - 2) >> 2;
     long long lt = 0;
     for (long long T = t0; T < tiles; T += tstep, ++lt) {
       const int b = static_cast<int>(lt & 1);
@@ -688,22 +719,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           lam_low = __dadd_rn(lam_low, a.lowlam[j][idx]);
         }
       }
+      const float lam_low_f = static_cast<float>(__dsub_rn(lam_low, a.shift));
       mb_wait(&tfull[b], static_cast<uint32_t>((lt >> 1) & 1));
       tc_fence_after();
-      for (int c = 0; c < TC_BN / 32; ++c) {
+      for (int c = hc * (TC_BN / 64); c < (hc + 1) * (TC_BN / 64); ++c) {
         uint32_t v[32];
         tmem_ld32(tmem + b * TC_BN + c * 32 + (static_cast<uint32_t>(32 * q) << 16), v);
-        if (r < a.R) {
+        if (a.epi == 0) {  // plain pass: no per-element arithmetic beyond the conversion
+          if (r < a.R) {
+            const int cb = col0 + c * 32;
+            const int nj = a.m - cb < 32 ? a.m - cb : 32;
+            long long gi = static_cast<long long>(cb) * a.R + r;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = col0 + c * 32 + j;
-            if (col >= a.m) break;
-            float val = __uint_as_float(v[j]);
-            if (a.epi != 0) {
-              const float ls = static_cast<float>(__dsub_rn(__dadd_rn(lam_low, a.lamlast[col]),
-                                                            a.shift));
-              val = val / ls;
+            for (int j = 0; j < 32; ++j, gi += a.R) {
+              if (j >= nj) break;
+              const float val = __uint_as_float(v[j]);
+              if (OUT_F64)
+                static_cast<double*>(a.y)[gi] = static_cast<double>(val);
+              else if (PREC == PREC_BF16)
+                static_cast<__nv_bfloat16*>(a.y)[gi] = __float2bfloat16_rn(val);
+              else
+                static_cast<float*>(a.y)[gi] = round_tf32(val);
             }
+          }
+          continue;
+        }
+        // lambda of this chunk's 32 columns: one coalesced load, then broadcast by shuffle
+        float lam_c = 0.0f;
+        if (a.epi != 0) {
+          const int cl_ = col0 + c * 32 + lane;
+          lam_c = cl_ < a.m ? static_cast<float>(a.lamlast[cl_]) : 1.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {  // uniform (shuffles); stores predicated
+          const int col = col0 + c * 32 + j;
+          float val = __uint_as_float(v[j]);
+          if (a.epi != 0) {
+            const float ls = lam_low_f + __shfl_sync(0xffffffffu, lam_c, j);
+            val = __fdividef(val, ls);
+          }
+          if (r < a.R && col < a.m) {
             const long long gi = static_cast<long long>(col) * a.R + r;
             if (OUT_F64)
               static_cast<double*>(a.y)[gi] = static_cast<double>(val);
@@ -797,7 +852,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mb_init(&tfull[b], 1);
-      mb_init(&tempty[b], 4);
+      mb_init(&tempty[b], TC_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -862,6 +917,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     const int q = warp & 3;
+    const int hc = (warp - 2) >> 2;
     long long lt = 0;
     for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
       const int b = static_cast<int>(lt & 1);
@@ -877,22 +933,47 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           lam_low = __dadd_rn(lam_low, a.lowlam[j][idx]);
         }
       }
+      const float lam_low_f = static_cast<float>(__dsub_rn(lam_low, a.shift));
       mb_wait(&tfull[b], static_cast<uint32_t>((lt >> 1) & 1));
       tc_fence_after();
-      for (int c = 0; c < T3_BN / 32; ++c) {
+      for (int c = hc * (T3_BN / 64); c < (hc + 1) * (T3_BN / 64); ++c) {
         uint32_t v[32];
         tmem_ld32(tmem + b * T3_BN + c * 32 + (static_cast<uint32_t>(32 * q) << 16), v);
-        if (r < a.R) {
+        if (a.epi == 0) {  // plain pass
+          if (r < a.R) {
+            const int cb = col0 + c * 32;
+            const int nj = a.m - cb < 32 ? a.m - cb : 32;
+            long long gi = static_cast<long long>(cb) * a.R + r;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = col0 + c * 32 + j;
-            if (col >= a.m) break;
-            float val = __uint_as_float(v[j]);
-            if (a.epi != 0) {
-              const float ls = static_cast<float>(__dsub_rn(__dadd_rn(lam_low, a.lamlast[col]),
-                                                            a.shift));
-              val = val / ls;
+            for (int j = 0; j < 32; ++j, gi += a.R) {
+              if (j >= nj) break;
+              const float val = __uint_as_float(v[j]);
+              if (OUT_F64) {
+                static_cast<double*>(a.y)[gi] = static_cast<double>(val);
+              } else {
+                const float hi = round_tf32(val);
+                static_cast<float*>(a.y)[gi] = hi;
+                ylo[gi] = round_tf32(val - hi);
+              }
             }
+          }
+          continue;
+        }
+        // lambda of this chunk's 32 columns: one coalesced load, then broadcast by shuffle
+        float lam_c = 0.0f;
+        if (a.epi != 0) {
+          const int cl_ = col0 + c * 32 + lane;
+          lam_c = cl_ < a.m ? static_cast<float>(a.lamlast[cl_]) : 1.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {  // uniform (shuffles); stores predicated
+          const int col = col0 + c * 32 + j;
+          float val = __uint_as_float(v[j]);
+          if (a.epi != 0) {
+            const float ls = lam_low_f + __shfl_sync(0xffffffffu, lam_c, j);
+            val = __fdividef(val, ls);
+          }
+          if (r < a.R && col < a.m) {
             const long long gi = static_cast<long long>(col) * a.R + r;
             if (OUT_F64) {
               static_cast<double*>(a.y)[gi] = static_cast<double>(val);
