@@ -384,10 +384,13 @@ class SeparableOperator:
     def solve_lowp(self, b: torch.Tensor, precision: str = "bf16", out=None) -> torch.Tensor:
         """Reduced-precision solve on the tcgen05 tensor cores (kronop_sep_solve_lowp, FP32
         accumulation in TMEM): "bf16" (BF16 storage, the paper's BF16 mode, ~1e-2 relative),
-        "tf32" (FP32 storage, TF32 products, ~1e-3) or "fp32" (3xTF32 on (hi, lo) pairs, the
-        paper's FP32 mode, ~1e-6)."""
+        "tf32" (FP32 storage, TF32 products, ~1e-3), "fp32" (3xTF32 on (hi, lo) pairs, the
+        paper's FP32 mode, ~1e-6), or FP64 emulated on the INT8 tensor cores (Ozaki scheme):
+        "ozaki" (7 slices of 8 bits, FP64-level), "ozaki6", "ozaki5" (fewer slices, ~1e-13 /
+        ~1e-11)."""
         out = self._out(b, out)
-        prec = {"bf16": 1, "tf32": 2, "fp32": 3}[precision]
+        prec = {"bf16": 1, "tf32": 2, "fp32": 3, "ozaki": 4, "ozaki7": 4, "ozaki6": 5,
+                "ozaki5": 6}[precision]
         with _Call(self.ctx):
             check(lib().kronop_sep_solve_lowp(self.ctx.h, self.h, _ptr(b), prec, _ptr(out)))
         return out

@@ -830,7 +830,7 @@ int kronop_op_destroy(kronop_op* op) {
       for (double* p : {op->fe[a], op->fo[a], op->be[a], op->bo[a]})
         if (p) cudaFree(p);
       for (void* p : {op->lp_fwd[a], op->lp_bwd[a], op->tf_fwd[a], op->tf_bwd[a], op->f3_fwd[a],
-                      op->f3_bwd[a]})
+                      op->f3_bwd[a], op->oz_fwd[a], op->oz_bwd[a]})
         if (p) cudaFree(p);
       if (!op->shared_axis[a]) {
         if (op->fwd[a]) cudaFree(op->fwd[a]);
@@ -911,11 +911,13 @@ int kronop_sep_solve_lowp(kronop_ctx* ctx, kronop_op* op, const double* b, int p
                           double* out) {
   return guard([&] {
     param_check(ctx && op && b && out && b != out, "solve_lowp: bad argument");
-    param_check(precision == KRONOP_PREC_BF16 || precision == KRONOP_PREC_TF32 ||
-                    precision == KRONOP_PREC_FP32X3,
+    param_check(precision >= KRONOP_PREC_BF16 && precision <= KRONOP_PREC_FP64_OZAKI5,
                 "solve_lowp: unsupported precision");
     check_solve_shift(*ctx, *op, op->shift);
-    sep_solve_lowp(*ctx, *op, b, out, precision);
+    if (precision >= KRONOP_PREC_FP64_OZAKI)
+      sep_solve_ozaki(*ctx, *op, b, out, 7 - (precision - KRONOP_PREC_FP64_OZAKI));
+    else
+      sep_solve_lowp(*ctx, *op, b, out, precision);
   });
 }
 

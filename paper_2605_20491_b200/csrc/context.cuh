@@ -63,6 +63,9 @@ struct kronop_op {
   void* tf_bwd[KRONOP_MAX_DIM] = {};
   void* f3_fwd[KRONOP_MAX_DIM] = {};  // (hi, lo) TF32 pairs for the 3xTF32 FP32 mode
   void* f3_bwd[KRONOP_MAX_DIM] = {};
+  void* oz_fwd[KRONOP_MAX_DIM] = {};  // tiled INT8 slices + row exponents (ozaki.cu)
+  void* oz_bwd[KRONOP_MAX_DIM] = {};
+  int oz_slices = 0;
   bool folded = false;
   int ne[KRONOP_MAX_DIM] = {}, no[KRONOP_MAX_DIM] = {};
   double* fe[KRONOP_MAX_DIM] = {};
@@ -74,6 +77,7 @@ struct kronop_op {
 
 namespace kronop_dev {
 void sep_solve_lowp(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int precision);
+void sep_solve_ozaki(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int slices);
 // Smallest free pool block with capacity >= n doubles, else a new cudaMalloc'd block.
 double* pool_get(kronop_ctx& ctx, size_t n);
 void pool_put(kronop_ctx& ctx, double* p);

@@ -1,0 +1,552 @@
+// FP64 emulation on the INT8 tensor cores (Ozaki scheme): the separable
+// solve (-Delta + V1 - shift)^{-1} b (operators.cpp:42-61) with every per-axis transform computed
+// as a sum of exact INT8 x INT8 -> INT32 products on tcgen05 (kind::i8, TMEM accumulators).
+//
+// Splitting. Every row of an operand (a K-run of the field, or a row of an axis matrix) gets a
+// power-of-two exponent e with max|x| < 2^e and is cut into S signed 8-bit slices by repeated
+// rounding with the base 254 (|t| <= 127 at every step, so no slice ever needs -128 or 128):
+//     t_0 = 127 x 2^-e,  a_s = rint(t_s),  t_{s+1} = 254 (t_s - a_s),   a_s in [-127, 127],
+//     x = 2^e / 127 * sum_{s<S} a_s 254^-s + r,     |r| <= 2^e / 127 * 254^-(S-1) / 2.
+// (Every operand is signed: the tcgen05 kind::i8 path as measured here gave wrong products for
+// unsigned slices >= 128 under mixed s8 / u8 descriptors, so no unsigned slices are used.) A dot
+// product of two split rows is then
+//     sum_k x_k y_k = 2^(ex+ey) / 127^2 * sum_{g<S} 254^-g G_g,
+//     G_g = sum_{s+t=g} sum_k a_s[k] b_t[k]   (exact in INT32: |G_g| <= S 127^2 K < 2^31)
+// with the products s + t >= S (weight <= 254^-S) dropped: S(S+1)/2 INT8 products, error
+// ~ K 254^-(S-1) max|x| max|y| per output. S = 7 carries ~55 bits, the FP64 DGEMM bound (the
+// splitting and the FP64 Horner combination add only FP64 roundings of the parts).
+//
+// Layout. Split operands are stored pre-tiled in the exact shared-memory image the MMA reads:
+// per (row panel of P rows, K-block of 32 bytes) one contiguous block of S slices, each slice in
+// the canonical no-swizzle K-major UMMA layout (8-row x 16-byte core matrices, K-adjacent core
+// matrices 128 B apart, 8-row groups 256 B apart). A pipeline stage is then two plain bulk copies
+// (cp.async.bulk, S x 4 KB of X slices for 128 rows + S x 2 KB of matrix slices for 64 outputs).
+//
+// Pass kernel (persistent, one CTA per SM): warp 0 = bulk-copy producer over a 4-stage ring;
+// warp 1 = TMEM allocator + single-thread MMA issuer: per stage, S(S+1)/2 tcgen05.mma
+// (M = 128 rows, N = 64 outputs, K = 32) into S INT32 accumulators (group g at TMEM columns
+// 64 g .. +64: 448 columns for S = 7); warps 2-9 = epilogue: Horner-combine the groups in FP64
+// (exact INT32 -> FP64, weights 254^-g), scale by 2^(ex+ey) / 127^2, the fused spectral divide
+// in FP64 (__ddiv_rn of the axis-order lambda sum, as mode_product_tma.cu), and the FP64 store of
+// the rotated output Y[i * R + r] (the contracted axis moves to the slow end, as in tc_lowp.cu).
+// A separate HBM-bound kernel splits each pass's FP64 output for the next pass.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "context.cuh"
+#include "kronop_internal.cuh"
+
+namespace kronop_dev {
+
+namespace {
+
+constexpr int OZ_BM = 128;  // field rows per tile (MMA M)
+constexpr int OZ_BN = 64;   // outputs per tile (MMA N)
+constexpr int OZ_BK = 32;   // K bytes per stage = one MMA
+constexpr int OZ_STAGES = 5;
+constexpr int OZ_KMAX = 3200;  // 8 staged rows of the split kernel in 227 KB (INT32 exact to 16384)
+constexpr int OZ_THREADS = 320;
+constexpr int OZ_EPI_WARPS = 8;
+constexpr int OZ_TMEM_COLS = 512;
+
+template <int S>
+struct OzGeom {
+  static constexpr int A_SLICE = OZ_BM * OZ_BK;  // 4 KB
+  static constexpr int B_SLICE = OZ_BN * OZ_BK;  // 2 KB
+  static constexpr int A = S * A_SLICE;
+  static constexpr int B = S * B_SLICE;
+  static constexpr int STAGE = A + B;
+  static constexpr int SMEM = OZ_STAGES * STAGE + 1024 + 256;
+};
+
+struct OzArgs {
+  const int8_t* xs;  // tiled slices of the field rows   [R/128][KB][S][128 x 32]
+  const int* xe;     // row exponents (R padded)
+  const int8_t* bs;  // tiled slices of the matrix rows  [m/64][KB][S][64 x 32]
+  const int* be;     // output-row exponents
+  double* y;
+  long long R;
+  int K, KB, m, ntn;
+  long long ntm;
+  int epi;  // 0 store, 1 divide by (lambda - shift)
+  double shift;
+  int nlow;
+  int lowext[KRONOP_MAX_DIM];
+  const double* lowlam[KRONOP_MAX_DIM];
+  const double* lamlast;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(uint64_t* b, int c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+// K-major, no-swizzle UMMA descriptor (cute/arch/mma_sm100_desc.hpp SmemDescriptor; canonical
+// layout ((8,m),(T,2)):((1T,SBO),(1,LBO)) of cute/atom/mma_traits_sm100.hpp): LBO = 128 B between
+// the two K-adjacent core matrices, SBO = 256 B between 8-row groups, version 1, layout 0.
+__device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(128 >> 4) << 16) |
+         (static_cast<uint64_t>(256 >> 4) << 32) | (1ull << 46);
+}
+// instruction descriptor: S8 x S8 -> S32, K-major A and B, N = 64, M = 128
+__host__ __device__ constexpr uint32_t oz_idesc() {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((OZ_BN >> 3) << 17) | ((OZ_BM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(oz_idesc()), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(OZ_THREADS, 1) oz_pass_kernel(const OzArgs a) {
+  using G = OzGeom<S>;
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + OZ_STAGES * G::STAGE);
+  uint64_t* empty = full + OZ_STAGES;
+  uint64_t* tfull = empty + OZ_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    mb_init(tfull, 1);
+    mb_init(tempty, OZ_EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     su32(tmem_slot)),
+                 "n"(OZ_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const long long tiles = a.ntm * a.ntn;  // output tiles fastest: CTAs share the row panel in L2
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      long long it = 0;
+      for (long long T = blockIdx.x; T < tiles; T += gridDim.x) {
+        const long long tp = T / a.ntn;
+        const long long tn = T - tp * a.ntn;
+        const int8_t* xa = a.xs + tp * a.KB * static_cast<long long>(G::A);
+        const int8_t* xb = a.bs + tn * a.KB * static_cast<long long>(G::B);
+        for (int kb = 0; kb < a.KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % OZ_STAGES);
+          const uint32_t ph = static_cast<uint32_t>((it / OZ_STAGES) & 1);
+          mb_wait(&empty[s], ph ^ 1);
+          unsigned char* st = sm + s * G::STAGE;
+          mb_expect_tx(&full[s], G::STAGE);
+          bulk_g2s(st, xa + static_cast<long long>(kb) * G::A, G::A, &full[s]);
+          bulk_g2s(st + G::A, xb + static_cast<long long>(kb) * G::B, G::B, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      long long it = 0, lt = 0;
+      for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
+        mb_wait(tempty, static_cast<uint32_t>((lt & 1) ^ 1));
+        tc_fence_after();
+        for (int kb = 0; kb < a.KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % OZ_STAGES);
+          const uint32_t ph = static_cast<uint32_t>((it / OZ_STAGES) & 1);
+          mb_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sa = su32(sm + s * G::STAGE), sb = sa + G::A;
+#pragma unroll
+          for (int i = 0; i < S; ++i)
+#pragma unroll
+            for (int j = 0; j < S - i; ++j)  // slice pair (i, j) -> group i + j
+              umma_i8(tmem + (i + j) * OZ_BN, oz_desc(sa + i * G::A_SLICE),
+                      oz_desc(sb + j * G::B_SLICE), (kb | i) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(tfull);
+      }
+    }
+  } else {  // epilogue warps 2..9: TMEM lane quadrant warp % 4, column half (warp - 2) / 4
+    const int q = warp & 3;
+    const int hc = (warp - 2) >> 2;
+    long long lt = 0;
+    for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
+      const long long tp = T / a.ntn;
+      const int tn = static_cast<int>(T - tp * a.ntn);
+      const long long r = tp * OZ_BM + 32 * q + lane;
+      const int c0 = tn * OZ_BN + hc * 32;
+      mb_wait(tfull, static_cast<uint32_t>(lt & 1));
+      tc_fence_after();
+      double acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+#pragma unroll 1
+      for (int g = S - 1; g >= 0; --g) {  // Horner from the smallest weight: acc = acc/254 + G_g
+        uint32_t v[32];
+        tmem_ld32(tmem + g * OZ_BN + hc * 32 + (static_cast<uint32_t>(32 * q) << 16), v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          acc[j] = fma(acc[j], 1.0 / 254.0, static_cast<double>(static_cast<int>(v[j])));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mb_arrive(tempty);  // accumulators free: next tile's MMAs overlap the stores
+      const bool live = r < a.R;
+      const int er = live ? a.xe[r] : 0;
+      double lam_low = 0.0;
+      if (a.epi != 0 && live) {  // axes below the contracted one, in axis order from 0.0
+        long long rr = r;
+        for (int j = 0; j < a.nlow; ++j) {
+          const long long idx = rr % a.lowext[j];
+          rr /= a.lowext[j];
+          lam_low = __dadd_rn(lam_low, a.lowlam[j][idx]);
+        }
+      }
+      const int ecol = c0 + lane < a.m ? a.be[c0 + lane] : 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {  // uniform (shuffles); stores predicated
+        const int col = c0 + j;
+        const int ec = __shfl_sync(0xffffffffu, ecol, j);
+        if (live && col < a.m) {
+          double val = ldexp(acc[j] * (1.0 / 16129.0), er + ec);  // 2^(ex+ey) / 127^2
+          if (a.epi == 1)
+            val = __ddiv_rn(val, __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift));
+          a.y[static_cast<long long>(col) * a.R + r] = val;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "n"(OZ_TMEM_COLS));
+  }
+}
+
+// One 16-byte chunk of a row: t holds 127 x 2^-e; S slices a_s = rint(t), t = 254 (t - a_s).
+template <int S>
+__device__ __forceinline__ void split16(double (&t)[16], uint32_t (&w)[S][4]) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[s][q] = 0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const double f = rint(t[u]);
+      t[u] = (t[u] - f) * 254.0;
+      w[s][u >> 2] |= (static_cast<uint32_t>(static_cast<int>(f)) & 0xFFu) << (8 * (u & 3));
+    }
+  }
+}
+
+// Tiled byte offset of (row rr of its P-row panel, 16-byte chunk c of K) within slice 0 of the
+// panel's K-block c / 2; slice s adds s * P * 32.
+template <int P>
+__device__ __forceinline__ long long tile_off(long long p, int KB, int S, int rr, int c) {
+  return ((p * KB + (c >> 1)) * S) * static_cast<long long>(P * OZ_BK) + (rr >> 3) * 256 +
+         (c & 1) * 128 + (rr & 7) * 16;
+}
+
+// Field rows (contiguous K-runs): a block stages 8 rows (one 8-row core-matrix group) in shared
+// memory with one coalesced read, takes the row maxima, and writes the slices so that 8 lanes
+// fill one 128-byte core matrix. Chunks are staged 17 doubles apart and rows ld = 4 (mod 16)
+// doubles apart, so the 32 lanes (8 rows x 4 chunks) of a chunk read hit 16 distinct bank pairs:
+// the 2-wavefront minimum. HBM-bound: 8 B read and
+// S B written per element.
+template <int S>
+__global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict__ x, long long R,
+                                                       int K, int KB, long long Rp,
+                                                       int8_t* __restrict__ out,
+                                                       int* __restrict__ ex) {
+  extern __shared__ double srow[];
+  __shared__ int sexp[8];
+  const int Kp = KB * OZ_BK;
+  const int nch = KB * 2;
+  const int ld = nch * 17 + ((4 - nch) & 15);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (long long r0 = blockIdx.x * 8LL; r0 < Rp; r0 += gridDim.x * 8LL) {
+    // stage: warp w loads row r0 + w
+    {
+      const long long r = r0 + warp;
+      double amax = 0.0;
+      for (int k = lane; k < Kp; k += 32) {
+        const double v = (r < R && k < K) ? x[r * K + k] : 0.0;
+        srow[warp * ld + (k >> 4) * 17 + (k & 15)] = v;
+        amax = fmax(amax, fabs(v));
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      int e = 0;
+      if (amax > 0.0) frexp(amax, &e);  // amax < 2^e
+      if (lane == 0) {
+        sexp[warp] = e;
+        if (r < Rp) ex[r] = e;
+      }
+    }
+    __syncthreads();
+    const long long p = r0 / OZ_BM;
+    const int rr0 = static_cast<int>(r0 - p * OZ_BM);
+    for (int item = tid; item < 8 * nch; item += 256) {
+      const int rw = item & 7, c = item >> 3;
+      const int e = sexp[rw];
+      double t[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) t[u] = ldexp(srow[rw * ld + c * 17 + u], -e) * 127.0;
+      uint32_t w[S][4];
+      split16<S>(t, w);
+      int8_t* base = out + tile_off<OZ_BM>(p, KB, S, rr0 + rw, c);
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2)
+        *reinterpret_cast<uint4*>(base + s2 * static_cast<long long>(OZ_BM * OZ_BK)) =
+            make_uint4(w[s2][0], w[s2][1], w[s2][2], w[s2][3]);
+    }
+    __syncthreads();
+  }
+}
+
+// Axis matrices (element (i, k) at M[i + lda k], rows i = outputs), split once per operator:
+// one warp per row, strided reads (small, cached).
+template <int S>
+__global__ void __launch_bounds__(256) k_oz_split_mat(const double* __restrict__ M, int lda,
+                                                      int m, int K, int KB, int mp,
+                                                      int8_t* __restrict__ out,
+                                                      int* __restrict__ ex) {
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int nch = KB * 2;
+  for (int r = w0; r < mp; r += nw) {
+    double amax = 0.0;
+    if (r < m)
+      for (int k = lane; k < K; k += 32) amax = fmax(amax, fabs(M[r + static_cast<long long>(lda) * k]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    int e = 0;
+    if (amax > 0.0) frexp(amax, &e);
+    if (lane == 0) ex[r] = e;
+    const int p = r / OZ_BN, rr = r - p * OZ_BN;
+    for (int c = lane; c < nch; c += 32) {
+      double t[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int k = c * 16 + u;
+        t[u] = (r < m && k < K) ? ldexp(M[r + static_cast<long long>(lda) * k], -e) * 127.0 : 0.0;
+      }
+      uint32_t w[S][4];
+      split16<S>(t, w);
+      int8_t* base = out + tile_off<OZ_BN>(p, KB, S, rr, c);
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2)
+        *reinterpret_cast<uint4*>(base + s2 * static_cast<long long>(OZ_BN * OZ_BK)) =
+            make_uint4(w[s2][0], w[s2][1], w[s2][2], w[s2][3]);
+    }
+  }
+}
+
+template <int S>
+void oz_split_rows(cudaStream_t st, const double* x, long long R, int K, int8_t* out, int* ex) {
+  const int KB = (K + OZ_BK - 1) / OZ_BK;
+  const long long Rp = (R + OZ_BM - 1) / OZ_BM * OZ_BM;
+  const int nch = KB * 2;
+  const size_t smem = static_cast<size_t>(8) * (nch * 17 + ((4 - nch) & 15)) * sizeof(double);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    KCUDA(cudaFuncSetAttribute(k_oz_split_rows<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+    attr = smem;
+  }
+  const long long groups = Rp / 8;
+  const int per_sm = smem <= 72 * 1024 ? 3 : 1;
+  const int blocks = static_cast<int>(groups < 148LL * per_sm * 4 ? groups : 148LL * per_sm * 4);
+  k_oz_split_rows<S><<<blocks, 256, smem, st>>>(x, R, K, KB, Rp, out, ex);
+  KCUDA(cudaGetLastError());
+}
+
+template <int S>
+void oz_split_mat(cudaStream_t st, const double* M, int lda, int m, int K, int8_t* out, int* ex) {
+  const int KB = (K + OZ_BK - 1) / OZ_BK;
+  const int mp = (m + OZ_BN - 1) / OZ_BN * OZ_BN;
+  const int blocks = (mp + 7) / 8;
+  k_oz_split_mat<S><<<blocks, 256, 0, st>>>(M, lda, m, K, KB, mp, out, ex);
+  KCUDA(cudaGetLastError());
+}
+
+template <int S>
+void oz_pass(cudaStream_t st, OzArgs a) {
+  using G = OzGeom<S>;
+  static int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    KCUDA(cudaFuncSetAttribute(oz_pass_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               G::SMEM));
+    return v;
+  }();
+  const long long tiles = a.ntm * a.ntn;
+  const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
+  oz_pass_kernel<S><<<grid, OZ_THREADS, G::SMEM, st>>>(a);
+  KCUDA(cudaGetLastError());
+}
+
+inline size_t oz_slice_bytes(long long rows, int K, int P, int S) {
+  const long long Rp = (rows + P - 1) / P * P;
+  const long long KB = (K + OZ_BK - 1) / OZ_BK;
+  return static_cast<size_t>(Rp * KB * OZ_BK * S);
+}
+
+template <int S>
+void sep_solve_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double* x) {
+  param_check(!op.folded, "solve_lowp: dense operators only");
+  const long long N = op.N;
+  cudaStream_t st = ctx.stream;
+  void** of = op.oz_fwd;
+  void** ob = op.oz_bwd;
+  if (!of[0] || op.oz_slices != S) {  // split copies of the transforms, made once per S
+    for (int a = 0; a < KRONOP_MAX_DIM; ++a)
+      for (void** p : {&of[a], &ob[a]})
+        if (*p) {
+          KCUDA(cudaFree(*p));
+          *p = nullptr;
+        }
+    for (int a = 0; a < op.d; ++a) {
+      const int n = op.n[a];
+      const size_t sb = oz_slice_bytes(n, n, OZ_BN, S);
+      const long long mp = (n + OZ_BN - 1) / OZ_BN * OZ_BN;
+      for (int dir = 0; dir < 2; ++dir) {
+        void* p = nullptr;
+        KCUDA(cudaMalloc(&p, sb + mp * sizeof(int)));
+        // matrix element (i, k) at M[i + lda * k]: rows i (outputs), contraction k
+        oz_split_mat<S>(st, dir == 0 ? op.fwd[a] : op.bwd[a], op.lda[a], n, n,
+                        static_cast<int8_t*>(p), reinterpret_cast<int*>(static_cast<char*>(p) + sb));
+        (dir == 0 ? of : ob)[a] = p;
+      }
+    }
+    op.oz_slices = S;
+  }
+  // workspace: one FP64 field (scratch[0]) + the current pass's slices and row exponents
+  size_t need = 0;
+  for (int a = 0; a < op.d; ++a) {
+    const long long R = N / op.n[a];
+    const size_t v = oz_slice_bytes(R, op.n[a], OZ_BM, S) + ((R + OZ_BM - 1) / OZ_BM * OZ_BM) * sizeof(int);
+    need = v > need ? v : need;
+  }
+  const size_t need_d = (need + 7) / 8 + 16;
+  ensure_scratch(ctx, need_d > static_cast<size_t>(N) ? need_d : static_cast<size_t>(N));
+  double* f = ctx.scratch[0];
+  int8_t* xs = reinterpret_cast<int8_t*>(ctx.scratch[1]);
+  const double* cur = b;
+  int k = 0;
+  for (int dir = 0; dir < 2; ++dir)
+    for (int a = 0; a < op.d; ++a, ++k) {
+      const bool last = dir == 1 && a == op.d - 1;
+      const int n = op.n[a];
+      const long long R = N / n;
+      const size_t xb = oz_slice_bytes(R, n, OZ_BM, S);
+      int* xe = reinterpret_cast<int*>(xs + xb);
+      oz_split_rows<S>(st, cur, R, n, xs, xe);
+      OzArgs oa{};
+      if (dir == 0 && a == op.d - 1) {
+        oa.epi = 1;
+        oa.shift = op.shift;
+        oa.nlow = op.d - 1;
+        for (int j = 0; j < op.d - 1; ++j) {
+          oa.lowext[j] = op.n[j];
+          oa.lowlam[j] = op.lam[j];
+        }
+        oa.lamlast = op.lam[a];
+      }
+      const void* mat = dir == 0 ? of[a] : ob[a];
+      const size_t mb = oz_slice_bytes(n, n, OZ_BN, S);
+      oa.xs = xs;
+      oa.xe = xe;
+      oa.bs = static_cast<const int8_t*>(mat);
+      oa.be = reinterpret_cast<const int*>(static_cast<const char*>(mat) + mb);
+      oa.y = last ? x : f;
+      oa.R = R;
+      oa.K = n;
+      oa.KB = (n + OZ_BK - 1) / OZ_BK;
+      oa.m = n;
+      oa.ntn = (n + OZ_BN - 1) / OZ_BN;
+      oa.ntm = (R + OZ_BM - 1) / OZ_BM;
+      oz_pass<S>(st, oa);
+      ctx.ws.launches += 2;
+      cur = f;
+    }
+}
+
+}  // namespace
+
+// (-Delta + V1 - shift)^{-1} b with FP64 accuracy from INT8 tensor-core products (Ozaki scheme,
+// `slices` 8-bit slices per operand: 5, 6 or 7). Real fields, FP64 device in and out.
+void sep_solve_ozaki(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int slices) {
+  for (int a = 0; a < op.d; ++a)
+    param_check(op.n[a] <= OZ_KMAX, "solve_lowp: Ozaki mode needs extents <= 3200");
+  if (slices == 5)
+    sep_solve_ozaki_impl<5>(ctx, op, b, x);
+  else if (slices == 6)
+    sep_solve_ozaki_impl<6>(ctx, op, b, x);
+  else
+    sep_solve_ozaki_impl<7>(ctx, op, b, x);
+}
+
+}  // namespace kronop_dev

@@ -752,3 +752,27 @@ def test_degenerate_and_mixed_extents(ctx, axes):
     p = dev(psi)
     op.propagate(p, 0.3, out=p)
     assert rel(host(p), ko.propagate(psi, 0.3)) < 1e-13
+
+
+# ------------------------------------------ FP64 emulation on INT8 tensor cores (Ozaki) --
+@pytest.mark.parametrize("axes", [[(8.0, 13, 5)] * 3, [(8.0, 5, 5), (8.0, 41, 1), (8.0, 17, 1)],
+                                  [(8.0, 4, 3), (6.0, 9, 5), (8.0, 3, 7)],
+                                  [(8.0, 61, 5)] * 2 + [(8.0, 5, 5)],
+                                  [(8.0, 3, 4)] * 4, [(8.0, 29, 5)]])
+@pytest.mark.parametrize("prec,tol", [("ozaki", 1e-12), ("ozaki6", 2e-10), ("ozaki5", 3e-8)])
+def test_ozaki_int8_solve(ctx, axes, prec, tol):
+    """(-Delta+V1)^-1 with every transform as exact INT8 tcgen05 products of 7-bit slices
+    (kind::i8, S32 accumulators in TMEM): equal to the FP64 (DMMA) solve to FP64 level with 7
+    slices; fewer slices lose 8 bits each. Ragged extents (K % 32, m % 64, R % 128 != 0) and
+    1-D / 4-D fields included."""
+    A = api()
+    grid = A.Grid([A.assemble_sem(*a) for a in axes])
+    op = grid.separable_operator(ctx, [lambda t: t * t + 0.5 * t] * grid.dim, 0.0)
+    n = grid.node_count()
+    b = dev(K.uniform_pm1(11, n))
+    x64 = host(op.solve(b))
+    xoz = host(op.solve_lowp(b, prec))
+    assert rel(xoz, x64) < tol
+    # the low-order slices matter: a second right-hand side at a very different scale
+    b2 = dev(K.uniform_pm1(12, n) * 1e-200)
+    assert rel(host(op.solve_lowp(b2, prec)), host(op.solve(b2))) < tol
