@@ -390,6 +390,37 @@ def folded_variant(A, grid, pot, ctx, b, x, bn, xn, op_dense, steps, world, loca
                       "tcgen05.mma kind::tf32 (M128 N128 K8) per term into an FP32 TMEM accumulator"}
         del xf
         torch.cuda.empty_cache()
+        # FP64 emulated on the INT8 tensor cores (Ozaki scheme, 7 signed slices of base 254,
+        # 28 exact INT8 products per transform): FP64-level agreement with the DMMA path
+        xo = torch.empty_like(x)
+        op_dense.solve_lowp(b, "ozaki", out=xo)
+        ref = op_dense.solve(b)
+        oz_err = float(torch.linalg.norm(xo - ref) / torch.linalg.norm(ref))
+        oz_max = float((xo - ref).abs().max() / ref.abs().max())
+        del ref
+        torch.cuda.synchronize()
+        e0.record(ctx.stream)
+        for _ in range(k):
+            op_dense.solve_lowp(b, "ozaki", out=xo)
+        e1.record(ctx.stream)
+        torch.cuda.synchronize()
+        to = max_over_ranks(world, e0.elapsed_time(e1) / 1e3 / k, "cuda:%d" % local)
+        int8_tops = 28 * 12.0 * n1 ** 4 / to / 1e12
+        bf["ozaki_fp64_solve"] = {
+            "value": world * N / to / 1e9, "unit": "GDoF/s", "ms_per_step": to * 1e3,
+            "rel_diff_vs_fp64": oz_err, "max_rel_diff_vs_fp64": oz_max,
+            "speedup_vs_dmma_fp64": None,
+            "int8_tops": int8_tops,
+            "frac_of_int8_peak": (int8_tops / (2 * bf16_peak)) if bf16_peak else None,
+            "int8_peak_src": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (dense INT8 = 2x BF16 "
+                             "on sm_100)",
+            "config": "same workload; FP64 emulation: per-row power-of-two scales, 7 signed "
+                      "8-bit slices (base 254) per operand, 28 tcgen05.mma kind::i8 "
+                      "(M128 N64 K32) products into 7 INT32 TMEM accumulators, FP64 Horner "
+                      "combination + FP64 spectral divide in the epilogue; HBM-bound split "
+                      "kernel between passes"}
+        del xo
+        torch.cuda.empty_cache()
     except Exception as e:  # reported, never silently replaced
         bf = {"bf16_solve": {"error": str(e)[:200]}}
     return {**bf, "folded_solve": {
@@ -476,6 +507,9 @@ def run_kronop(args):
 
     variants = {} if args.no_extras else folded_variant(A, grid, pot, ctx, b, x, bn, xn, op,
                                                         args.steps, world, local)
+    oz = variants.get("ozaki_fp64_solve")
+    if oz and oz.get("ms_per_step"):
+        oz["speedup_vs_dmma_fp64"] = t_step * 1e3 / oz["ms_per_step"]
     extras = {} if args.no_extras else secondary_metrics(A, P, ctx, local)
     cpu = None
     if rank == 0 and not args.no_cpu:

@@ -30,6 +30,8 @@
 // in FP64 (__ddiv_rn of the axis-order lambda sum, as mode_product_tma.cu), and the FP64 store of
 // the rotated output Y[i * R + r] (the contracted axis moves to the slow end, as in tc_lowp.cu).
 // A separate HBM-bound kernel splits each pass's FP64 output for the next pass.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -50,6 +52,7 @@ constexpr int OZ_KMAX = 3200;  // 8 staged rows of the split kernel in 227 KB (I
 constexpr int OZ_THREADS = 320;
 constexpr int OZ_EPI_WARPS = 8;
 constexpr int OZ_TMEM_COLS = 512;
+constexpr int OZ_PAIR = 2 * OZ_BM;  // rows of a 2-SM pair tile; field slices are padded to it
 
 template <int S>
 struct OzGeom {
@@ -119,6 +122,26 @@ __device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(128 >> 4) << 16) |
          (static_cast<uint64_t>(256 >> 4) << 32) | (1ull << 46);
 }
+// The same descriptor split in halves: the low word carries the start address, so the slices of
+// a stage are reached by adding (offset >> 4) to one precomputed word (addresses < 256 KB: no
+// carry out of the 14-bit field).
+constexpr uint32_t kOzDescHi = (256 >> 4) | (1u << 14);
+__device__ __forceinline__ uint32_t oz_desc_lo(uint32_t saddr) {
+  return ((saddr >> 4) & 0x3FFF) | ((128 >> 4) << 16);
+}
+__device__ __forceinline__ uint64_t oz_desc_of(uint32_t lo) {
+  return (static_cast<uint64_t>(kOzDescHi) << 32) | lo;
+}
+// one lane of a converged warp (elect.sync): the MMA warp runs its loop converged and only the
+// issue is single-threaded, so the descriptors stay in uniform registers
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, %1;\n@px mov.s32 %0, 1;\n}\n"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
 // instruction descriptor: S8 x S8 -> S32, K-major A and B, N = 64, M = 128
 __host__ __device__ constexpr uint32_t oz_idesc() {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((OZ_BN >> 3) << 17) | ((OZ_BM >> 4) << 24);
@@ -146,6 +169,55 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// Epilogue, part 1: Horner-combine this warp's 32 x 32 block of the S group accumulators
+// (TMEM lane quadrant q, column half hc) from the smallest weight: acc = acc / 254 + G_g.
+template <int S>
+__device__ __forceinline__ void oz_drain(uint32_t tmem, int q, int hc, double (&acc)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+#pragma unroll 1
+  for (int g = S - 1; g >= 0; --g) {
+    uint32_t v[32];
+    tmem_ld32(tmem + g * OZ_BN + hc * 32 + (static_cast<uint32_t>(32 * q) << 16), v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      acc[j] = fma(acc[j], 1.0 / 254.0, static_cast<double>(static_cast<int>(v[j])));
+  }
+}
+
+// Epilogue, part 2: scale by 2^(ex+ey) / 127^2, the spectral divide (lambda summed in axis order
+// from 0.0, minus the shift, IEEE divide: operators.cpp:57), rotated FP64 store y[col * R + r].
+__device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, int lane,
+                                         const double (&acc)[32]) {
+  const bool live = r < a.R;
+  const int er = live ? a.xe[r] : 0;
+  double lam_low = 0.0;
+  if (a.epi != 0 && live) {  // axes below the contracted one, in axis order from 0.0
+    long long rr = r;
+    for (int j = 0; j < a.nlow; ++j) {
+      const long long idx = rr % a.lowext[j];
+      rr /= a.lowext[j];
+      lam_low = __dadd_rn(lam_low, a.lowlam[j][idx]);
+    }
+  }
+  const int ecol = c0 + lane < a.m ? a.be[c0 + lane] : 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {  // uniform (shuffles); stores predicated
+    const int col = c0 + j;
+    const int ec = __shfl_sync(0xffffffffu, ecol, j);
+    if (live && col < a.m) {
+      const int E = er + ec;  // 2^(ex+ey) / 127^2: exponent bits directly when in normal range
+      const double v0 = acc[j] * (1.0 / 16129.0);
+      double val = (E > -1000 && E < 1000)
+                       ? v0 * __longlong_as_double(static_cast<long long>(1023 + E) << 52)
+                       : ldexp(v0, E);
+      if (a.epi == 1)
+        val = __ddiv_rn(val, __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift));
+      a.y[static_cast<long long>(col) * a.R + r] = val;
+    }
+  }
 }
 
 template <int S>
@@ -201,28 +273,31 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_pass_kernel(const OzArgs a) 
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
-      long long it = 0, lt = 0;
-      for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
-        mb_wait(tempty, static_cast<uint32_t>((lt & 1) ^ 1));
+  } else if (warp == 1) {  // MMA warp (converged; one elected lane issues)
+    long long it = 0, lt = 0;
+    for (long long T = blockIdx.x; T < tiles; T += gridDim.x, ++lt) {
+      mb_wait(tempty, static_cast<uint32_t>((lt & 1) ^ 1));
+      tc_fence_after();
+      for (int kb = 0; kb < a.KB; ++kb, ++it) {
+        const int s = static_cast<int>(it % OZ_STAGES);
+        const uint32_t ph = static_cast<uint32_t>((it / OZ_STAGES) & 1);
+        mb_wait(&full[s], ph);
         tc_fence_after();
-        for (int kb = 0; kb < a.KB; ++kb, ++it) {
-          const int s = static_cast<int>(it % OZ_STAGES);
-          const uint32_t ph = static_cast<uint32_t>((it / OZ_STAGES) & 1);
-          mb_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t sa = su32(sm + s * G::STAGE), sb = sa + G::A;
+        const uint32_t sa = su32(sm + s * G::STAGE);
+        const uint32_t la = oz_desc_lo(sa), lb = oz_desc_lo(sa + G::A);
+        if (elect_one()) {
 #pragma unroll
           for (int i = 0; i < S; ++i)
 #pragma unroll
             for (int j = 0; j < S - i; ++j)  // slice pair (i, j) -> group i + j
-              umma_i8(tmem + (i + j) * OZ_BN, oz_desc(sa + i * G::A_SLICE),
-                      oz_desc(sb + j * G::B_SLICE), (kb | i) != 0);
+              umma_i8(tmem + (i + j) * OZ_BN, oz_desc_of(la + ((i * G::A_SLICE) >> 4)),
+                      oz_desc_of(lb + ((j * G::B_SLICE) >> 4)), (kb | i) != 0);
           umma_commit(&empty[s]);
         }
-        umma_commit(tfull);
+        __syncwarp();
       }
+      if (elect_one()) umma_commit(tfull);
+      __syncwarp();
     }
   } else {  // epilogue warps 2..9: TMEM lane quadrant warp % 4, column half (warp - 2) / 4
     const int q = warp & 3;
@@ -236,42 +311,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_pass_kernel(const OzArgs a) 
       mb_wait(tfull, static_cast<uint32_t>(lt & 1));
       tc_fence_after();
       double acc[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = 0.0;
-#pragma unroll 1
-      for (int g = S - 1; g >= 0; --g) {  // Horner from the smallest weight: acc = acc/254 + G_g
-        uint32_t v[32];
-        tmem_ld32(tmem + g * OZ_BN + hc * 32 + (static_cast<uint32_t>(32 * q) << 16), v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          acc[j] = fma(acc[j], 1.0 / 254.0, static_cast<double>(static_cast<int>(v[j])));
-      }
+      oz_drain<S>(tmem, q, hc, acc);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mb_arrive(tempty);  // accumulators free: next tile's MMAs overlap the stores
-      const bool live = r < a.R;
-      const int er = live ? a.xe[r] : 0;
-      double lam_low = 0.0;
-      if (a.epi != 0 && live) {  // axes below the contracted one, in axis order from 0.0
-        long long rr = r;
-        for (int j = 0; j < a.nlow; ++j) {
-          const long long idx = rr % a.lowext[j];
-          rr /= a.lowext[j];
-          lam_low = __dadd_rn(lam_low, a.lowlam[j][idx]);
-        }
-      }
-      const int ecol = c0 + lane < a.m ? a.be[c0 + lane] : 0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {  // uniform (shuffles); stores predicated
-        const int col = c0 + j;
-        const int ec = __shfl_sync(0xffffffffu, ecol, j);
-        if (live && col < a.m) {
-          double val = ldexp(acc[j] * (1.0 / 16129.0), er + ec);  // 2^(ex+ey) / 127^2
-          if (a.epi == 1)
-            val = __ddiv_rn(val, __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift));
-          a.y[static_cast<long long>(col) * a.R + r] = val;
-        }
-      }
+      oz_store(a, r, c0, lane, acc);
     }
   }
   tc_fence_before();
@@ -283,18 +327,198 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_pass_kernel(const OzArgs a) 
   }
 }
 
+// ------------------------------------------------------------------ 2-SM (cta_group::2) --
+// A CTA pair computes a 256-row x 64-output tile with tcgen05.mma.cta_group::2 (M = 256, N = 64,
+// K = 32) issued by the leader: each CTA stages its own 128 rows of field slices (S x 4 KB) and
+// its 32-output half of the matrix slices (S x 1 KB) per stage, so per SM the tensor core reads
+// 5 KB of shared memory per 128 x 64 x 32 block instead of 6 KB, and the matrix crosses L2 -> SM
+// once per pair. Protocol as tc2_pass_kernel (tc_lowp.cu): both CTAs' TMA loads (a 2-D byte view
+// of the tiled buffers, 128-byte rows, no swizzle) complete on the leader's full barrier, the
+// leader's commits multicast to both CTAs' empty / accumulator-full barriers, and both CTAs'
+// epilogue warps release the leader's accumulator-empty barrier.
+template <int S>
+struct Oz2Geom {
+  static constexpr int A_SLICE = OZ_BM * OZ_BK;        // 4 KB
+  static constexpr int B_SLICE = (OZ_BN / 2) * OZ_BK;  // 1 KB
+  static constexpr int A = S * A_SLICE;
+  static constexpr int B = S * B_SLICE;
+  static constexpr int STAGE = A + B;
+  static constexpr int STAGES = (200 * 1024) / STAGE < 8 ? (200 * 1024) / STAGE : 8;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+constexpr uint32_t kOzPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the leader's barrier
+
+__host__ __device__ constexpr uint32_t oz2_idesc() {  // S8 x S8 -> S32, M = 256 (pair), N = 64
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((OZ_BN >> 3) << 17) | ((OZ_PAIR >> 4) << 24);
+}
+__device__ __forceinline__ void umma2_i8(uint32_t d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}\n" ::"r"(d),
+      "l"(da), "l"(db), "r"(oz2_idesc()), "r"(acc), "r"(0u));
+}
+__device__ __forceinline__ void umma2_commit_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;\n" ::"r"(su32(bar)),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
+__device__ __forceinline__ void tma_rows_2sm(void* dst, const CUtensorMap* map, int row,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(su32(dst)),
+      "l"(map), "r"(0), "r"(row), "r"(su32(bar) & kOzPeerMask)
+      : "memory");
+}
+__device__ __forceinline__ void mb_arrive_rank(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(su32(bar)),
+      "r"(rank)
+      : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
+template <int S>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    oz2_pass_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tb,
+                    const OzArgs a) {
+  using G = Oz2Geom<S>;
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + G::STAGES * G::STAGE);
+  uint64_t* empty = full + G::STAGES;
+  uint64_t* tfull = empty + G::STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t crank = cl_rank();
+  const bool leader = crank == 0;
+  if (tid == 0) {
+    for (int s = 0; s < G::STAGES; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    mb_init(tfull, 1);
+    mb_init(tempty, 2 * OZ_EPI_WARPS);  // the epilogue warps of both CTAs
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     su32(tmem_slot)),
+                 "n"(OZ_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cl_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const long long pair_tm = a.ntm / 2;  // 256-row panels (field slices padded to them)
+  const long long tiles = pair_tm * a.ntn;
+  const long long t0 = blockIdx.x / 2, tstep = gridDim.x / 2;
+  if (warp == 0) {
+    if (lane == 0) {  // producer (both CTAs): byte-view rows of 128 B
+      long long it = 0;
+      for (long long T = t0; T < tiles; T += tstep) {
+        const long long tp = T / a.ntn;
+        const long long tn = T - tp * a.ntn;
+        const long long arow0 = (tp * 2 + crank) * a.KB * (G::A / 128);
+        const long long brow0 = (tn * 2 + crank) * a.KB * (G::B / 128);
+        for (int kb = 0; kb < a.KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % G::STAGES);
+          mb_wait(&empty[s], static_cast<uint32_t>((it / G::STAGES) & 1) ^ 1);
+          unsigned char* st = sm + s * G::STAGE;
+          if (leader) mb_expect_tx(&full[s], 2 * G::STAGE);  // both CTAs' bytes land on it
+          tma_rows_2sm(st, &tx, static_cast<int>(arow0 + kb * (G::A / 128)), &full[s]);
+          tma_rows_2sm(st + G::A, &tb, static_cast<int>(brow0 + kb * (G::B / 128)), &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {  // MMA warp of the leader (converged; one elected lane issues)
+      long long it = 0, lt = 0;
+      for (long long T = t0; T < tiles; T += tstep, ++lt) {
+        mb_wait(tempty, static_cast<uint32_t>((lt & 1) ^ 1));
+        tc_fence_after();
+        for (int kb = 0; kb < a.KB; ++kb, ++it) {
+          const int s = static_cast<int>(it % G::STAGES);
+          mb_wait(&full[s], static_cast<uint32_t>((it / G::STAGES) & 1));
+          tc_fence_after();
+          const uint32_t sa = su32(sm + s * G::STAGE);
+          const uint32_t la = oz_desc_lo(sa), lb = oz_desc_lo(sa + G::A);
+          if (elect_one()) {
+#pragma unroll
+            for (int i = 0; i < S; ++i)
+#pragma unroll
+              for (int j = 0; j < S - i; ++j)
+                umma2_i8(tmem + (i + j) * OZ_BN, oz_desc_of(la + ((i * G::A_SLICE) >> 4)),
+                         oz_desc_of(lb + ((j * G::B_SLICE) >> 4)), (kb | i) != 0);
+            umma2_commit_mc(&empty[s]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) umma2_commit_mc(tfull);
+        __syncwarp();
+      }
+    }
+  } else {  // epilogue warps, both CTAs: this CTA's 128 rows x 64 outputs
+    const int q = warp & 3;
+    const int hc = (warp - 2) >> 2;
+    long long lt = 0;
+    for (long long T = t0; T < tiles; T += tstep, ++lt) {
+      const long long tp = T / a.ntn;
+      const int tn = static_cast<int>(T - tp * a.ntn);
+      const long long r = (tp * 2 + crank) * OZ_BM + 32 * q + lane;
+      const int c0 = tn * OZ_BN + hc * 32;
+      mb_wait(tfull, static_cast<uint32_t>(lt & 1));
+      tc_fence_after();
+      double acc[32];
+      oz_drain<S>(tmem, q, hc, acc);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mb_arrive_rank(tempty, 0);  // the leader's barrier
+      oz_store(a, r, c0, lane, acc);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cl_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "n"(OZ_TMEM_COLS));
+  }
+}
+
 // One 16-byte chunk of a row: t holds 127 x 2^-e; S slices a_s = rint(t), t = 254 (t - a_s).
+// rint by the 1.5 * 2^52 shifter: y = t + M rounds t to the nearest integer (ties to even, as
+// rint) into the low mantissa bits, so the INT8 value is the low word of y (|t| <= 127) and
+// y - M is rint(t) as a double: three FP64 adds / one multiply per slice, no conversions.
 template <int S>
 __device__ __forceinline__ void split16(double (&t)[16], uint32_t (&w)[S][4]) {
+  constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
 #pragma unroll
   for (int s = 0; s < S; ++s) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) w[s][q] = 0;
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const double f = rint(t[u]);
-      t[u] = (t[u] - f) * 254.0;
-      w[s][u >> 2] |= (static_cast<uint32_t>(static_cast<int>(f)) & 0xFFu) << (8 * (u & 3));
+      const double y = __dadd_rn(t[u], kShift);
+      const double f = __dsub_rn(y, kShift);
+      t[u] = __dmul_rn(__dsub_rn(t[u], f), 254.0);
+      w[s][u >> 2] |= (static_cast<uint32_t>(__double2loint(y)) & 0xFFu) << (8 * (u & 3));
     }
   }
 }
@@ -329,10 +553,21 @@ __global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict_
     {
       const long long r = r0 + warp;
       double amax = 0.0;
-      for (int k = lane; k < Kp; k += 32) {
-        const double v = (r < R && k < K) ? x[r * K + k] : 0.0;
-        srow[warp * ld + (k >> 4) * 17 + (k & 15)] = v;
-        amax = fmax(amax, fabs(v));
+      for (int k0 = 0; k0 < Kp; k0 += 256) {  // 8 independent loads in flight per lane
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = k0 + u * 32 + lane;
+          v[u] = (r < R && k < K) ? __ldcs(x + r * K + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = k0 + u * 32 + lane;
+          if (k < Kp) {
+            srow[warp * ld + (k >> 4) * 17 + (k & 15)] = v[u];
+            amax = fmax(amax, fabs(v[u]));
+          }
+        }
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -349,9 +584,15 @@ __global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict_
     for (int item = tid; item < 8 * nch; item += 256) {
       const int rw = item & 7, c = item >> 3;
       const int e = sexp[rw];
+      const double sc = ldexp(127.0, -e);
       double t[16];
+      if (e > -900) {  // 127 x 2^-e is finite: one exact-scale multiply
 #pragma unroll
-      for (int u = 0; u < 16; ++u) t[u] = ldexp(srow[rw * ld + c * 17 + u], -e) * 127.0;
+        for (int u = 0; u < 16; ++u) t[u] = srow[rw * ld + c * 17 + u] * sc;
+      } else {  // rows of (near-)subnormals
+#pragma unroll
+        for (int u = 0; u < 16; ++u) t[u] = ldexp(srow[rw * ld + c * 17 + u], -e) * 127.0;
+      }
       uint32_t w[S][4];
       split16<S>(t, w);
       int8_t* base = out + tile_off<OZ_BM>(p, KB, S, rr0 + rw, c);
@@ -366,7 +607,7 @@ __global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict_
 
 // Axis matrices (element (i, k) at M[i + lda k], rows i = outputs), split once per operator:
 // one warp per row, strided reads (small, cached).
-template <int S>
+template <int S, int P>
 __global__ void __launch_bounds__(256) k_oz_split_mat(const double* __restrict__ M, int lda,
                                                       int m, int K, int KB, int mp,
                                                       int8_t* __restrict__ out,
@@ -384,20 +625,22 @@ __global__ void __launch_bounds__(256) k_oz_split_mat(const double* __restrict__
     int e = 0;
     if (amax > 0.0) frexp(amax, &e);
     if (lane == 0) ex[r] = e;
-    const int p = r / OZ_BN, rr = r - p * OZ_BN;
+    const int p = r / P, rr = r - p * P;
+    const double sc = ldexp(127.0, -e);
     for (int c = lane; c < nch; c += 32) {
       double t[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int k = c * 16 + u;
-        t[u] = (r < m && k < K) ? ldexp(M[r + static_cast<long long>(lda) * k], -e) * 127.0 : 0.0;
+        const double v = (r < m && k < K) ? M[r + static_cast<long long>(lda) * k] : 0.0;
+        t[u] = e > -900 ? v * sc : ldexp(v, -e) * 127.0;
       }
       uint32_t w[S][4];
       split16<S>(t, w);
-      int8_t* base = out + tile_off<OZ_BN>(p, KB, S, rr, c);
+      int8_t* base = out + tile_off<P>(p, KB, S, rr, c);
 #pragma unroll
       for (int s2 = 0; s2 < S; ++s2)
-        *reinterpret_cast<uint4*>(base + s2 * static_cast<long long>(OZ_BN * OZ_BK)) =
+        *reinterpret_cast<uint4*>(base + s2 * static_cast<long long>(P * OZ_BK)) =
             make_uint4(w[s2][0], w[s2][1], w[s2][2], w[s2][3]);
     }
   }
@@ -406,7 +649,7 @@ __global__ void __launch_bounds__(256) k_oz_split_mat(const double* __restrict__
 template <int S>
 void oz_split_rows(cudaStream_t st, const double* x, long long R, int K, int8_t* out, int* ex) {
   const int KB = (K + OZ_BK - 1) / OZ_BK;
-  const long long Rp = (R + OZ_BM - 1) / OZ_BM * OZ_BM;
+  const long long Rp = (R + OZ_PAIR - 1) / OZ_PAIR * OZ_PAIR;  // whole 256-row pair panels
   const int nch = KB * 2;
   const size_t smem = static_cast<size_t>(8) * (nch * 17 + ((4 - nch) & 15)) * sizeof(double);
   static size_t attr = 0;
@@ -422,12 +665,18 @@ void oz_split_rows(cudaStream_t st, const double* x, long long R, int K, int8_t*
   KCUDA(cudaGetLastError());
 }
 
+// P = 64 (1-SM kernel: one 64-output tile per block) or 32 (2-SM kernel: each CTA of the pair
+// stages its 32-output half of the tile)
 template <int S>
-void oz_split_mat(cudaStream_t st, const double* M, int lda, int m, int K, int8_t* out, int* ex) {
+void oz_split_mat(cudaStream_t st, const double* M, int lda, int m, int K, int P, int8_t* out,
+                  int* ex) {
   const int KB = (K + OZ_BK - 1) / OZ_BK;
   const int mp = (m + OZ_BN - 1) / OZ_BN * OZ_BN;
   const int blocks = (mp + 7) / 8;
-  k_oz_split_mat<S><<<blocks, 256, 0, st>>>(M, lda, m, K, KB, mp, out, ex);
+  if (P == 32)
+    k_oz_split_mat<S, 32><<<blocks, 256, 0, st>>>(M, lda, m, K, KB, mp, out, ex);
+  else
+    k_oz_split_mat<S, OZ_BN><<<blocks, 256, 0, st>>>(M, lda, m, K, KB, mp, out, ex);
   KCUDA(cudaGetLastError());
 }
 
@@ -448,10 +697,77 @@ void oz_pass(cudaStream_t st, OzArgs a) {
   KCUDA(cudaGetLastError());
 }
 
-inline size_t oz_slice_bytes(long long rows, int K, int P, int S) {
-  const long long Rp = (rows + P - 1) / P * P;
+PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    KCUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr));
+    if (qr != cudaDriverEntryPointSuccess || !p)
+      fail(KRONOP_ERUNTIME, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D byte view of a tiled slice buffer: rows of 128 bytes, box = one CTA's stage part
+void oz_encode_rows(CUtensorMap* map, const void* base, size_t bytes, int box_rows) {
+  const cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(bytes / 128)};
+  const cuuint64_t str[1] = {128};
+  const cuuint32_t box[2] = {128, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = oz_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base),
+                                    dims, str, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(KRONOP_ERUNTIME, "cuTensorMapEncodeTiled (Ozaki slices) failed");
+}
+
+template <int S>
+void oz2_pass(cudaStream_t st, OzArgs a, size_t xbytes, size_t bbytes) {
+  using G = Oz2Geom<S>;
+  static int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    KCUDA(cudaFuncSetAttribute(oz2_pass_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               G::SMEM));
+    return v;
+  }();
+  CUtensorMap tx, tb;
+  oz_encode_rows(&tx, a.xs, xbytes, G::A / 128);
+  oz_encode_rows(&tb, a.bs, bbytes, G::B / 128);
+  const long long pairs = (a.ntm / 2) * a.ntn;
+  const long long g = 2 * (pairs < sms / 2 ? pairs : sms / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(g));
+  cfg.blockDim = dim3(OZ_THREADS);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KCUDA(cudaLaunchKernelEx(&cfg, oz2_pass_kernel<S>, tx, tb, a));
+}
+
+// bytes of a tiled slice buffer: rows padded to `pad`, K to whole 32-byte blocks
+inline size_t oz_slice_bytes(long long rows, int K, int pad, int S) {
+  const long long Rp = (rows + pad - 1) / pad * pad;
   const long long KB = (K + OZ_BK - 1) / OZ_BK;
   return static_cast<size_t>(Rp * KB * OZ_BK * S);
+}
+
+// KRONOP_OZ_2SM=0 selects the 1-SM kernel (M = 128); default: CTA pairs (M = 256)
+bool oz_two_sm() {
+  static const bool v = [] {
+    const char* e = getenv("KRONOP_OZ_2SM");
+    return !(e && e[0] == '0');
+  }();
+  return v;
 }
 
 template <int S>
@@ -459,9 +775,12 @@ void sep_solve_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, doubl
   param_check(!op.folded, "solve_lowp: dense operators only");
   const long long N = op.N;
   cudaStream_t st = ctx.stream;
+  const bool two = oz_two_sm();
+  const int bpan = two ? OZ_BN / 2 : OZ_BN;  // matrix panel rows per CTA
+  const int key = S * 2 + (two ? 1 : 0);
   void** of = op.oz_fwd;
   void** ob = op.oz_bwd;
-  if (!of[0] || op.oz_slices != S) {  // split copies of the transforms, made once per S
+  if (!of[0] || op.oz_slices != key) {  // split copies of the transforms, made once per mode
     for (int a = 0; a < KRONOP_MAX_DIM; ++a)
       for (void** p : {&of[a], &ob[a]})
         if (*p) {
@@ -476,18 +795,19 @@ void sep_solve_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, doubl
         void* p = nullptr;
         KCUDA(cudaMalloc(&p, sb + mp * sizeof(int)));
         // matrix element (i, k) at M[i + lda * k]: rows i (outputs), contraction k
-        oz_split_mat<S>(st, dir == 0 ? op.fwd[a] : op.bwd[a], op.lda[a], n, n,
+        oz_split_mat<S>(st, dir == 0 ? op.fwd[a] : op.bwd[a], op.lda[a], n, n, bpan,
                         static_cast<int8_t*>(p), reinterpret_cast<int*>(static_cast<char*>(p) + sb));
         (dir == 0 ? of : ob)[a] = p;
       }
     }
-    op.oz_slices = S;
+    op.oz_slices = key;
   }
   // workspace: one FP64 field (scratch[0]) + the current pass's slices and row exponents
   size_t need = 0;
   for (int a = 0; a < op.d; ++a) {
     const long long R = N / op.n[a];
-    const size_t v = oz_slice_bytes(R, op.n[a], OZ_BM, S) + ((R + OZ_BM - 1) / OZ_BM * OZ_BM) * sizeof(int);
+    const size_t v = oz_slice_bytes(R, op.n[a], OZ_PAIR, S) +
+                     ((R + OZ_PAIR - 1) / OZ_PAIR * OZ_PAIR) * sizeof(int);
     need = v > need ? v : need;
   }
   const size_t need_d = (need + 7) / 8 + 16;
@@ -501,7 +821,7 @@ void sep_solve_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, doubl
       const bool last = dir == 1 && a == op.d - 1;
       const int n = op.n[a];
       const long long R = N / n;
-      const size_t xb = oz_slice_bytes(R, n, OZ_BM, S);
+      const size_t xb = oz_slice_bytes(R, n, OZ_PAIR, S);
       int* xe = reinterpret_cast<int*>(xs + xb);
       oz_split_rows<S>(st, cur, R, n, xs, xe);
       OzArgs oa{};
@@ -527,8 +847,11 @@ void sep_solve_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, doubl
       oa.KB = (n + OZ_BK - 1) / OZ_BK;
       oa.m = n;
       oa.ntn = (n + OZ_BN - 1) / OZ_BN;
-      oa.ntm = (R + OZ_BM - 1) / OZ_BM;
-      oz_pass<S>(st, oa);
+      oa.ntm = (R + OZ_PAIR - 1) / OZ_PAIR * 2;  // 128-row panels, even count
+      if (two)
+        oz2_pass<S>(st, oa, xb, mb);
+      else
+        oz_pass<S>(st, oa);
       ctx.ws.launches += 2;
       cur = f;
     }
