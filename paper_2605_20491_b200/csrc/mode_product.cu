@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) mode_product_kernel(const KArgs a
     xsm[s] = LOADER == LD_CONTIG ? r * XL::STRIDE + k : k * XL::STRIDE + r;
   }
   constexpr int ACH = BK * BN / 2 / NTHREADS;  // A chunks (16 B) per thread per stage
-  int aoff[ACH], asm_[ACH];
+  int aoff[ACH], asm_[ACH], akk[ACH];
 #pragma unroll
   for (int s = 0; s < ACH; ++s) {
     const int c = tid + NTHREADS * s;
@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) mode_product_kernel(const KArgs a
     const int k = c / (BN / 2);
     aoff[s] = (col0 + nn) + lda * k;
     asm_[s] = k * TC::SAN + nn;
+    akk[s] = k;
   }
 
   auto load_stage = [&](int slot, int kt) {
@@ -194,8 +195,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) mode_product_kernel(const KArgs a
     }
     double* da = sa + slot * (BK * TC::SAN);
     const double* ak = a + (long long)lda * k0;
+    // matrix columns past nk are zero-filled, never read: the padded device copy holds
+    // pad_up(nk, 16) columns but a BK = 32 stage can reach further (and 0 * NaN garbage from
+    // whatever lies beyond the allocation would poison the sum)
 #pragma unroll
-    for (int s = 0; s < ACH; ++s) cp_async16(da + asm_[s], ak + aoff[s], true);
+    for (int s = 0; s < ACH; ++s) {
+      const bool ok = k0 + akk[s] < nk;
+      cp_async16(da + asm_[s], ok ? ak + aoff[s] : a, ok);
+    }
   };
 
   double acc[TC::RB][TC::CB][2];

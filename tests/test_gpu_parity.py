@@ -772,7 +772,17 @@ def test_ozaki_int8_solve(ctx, axes, prec, tol):
     b = dev(K.uniform_pm1(11, n))
     x64 = host(op.solve(b))
     xoz = host(op.solve_lowp(b, prec))
+    assert np.isfinite(x64).all()
+    bad = np.flatnonzero(~np.isfinite(xoz))
+    assert bad.size == 0, (bad.size, bad[:8], grid.shape)
     assert rel(xoz, x64) < tol
     # the low-order slices matter: a second right-hand side at a very different scale
-    b2 = dev(K.uniform_pm1(12, n) * 1e-200)
-    assert rel(host(op.solve_lowp(b2, prec)), host(op.solve(b2))) < tol
+    b2h = K.uniform_pm1(12, n) * 1e-200
+    b2 = dev(b2h)
+    z2 = host(op.solve(b2)) * 1e200  # (norms underflow)
+    y2 = host(op.solve_lowp(b2, prec)) * 1e200
+    assert np.array_equal(host(b2), b2h)  # the input is not touched
+    zb = np.flatnonzero(~np.isfinite(z2))
+    assert zb.size == 0, (zb.size, zb[:6], z2[zb[:3]], grid.shape, np.flatnonzero(~np.isfinite(y2)).size)
+    assert rel(y2, z2) < tol
+    assert np.array_equal(host(op.solve(b2)) * 1e200, z2)
