@@ -322,6 +322,12 @@ class SeparableOperator {
                  DeviceField<std::complex<double>>& out) const {
     check(kronop_sep_propagate(ctx_->get(), op_.get(), psi.data(), dt, out.data()));
   }
+  // Separately reported solve variants on the tcgen05 tensor cores (real fields):
+  // KRONOP_PREC_BF16 / _TF32 / _FP32X3 (the paper's reduced-precision rows) and
+  // KRONOP_PREC_FP64_OZAKI (FP64 emulated on the INT8 tensor cores; _OZAKI6 / _OZAKI5 fewer slices)
+  void solve_variant(const DeviceField<double>& b, int precision, DeviceField<double>& out) const {
+    check(kronop_sep_solve_lowp(ctx_->get(), op_.get(), b.data(), precision, out.data()));
+  }
   // value-semantics forms of the reference (operators.hpp:32-46)
   template <typename S>
   TensorField<S> apply(const TensorField<S>& u) const {

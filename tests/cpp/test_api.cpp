@@ -131,6 +131,18 @@ int main() {
     CHECK(rep.history.size() == 2 && rep.history[1] <= 1e-10);
     std::printf("ok pcg exact preconditioner: %d iteration(s), residual %.3e\n", rep.iterations,
                 rep.final_residual);
+    // FP64 emulated on the INT8 tensor cores: the same solve to FP64 level
+    DeviceField<double> d64(ctx, RealField({n, n, n})), doz(ctx, RealField({n, n, n}));
+    op.solve(db, d64);
+    op.solve_variant(db, KRONOP_PREC_FP64_OZAKI, doz);
+    const RealField h64 = d64.download(), hoz = doz.download();
+    double e2 = 0.0, n2 = 0.0;
+    for (std::size_t k = 0; k < h64.size(); ++k) {
+      e2 += (hoz[k] - h64[k]) * (hoz[k] - h64[k]);
+      n2 += h64[k] * h64[k];
+    }
+    CHECK(std::sqrt(e2 / n2) < 1e-12);
+    std::printf("ok ozaki solve variant rel diff %.3e\n", std::sqrt(e2 / n2));
   }
 
   // test_splitting.cpp:29-35 — Yoshida coefficients
