@@ -395,6 +395,19 @@ class SeparableOperator:
             check(lib().kronop_sep_solve_lowp(self.ctx.h, self.h, _ptr(b), prec, _ptr(out)))
         return out
 
+    def propagate_lowp(self, psi: torch.Tensor, dt: float, precision: str = "ozaki",
+                       out=None) -> torch.Tensor:
+        """exp(-i dt (-Delta+V1)) psi with FP64 emulated on the INT8 tensor cores
+        (kronop_sep_propagate_lowp): "ozaki" (7 slices), "ozaki6", "ozaki5"."""
+        if not psi.is_complex():
+            raise ValueError("propagate_lowp needs a complex128 field")
+        out = self._out(psi, out)
+        prec = {"ozaki": 4, "ozaki7": 4, "ozaki6": 5, "ozaki5": 6}[precision]
+        with _Call(self.ctx):
+            check(lib().kronop_sep_propagate_lowp(self.ctx.h, self.h, _ptr(psi), C.c_double(dt),
+                                                  prec, _ptr(out)))
+        return out
+
     def solve_bf16(self, b: torch.Tensor, out=None) -> torch.Tensor:
         return self.solve_lowp(b, "bf16", out)
 

@@ -921,6 +921,16 @@ int kronop_sep_solve_lowp(kronop_ctx* ctx, kronop_op* op, const double* b, int p
   });
 }
 
+int kronop_sep_propagate_lowp(kronop_ctx* ctx, kronop_op* op, const double* psi, double dt,
+                              int precision, double* out) {
+  return guard([&] {
+    param_check(ctx && op && psi && out && psi != out, "propagate_lowp: bad argument");
+    param_check(precision >= KRONOP_PREC_FP64_OZAKI && precision <= KRONOP_PREC_FP64_OZAKI5,
+                "propagate_lowp: unsupported precision");
+    sep_propagate_ozaki(*ctx, *op, psi, dt, out, 7 - (precision - KRONOP_PREC_FP64_OZAKI));
+  });
+}
+
 int kronop_full_apply(kronop_ctx* ctx, const kronop_op* op, const double* diag, double sigma,
                       const double* u, int is_complex, double* out) {
   return guard([&] {

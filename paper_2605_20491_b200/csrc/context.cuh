@@ -78,6 +78,8 @@ struct kronop_op {
 namespace kronop_dev {
 void sep_solve_lowp(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int precision);
 void sep_solve_ozaki(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int slices);
+void sep_propagate_ozaki(kronop_ctx& ctx, kronop_op& op, const double* psi, double dt, double* out,
+                         int slices);
 // Smallest free pool block with capacity >= n doubles, else a new cudaMalloc'd block.
 double* pool_get(kronop_ctx& ctx, size_t n);
 void pool_put(kronop_ctx& ctx, double* p);

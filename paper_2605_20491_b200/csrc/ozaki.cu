@@ -73,8 +73,8 @@ struct OzArgs {
   long long R;
   int K, KB, m, ntn;
   long long ntm;
-  int epi;  // 0 store, 1 divide by (lambda - shift)
-  double shift;
+  int epi;  // 0 store, 1 divide by (lambda - shift), 3 complex phase exp(-i (lambda - shift) dt)
+  double shift, dt;
   int nlow;
   int lowext[KRONOP_MAX_DIM];
   const double* lowlam[KRONOP_MAX_DIM];
@@ -195,7 +195,7 @@ __device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, i
   const int er = live ? a.xe[r] : 0;
   double lam_low = 0.0;
   if (a.epi != 0 && live) {  // axes below the contracted one, in axis order from 0.0
-    long long rr = r;
+    long long rr = a.epi == 3 ? (r >> 1) : r;  // complex: rows are (re, im) pairs
     for (int j = 0; j < a.nlow; ++j) {
       const long long idx = rr % a.lowext[j];
       rr /= a.lowext[j];
@@ -207,16 +207,26 @@ __device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, i
   for (int j = 0; j < 32; ++j) {  // uniform (shuffles); stores predicated
     const int col = c0 + j;
     const int ec = __shfl_sync(0xffffffffu, ecol, j);
-    if (live && col < a.m) {
-      const int E = er + ec;  // 2^(ex+ey) / 127^2: exponent bits directly when in normal range
-      const double v0 = acc[j] * (1.0 / 16129.0);
-      double val = (E > -1000 && E < 1000)
-                       ? v0 * __longlong_as_double(static_cast<long long>(1023 + E) << 52)
-                       : ldexp(v0, E);
-      if (a.epi == 1)
-        val = __ddiv_rn(val, __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift));
-      a.y[static_cast<long long>(col) * a.R + r] = val;
+    const int E = er + ec;  // 2^(ex+ey) / 127^2: exponent bits directly when in normal range
+    const double v0 = acc[j] * (1.0 / 16129.0);
+    double val = (E > -1000 && E < 1000)
+                     ? v0 * __longlong_as_double(static_cast<long long>(1023 + E) << 52)
+                     : ldexp(v0, E);
+    if (a.epi == 3) {  // partner row (re <-> im) is the neighbouring lane; as epilogue.cuh
+      const double other = __shfl_xor_sync(0xffffffffu, val, 1);
+      if (live && col < a.m) {
+        const double ls = __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift);
+        double sn, cs;
+        sincos(__dmul_rn(-ls, a.dt), &sn, &cs);
+        const bool is_im = (r & 1) != 0;
+        const double re = is_im ? other : val, im = is_im ? val : other;
+        val = is_im ? __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs))
+                    : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
+      }
+    } else if (a.epi == 1 && live && col < a.m) {
+      val = __ddiv_rn(val, __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift));
     }
+    if (live && col < a.m) a.y[static_cast<long long>(col) * a.R + r] = val;
   }
 }
 
@@ -539,7 +549,7 @@ __device__ __forceinline__ long long tile_off(long long p, int KB, int S, int rr
 // S B written per element.
 template <int S>
 __global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict__ x, long long R,
-                                                       int K, int KB, long long Rp,
+                                                       int K, int KB, long long Rp, int gather,
                                                        int8_t* __restrict__ out,
                                                        int* __restrict__ ex) {
   extern __shared__ double srow[];
@@ -552,13 +562,20 @@ __global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict_
     // stage: warp w loads row r0 + w
     {
       const long long r = r0 + warp;
+      // gather (interleaved complex field, component c fastest in memory): row r = (q, c) with
+      // c = r / (R / 2) the slow part of the row index, element k at x[(q K + k) 2 + c]
+      const long long Rh = R >> 1;
+      const long long rq = gather ? (r < R ? r % Rh : 0) : r;
+      const long long rc = gather ? (r < R ? r / Rh : 0) : 0;
       double amax = 0.0;
       for (int k0 = 0; k0 < Kp; k0 += 256) {  // 8 independent loads in flight per lane
         double v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int k = k0 + u * 32 + lane;
-          v[u] = (r < R && k < K) ? __ldcs(x + r * K + k) : 0.0;
+          v[u] = (r < R && k < K)
+                     ? __ldcs(gather ? x + (rq * K + k) * 2 + rc : x + r * K + k)
+                     : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -647,7 +664,8 @@ __global__ void __launch_bounds__(256) k_oz_split_mat(const double* __restrict__
 }
 
 template <int S>
-void oz_split_rows(cudaStream_t st, const double* x, long long R, int K, int8_t* out, int* ex) {
+void oz_split_rows(cudaStream_t st, const double* x, long long R, int K, int gather, int8_t* out,
+                   int* ex) {
   const int KB = (K + OZ_BK - 1) / OZ_BK;
   const long long Rp = (R + OZ_PAIR - 1) / OZ_PAIR * OZ_PAIR;  // whole 256-row pair panels
   const int nch = KB * 2;
@@ -661,7 +679,7 @@ void oz_split_rows(cudaStream_t st, const double* x, long long R, int K, int8_t*
   const long long groups = Rp / 8;
   const int per_sm = smem <= 72 * 1024 ? 3 : 1;
   const int blocks = static_cast<int>(groups < 148LL * per_sm * 4 ? groups : 148LL * per_sm * 4);
-  k_oz_split_rows<S><<<blocks, 256, smem, st>>>(x, R, K, KB, Rp, out, ex);
+  k_oz_split_rows<S><<<blocks, 256, smem, st>>>(x, R, K, KB, Rp, gather, out, ex);
   KCUDA(cudaGetLastError());
 }
 
@@ -771,9 +789,11 @@ bool oz_two_sm() {
 }
 
 template <int S>
-void sep_solve_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double* x) {
+void sep_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, bool propagate,
+                    double dt) {
   param_check(!op.folded, "solve_lowp: dense operators only");
   const long long N = op.N;
+  const int cf = propagate ? 2 : 1;  // complex: 2 real rows per fibre
   cudaStream_t st = ctx.stream;
   const bool two = oz_two_sm();
   const int bpan = two ? OZ_BN / 2 : OZ_BN;  // matrix panel rows per CTA
@@ -805,13 +825,13 @@ void sep_solve_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, doubl
   // workspace: one FP64 field (scratch[0]) + the current pass's slices and row exponents
   size_t need = 0;
   for (int a = 0; a < op.d; ++a) {
-    const long long R = N / op.n[a];
+    const long long R = cf * (N / op.n[a]);
     const size_t v = oz_slice_bytes(R, op.n[a], OZ_PAIR, S) +
                      ((R + OZ_PAIR - 1) / OZ_PAIR * OZ_PAIR) * sizeof(int);
     need = v > need ? v : need;
   }
   const size_t need_d = (need + 7) / 8 + 16;
-  ensure_scratch(ctx, need_d > static_cast<size_t>(N) ? need_d : static_cast<size_t>(N));
+  ensure_scratch(ctx, need_d > static_cast<size_t>(cf * N) ? need_d : static_cast<size_t>(cf * N));
   double* f = ctx.scratch[0];
   int8_t* xs = reinterpret_cast<int8_t*>(ctx.scratch[1]);
   const double* cur = b;
@@ -820,13 +840,15 @@ void sep_solve_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, doubl
     for (int a = 0; a < op.d; ++a, ++k) {
       const bool last = dir == 1 && a == op.d - 1;
       const int n = op.n[a];
-      const long long R = N / n;
+      const long long R = cf * (N / n);
       const size_t xb = oz_slice_bytes(R, n, OZ_PAIR, S);
       int* xe = reinterpret_cast<int*>(xs + xb);
-      oz_split_rows<S>(st, cur, R, n, xs, xe);
+      // complex: the first pass of each direction reads the interleaved layout (re/im fastest)
+      oz_split_rows<S>(st, cur, R, n, propagate && a == 0 ? 1 : 0, xs, xe);
       OzArgs oa{};
       if (dir == 0 && a == op.d - 1) {
-        oa.epi = 1;
+        oa.epi = propagate ? 3 : 1;
+        oa.dt = dt;
         oa.shift = op.shift;
         oa.nlow = op.d - 1;
         for (int j = 0; j < op.d - 1; ++j) {
@@ -865,11 +887,26 @@ void sep_solve_ozaki(kronop_ctx& ctx, kronop_op& op, const double* b, double* x,
   for (int a = 0; a < op.d; ++a)
     param_check(op.n[a] <= OZ_KMAX, "solve_lowp: Ozaki mode needs extents <= 3200");
   if (slices == 5)
-    sep_solve_ozaki_impl<5>(ctx, op, b, x);
+    sep_ozaki_impl<5>(ctx, op, b, x, false, 0.0);
   else if (slices == 6)
-    sep_solve_ozaki_impl<6>(ctx, op, b, x);
+    sep_ozaki_impl<6>(ctx, op, b, x, false, 0.0);
   else
-    sep_solve_ozaki_impl<7>(ctx, op, b, x);
+    sep_ozaki_impl<7>(ctx, op, b, x, false, 0.0);
+}
+
+// exp(-i dt (-Delta + V1 - shift)) psi (operators.cpp:63-75) on the same INT8 path: complex
+// interleaved FP64 in and out; re and im travel as separate real rows through the transforms
+// (the matrices are real) and meet again in the phase epilogue of the last forward pass.
+void sep_propagate_ozaki(kronop_ctx& ctx, kronop_op& op, const double* psi, double dt, double* out,
+                         int slices) {
+  for (int a = 0; a < op.d; ++a)
+    param_check(op.n[a] <= OZ_KMAX, "propagate_lowp: Ozaki mode needs extents <= 3200");
+  if (slices == 5)
+    sep_ozaki_impl<5>(ctx, op, psi, out, true, dt);
+  else if (slices == 6)
+    sep_ozaki_impl<6>(ctx, op, psi, out, true, dt);
+  else
+    sep_ozaki_impl<7>(ctx, op, psi, out, true, dt);
 }
 
 }  // namespace kronop_dev

@@ -786,3 +786,23 @@ def test_ozaki_int8_solve(ctx, axes, prec, tol):
     assert zb.size == 0, (zb.size, zb[:6], z2[zb[:3]], grid.shape, np.flatnonzero(~np.isfinite(y2)).size)
     assert rel(y2, z2) < tol
     assert np.array_equal(host(op.solve(b2)) * 1e200, z2)
+
+
+@pytest.mark.parametrize("axes", [[(8.0, 13, 5)] * 3, [(8.0, 5, 5), (8.0, 41, 1), (8.0, 17, 1)],
+                                  [(8.0, 4, 3), (6.0, 9, 5)], [(8.0, 29, 5)],
+                                  [(8.0, 3, 4)] * 4])
+def test_ozaki_int8_propagate(ctx, axes):
+    """exp(-i dt (-Delta+V1)) on the INT8 path: re and im as separate real rows through the
+    transforms, the phase in the epilogue of the last forward pass; equal to the FP64 (DMMA)
+    propagate to FP64 level (the bound scales with dt * lambda_max like the folded test)."""
+    A = api()
+    grid = A.Grid([A.assemble_sem(*a) for a in axes])
+    op = grid.separable_operator(ctx, [lambda t: t * t + 0.5 * t] * grid.dim, 0.25)
+    psi = dev(K.seeded_complex_field(grid.shape, 21).reshape(-1))
+    lmax = sum(float(np.max(a.eigenvalues)) for a in op.axes)
+    for dt in (0.0, 1e-3, 0.05):
+        ref = host(op.propagate(psi, dt))
+        got = host(op.propagate_lowp(psi, dt, "ozaki"))
+        assert np.isfinite(got).all()
+        assert rel(got, ref) < max(1e-12, 64 * 2.2e-16 * lmax * dt), dt
+    assert rel(host(op.propagate_lowp(psi, 0.05, "ozaki5")), host(op.propagate(psi, 0.05))) < 3e-8
