@@ -94,6 +94,7 @@ PROTOTYPES = {
     "kronop_ctx_trim": (I, [P]),
     "kronop_sep_solve_lowp": (I, [P, P, P, I, P]),
     "kronop_sep_propagate_lowp": (I, [P, P, P, D, I, P]),
+    "kronop_op_set_precision": (I, [P, P, I]),
     "kronop_field_dump": (I, [P, C.c_char_p, I, IP, I, P]),
     "kronop_field_dump_host": (I, [C.c_char_p, I, IP, I, DP]),
     "kronop_field_load_header": (I, [C.c_char_p, IP, IP, IP]),

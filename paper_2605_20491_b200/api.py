@@ -395,6 +395,15 @@ class SeparableOperator:
             check(lib().kronop_sep_solve_lowp(self.ctx.h, self.h, _ptr(b), prec, _ptr(out)))
         return out
 
+    def set_precision(self, precision: str = "fp64"):
+        """kronop_op_set_precision: run every later transform of this operator (and the drivers
+        built on it: PCG, inverse iteration, GPE, splitting) in "fp64" (DMMA, default) or FP64
+        emulated on the INT8 tensor cores ("ozaki", "ozaki6", "ozaki5")."""
+        prec = {"fp64": 0, "ozaki": 4, "ozaki7": 4, "ozaki6": 5, "ozaki5": 6}[precision]
+        with _Call(self.ctx):
+            check(lib().kronop_op_set_precision(self.ctx.h, self.h, prec))
+        return self
+
     def propagate_lowp(self, psi: torch.Tensor, dt: float, precision: str = "ozaki",
                        out=None) -> torch.Tensor:
         """exp(-i dt (-Delta+V1)) psi with FP64 emulated on the INT8 tensor cores

@@ -322,6 +322,13 @@ static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double
 
 void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
                    SepKind kind, double shift, double dt, const double* diag, double sigma) {
+  if (op.exec_prec >= KRONOP_PREC_FP64_OZAKI && !op.folded && (kind != SEP_PROPAGATE || cplx)) {
+    // kronop_op_set_precision: every transform of this operator on the INT8 path (ozaki.cu)
+    const int epi = kind == SEP_SOLVE ? 1 : kind == SEP_APPLY ? 2 : 3;
+    sep_ozaki(ctx, const_cast<kronop_op&>(op), in, out, cplx, epi, shift, dt, diag, sigma,
+              7 - (op.exec_prec - KRONOP_PREC_FP64_OZAKI));
+    return;
+  }
   if (op.folded) {
     sep_transform_folded(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
     return;
@@ -918,6 +925,23 @@ int kronop_sep_solve_lowp(kronop_ctx* ctx, kronop_op* op, const double* b, int p
       sep_solve_ozaki(*ctx, *op, b, out, 7 - (precision - KRONOP_PREC_FP64_OZAKI));
     else
       sep_solve_lowp(*ctx, *op, b, out, precision);
+  });
+}
+
+int kronop_op_set_precision(kronop_ctx* ctx, kronop_op* op, int precision) {
+  return guard([&] {
+    param_check(ctx && op, "op_set_precision: null argument");
+    param_check(precision == KRONOP_PREC_FP64 ||
+                    (precision >= KRONOP_PREC_FP64_OZAKI && precision <= KRONOP_PREC_FP64_OZAKI5),
+                "op_set_precision: unsupported precision");
+    param_check(precision == KRONOP_PREC_FP64 || !op->folded,
+                "op_set_precision: the INT8 path takes dense operators only");
+    if (precision != KRONOP_PREC_FP64) {
+      for (int a = 0; a < op->d; ++a)
+        param_check(op->n[a] <= 3200, "op_set_precision: Ozaki mode needs extents <= 3200");
+      ozaki_prepare(*ctx, *op, 7 - (precision - KRONOP_PREC_FP64_OZAKI));
+    }
+    op->exec_prec = precision;
   });
 }
 

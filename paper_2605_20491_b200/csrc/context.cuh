@@ -66,6 +66,7 @@ struct kronop_op {
   void* oz_fwd[KRONOP_MAX_DIM] = {};  // tiled INT8 slices + row exponents (ozaki.cu)
   void* oz_bwd[KRONOP_MAX_DIM] = {};
   int oz_slices = 0;
+  int exec_prec = 0;  // kronop_op_set_precision: 0 = FP64 DMMA, KRONOP_PREC_FP64_OZAKI* = INT8
   bool folded = false;
   int ne[KRONOP_MAX_DIM] = {}, no[KRONOP_MAX_DIM] = {};
   double* fe[KRONOP_MAX_DIM] = {};
@@ -80,6 +81,9 @@ void sep_solve_lowp(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, 
 void sep_solve_ozaki(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int slices);
 void sep_propagate_ozaki(kronop_ctx& ctx, kronop_op& op, const double* psi, double dt, double* out,
                          int slices);
+void sep_ozaki(kronop_ctx& ctx, kronop_op& op, const double* in, double* out, int cplx, int epi,
+               double shift, double dt, const double* diag, double sigma, int slices);
+void ozaki_prepare(kronop_ctx& ctx, kronop_op& op, int slices);
 // Smallest free pool block with capacity >= n doubles, else a new cudaMalloc'd block.
 double* pool_get(kronop_ctx& ctx, size_t n);
 void pool_put(kronop_ctx& ctx, double* p);

@@ -73,8 +73,12 @@ struct OzArgs {
   long long R;
   int K, KB, m, ntn;
   long long ntm;
-  int epi;  // 0 store, 1 divide by (lambda - shift), 3 complex phase exp(-i (lambda - shift) dt)
+  int epi;  // 0 store, 1 divide by / 2 multiply by (lambda - shift), 3 complex phase
   double shift, dt;
+  int axpy, cplx;      // last pass: + diag .* u - sigma u (operators.cpp:102)
+  const double* diag;  // spatial (real), may be null
+  const double* u;     // the transform's input, final layout
+  double sigma;
   int nlow;
   int lowext[KRONOP_MAX_DIM];
   const double* lowlam[KRONOP_MAX_DIM];
@@ -195,7 +199,7 @@ __device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, i
   const int er = live ? a.xe[r] : 0;
   double lam_low = 0.0;
   if (a.epi != 0 && live) {  // axes below the contracted one, in axis order from 0.0
-    long long rr = a.epi == 3 ? (r >> 1) : r;  // complex: rows are (re, im) pairs
+    long long rr = a.cplx ? (r >> 1) : r;  // complex: rows are (re, im) pairs
     for (int j = 0; j < a.nlow; ++j) {
       const long long idx = rr % a.lowext[j];
       rr /= a.lowext[j];
@@ -223,10 +227,17 @@ __device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, i
         val = is_im ? __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs))
                     : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
       }
-    } else if (a.epi == 1 && live && col < a.m) {
-      val = __ddiv_rn(val, __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift));
+    } else if ((a.epi == 1 || a.epi == 2) && live && col < a.m) {
+      const double ls = __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift);
+      val = a.epi == 1 ? __ddiv_rn(val, ls) : __dmul_rn(val, ls);
     }
-    if (live && col < a.m) a.y[static_cast<long long>(col) * a.R + r] = val;
+    const long long yi = static_cast<long long>(col) * a.R + r;
+    if (a.axpy && live && col < a.m) {  // as the DMMA epilogue: (val + diag u) - sigma u
+      const double uu = a.u[yi];
+      if (a.diag) val = __dadd_rn(val, __dmul_rn(a.diag[a.cplx ? (yi >> 1) : yi], uu));
+      if (a.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(a.sigma, uu));
+    }
+    if (live && col < a.m) a.y[yi] = val;
   }
 }
 
@@ -789,10 +800,11 @@ bool oz_two_sm() {
 }
 
 template <int S>
-void sep_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, bool propagate,
-                    double dt) {
+void sep_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int cplx, int epi,
+                    double shift, double dt, const double* diag, double sigma) {
   param_check(!op.folded, "solve_lowp: dense operators only");
   const long long N = op.N;
+  const bool propagate = cplx != 0;  // complex field (the gather / pairing below)
   const int cf = propagate ? 2 : 1;  // complex: 2 real rows per fibre
   cudaStream_t st = ctx.stream;
   const bool two = oz_two_sm();
@@ -846,10 +858,17 @@ void sep_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, 
       // complex: the first pass of each direction reads the interleaved layout (re/im fastest)
       oz_split_rows<S>(st, cur, R, n, propagate && a == 0 ? 1 : 0, xs, xe);
       OzArgs oa{};
+      oa.cplx = cplx;
+      if (last && (diag != nullptr || sigma != 0.0)) {
+        oa.axpy = 1;
+        oa.diag = diag;
+        oa.u = b;
+        oa.sigma = sigma;
+      }
       if (dir == 0 && a == op.d - 1) {
-        oa.epi = propagate ? 3 : 1;
+        oa.epi = epi;
         oa.dt = dt;
-        oa.shift = op.shift;
+        oa.shift = shift;
         oa.nlow = op.d - 1;
         for (int j = 0; j < op.d - 1; ++j) {
           oa.lowext[j] = op.n[j];
@@ -881,17 +900,39 @@ void sep_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, 
 
 }  // namespace
 
+// Any separable transform on the INT8 path: cplx (interleaved complex field), epi 1 divide /
+// 2 multiply by (lambda - shift) / 3 phase, optional last-pass AXPY (+ diag u - sigma u).
+void sep_ozaki(kronop_ctx& ctx, kronop_op& op, const double* in, double* out, int cplx, int epi,
+               double shift, double dt, const double* diag, double sigma, int slices) {
+  for (int a = 0; a < op.d; ++a)
+    param_check(op.n[a] <= OZ_KMAX, "Ozaki mode needs extents <= 3200");
+  if (slices == 5)
+    sep_ozaki_impl<5>(ctx, op, in, out, cplx, epi, shift, dt, diag, sigma);
+  else if (slices == 6)
+    sep_ozaki_impl<6>(ctx, op, in, out, cplx, epi, shift, dt, diag, sigma);
+  else
+    sep_ozaki_impl<7>(ctx, op, in, out, cplx, epi, shift, dt, diag, sigma);
+}
+
+// kronop_op_set_precision: everything a later (possibly graph-captured) call would allocate or
+// initialise - the split matrices, the workspace for complex fields, the kernels' attributes -
+// is done here, by one throw-away transform of a zero field.
+void ozaki_prepare(kronop_ctx& ctx, kronop_op& op, int slices) {
+  const size_t n2 = 2 * static_cast<size_t>(op.N);
+  double* z = nullptr;
+  KCUDA(cudaMallocAsync(&z, 2 * n2 * sizeof(double), ctx.stream));
+  KCUDA(cudaMemsetAsync(z, 0, n2 * sizeof(double), ctx.stream));
+  sep_ozaki(ctx, op, z, z + n2, 1, 3, op.shift, 0.0, nullptr, 0.0, slices);
+  KCUDA(cudaFreeAsync(z, ctx.stream));
+  KCUDA(cudaStreamSynchronize(ctx.stream));
+}
+
 // (-Delta + V1 - shift)^{-1} b with FP64 accuracy from INT8 tensor-core products (Ozaki scheme,
 // `slices` 8-bit slices per operand: 5, 6 or 7). Real fields, FP64 device in and out.
 void sep_solve_ozaki(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, int slices) {
   for (int a = 0; a < op.d; ++a)
     param_check(op.n[a] <= OZ_KMAX, "solve_lowp: Ozaki mode needs extents <= 3200");
-  if (slices == 5)
-    sep_ozaki_impl<5>(ctx, op, b, x, false, 0.0);
-  else if (slices == 6)
-    sep_ozaki_impl<6>(ctx, op, b, x, false, 0.0);
-  else
-    sep_ozaki_impl<7>(ctx, op, b, x, false, 0.0);
+  sep_ozaki(ctx, op, b, x, 0, 1, op.shift, 0.0, nullptr, 0.0, slices);
 }
 
 // exp(-i dt (-Delta + V1 - shift)) psi (operators.cpp:63-75) on the same INT8 path: complex
@@ -901,12 +942,7 @@ void sep_propagate_ozaki(kronop_ctx& ctx, kronop_op& op, const double* psi, doub
                          int slices) {
   for (int a = 0; a < op.d; ++a)
     param_check(op.n[a] <= OZ_KMAX, "propagate_lowp: Ozaki mode needs extents <= 3200");
-  if (slices == 5)
-    sep_ozaki_impl<5>(ctx, op, psi, out, true, dt);
-  else if (slices == 6)
-    sep_ozaki_impl<6>(ctx, op, psi, out, true, dt);
-  else
-    sep_ozaki_impl<7>(ctx, op, psi, out, true, dt);
+  sep_ozaki(ctx, op, psi, out, 1, 3, op.shift, dt, nullptr, 0.0, slices);
 }
 
 }  // namespace kronop_dev

@@ -806,3 +806,38 @@ def test_ozaki_int8_propagate(ctx, axes):
         assert np.isfinite(got).all()
         assert rel(got, ref) < max(1e-12, 64 * 2.2e-16 * lmax * dt), dt
     assert rel(host(op.propagate_lowp(psi, 0.05, "ozaki5")), host(op.propagate(psi, 0.05))) < 3e-8
+
+
+@pytest.mark.parametrize("kind,cells", [("stirrer", 4), ("quartic", 5)])
+def test_ozaki_execution_precision_drivers(ctx, kind, cells):
+    """kronop_op_set_precision("ozaki"): every transform of the operator - and so the graph-
+    captured device PCG built on it - runs on the INT8 path. Same iteration count and residual
+    history as the oracle (acceptance.cpp:202-236 instances), apply / solve / FullOperator apply
+    (V2, sigma) / complex solve equal to the FP64 operator's to 1e-12."""
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(8.0, cells, 6, 3)
+    pot = P.build_potential(kind, grid)
+    op64 = grid.separable_operator(ctx, pot.separable)
+    op = grid.separable_operator(ctx, pot.separable).set_precision("ozaki")
+    v2 = pot.v2_device()
+    b = A.splitmix_uniform(ctx, 1, grid.node_count())
+    for f in ("apply", "solve"):
+        assert rel(host(getattr(op, f)(b)), host(getattr(op64, f)(b))) < 1e-12, f
+    psi = dev(K.seeded_complex_field(grid.shape, 5).reshape(-1))
+    assert rel(host(op.solve(psi)), host(op64.solve(psi))) < 1e-12
+    fo, fo64 = A.FullOperator(op, v2), A.FullOperator(op64, v2)
+    assert rel(host(fo.apply(b)), host(fo64.apply(b))) < 1e-12
+    x = torch.zeros_like(b)
+    cfg = A.PcgConfig(rel_tol=1e-8, record_history=True)
+    rep = A.pcg(A.apply_map(op, v2), A.solve_map(op), b, x, cfg)
+    b_np = host(b)
+    kg = K.Grid.sem(8.0, cells, 6, 3)
+    kop = K.build_full_operator(kg, K.build_potential(kind, kg))
+    xr = np.zeros_like(b_np)
+    krep = K.pcg(kop.apply, kop.sep.solve, b_np, xr, K.PcgConfig(rel_tol=1e-8, record_history=True))
+    assert rep.converged and rep.iterations == krep.iterations
+    assert np.allclose(rep.history, krep.history, rtol=1e-8, atol=0)
+    assert rel(host(x), xr) < 1e-10
+    op.set_precision("fp64")  # back to DMMA
+    assert rel(host(op.solve(b)), host(op64.solve(b))) == 0.0
