@@ -15,7 +15,7 @@ ctx = A.Context(0)
 cells = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 g = A.Grid.sem(8.0, cells, 5, 3)
 pot = P.build_potential("sep-osc", g, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
-bdiag = torch.from_numpy(np.ascontiguousarray(P.separable_sum(g, pot))).cuda()
+bdiag = torch.from_numpy(np.array(P.separable_sum(g, pot))).cuda()
 box = g.sample(lambda c: np.sin(np.pi * (c[0] + 8.0) / 16.0) * np.sin(np.pi * (c[1] + 8.0) / 16.0)
                * np.sin(np.pi * (c[2] + 8.0) / 16.0))
 psi0 = torch.from_numpy(box.astype(np.complex128)).cuda()
@@ -23,8 +23,10 @@ spec = A.SplitSpec(quad_points=1, composition="single", dt=5e-3, total_time=0.1,
                    merge_across_steps=True)
 out = {"n": g.shape[0]}
 states = {}
-for name, folded in (("dense", False), ("folded", True)):
+for name, folded in (("dense", False), ("folded", True), ("ozaki", False)):
     lap = g.laplacian(ctx, folded=folded)
+    if name == "ozaki":
+        lap.set_precision("ozaki")
     A.evolve(A.SplitSpec(quad_points=1, dt=5e-3, total_time=1e-2, merge_across_steps=True), lap,
              bdiag, psi0)
     torch.cuda.synchronize()
@@ -35,6 +37,7 @@ for name, folded in (("dense", False), ("folded", True)):
     out[name] = {"steps_per_s": steps / t, "steps": steps, "s": t}
     states[name] = state
     del lap
-d = states["folded"] - states["dense"]
-out["rel_diff"] = float(torch.linalg.norm(d) / torch.linalg.norm(states["dense"]))
+for k in ("folded", "ozaki"):
+    d = states[k] - states["dense"]
+    out["rel_diff_" + k] = float(torch.linalg.norm(d) / torch.linalg.norm(states["dense"]))
 print(json.dumps(out))
