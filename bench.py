@@ -591,12 +591,14 @@ def run_kronop(args):
     bh.copy_(b.cpu())
     bn, xn = bh.numpy(), xh.numpy()
     op.solve_host(bn, xn)  # warm (sizes the staging buffers)
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(1, min(args.steps, 5))
     barrier(world)
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    e2e_ts = []
+    for _ in range(e2e_steps):  # median step: the VM's host-memory / PCIe rate is noisy
+        t0 = time.perf_counter()
         op.solve_host(bn, xn)
-    t_e2e = (time.perf_counter() - t0) / e2e_steps
+        e2e_ts.append(time.perf_counter() - t0)
+    t_e2e = float(np.median(e2e_ts))
     t_e2e = max_over_ranks(world, t_e2e, "cuda:%d" % local)
     e2e_value = world * N / t_e2e / 1e9
 
@@ -633,7 +635,8 @@ def run_kronop(args):
                          "per_axis_ms": [t * 1e3 for t in per_axis],
                          "peak_src": peaks["fp64_src"]},
             "e2e": {"value": e2e_value, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * N,
-                    "d2h_bytes_per_step": 8 * N, "ms_per_step": t_e2e * 1e3},
+                    "d2h_bytes_per_step": 8 * N, "ms_per_step": t_e2e * 1e3,
+                    "step_ms": [round(t * 1e3, 1) for t in e2e_ts], "aggregate": "median step"},
             "gpu_launches": int(launches),
             "secondary": extras,
             "variants": variants,
