@@ -339,7 +339,7 @@ def _norm(t: torch.Tensor) -> float:
 def full_operator(rc: RunContext, grid: A.Grid, pot) -> A.FullOperator:
     """build_full_operator (grid.cpp / potentials.cpp:132-138): separable part on the axes,
     V2 as the nodal diagonal."""
-    sep = grid.separable_operator(rc.ctx, pot.separable)
+    sep = _exec_precision(rc, grid.separable_operator(rc.ctx, pot.separable))
     return A.FullOperator(sep, pot.v2_device("cuda:%d" % rc.ctx.device))
 
 
@@ -412,6 +412,17 @@ def maybe_export(rc: RunContext, grid: A.Grid, field: torch.Tensor):  # harness.
                 xb = 0.0 if res == 1 else -bb.half_width + 2.0 * bb.half_width * j / (res - 1.0)
                 csv.row([xa, xb, float(values[i, j])])
         csv.close()
+
+
+def _exec_precision(rc, op):
+    """Optional key `device.precision` (not in the reference grammar): "fp64" (default, DMMA) or
+    "ozaki" / "ozaki6" / "ozaki5" - every transform of the operator (and the PCG / inverse
+    iteration / GPE / splitting drivers on it) on the INT8 tensor cores (kronop_op_set_precision).
+    """
+    prec = rc.cfg.get_string("device.precision", "fp64")
+    if prec != "fp64" and op is not None:
+        op.set_precision(prec)
+    return op
 
 
 def cmd_solve(rc: RunContext, gs: GridSpec):  # harness.cpp:212-283
@@ -488,7 +499,7 @@ def cmd_gpe(rc: RunContext, gs: GridSpec):  # harness.cpp:317-372
     grid = gs.build(0)
     kind, params = read_potential(rc.cfg, gs.dimension)
     ham = full_operator(rc, grid, build_pot(kind, params, grid))
-    lap = grid.laplacian(rc.ctx)
+    lap = _exec_precision(rc, grid.laplacian(rc.ctx))
     beta = rc.cfg.get_real("gpe.beta", 0.0)
     flow = rc.cfg.get_string("gpe.flow", "h1")
     if flow not in ("h1", "au"):
@@ -529,15 +540,16 @@ def cmd_propagate(rc: RunContext, gs: GridSpec, table: bool):  # harness.cpp:374
     split = rc.cfg.get_string("propagate.split", "kinetic")
     v1 = separable_sum_field(grid, pot)
     if split == "kinetic":
-        a = grid.laplacian(rc.ctx)
+        a = _exec_precision(rc, grid.laplacian(rc.ctx))
         b = v1 + (pot.nonseparable if pot.nonseparable is not None else 0.0)
     elif split == "kinetic+v1":
-        a = grid.separable_operator(rc.ctx, pot.separable)
+        a = _exec_precision(rc, grid.separable_operator(rc.ctx, pot.separable))
         b = pot.nonseparable if pot.nonseparable is not None else np.zeros(grid.node_count())
     else:
         raise _perr("propagate.split must be kinetic or kinetic+v1")
     b_diag = _dev(rc, np.asarray(b, dtype=np.float64))
-    full = grid.separable_operator(rc.ctx, pot.separable) if fully_separable else None
+    full = (_exec_precision(rc, grid.separable_operator(rc.ctx, pot.separable))
+            if fully_separable else None)
     spec = A.SplitSpec(quad_points=rc.cfg.get_int("propagate.M", 1))
     comp = rc.cfg.get_string("propagate.composition", "qhop")
     if comp not in ("qhop", "yoshida"):
@@ -614,7 +626,7 @@ def cmd_pcg_bench(rc: RunContext, gs: GridSpec):  # harness.cpp:495-567
         grid = gs.build(level)
         pot = build_pot(kind, params, grid)
         op = full_operator(rc, grid, pot)
-        lap = grid.laplacian(rc.ctx)
+        lap = _exec_precision(rc, grid.laplacian(rc.ctx))
         _sync()
         setup_s = time.perf_counter() - t0
         if pre == "separable":

@@ -120,6 +120,18 @@ def test_harness_pcg_bench_and_ground_state(ctx, tmp_path):
     rows = _rows(os.path.join(out, "ground_state.csv"))
     assert [int(x["n"]) for x in rows] == [39, 79]
     assert abs(float(rows[-1]["eigenvalue"]) - 5.286155366963) < 1e-6 * 5.3
+    # device.precision = ozaki: the same commands with every transform on the INT8 path
+    rc, out = _run(tmp_path, "[run]\ncommand = pcg-bench\n[grid]\nL = 8\ndegree = 6\ncells = 8\n"
+                   "[potential]\nkind = stirrer\n[pcg]\ntol = 1e-8\n[device]\nprecision = ozaki\n", ctx)
+    assert rc == 0
+    ro = _rows(os.path.join(out, "pcg_bench.csv"))[0]
+    assert int(ro["iterations"]) == krep.iterations and ro["converged"] == "true"
+    rc, out = _run(tmp_path, "[run]\ncommand = ground-state\noutput_dir = y\n[grid]\nL = 8\n"
+                   "degree = 20\ncells = 2, 4\n[potential]\nkind = stirrer\n"
+                   "[device]\nprecision = ozaki\n", ctx)
+    assert rc == 0
+    ro = _rows(os.path.join(out, "ground_state.csv"))
+    assert abs(float(ro[-1]["eigenvalue"]) - float(rows[-1]["eigenvalue"])) < 1e-11 * 5.3
 
 
 @pytest.mark.gpu
