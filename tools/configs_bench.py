@@ -5,6 +5,7 @@ config 3: stirrer 512^3 (Q19 x 27 cells, L=8): PCG time-to-tol at 1e-8 and 1e-12
           (sigma = 0.9 lambda_min, eigen tol 1e-12, inner PCG tol 1e-12, stagnation 100).
 config 4: GPE a_u flow at 1024^3 (sep-osc amp 100 quad 1, Q25 x 41 cells, L=8, beta = 1600,
           tau = 1, constant init): seconds and PCG iterations per outer iteration (2 iterations).
+"3oz" / "4oz": configs 3 / 4 with kronop_op_set_precision("ozaki") (FP64 emulated on INT8).
 config 5: 6D n=29 (coulomb-3d2, L=5, Q10 x 3) and 9D n=9 (coulomb-3d3, L=3, Q5 x 2) complex128:
           one A-propagation (split=kinetic) and Strang steps/s (qHOP M=1, merge, dt=0.005).
 All times are device time (CUDA events / synchronised wall clock around device-resident calls).
@@ -30,10 +31,10 @@ def timed(fn):
     return r, time.perf_counter() - t0
 
 
-def config3(ctx, out):
+def config3(ctx, out, prec="fp64"):
     g = A.Grid.sem(8.0, 27, 19, 3)
     pot = P.build_potential("stirrer", g)
-    op = g.separable_operator(ctx, pot.separable)
+    op = g.separable_operator(ctx, pot.separable).set_precision(prec)
     v2 = pot.v2_device()
     b = A.splitmix_uniform(ctx, 1, g.node_count())
     res = {"n": g.shape[0], "dof": g.node_count()}
@@ -50,18 +51,18 @@ def config3(ctx, out):
                                 "outer_iterations": r.outer_iterations,
                                 "total_inner_iterations": r.total_inner_iterations,
                                 "converged": r.converged}
-    out["config3_stirrer_512"] = res
+    out["config3_stirrer_512" + ("" if prec == "fp64" else "_" + prec)] = res
 
 
-def config4(ctx, out, iters=2):
+def config4(ctx, out, iters=2, prec="fp64"):
     g = A.Grid.sem(8.0, 41, 25, 3)
     pot = P.build_potential("sep-osc", g, quad_coeffs=[1.0] * 3, osc_amplitude=100.0)
-    ham = A.FullOperator(g.separable_operator(ctx, pot.separable))
-    lap = g.laplacian(ctx)
+    ham = A.FullOperator(g.separable_operator(ctx, pot.separable).set_precision(prec))
+    lap = g.laplacian(ctx).set_precision(prec)
     cfg = A.GpeFlowConfig(kind="au", step=1.0, init="constant", energy_rel_tol=1e-30,
                           max_iterations=iters, record_history=True)
     r, t = timed(lambda: A.gpe_gradient_flow(ham, lap, 1600.0, cfg))
-    out["config4_gpe_au_1024"] = {
+    out["config4_gpe_au_1024" + ("" if prec == "fp64" else "_" + prec)] = {
         "n": g.shape[0], "dof": g.node_count(), "beta": 1600.0, "outer_iterations": r.iterations,
         "seconds_total": t, "seconds_per_outer": t / max(1, r.iterations),
         "pcg_iterations_total": r.linear_solves,
@@ -103,6 +104,11 @@ def main():
         config5(ctx, out)
     if "4" in which:
         config4(ctx, out)
+    # the same with every transform on the INT8 path (kronop_op_set_precision)
+    if "3oz" in which:
+        config3(ctx, out, "ozaki")
+    if "4oz" in which:
+        config4(ctx, out, prec="ozaki")
     print(json.dumps(out))
 
 
