@@ -322,7 +322,7 @@ static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double
 
 void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
                    SepKind kind, double shift, double dt, const double* diag, double sigma) {
-  if (op.exec_prec >= KRONOP_PREC_FP64_OZAKI && !op.folded && (kind != SEP_PROPAGATE || cplx)) {
+  if (op.exec_prec >= KRONOP_PREC_FP64_OZAKI && (kind != SEP_PROPAGATE || cplx)) {
     // kronop_op_set_precision: every transform of this operator on the INT8 path (ozaki.cu)
     const int epi = kind == SEP_SOLVE ? 1 : kind == SEP_APPLY ? 2 : 3;
     sep_ozaki(ctx, const_cast<kronop_op&>(op), in, out, cplx, epi, shift, dt, diag, sigma,
@@ -837,7 +837,7 @@ int kronop_op_destroy(kronop_op* op) {
       for (double* p : {op->fe[a], op->fo[a], op->be[a], op->bo[a]})
         if (p) cudaFree(p);
       for (void* p : {op->lp_fwd[a], op->lp_bwd[a], op->tf_fwd[a], op->tf_bwd[a], op->f3_fwd[a],
-                      op->f3_bwd[a], op->oz_fwd[a], op->oz_bwd[a]})
+                      op->f3_bwd[a], op->oz_fwd[a], op->oz_bwd[a], op->oz_fo[a], op->oz_bo[a]})
         if (p) cudaFree(p);
       if (!op->shared_axis[a]) {
         if (op->fwd[a]) cudaFree(op->fwd[a]);
@@ -934,8 +934,6 @@ int kronop_op_set_precision(kronop_ctx* ctx, kronop_op* op, int precision) {
     param_check(precision == KRONOP_PREC_FP64 ||
                     (precision >= KRONOP_PREC_FP64_OZAKI && precision <= KRONOP_PREC_FP64_OZAKI5),
                 "op_set_precision: unsupported precision");
-    param_check(precision == KRONOP_PREC_FP64 || !op->folded,
-                "op_set_precision: the INT8 path takes dense operators only");
     if (precision != KRONOP_PREC_FP64) {
       for (int a = 0; a < op->d; ++a)
         param_check(op->n[a] <= 3200, "op_set_precision: Ozaki mode needs extents <= 3200");

@@ -65,6 +65,8 @@ struct kronop_op {
   void* f3_bwd[KRONOP_MAX_DIM] = {};
   void* oz_fwd[KRONOP_MAX_DIM] = {};  // tiled INT8 slices + row exponents (ozaki.cu)
   void* oz_bwd[KRONOP_MAX_DIM] = {};
+  void* oz_fo[KRONOP_MAX_DIM] = {};  // folded operators: odd blocks (oz_fwd / oz_bwd: even)
+  void* oz_bo[KRONOP_MAX_DIM] = {};
   int oz_slices = 0;
   int exec_prec = 0;  // kronop_op_set_precision: 0 = FP64 DMMA, KRONOP_PREC_FP64_OZAKI* = INT8
   bool folded = false;

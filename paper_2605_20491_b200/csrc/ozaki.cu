@@ -39,6 +39,7 @@
 
 #include "context.cuh"
 #include "kronop_internal.cuh"
+#include "vector_ops.cuh"
 
 namespace kronop_dev {
 
@@ -207,10 +208,14 @@ __device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, i
     }
   }
   const int ecol = c0 + lane < a.m ? a.be[c0 + lane] : 0;
+  // this chunk's 32 column eigenvalues: one coalesced load, then broadcast by shuffle (a load
+  // per element would serialise behind the stores, which may alias)
+  const double lamc = a.epi != 0 && c0 + lane < a.m ? a.lamlast[c0 + lane] : 0.0;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {  // uniform (shuffles); stores predicated
     const int col = c0 + j;
     const int ec = __shfl_sync(0xffffffffu, ecol, j);
+    const double lj = __shfl_sync(0xffffffffu, lamc, j);
     const int E = er + ec;  // 2^(ex+ey) / 127^2: exponent bits directly when in normal range
     const double v0 = acc[j] * (1.0 / 16129.0);
     double val = (E > -1000 && E < 1000)
@@ -219,7 +224,7 @@ __device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, i
     if (a.epi == 3) {  // partner row (re <-> im) is the neighbouring lane; as epilogue.cuh
       const double other = __shfl_xor_sync(0xffffffffu, val, 1);
       if (live && col < a.m) {
-        const double ls = __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift);
+        const double ls = __dsub_rn(__dadd_rn(lam_low, lj), a.shift);
         double sn, cs;
         sincos(__dmul_rn(-ls, a.dt), &sn, &cs);
         const bool is_im = (r & 1) != 0;
@@ -228,7 +233,7 @@ __device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, i
                     : __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
       }
     } else if ((a.epi == 1 || a.epi == 2) && live && col < a.m) {
-      const double ls = __dsub_rn(__dadd_rn(lam_low, a.lamlast[col]), a.shift);
+      const double ls = __dsub_rn(__dadd_rn(lam_low, lj), a.shift);
       val = a.epi == 1 ? __ddiv_rn(val, ls) : __dmul_rn(val, ls);
     }
     const long long yi = static_cast<long long>(col) * a.R + r;
@@ -561,6 +566,7 @@ __device__ __forceinline__ long long tile_off(long long p, int KB, int S, int rr
 template <int S>
 __global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict__ x, long long R,
                                                        int K, int KB, long long Rp, int gather,
+                                                       long long ldr, long long off,
                                                        int8_t* __restrict__ out,
                                                        int* __restrict__ ex) {
   extern __shared__ double srow[];
@@ -585,7 +591,7 @@ __global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict_
         for (int u = 0; u < 8; ++u) {
           const int k = k0 + u * 32 + lane;
           v[u] = (r < R && k < K)
-                     ? __ldcs(gather ? x + (rq * K + k) * 2 + rc : x + r * K + k)
+                     ? __ldcs(gather ? x + (rq * ldr + off + k) * 2 + rc : x + r * ldr + off + k)
                      : 0.0;
         }
 #pragma unroll
@@ -676,7 +682,9 @@ __global__ void __launch_bounds__(256) k_oz_split_mat(const double* __restrict__
 
 template <int S>
 void oz_split_rows(cudaStream_t st, const double* x, long long R, int K, int gather, int8_t* out,
-                   int* ex) {
+                   int* ex, long long ldr = -1, long long off = 0) {
+  // row r of K values starts at x + r * ldr + off (ldr = K: contiguous runs); the even / odd
+  // halves of a folded axis are the sub-runs [0, ne) and [ne, n) of rows of length n
   const int KB = (K + OZ_BK - 1) / OZ_BK;
   const long long Rp = (R + OZ_PAIR - 1) / OZ_PAIR * OZ_PAIR;  // whole 256-row pair panels
   const int nch = KB * 2;
@@ -690,7 +698,8 @@ void oz_split_rows(cudaStream_t st, const double* x, long long R, int K, int gat
   const long long groups = Rp / 8;
   const int per_sm = smem <= 72 * 1024 ? 3 : 1;
   const int blocks = static_cast<int>(groups < 148LL * per_sm * 4 ? groups : 148LL * per_sm * 4);
-  k_oz_split_rows<S><<<blocks, 256, smem, st>>>(x, R, K, KB, Rp, gather, out, ex);
+  k_oz_split_rows<S><<<blocks, 256, smem, st>>>(x, R, K, KB, Rp, gather, ldr < 0 ? K : ldr, off,
+                                                 out, ex);
   KCUDA(cudaGetLastError());
 }
 
@@ -898,6 +907,119 @@ void sep_ozaki_impl(kronop_ctx& ctx, kronop_op& op, const double* b, double* x, 
     }
 }
 
+// The even/odd folded operator (kronop_op_create_folded) on the INT8 path: per axis the fold
+// kernel (vector_ops.cu) puts the axis in [even half | odd half] order, the split kernel reads
+// the two sub-runs as separate rows with their own exponents, and two INT8 passes with the
+// half-size matrices write the two mode blocks of the rotated output (the folded mode order the
+// lambda arrays use). Backward passes write the two physical halves and the unfold kernel
+// (with the FullOperator AXPY on the last axis) restores the axis. Half the INT8 products of the
+// dense operator, plus one fold / unfold HBM pass per axis.
+template <int S>
+void sep_ozaki_folded_impl(kronop_ctx& ctx, kronop_op& op, const double* in, double* out,
+                           int cplx, int epi, double shift, double dt, const double* diag,
+                           double sigma) {
+  const long long N = op.N;
+  const int cf = cplx ? 2 : 1;
+  cudaStream_t st = ctx.stream;
+  const bool two = oz_two_sm();
+  const int bpan = two ? OZ_BN / 2 : OZ_BN;
+  const int key = 1000 + S * 2 + (two ? 1 : 0);
+  void** se[2] = {op.oz_fwd, op.oz_bwd};  // even blocks
+  void** so[2] = {op.oz_fo, op.oz_bo};    // odd blocks
+  if (!op.oz_fwd[0] || op.oz_slices != key) {
+    for (int a = 0; a < KRONOP_MAX_DIM; ++a)
+      for (void** p : {&op.oz_fwd[a], &op.oz_bwd[a], &op.oz_fo[a], &op.oz_bo[a]})
+        if (*p) {
+          KCUDA(cudaFree(*p));
+          *p = nullptr;
+        }
+    for (int a = 0; a < op.d; ++a)
+      for (int dir = 0; dir < 2; ++dir)
+        for (int h = 0; h < 2; ++h) {
+          const int m = h == 0 ? op.ne[a] : op.no[a];
+          if (m == 0) continue;
+          const double* M = dir == 0 ? (h == 0 ? op.fe[a] : op.fo[a]) : (h == 0 ? op.be[a] : op.bo[a]);
+          const int lda = h == 0 ? op.lda_e[a] : op.lda_o[a];
+          const size_t sb = oz_slice_bytes(m, m, OZ_BN, S);
+          const long long mp = (m + OZ_BN - 1) / OZ_BN * OZ_BN;
+          void* p = nullptr;
+          KCUDA(cudaMalloc(&p, sb + mp * sizeof(int)));
+          oz_split_mat<S>(st, M, lda, m, m, bpan, static_cast<int8_t*>(p),
+                          reinterpret_cast<int*>(static_cast<char*>(p) + sb));
+          (h == 0 ? se : so)[dir][a] = p;
+        }
+    op.oz_slices = key;
+  }
+  size_t need = 0;
+  for (int a = 0; a < op.d; ++a) {
+    const long long R = cf * (N / op.n[a]);
+    const size_t v = oz_slice_bytes(R, op.ne[a], OZ_PAIR, S) +
+                     ((R + OZ_PAIR - 1) / OZ_PAIR * OZ_PAIR) * sizeof(int);
+    need = v > need ? v : need;
+  }
+  const size_t need_d = (need + 7) / 8 + 16;
+  ensure_scratch(ctx, need_d > static_cast<size_t>(cf * N) ? need_d : static_cast<size_t>(cf * N));
+  double* fa = ctx.scratch[0];                                  // folded input of a pass
+  int8_t* xs = reinterpret_cast<int8_t*>(ctx.scratch[1]);      // slices + row exponents
+  double* fb = ensure_tmp(ctx, static_cast<size_t>(cf * N));   // pass output
+  auto half_pass = [&](const double* src, double* dst, int a, int dir, int h, bool spectral) {
+    const int n = op.n[a];
+    const int m = h == 0 ? op.ne[a] : op.no[a];
+    if (m == 0) return;
+    const long long off = h == 0 ? 0 : op.ne[a];
+    const long long R = cf * (N / n);
+    const size_t xb = oz_slice_bytes(R, m, OZ_PAIR, S);
+    int* xe = reinterpret_cast<int*>(xs + xb);
+    oz_split_rows<S>(st, src, R, m, cplx && a == 0 ? 1 : 0, xs, xe, n, off);
+    OzArgs oa{};
+    oa.cplx = cplx;
+    if (spectral) {
+      oa.epi = epi;
+      oa.dt = dt;
+      oa.shift = shift;
+      oa.nlow = op.d - 1;
+      for (int j = 0; j < op.d - 1; ++j) {
+        oa.lowext[j] = op.n[j];
+        oa.lowlam[j] = op.lam[j];
+      }
+      oa.lamlast = op.lam[a] + off;
+    }
+    const void* mat = (h == 0 ? se : so)[dir][a];
+    const size_t mb = oz_slice_bytes(m, m, OZ_BN, S);
+    oa.xs = xs;
+    oa.xe = xe;
+    oa.bs = static_cast<const int8_t*>(mat);
+    oa.be = reinterpret_cast<const int*>(static_cast<const char*>(mat) + mb);
+    oa.y = dst + off * R;
+    oa.R = R;
+    oa.K = m;
+    oa.KB = (m + OZ_BK - 1) / OZ_BK;
+    oa.m = m;
+    oa.ntn = (m + OZ_BN - 1) / OZ_BN;
+    oa.ntm = (R + OZ_PAIR - 1) / OZ_PAIR * 2;
+    if (two)
+      oz2_pass<S>(st, oa, xb, mb);
+    else
+      oz_pass<S>(st, oa);
+    ctx.ws.launches += 2;
+  };
+  const double* cur = in;
+  for (int a = 0; a < op.d; ++a) {  // forward: fold the (fastest) axis, two half passes
+    const int n = op.n[a];
+    const long long pre = cplx && a == 0 ? 2 : 1;
+    launch_fold(st, ctx.ws, cur, fa, pre, n, cf * N / (n * pre));
+    for (int h = 0; h < 2; ++h) half_pass(fa, fb, a, 0, h, a == op.d - 1);
+    cur = fb;
+  }
+  for (int a = 0; a < op.d; ++a) {  // backward: two half passes, unfold the (slowest) axis
+    const int n = op.n[a];
+    for (int h = 0; h < 2; ++h) half_pass(fb, fa, a, 1, h, false);
+    const bool last = a == op.d - 1;
+    launch_unfold(st, ctx.ws, fa, last ? out : fb, cf * N / n, n, 1, last ? diag : nullptr,
+                  last ? in : nullptr, last ? sigma : 0.0, cplx);
+  }
+}
+
 }  // namespace
 
 // Any separable transform on the INT8 path: cplx (interleaved complex field), epi 1 divide /
@@ -906,6 +1028,15 @@ void sep_ozaki(kronop_ctx& ctx, kronop_op& op, const double* in, double* out, in
                double shift, double dt, const double* diag, double sigma, int slices) {
   for (int a = 0; a < op.d; ++a)
     param_check(op.n[a] <= OZ_KMAX, "Ozaki mode needs extents <= 3200");
+  if (op.folded) {
+    if (slices == 5)
+      sep_ozaki_folded_impl<5>(ctx, op, in, out, cplx, epi, shift, dt, diag, sigma);
+    else if (slices == 6)
+      sep_ozaki_folded_impl<6>(ctx, op, in, out, cplx, epi, shift, dt, diag, sigma);
+    else
+      sep_ozaki_folded_impl<7>(ctx, op, in, out, cplx, epi, shift, dt, diag, sigma);
+    return;
+  }
   if (slices == 5)
     sep_ozaki_impl<5>(ctx, op, in, out, cplx, epi, shift, dt, diag, sigma);
   else if (slices == 6)

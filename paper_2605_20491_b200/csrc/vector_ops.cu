@@ -398,24 +398,45 @@ __device__ __forceinline__ double unfold_value(const double* z, long long base, 
   return z[base + pre * no];  // middle node
 }
 
+// one (i, mirror) pair per row: both outputs from the same two loads (each input read once)
+__device__ __forceinline__ double fold_axpy(double v, long long yi, const double* diag,
+                                            const double* u, double sigma, int cplx) {
+  const double uu = u[yi];
+  if (diag) v = __dadd_rn(v, __dmul_rn(diag[cplx ? (yi >> 1) : yi], uu));
+  if (sigma != 0.0) v = __dsub_rn(v, __dmul_rn(sigma, uu));
+  return v;
+}
 template <bool UNFOLD>
 __global__ void k_fold_wide(const double* __restrict__ x, double* __restrict__ y, long long pre,
                             int n, long long post, const double* diag, const double* u,
                             double sigma, int cplx) {
-  const long long rows = static_cast<long long>(n) * post;
+  const int no = n / 2, ne = n - no;
+  const long long rows = static_cast<long long>(ne) * post;
+  const bool axpy = UNFOLD && (diag || sigma != 0.0);
   for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
-    const long long q = row / n;
-    const int i = static_cast<int>(row - q * n);
+    const long long q = row / ne;
+    const int i = static_cast<int>(row - q * ne);
     const long long base = pre * n * q;
+    // fold: (x_i, x_{n-1-i}) -> (y_i, y_{ne+i});  unfold: (z_i, z_{ne+i}) -> (y_i, y_{n-1-i})
+    const long long s0 = base + pre * i;
+    const long long s1 = base + pre * (UNFOLD ? ne + i : n - 1 - i);
+    const long long d0 = base + pre * i;
+    const long long d1 = base + pre * (UNFOLD ? n - 1 - i : ne + i);
+    const bool mid = i >= no;  // middle node (n odd): a copy
     for (long long p = threadIdx.x; p < pre; p += blockDim.x) {
-      double v = UNFOLD ? unfold_value(x, base + p, pre, n, i) : fold_value(x, base + p, pre, n, i);
-      const long long yi = base + p + pre * i;
-      if (UNFOLD && (diag || sigma != 0.0)) {
-        const double uu = u[yi];
-        if (diag) v = __dadd_rn(v, __dmul_rn(diag[cplx ? (yi >> 1) : yi], uu));
-        if (sigma != 0.0) v = __dsub_rn(v, __dmul_rn(sigma, uu));
+      const double a = x[s0 + p];
+      if (mid) {
+        y[d0 + p] = axpy ? fold_axpy(a, d0 + p, diag, u, sigma, cplx) : a;
+        continue;
       }
-      y[yi] = v;
+      const double b = x[s1 + p];
+      double v0 = __dadd_rn(a, b), v1 = __dsub_rn(a, b);
+      if (axpy) {
+        v0 = fold_axpy(v0, d0 + p, diag, u, sigma, cplx);
+        v1 = fold_axpy(v1, d1 + p, diag, u, sigma, cplx);
+      }
+      y[d0 + p] = v0;
+      y[d1 + p] = v1;
     }
   }
 }
@@ -446,7 +467,7 @@ static void launch_fold_impl(cudaStream_t s, Workspace& ws, const double* x, dou
                              long long pre, int n, long long post, const double* diag,
                              const double* u, double sigma, int cplx, bool unfold) {
   if (pre >= 32) {
-    const long long rows = static_cast<long long>(n) * post;
+    const long long rows = static_cast<long long>(n - n / 2) * post;
     const unsigned grid = static_cast<unsigned>(rows < 1184 * 4 ? rows : 1184 * 4);
     const int thr = pre >= 256 ? 256 : 128;
     if (unfold)

@@ -841,3 +841,34 @@ def test_ozaki_execution_precision_drivers(ctx, kind, cells):
     assert rel(host(x), xr) < 1e-10
     op.set_precision("fp64")  # back to DMMA
     assert rel(host(op.solve(b)), host(op64.solve(b))) == 0.0
+
+
+@pytest.mark.parametrize("spec", [(8.0, 4, 7, 3), (8.0, 3, 5, 3), (2.0, 3, 4, 2), (1.5, 5, 6, 1),
+                                  (8.0, 13, 5, 3), (1.0, 1, 3, 4)])
+def test_ozaki_folded_operator(ctx, spec):
+    """The even/odd folded operator on the INT8 path (fold, two half-size INT8 passes per axis,
+    unfold with the FullOperator AXPY): apply / solve / propagate / FullOperator apply equal to
+    the dense FP64 operator's, real and complex, odd and even extents."""
+    A = api()
+    grid = A.Grid.sem(*spec)
+    f = [lambda t: t * t] * grid.dim
+    op = grid.separable_operator(ctx, f, 0.5)
+    fo = grid.separable_operator(ctx, f, 0.5, folded=True).set_precision("ozaki")
+    n = grid.node_count()
+    u = dev(K.uniform_pm1(31, n))
+    psi = dev(K.seeded_complex_field(grid.shape, 32).reshape(-1))
+    for a, b in ((fo.apply(u), op.apply(u)), (fo.solve(u), op.solve(u)),
+                 (fo.apply(psi), op.apply(psi)), (fo.solve(psi), op.solve(psi))):
+        assert np.isfinite(host(a)).all() and rel(host(a), host(b)) < 1e-12
+    lmax = max(abs(fo.info()[2]), 1.0)
+    for dt in (0.11, -1.3):
+        bound = max(1e-12, 64 * 2.2e-16 * lmax * abs(dt))
+        assert rel(host(fo.propagate(psi, dt)), host(op.propagate(psi, dt))) < bound
+    v2 = grid.sample(lambda c: 2.0 * np.exp(-sum((ci - 0.3) ** 2 for ci in c)))
+    fa, fb = A.FullOperator(fo, dev(v2)), A.FullOperator(op, dev(v2))
+    assert rel(host(fa.apply(u, sigma=0.7)), host(fb.apply(u, sigma=0.7))) < 1e-12
+    x = torch.zeros_like(u)
+    rep = A.pcg(A.apply_map(fo, dev(v2)), A.solve_map(fo), u, x, A.PcgConfig(rel_tol=1e-10))
+    rep64 = A.pcg(A.apply_map(op, dev(v2)), A.solve_map(op), u, torch.zeros_like(u),
+                  A.PcgConfig(rel_tol=1e-10))
+    assert rep.converged and rep.iterations == rep64.iterations
