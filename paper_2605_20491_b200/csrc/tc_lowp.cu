@@ -127,6 +127,17 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
+// one lane of a converged warp: the MMA warps run their loops converged and only the issue is
+// single-threaded, so descriptors stay in uniform registers (a lane-0 branch made the compiler
+// wrap every tcgen05.mma in an ELECT / BRA.U.ANY loop; see ozaki.cu)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, %1;\n@px mov.s32 %0, 1;\n}\n"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
 // K-major, 128-byte-swizzled UMMA shared-memory descriptor (cute/arch/mma_sm100_desc.hpp layout):
 // start >> 4 | LBO 1 | SBO 1024 B (8-row groups) | version 1 (Blackwell) | SWIZZLE_128B.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
@@ -258,7 +269,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
+    {  // MMA warp (converged; one elected lane issues)
       long long it = 0, lt = 0;
       for (long long T = t0; T < tiles; T += tstep, ++lt) {
         const int b = static_cast<int>(lt & 1);
@@ -272,15 +283,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mb_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t sa = su32(sm + s * TC_STAGE), sb = sa + TC_A_BYTES;
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / TcTraits<PREC>::UK; ++kk)  // 32 bytes of K per instruction
-            umma<PREC>(d, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
-          if (CL == 1)
-            umma_commit(&empty[s]);  // smem stage free once these MMAs have read it
-          else
-            umma_commit_mc(&empty[s], 0x3);  // ... in both CTAs (the peer multicasts into it)
+            for (int kk = 0; kk < BK / TcTraits<PREC>::UK; ++kk)  // 32 bytes of K per instruction
+              umma<PREC>(d, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
+            if (CL == 1)
+              umma_commit(&empty[s]);  // smem stage free once these MMAs have read it
+            else
+              umma_commit_mc(&empty[s], 0x3);  // ... in both CTAs (the peer multicasts into it)
+          }
+          __syncwarp();
         }
-        umma_commit(&tfull[b]);  // accumulator b complete
+        if (elect_one()) umma_commit(&tfull[b]);  // accumulator b complete
+        __syncwarp();
       }
     }
   } else {  // epilogue warps 2..9: TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4
@@ -681,7 +696,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {  // MMA issuer: the leader only
+    if (leader) {  // MMA warp of the leader (converged; one elected lane issues)
       long long it = 0, lt = 0;
       for (long long T = t0; T < tiles; T += tstep, ++lt) {
         const int b = static_cast<int>(lt & 1);
@@ -693,12 +708,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mb_wait(&full[s], static_cast<uint32_t>((it / T2_STAGES) & 1));
           tc_fence_after();
           const uint32_t sa = su32(sm + s * T2_STAGE), sb = sa + T2_A;
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / TcTraits<PREC>::UK; ++kk)
-            umma2<PREC>(d, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
-          umma2_commit_mc(&empty[s]);
+            for (int kk = 0; kk < BK / TcTraits<PREC>::UK; ++kk)
+              umma2<PREC>(d, umma_desc(sa + kk * 32), umma_desc(sb + kk * 32), (kb | kk) != 0);
+            umma2_commit_mc(&empty[s]);
+          }
+          __syncwarp();
         }
-        umma2_commit_mc(&tfull[b]);
+        if (elect_one()) umma2_commit_mc(&tfull[b]);
+        __syncwarp();
       }
     }
   } else {  // epilogue warps, both CTAs: this CTA's 128 rows x 256 columns
