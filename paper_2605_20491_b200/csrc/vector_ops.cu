@@ -413,7 +413,14 @@ __global__ void k_fold_wide(const double* __restrict__ x, double* __restrict__ y
   const int no = n / 2, ne = n - no;
   const long long rows = static_cast<long long>(ne) * post;
   const bool axpy = UNFOLD && (diag || sigma != 0.0);
-  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+  // work items = (pair row, chunk of the pre range): enough blocks in flight even when there
+  // are few pair rows (the slowest axis of a 1024^3 field: 512 rows of 1 M elements)
+  constexpr long long kChunk = 16384;
+  const long long nch = (pre + kChunk - 1) / kChunk;
+  for (long long w = blockIdx.x; w < rows * nch; w += gridDim.x) {
+    const long long row = w / nch;
+    const long long p0 = (w - row * nch) * kChunk;
+    const long long p1 = p0 + kChunk < pre ? p0 + kChunk : pre;
     const long long q = row / ne;
     const int i = static_cast<int>(row - q * ne);
     const long long base = pre * n * q;
@@ -423,7 +430,7 @@ __global__ void k_fold_wide(const double* __restrict__ x, double* __restrict__ y
     const long long d0 = base + pre * i;
     const long long d1 = base + pre * (UNFOLD ? n - 1 - i : ne + i);
     const bool mid = i >= no;  // middle node (n odd): a copy
-    for (long long p = threadIdx.x; p < pre; p += blockDim.x) {
+    for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
       const double a = x[s0 + p];
       if (mid) {
         y[d0 + p] = axpy ? fold_axpy(a, d0 + p, diag, u, sigma, cplx) : a;
@@ -467,7 +474,7 @@ static void launch_fold_impl(cudaStream_t s, Workspace& ws, const double* x, dou
                              long long pre, int n, long long post, const double* diag,
                              const double* u, double sigma, int cplx, bool unfold) {
   if (pre >= 32) {
-    const long long rows = static_cast<long long>(n - n / 2) * post;
+    const long long rows = static_cast<long long>(n - n / 2) * post * ((pre + 16383) / 16384);
     const unsigned grid = static_cast<unsigned>(rows < 1184 * 4 ? rows : 1184 * 4);
     const int thr = pre >= 256 ? 256 : 128;
     if (unfold)
