@@ -314,8 +314,7 @@ static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double
         e.u = in;
         e.sigma = sigma;
       }
-      launch_fused_rot(ctx.stream, src, dst, cplx, f, n, op.N, mats, lda, e);
-      ctx.ws.launches += 1;
+      ctx.ws.launches += launch_fused_rot(ctx.stream, src, dst, cplx, f, n, op.N, mats, lda, e);
       src = dst;
     }
 }

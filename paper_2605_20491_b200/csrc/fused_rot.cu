@@ -505,14 +505,143 @@ int choose_kpat(int S, int m, int K4, bool last, int C, int F, int lcq) {
   return best;
 }
 
+// Standalone spectral pass over a field in the original axis order (what the last forward group
+// launch leaves behind), used when the contraction runs on the epilogue-free kernels: the
+// per-element epilogue (one sincos per pair for the phase) then runs at full occupancy instead of
+// on the 16 warps of the contraction kernel. lambda is the direct sum in axis order from 0.0 and
+// every operation matches store_tile, so the result is bit-identical to the fused epilogue.
+// Layout: a row = the first m axes (L = prod n[0..m) <= SP_LMAX entries, lambda prefix sums in
+// shared memory); a block handles rows_per_block consecutive rows, the hi-axis eigenvalues of each row
+// staged once in shared memory.
+constexpr int SP_LMAX = 2048;
+constexpr int SP_THREADS = 256;
+struct SpecArgs {
+  double* y;
+  int C, d, m, L, rows_per_block, kind;
+  float inv_L;  // 1 / L (fast_div)
+  long long rows;
+  int n[KRONOP_MAX_DIM];
+  const double* lam[KRONOP_MAX_DIM];
+  double shift, dt;
+};
+
+__global__ void __launch_bounds__(SP_THREADS) spectral_pass_kernel(const __grid_constant__ SpecArgs A) {
+  __shared__ double lam_lo[SP_LMAX];
+  extern __shared__ double hv[];  // rows_per_block x (d - m)
+  const int tid = threadIdx.x;
+  for (int lo = tid; lo < A.L; lo += SP_THREADS) {
+    int r = lo;
+    double lam = 0.0;
+    for (int a = 0; a < A.m; ++a) {
+      const int q = r / A.n[a];
+      lam = __dadd_rn(lam, A.lam[a][r - q * A.n[a]]);
+      r = q;
+    }
+    lam_lo[lo] = lam;
+  }
+  const int nh = A.d - A.m;
+  const int RB = A.rows_per_block;
+  const long long nchunks = (A.rows + RB - 1) / RB;
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long r0 = ch * RB;
+    const int rv = static_cast<int>(A.rows - r0 < RB ? A.rows - r0 : RB);
+    __syncthreads();  // lam_lo ready / previous chunk's hv consumed
+    for (int t = tid; t < rv * nh; t += SP_THREADS) {
+      const int ri = t / nh, j = t - ri * nh;
+      long long r = r0 + ri;
+      for (int a = A.m; a < A.m + j; ++a) r /= A.n[a];
+      const int a = A.m + j;
+      hv[ri * nh + j] = A.lam[a][r % A.n[a]];
+    }
+    __syncthreads();
+    const int units = rv * A.L;
+    double* base = A.y + static_cast<long long>(A.C) * A.L * r0;
+    // 4 units per thread per round: loads issued before the (latency-bound) sincos chains
+    for (int u0 = tid; u0 < units; u0 += 4 * SP_THREADS) {
+      double2 v[4];
+      double ls[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int u = u0 + k * SP_THREADS;
+        if (u < units) {
+          const int ri = fast_div(u, A.L, A.inv_L), lo = u - ri * A.L;
+          if (A.C == 2) {
+            v[k] = reinterpret_cast<const double2*>(base)[u];
+          } else {
+            v[k].x = base[u];
+            v[k].y = 0.0;
+          }
+          double lam = lam_lo[lo];
+          for (int j = 0; j < nh; ++j) lam = __dadd_rn(lam, hv[ri * nh + j]);
+          ls[k] = __dsub_rn(lam, A.shift);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int u = u0 + k * SP_THREADS;
+        if (u >= units) break;
+        if (A.C == 2) {
+          double2 w = v[k];
+          if (A.kind == EPI_SPEC_MUL) {
+            w.x = __dmul_rn(w.x, ls[k]);
+            w.y = __dmul_rn(w.y, ls[k]);
+          } else if (A.kind == EPI_SPEC_DIV) {
+            w.x = __ddiv_rn(w.x, ls[k]);
+            w.y = __ddiv_rn(w.y, ls[k]);
+          } else {  // operators.cpp:68-71
+            const double phase = __dmul_rn(-ls[k], A.dt);
+            double sn, cs;
+            sincos(phase, &sn, &cs);
+            w.x = __dsub_rn(__dmul_rn(v[k].x, cs), __dmul_rn(v[k].y, sn));
+            w.y = __dadd_rn(__dmul_rn(v[k].x, sn), __dmul_rn(v[k].y, cs));
+          }
+          reinterpret_cast<double2*>(base)[u] = w;
+        } else {
+          base[u] = A.kind == EPI_SPEC_MUL ? __dmul_rn(v[k].x, ls[k]) : __ddiv_rn(v[k].x, ls[k]);
+        }
+      }
+    }
+  }
+}
+
+void launch_spectral_pass(cudaStream_t s, double* y, int C, int d, const int* n,
+                          const double* const* lam, long long N, int kind, double shift,
+                          double dt) {
+  SpecArgs a{};
+  a.y = y;
+  a.C = C;
+  a.d = d;
+  a.kind = kind;
+  a.shift = shift;
+  a.dt = dt;
+  a.m = 0;
+  a.L = 1;
+  for (int j = 0; j < d; ++j) {
+    a.n[j] = n[j];
+    a.lam[j] = lam[j];
+  }
+  while (a.m < d && a.L * n[a.m] <= SP_LMAX) a.L *= n[a.m++];
+  param_check(a.m >= 1, "spectral pass: leading extent too large");
+  a.inv_L = 1.0f / static_cast<float>(a.L);
+  a.rows = N / a.L;
+  a.rows_per_block = 1;
+  while (a.rows_per_block * 2 * a.L <= 4096) a.rows_per_block *= 2;
+  const int nh = d - a.m;
+  const size_t smem = sizeof(double) * static_cast<size_t>(a.rows_per_block * (nh > 0 ? nh : 1));
+  const long long nchunks = (a.rows + a.rows_per_block - 1) / a.rows_per_block;
+  const long long grid = nchunks < 148LL * 8 ? nchunks : 148LL * 8;
+  spectral_pass_kernel<<<static_cast<unsigned>(grid), SP_THREADS, smem, s>>>(a);
+  KCUDA(cudaGetLastError());
+}
+
 }  // namespace
 
 void prime_fused_rot_kernels() {}
 
 bool fused_rot_eligible(const double* x) { return (reinterpret_cast<uintptr_t>(x) & 15u) == 0; }
 
-void launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f, const int* n,
-                      long long N, const double* const* mats, const int* lda, const RotEpi& epi) {
+int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f, const int* n,
+                     long long N, const double* const* mats, const int* lda, const RotEpi& epi) {
   param_check(f >= 1 && f <= RT_MAXF, "fused_rot: group size");
   RotArgs a{};
   a.x = x;
@@ -564,14 +693,28 @@ void launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int 
     const char* e = getenv("KRONOP_ROT_NO_DFMA");  // A/B switch: DMMA for every extent
     return e && e[0] == '1';
   }();
-  // the spectral launch keeps the 16-warp DMMA kernel: its store pass (one sincos per pair) is
-  // latency bound and needs the warps more than the contraction needs DFMA's efficiency
+  // A/B switch for the phase (last forward) launch: 0 = epilogue fused into the 16-warp DMMA
+  // kernel; 1 = contraction on the epilogue-free kernels + the standalone spectral pass when the
+  // DFMA kernel serves the group; 2 (default) = that split for every extent (9D n = 9 propagate
+  // 29.7 -> 26.7 ms, 6D n = 29 51.7 -> 50.8 ms, bit-identical; tools/microbench/spec_split.py). The divide / multiply
+  // epilogues stay fused (measured: splitting them costs the extra field round trip)
+  static const int spec_split = [] {
+    const char* e = getenv("KRONOP_ROT_SPEC_SPLIT");
+    return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
+  }();
   const bool spectral = epi.kind == EPI_SPEC_MUL || epi.kind == EPI_SPEC_DIV ||
                         epi.kind == EPI_SPEC_PHASE;
-  if (same && maxn >= 2 && maxn <= 10 && !no_dfma && !spectral) {
+  const bool dfma_ok = same && maxn >= 2 && maxn <= 10 && !no_dfma;
+  const bool split = epi.kind == EPI_SPEC_PHASE && (spec_split == 2 || (spec_split == 1 && dfma_ok));
+  if (split) a.epi = EPI_STORE;
+  // fused epilogue: the spectral launch keeps the 16-warp DMMA kernel (its store pass, one sincos
+  // per pair, is latency bound and needs the warps more than the contraction needs DFMA)
+  bool launched = false;
+  if (dfma_ok && (!spectral || split)) {
+    launched = true;
     switch (f * 16 + maxn) {
 #define RT_DF(F, N) \
-  case F * 16 + N: launch_rot<F, 1, 1, N>(s, a); return;
+  case F * 16 + N: launch_rot<F, 1, 1, N>(s, a); break;
       RT_DF(1, 2) RT_DF(1, 3) RT_DF(1, 4) RT_DF(1, 5) RT_DF(1, 6) RT_DF(1, 7) RT_DF(1, 8)
       RT_DF(1, 9) RT_DF(1, 10)
       RT_DF(2, 2) RT_DF(2, 3) RT_DF(2, 4) RT_DF(2, 5) RT_DF(2, 6) RT_DF(2, 7) RT_DF(2, 8)
@@ -579,19 +722,35 @@ void launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int 
       RT_DF(3, 2) RT_DF(3, 3) RT_DF(3, 4) RT_DF(3, 5) RT_DF(3, 6) RT_DF(3, 7) RT_DF(3, 8)
       RT_DF(3, 9) RT_DF(3, 10)
 #undef RT_DF
-      default: break;
+      default: launched = false; break;
     }
   }
-  if (f == 1)
-    launch_rot_nf<1>(s, a, maxn);
-  else if (f == 2)
-    launch_rot_nf<2>(s, a, maxn);
-  else if (maxn <= 4)  // F <= 1024 -> n <= 10 for three axes
-    launch_rot<3, 1, 1>(s, a);
-  else if (maxn <= 8)
-    launch_rot<3, 2, 1>(s, a);
-  else
-    launch_rot<3, 3, 2>(s, a);
+  if (!launched) {
+    if (f == 1)
+      launch_rot_nf<1>(s, a, maxn);
+    else if (f == 2)
+      launch_rot_nf<2>(s, a, maxn);
+    else if (maxn <= 4)  // F <= 1024 -> n <= 10 for three axes
+      launch_rot<3, 1, 1>(s, a);
+    else if (maxn <= 8)
+      launch_rot<3, 2, 1>(s, a);
+    else
+      launch_rot<3, 3, 2>(s, a);
+  }
+  if (!split) return 1;
+  // the output is back in the original axis order: the axes below the group, then the group
+  int dims[KRONOP_MAX_DIM];
+  const double* lams[KRONOP_MAX_DIM];
+  for (int j = 0; j < epi.nq; ++j) {
+    dims[j] = static_cast<int>(epi.qext[j]);
+    lams[j] = epi.lam_q[j];
+  }
+  for (int j = 0; j < f; ++j) {
+    dims[epi.nq + j] = n[j];
+    lams[epi.nq + j] = epi.lam_g[j];
+  }
+  launch_spectral_pass(s, y, a.C, epi.nq + f, dims, lams, N, epi.kind, epi.shift, epi.dt);
+  return 2;
 }
 
 }  // namespace kronop_dev

@@ -98,8 +98,9 @@ struct RotEpi {
 };
 void prime_fused_rot_kernels();
 bool fused_rot_eligible(const double* x);
-void launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f, const int* n,
-                      long long N, const double* const* mats, const int* lda, const RotEpi& epi);
+// returns the number of kernels launched (2 when the spectral epilogue runs as its own pass)
+int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f, const int* n,
+                     long long N, const double* const* mats, const int* lda, const RotEpi& epi);
 
 // Fused small-extent multi-axis transform (fused_small.cu), used when every axis has n <= 32.
 void prime_fused_small_kernels();

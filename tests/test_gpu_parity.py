@@ -872,3 +872,42 @@ def test_ozaki_folded_operator(ctx, spec):
     rep64 = A.pcg(A.apply_map(op, dev(v2)), A.solve_map(op), u, torch.zeros_like(u),
                   A.PcgConfig(rel_tol=1e-10))
     assert rep.converged and rep.iterations == rep64.iterations
+
+
+_SPLIT_CHILD = r"""
+import hashlib, sys
+import torch
+sys.path.insert(0, %r)
+from paper_2605_20491_b200 import api as A
+from oracle import kronop_oracle as K
+ctx = A.Context(0)
+h = hashlib.sha1()
+for spec in [(3.0, 2, 2, 9), (5.0, 2, 3, 6), (2.0, 1, 7, 4), (8.0, 3, 11, 2)]:
+    g = A.Grid.sem(*spec)
+    op = g.separable_operator(ctx, [(lambda t: t * t)] * g.dim, 0.25)
+    u = torch.from_numpy(K.uniform_pm1(7, g.node_count())).cuda()
+    psi = torch.from_numpy(K.seeded_complex_field(g.shape, 8)).cuda()
+    for t in (op.apply(u), op.solve(u), op.solve(psi), op.propagate(psi, 0.07)):
+        h.update(torch.view_as_real(t).cpu().numpy().tobytes() if t.is_complex()
+                 else t.cpu().numpy().tobytes())
+print(h.hexdigest())
+"""
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_small_extent_spectral_split_bitwise(mode):
+    """The standalone spectral pass after an epilogue-free contraction (KRONOP_ROT_SPEC_SPLIT = 1,
+    or 2, the default) gives bit-identical apply / solve / propagate results to the epilogue fused
+    into the DMMA contraction (= 0) on 9D / 6D / 4D / 2D grids."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _SPLIT_CHILD % root
+    dig = {}
+    for m in ("0", mode):
+        p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                           env=dict(os.environ, KRONOP_ROT_SPEC_SPLIT=m), timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        dig[m] = p.stdout.strip().splitlines()[-1]
+    assert dig["0"] == dig[mode]
