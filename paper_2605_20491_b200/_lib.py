@@ -135,6 +135,7 @@ PROTOTYPES = {
     "kronop_host_build_hermite_axis": (I, [I, DP, DP, DP, DP]),
     "kronop_host_build_sem_axis_folded": (I, [D, I, I] + [DP] * 8),
     "kronop_splitmix_uniform": (I, [P, C.c_uint64, C.c_uint64, C.c_size_t, P]),
+    "kronop_selftest_division": (I, [P, P, P, C.c_size_t, P]),
 }
 
 _lib = None

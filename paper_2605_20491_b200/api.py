@@ -448,6 +448,20 @@ class SeparableOperator:
                                        int(x.is_complex()), _ptr(out)))
         return out
 
+    EPI = {"store": 0, "mul": 1, "div": 2, "phase": 3, "axpy": 4}
+
+    def transform_pass_ex(self, x: torch.Tensor, axis: int, forward: bool = True,
+                          epilogue: str = "store", dt: float = 0.0, diag=None, sigma: float = 0.0,
+                          u=None, out=None):
+        """One pass with a fused epilogue (kronop_op_pass_ex): "store", "mul" / "div" (spectral
+        x / ÷ (lambda - shift)), "phase" (x exp(-i (lambda - shift) dt)), "axpy" (+ diag u - sigma u)."""
+        out = self._out(x, out)
+        with _Call(self.ctx):
+            check(lib().kronop_op_pass_ex(self.ctx.h, self.h, axis, int(forward), _ptr(x),
+                                          int(x.is_complex()), _ptr(out), self.EPI[epilogue],
+                                          C.c_double(dt), _ptr(diag), C.c_double(sigma), _ptr(u)))
+        return out
+
     # host-buffer (end-to-end) variants
     def solve_host(self, b: np.ndarray, out: np.ndarray, is_complex=None):
         """kronop_sep_solve_host: host in / host out, copies overlapped with the passes."""

@@ -1154,6 +1154,20 @@ int kronop_splitmix_uniform(kronop_ctx* ctx, uint64_t seed, uint64_t start, size
   });
 }
 
+int kronop_selftest_division(kronop_ctx* ctx, const double* a, const double* b, size_t n,
+                             unsigned long long* mismatches) {
+  return guard([&] {
+    unsigned long long* d = nullptr;
+    KCUDA(cudaMallocAsync(&d, sizeof(unsigned long long), ctx->stream));
+    KCUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), ctx->stream));
+    launch_div_selftest(ctx->stream, ctx->ws, a, b, d, static_cast<long long>(n));
+    KCUDA(cudaMemcpyAsync(mismatches, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+    KCUDA(cudaFreeAsync(d, ctx->stream));
+    KCUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 // ------------------------------------------------------------------------ host setup --
 int kronop_host_gll_rule(int degree, double* nodes, double* weights, double* diff) {
   return guard([&] {

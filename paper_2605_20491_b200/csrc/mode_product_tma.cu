@@ -65,7 +65,11 @@ struct Cfg {
   static constexpr int X_BYTES = BM * BK * 8;
   static constexpr int A_BYTES = BN * BK * 8;
   static constexpr int STAGE_BYTES = X_BYTES + A_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 64 /*barriers*/;
+  // + per-warp tables of the spectral-divide epilogue (EK_DIV): row lambda partial sums (WTM)
+  //   and column eigenvalues (WTN) of the warp's current tile
+  static constexpr int WTAB = WTM + WTN;
+  static constexpr int SMEM =
+      STAGES * STAGE_BYTES + 1024 /*align*/ + 64 /*barriers*/ + NCONS * WTAB * 8;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -160,6 +164,16 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 
 __device__ __forceinline__ int chS(int g) { return ((g & 1) << 2) | (g >> 1); }
 
+// Epilogue specialisations (compile-time, so each kernel carries only its own epilogue code: the
+// general one, with every kind behind runtime branches, is large enough to miss in the
+// instruction cache when unrolled over 64 accumulators per thread):
+//   EK_GENERIC  every EpiParams kind (runtime dispatch; out-of-line per-element helpers)
+//   EK_STORE    plain store
+//   EK_DIV      spectral divide on the last real-view axis (the solve's fused pass): per-warp
+//               tables of the row lambda partial sums and column eigenvalues, built before the K
+//               loop, and the divisions of one row batch issued together (div_rn_fast)
+enum { EK_GENERIC = 0, EK_STORE = 1, EK_DIV = 2 };
+
 struct TArgs {
   double* y;
   int x2d;  // STRIDED with post == 1: X is the 2-D (pre x nk) tensor map
@@ -183,16 +197,18 @@ __device__ __forceinline__ int col_map(int jc, int n) {
   return (jc >> 1) * 16 + 2 * chS(n) + (jc & 1);
 }
 
-template <int BN, int LOADER, int CL>
+template <int BN, int LOADER, int CL, int EK>
 __global__ void __launch_bounds__(NTHREADS, 1)
     mode_product_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                             const __grid_constant__ CUtensorMap tma, const TArgs args) {
   using C = Cfg<BN>;
+  if (args.ep.active && *args.ep.active == 0) return;  // whole CTA: before any barrier init
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
+  double* s_tab = reinterpret_cast<double*>(smem + STAGES * C::STAGE_BYTES + 64);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -335,6 +351,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const long long panel = T / ngroups;
     const long long row0 = panel * BM;
     const int col0 = (static_cast<int>(T - panel * ngroups) * CL + static_cast<int>(crank)) * BN;
+    double* w_rowlam = s_tab + warp * C::WTAB;
+    double* w_collam = w_rowlam + C::WTM;
+    if (EK == EK_DIV) {
+      // this warp's rows / columns of the tile: one index decomposition per row (32-bit: TMA
+      // passes have R < 2^31) and one eigenvalue load per column, latency hidden behind the
+      // first stage's wait; the warp owns its table (no CTA barrier couples the warps)
+      __syncwarp();
+#pragma unroll
+      for (int k = lane; k < C::WTM; k += 32) {
+        const long long r = row0 + wm * C::WTM + k;
+        w_rowlam[k] = r < R ? lambda_partial_low_ext(ep, r % pre, ep.axis) : 0.0;
+      }
+      const int c = col0 + wn * C::WTN + lane;
+      w_collam[lane] = c < m ? ep.lam[ep.axis][c] : 0.0;
+      __syncwarp();
+    }
     double acc[C::RT][C::CT][2];
 #pragma unroll
     for (int i = 0; i < C::RT; ++i)
@@ -424,33 +456,76 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 
     // --------------------------------------------------------------------- epilogue --
+    if (EK == EK_DIV) {
+      // lambda = (lo + L_axis[i]) in axis order (direct_sum_grid), true division by
+      // (lambda - shift) (operators.cpp:56-57): a row's 2 CT divisions are in flight together
 #pragma unroll
-    for (int j = 0; j < C::RT; ++j) {
-      const long long r = row0 + wm * C::WTM + row_map<BN, LOADER>(j, g);
-      const bool rok = r < R;
-      const long long rr = rok ? r : 0;
-      const long long q = rr / pre;
-      const long long p = rr - q * pre;
-      const long long ybase = p + q * args.ldy;
-      const double lam_lo = spectral ? lambda_partial_low_ext(ep, p, ep.axis) : 0.0;
+      for (int j = 0; j < C::RT; ++j) {
+        const int lr = row_map<BN, LOADER>(j, g);
+        const long long r = row0 + wm * C::WTM + lr;
+        const bool rok = r < R;
+        const long long q = rok ? r / pre : 0;
+        const long long ybase = (rok ? r - q * pre : 0) + q * args.ldy;
+        const double lam_lo = w_rowlam[lr];
+        double qv[C::CT][2], dv[C::CT][2];
+        bool all_ok = true;
 #pragma unroll
-      for (int jc = 0; jc < C::CT; ++jc) {
+        for (int jc = 0; jc < C::CT; ++jc)
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
-          const bool ok = rok && i < m;
-          double val = acc[j][jc][v];
-          const long long yi = ybase + pre * static_cast<long long>(ok ? i : 0);
-          if (spectral) {
-            // PHASE: the re/im partner (row r ^ 1) is this thread's tile j ^ 1 (paired maps)
-            const double other = ep.kind == EPI_SPEC_PHASE ? acc[j ^ 1][jc][v] : 0.0;
-            val = spectral_epilogue_ext(ep, val, other, lam_lo, ep.axis, ok ? i : -1, q, p);
-          } else if (ep.kind == EPI_AXPY_DIAG && ok) {
-            const double uu = ep.u[yi];
-            if (ep.diag) val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (yi >> 1) : yi], uu));
-            if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+          for (int v = 0; v < 2; ++v) {
+            const int lc = col_map<BN, LOADER>(jc, 2 * t + v);
+            dv[jc][v] = __dsub_rn(__dadd_rn(lam_lo, w_collam[lc]), ep.shift);
+            bool ok;
+            qv[jc][v] = div_rn_fast(acc[j][jc][v], dv[jc][v], ok);
+            all_ok = all_ok && ok;
           }
-          if (ok) args.y[yi] = val;
+        if (!all_ok) {
+#pragma unroll
+          for (int jc = 0; jc < C::CT; ++jc)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) qv[jc][v] = __ddiv_rn(acc[j][jc][v], dv[jc][v]);
+        }
+#pragma unroll
+        for (int jc = 0; jc < C::CT; ++jc)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
+            if (rok && i < m) args.y[ybase + pre * static_cast<long long>(i)] = qv[jc][v];
+          }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < C::RT; ++j) {
+        const long long r = row0 + wm * C::WTM + row_map<BN, LOADER>(j, g);
+        const bool rok = r < R;
+        const long long rr = rok ? r : 0;
+        const long long q = rr / pre;
+        const long long p = rr - q * pre;
+        const long long ybase = p + q * args.ldy;
+        const double lam_lo =
+            (EK == EK_GENERIC && spectral) ? lambda_partial_low_ext(ep, p, ep.axis) : 0.0;
+#pragma unroll
+        for (int jc = 0; jc < C::CT; ++jc) {
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
+            const bool ok = rok && i < m;
+            double val = acc[j][jc][v];
+            const long long yi = ybase + pre * static_cast<long long>(ok ? i : 0);
+            if (EK == EK_GENERIC) {
+              if (spectral) {
+                // PHASE: the re/im partner (row r ^ 1) is this thread's tile j ^ 1 (paired maps)
+                const double other = ep.kind == EPI_SPEC_PHASE ? acc[j ^ 1][jc][v] : 0.0;
+                val = spectral_epilogue_ext(ep, val, other, lam_lo, ep.axis, ok ? i : -1, q, p);
+              } else if (ep.kind == EPI_AXPY_DIAG && ok) {
+                const double uu = ep.u[yi];
+                if (ep.diag)
+                  val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (yi >> 1) : yi], uu));
+                if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+              }
+            }
+            if (ok) args.y[yi] = val;
+          }
         }
       }
     }
@@ -483,11 +558,15 @@ void encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims
 
 template <int BN, int LOADER>
 void set_attr_tma() {
-  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1>,
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, EK_GENERIC>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
-  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 2>,
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, EK_STORE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
-  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 4>,
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, EK_DIV>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 2, EK_GENERIC>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 4, EK_GENERIC>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
 }
 
@@ -507,7 +586,8 @@ int cluster_grid(int num_sms) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, mode_product_tma_kernel<BN, LOADER, CL>, &cfg) !=
+    if (cudaOccupancyMaxActiveClusters(&n, mode_product_tma_kernel<BN, LOADER, CL, EK_GENERIC>,
+                                       &cfg) !=
         cudaSuccess) {
       (void)cudaGetLastError();
       return 0;
@@ -532,7 +612,8 @@ void launch_cl(cudaStream_t s, int blocks, const CUtensorMap& tmx, const CUtenso
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KCUDA(cudaLaunchKernelEx(&cfg, mode_product_tma_kernel<BN, LOADER, CL>, tmx, tmA, ta));
+  KCUDA(cudaLaunchKernelEx(&cfg, mode_product_tma_kernel<BN, LOADER, CL, EK_GENERIC>, tmx, tmA,
+                           ta));
 }
 
 // Cluster size. Default 1: measured on B200 (profiles/r01_tma_cluster_experiment.json), 2-CTA
@@ -564,8 +645,17 @@ void launch_tma(cudaStream_t s, int num_sms, long long ntiles_m, int ntiles_n,
     launch_cl<BN, LOADER, 2>(s, cluster_grid<BN, LOADER, 2>(num_sms), tmx, tmA, ta);
   } else {
     const long long blocks = tiles < num_sms ? tiles : num_sms;  // one CTA per SM
-    mode_product_tma_kernel<BN, LOADER, 1>
-        <<<static_cast<unsigned>(blocks), NTHREADS, Cfg<BN>::SMEM, s>>>(tmx, tmA, ta);
+    const EpiParams& ep = ta.ep;
+    const dim3 grid(static_cast<unsigned>(blocks));
+    if (ep.kind == EPI_STORE)
+      mode_product_tma_kernel<BN, LOADER, 1, EK_STORE><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(
+          tmx, tmA, ta);
+    else if (ep.kind == EPI_SPEC_DIV && ep.axis + 1 == ep.ndims && ep.lam[ep.axis] != nullptr)
+      mode_product_tma_kernel<BN, LOADER, 1, EK_DIV><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(
+          tmx, tmA, ta);
+    else
+      mode_product_tma_kernel<BN, LOADER, 1, EK_GENERIC><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(
+          tmx, tmA, ta);
   }
 }
 

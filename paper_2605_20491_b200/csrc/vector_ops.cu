@@ -13,6 +13,7 @@
 // Elementwise kernels use 16-byte vector loads where the layout allows and a grid of
 // 148 SMs x 8 blocks (persistent grid-stride), which saturates HBM on B200.
 #include "vector_ops.cuh"
+#include "epilogue.cuh"
 
 namespace kronop_dev {
 
@@ -342,6 +343,30 @@ __global__ void k_splitmix(double* out, unsigned long long seed, unsigned long l
 void launch_splitmix(cudaStream_t s, Workspace& ws, double* out, unsigned long long seed,
                      unsigned long long start, long long n) {
   k_splitmix<<<kEltBlocks, kThreads, 0, s>>>(out, seed, start, n);
+  ws.launches += 1;
+  KCUDA(cudaGetLastError());
+}
+
+// Self-test of the batched division fast path used by the TMA divide epilogue: out[i] = 1 where
+// div_rn_fast (with the __ddiv_rn fallback) differs from __ddiv_rn bit for bit, else 0.
+__global__ void k_div_selftest(const double* a, const double* b, unsigned long long* bad,
+                               long long n) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  unsigned long long cnt = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += stride) {
+    bool ok;
+    double q = kronop_dev::div_rn_fast(a[i], b[i], ok);
+    const double ref = __ddiv_rn(a[i], b[i]);
+    if (!ok) q = __ddiv_rn(a[i], b[i]);
+    if (__double_as_longlong(q) != __double_as_longlong(ref)) ++cnt;
+  }
+  if (cnt) atomicAdd(bad, cnt);
+}
+
+void launch_div_selftest(cudaStream_t s, Workspace& ws, const double* a, const double* b,
+                         unsigned long long* bad, long long n) {
+  k_div_selftest<<<kEltBlocks, kThreads, 0, s>>>(a, b, bad, n);
   ws.launches += 1;
   KCUDA(cudaGetLastError());
 }

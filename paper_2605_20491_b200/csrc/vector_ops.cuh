@@ -46,6 +46,8 @@ void launch_phase(cudaStream_t s, Workspace& ws, double* psi, const double* b, d
                   long long n);
 void launch_generate(cudaStream_t s, Workspace& ws, double* out, const IndexGeomHost& g,
                      const double* const* vecs, int mode);
+void launch_div_selftest(cudaStream_t s, Workspace& ws, const double* a, const double* b,
+                         unsigned long long* bad, long long n);
 void launch_splitmix(cudaStream_t s, Workspace& ws, double* out, unsigned long long seed,
                      unsigned long long start, long long n);
 void launch_axpby(cudaStream_t s, Workspace& ws, double* y, const double* x, double a, double b,
