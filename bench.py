@@ -7,11 +7,13 @@ L = 8 (n = 1024), harmonic V1 = x^2 per axis, rhs = SplitMix64(seed = 1) uniform
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kronop|reference] [--n 1024]
 
---impl reference times the reference algorithm's CPU implementation (the numpy oracle port: the
-C++ reference cannot be built here) on the host cores, on a bounded sample.
-Multi-GPU (torchrun, one rank per GPU, NCCL): the same 1024^3 solve is slab-decomposed over the N
-ranks (paper_2605_20491_b200/slab.py): axes 0-1 local, two all-to-all transposes for
-the last axis; total work fixed => "scaling": "strong"; time = max over ranks of CUDA-event time.
+--impl reference times the reference's CPU path on the host cores at the same 1024^3 workload (no
+scaling): the C++ -O3 -fopenmp restatement of tensor.cpp / operators.cpp in oracle/cpu (the
+reference itself cannot be built here, Eigen3 is absent), one full solve per step.
+Multi-GPU (--gpus N self-launches torch.distributed.run; one rank per GPU): the same solve is
+slab-decomposed through the C-ABI (kronop_slab_create_nccl, csrc/slab.cu): axes 0-1
+local, two NCCL all-to-all transposes for the last axis; total work fixed => "scaling": "strong";
+time = max over ranks of CUDA-event time. --n 2048 selects the 2048^3 scaling grid (Q3 x 683).
 """
 import argparse
 import json
@@ -121,9 +123,17 @@ def max_over_ranks(world, v, device):
 
 
 def workload_config(n):
-    cells = (n + 1) // 5
-    assert cells * 5 - 1 == n, "n must be 5*cells - 1 ... use n = 1024 (205 cells)"
-    return cells
+    """SEM cells of the workload family at extent n = cells * degree - 1 (basis1d.cpp:23,55):
+    Q5 for the BASELINE 1024^3 config (205 cells), Q3 for the 2048^3 scaling grid (683 cells,
+    SURVEY.md §8a C4)."""
+    for k in (5, 3):
+        if (n + 1) % k == 0:
+            return (n + 1) // k
+    raise SystemExit("n must be 5*cells - 1 or 3*cells - 1 (1024 = Q5 x 205, 2048 = Q3 x 683)")
+
+
+def workload_degree(n):
+    return 5 if (n + 1) % 5 == 0 else 3
 
 
 # -------------------------------------------------------------------------- CPU arm --
@@ -145,7 +155,7 @@ def cpu_reference_operator(n):
     the oracle's axis factorisation (numpy build_axis; harmonic V1, so the three axes are equal)."""
     from oracle import kronop_oracle as K
     from oracle import kronop_cpu as KC
-    ax = K.build_axis(K.assemble_sem(8.0, workload_config(n), 5), lambda t: t * t)
+    ax = K.build_axis(K.assemble_sem(8.0, workload_config(n), workload_degree(n)), lambda t: t * t)
     return KC, KC.CpuOperator([ax] * 3)
 
 
@@ -263,23 +273,30 @@ def secondary_metrics(A, P, ctx, device):
     box = g.sample(lambda c: np.sin(np.pi * (c[0] + 8.0) / 16.0) * np.sin(np.pi * (c[1] + 8.0) / 16.0)
                    * np.sin(np.pi * (c[2] + 8.0) / 16.0))
     psi0 = torch.from_numpy(box.astype(np.complex128)).to("cuda:%d" % device)
-    spec = A.SplitSpec(quad_points=1, composition="single", dt=5e-3, total_time=0.1,
+    spec = A.SplitSpec(quad_points=1, composition="single", dt=1e-3, total_time=0.1,
                        merge_across_steps=True)
-    A.evolve(A.SplitSpec(quad_points=1, dt=5e-3, total_time=1e-2, merge_across_steps=True), lap,
+    A.evolve(A.SplitSpec(quad_points=1, dt=1e-3, total_time=5e-3, merge_across_steps=True), lap,
              bdiag, psi0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     state, err, steps = A.evolve(spec, lap, bdiag, psi0)
     torch.cuda.synchronize()
     t = time.perf_counter() - t0
+    # error against the exact propagator of the full separable H (splitting.cpp:127-141), untimed
+    full = g.separable_operator(ctx, pot.separable)
+    psi0n = psi0 / torch.linalg.norm(psi0)
+    split_err = float(torch.linalg.norm(state - full.propagate(psi0n, 0.1)))
+    del full, psi0n
     out["splitstep_steps_per_s"] = {
         "value": steps / t, "unit": "steps/s", "steps": steps, "seconds": t, "n": g.shape[0],
+        "error_vs_exact": split_err, "paper_error": 5.21e-5,
         "config": "Strang (qHOP M=1) with cross-step merge, 499^3 complex128 (SEM Q5 x 100 cells, "
-                  "L=8), A=-Delta, B=sep-osc V, box psi0, dt=5e-3, T=0.1 (PAPER.md:1381 setup)"}
+                  "L=8), A=-Delta, B=sep-osc V, box psi0, dt=1e-3, T=0.1: the PAPER.md:1378-1381 "
+                  "row (M=1, dt=0.001: error 5.21e-5, 100 steps in 9.5 s on GH200)"}
     # the same run with the even/odd folded kinetic operator (-Delta on the symmetric SEM grid
     # commutes with x -> -x per axis): half the transform flops, same state to ~1e-12
     lapf = g.laplacian(ctx, folded=True)
-    A.evolve(A.SplitSpec(quad_points=1, dt=5e-3, total_time=1e-2, merge_across_steps=True), lapf,
+    A.evolve(A.SplitSpec(quad_points=1, dt=1e-3, total_time=5e-3, merge_across_steps=True), lapf,
              bdiag, psi0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -293,7 +310,7 @@ def secondary_metrics(A, P, ctx, device):
                   "(kronop_op_create_folded)"}
     try:  # variant: the dense kinetic operator on the INT8 path (kronop_op_set_precision)
         lap.set_precision("ozaki")
-        A.evolve(A.SplitSpec(quad_points=1, dt=5e-3, total_time=1e-2, merge_across_steps=True),
+        A.evolve(A.SplitSpec(quad_points=1, dt=1e-3, total_time=5e-3, merge_across_steps=True),
                  lap, bdiag, psi0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -301,7 +318,7 @@ def secondary_metrics(A, P, ctx, device):
         torch.cuda.synchronize()
         to = time.perf_counter() - t0
         lapf.set_precision("ozaki")
-        A.evolve(A.SplitSpec(quad_points=1, dt=5e-3, total_time=1e-2, merge_across_steps=True),
+        A.evolve(A.SplitSpec(quad_points=1, dt=1e-3, total_time=5e-3, merge_across_steps=True),
                  lapf, bdiag, psi0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -590,7 +607,7 @@ def run_kronop(args):
     peaks = load_peaks()
     n = args.n
     cells = workload_config(n)
-    grid = A.Grid.sem(8.0, cells, 5, 3)
+    grid = A.Grid.sem(8.0, cells, workload_degree(n), 3)
     pot = P.build_potential("harmonic", grid)
     ctx = A.Context(local)
     op = grid.separable_operator(ctx, pot.separable)
@@ -715,28 +732,34 @@ def run_kronop(args):
 
 
 def run_kronop_slab(args):
-    """N > 1: slab-decomposed solve of the 1024^3 workload (strong scaling)."""
+    """N > 1 (one process per GPU, launched by torch.distributed.run): the same solve,
+    slab-decomposed through the C-ABI (kronop_slab_create_nccl, csrc/slab.cu): axes 0-1 local,
+    two NCCL all-to-all transposes (grouped send / recv per plane) for the last axis. Total work
+    fixed => "scaling": "strong"; time = max over ranks of the CUDA-event time on the rank's
+    stream. --n 2048 runs the 2048^3 scaling grid (Q3 x 683 cells, 64 GiB per field)."""
     import torch
     import torch.distributed as dist
     world, rank, local = dist_init()
     torch.cuda.set_device(local)
     from paper_2605_20491_b200 import api as A
-    from paper_2605_20491_b200 import potentials as P
     from paper_2605_20491_b200 import slab as S
     peaks = load_peaks()
     n = args.n
-    grid = A.Grid.sem(8.0, workload_config(n), 5, 3)
-    pot = P.build_potential("harmonic", grid)
-    axes = [A.build_axis(grid.axes[a], fvals=np.array([pot.separable[a](float(x))
-                                                         for x in grid.axes[a].nodes]))
-            for a in range(3)]
+    grid = A.Grid.sem(8.0, workload_config(n), workload_degree(n), 3)
+    ax = A.build_axis(grid.axes[0], fvals=np.array([float(x) * float(x)
+                                                     for x in grid.axes[0].nodes]))
     ctx = A.Context(local)
-    op = S.SlabOperator(axes, S.KronopPassBackend(ctx), shift=0.0)
+    uid = [S.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    so = S.DeviceSlabOperator([ax] * 3, ctx=ctx, rank=rank, nranks=world, unique_id=uid[0])
+    pt = so.parts[0]
     plane = n * n
-    z0 = op.z0[rank]
-    b = A.splitmix_uniform(ctx, 1, op.local_size(), start=z0 * plane)
+    b = [A.splitmix_uniform(ctx, 1, pt["elems"], start=pt["z0"] * plane)]
+    x = [torch.empty_like(b[0])]
+    stream = pt["stream"]
     for _ in range(args.warmup):
-        x = op.solve(b)
+        so.solve(b, out=x)
     torch.cuda.synchronize()
     launches0 = ctx.launch_count()
     sampler = ClockSampler(local)
@@ -744,10 +767,10 @@ def run_kronop_slab(args):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
+    e0.record(stream)
     for _ in range(args.steps):
-        x = op.solve(b)
-    e1.record()
+        so.solve(b, out=x)
+    e1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     clocks = sampler.stop()
@@ -756,45 +779,60 @@ def run_kronop_slab(args):
     N = n ** 3
     value = N / t_step / 1e9
     # end to end: this rank's slab from pinned host memory, solve, back to pinned host memory
-    bh = torch.empty(op.local_size(), dtype=torch.float64, pin_memory=True)
-    bh.copy_(b.cpu())
-    xh = torch.empty(op.local_size(), dtype=torch.float64, pin_memory=True)
+    bh = torch.empty(pt["elems"], dtype=torch.float64, pin_memory=True)
+    bh.copy_(b[0].cpu())
+    xh = torch.empty(pt["elems"], dtype=torch.float64, pin_memory=True)
+    k = max(1, min(args.steps, 3))
     barrier(world)
     t0 = time.perf_counter()
-    for _ in range(max(1, min(args.steps, 3))):
-        xd = op.solve(bh.to("cuda:%d" % local, non_blocking=True))
-        xh.copy_(xd, non_blocking=True)
+    for _ in range(k):
+        bd = [bh.to("cuda:%d" % local, non_blocking=True)]
+        xd = so.solve(bd)
+        xh.copy_(xd[0], non_blocking=True)
         torch.cuda.synchronize()
-    t_e2e = max_over_ranks(world, (time.perf_counter() - t0) / max(1, min(args.steps, 3)),
-                           "cuda:%d" % local)
+    t_e2e = max_over_ranks(world, (time.perf_counter() - t0) / k, "cuda:%d" % local)
+    tfl = 12.0 * n ** 4 / t_step / 1e12
     if rank == 0:
         line = {
             "metric": "(-Delta+V1)^-1 apply GDoF/s at 1024^3 fp64",
             "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "3D (-Delta+V1)^-1 solve, harmonic V1, SEM Q5 205 cells L=8, "
-                                   "n=%d, slab-decomposed over %d GPUs (2 all-to-all per solve)"
-                                   % (n, world),
+            "config": {"workload": "3D (-Delta+V1)^-1 solve, harmonic V1, SEM Q%d %d cells L=8, "
+                                   "n=%d, slab-decomposed over %d GPUs through kronop_slab_* "
+                                   "(NCCL, 2 all-to-all per solve)"
+                                   % (workload_degree(n), workload_config(n), n, world),
                        "n": n, "dof": N, "parallelism": "slab%d" % world,
                        "l2": "inputs larger than L2; no flush"},
-            "tflops": 12.0 * n ** 4 / t_step / 1e12,
-            "roofline": {"bound": "tensor", "achieved": 12.0 * n ** 4 / t_step / 1e12 / world,
-                         "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                         "frac": 12.0 * n ** 4 / t_step / 1e12 / world / peaks["fp64_tflops"],
+            "tflops": tfl,
+            "roofline": {"bound": "tensor", "achieved": tfl / world, "peak": peaks["fp64_tflops"],
+                         "unit": "TFLOP/s", "frac": tfl / world / peaks["fp64_tflops"],
                          "traffic": None, "note": "per-GPU FLOP rate of the whole slab solve "
                                                   "(transposes included)"},
             "e2e": {"value": N / t_e2e / 1e9, "unit": "GDoF/s",
-                    "h2d_bytes_per_step": 8 * op.local_size(),
-                    "d2h_bytes_per_step": 8 * op.local_size(), "ms_per_step": t_e2e * 1e3},
+                    "h2d_bytes_per_step": 8 * pt["elems"], "d2h_bytes_per_step": 8 * pt["elems"],
+                    "ms_per_step": t_e2e * 1e3, "per_rank_bytes": True},
             "gpu_launches": int(launches),
             "clocks": clocks,
             "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
+    so.close()
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
+
+
+def self_launch(args):
+    """`bench.py --gpus N` without a launcher: re-run under torch.distributed.run with N ranks."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -808,6 +846,8 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--slab", action="store_true", help="force the slab-decomposed path (any N)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.slab:

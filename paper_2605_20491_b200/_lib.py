@@ -136,6 +136,23 @@ PROTOTYPES = {
     "kronop_host_build_sem_axis_folded": (I, [D, I, I] + [DP] * 8),
     "kronop_splitmix_uniform": (I, [P, C.c_uint64, C.c_uint64, C.c_size_t, P]),
     "kronop_selftest_division": (I, [P, P, P, C.c_size_t, P]),
+    "kronop_slab_plan": (I, [I, I, IP, IP]),
+    "kronop_nccl_load": (I, [C.c_char_p]),
+    "kronop_nccl_unique_id": (I, [C.c_char_p]),
+    "kronop_slab_create": (I, [I, IP, I, IP, P, P, P, P, D, P]),
+    "kronop_slab_create_nccl": (I, [P, C.c_char_p, I, I, I, IP, P, P, P, P, D, P]),
+    "kronop_slab_destroy": (I, [P]),
+    "kronop_slab_info": (I, [P, IP, IP, IP]),
+    "kronop_slab_part": (I, [P, I, IP, C.POINTER(C.c_void_p), C.POINTER(C.c_longlong),
+                             C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+    "kronop_slab_set_shift": (I, [P, D]),
+    "kronop_slab_synchronize": (I, [P]),
+    "kronop_slab_apply": (I, [P, P, I, P, D, P]),
+    "kronop_slab_solve": (I, [P, P, I, P]),
+    "kronop_slab_propagate": (I, [P, P, D, P]),
+    "kronop_slab_dot": (I, [P, P, P, I, DP]),
+    "kronop_slab_pcg": (I, [P, P, D, P, P, C.POINTER(PcgConfig), C.POINTER(PcgReport), DP]),
+    "kronop_slab_gpe_au": (I, [P, P, D, C.POINTER(GpeConfig), P, P, C.POINTER(GpeResult), DP]),
 }
 
 _lib = None

@@ -119,7 +119,7 @@ void run_pass(kronop_ctx& ctx, const double* x, double* y, View& v, int raxis, c
   v.ext[raxis] = m;
 }
 
-// Small-extent path: consecutive axes fused per HBM round trip (fused_small.cu).
+// Small-extent path: consecutive axes fused per HBM round trip (fused_rot.cu).
 static bool use_fused_small(const kronop_op& op) {
   static const bool disabled = [] {
     const char* e = getenv("KRONOP_DISABLE_FUSED_SMALL");  // A/B switch for profiling
@@ -129,63 +129,6 @@ static bool use_fused_small(const kronop_op& op) {
   for (int a = 0; a < op.d; ++a)
     if (op.n[a] > 32) return false;
   return true;
-}
-
-static void sep_transform_fused_small(kronop_ctx& ctx, const kronop_op& op, const double* in,
-                                      double* out, int cplx, SepKind kind, double shift, double dt,
-                                      const double* diag, double sigma) {
-  View v = make_view(op.d, op.n, cplx);
-  ensure_scratch(ctx, static_cast<size_t>(v.total()));
-  // groups of consecutive spatial axes: up to 3 axes, fused extent <= 1024
-  std::vector<std::pair<int, int>> groups;  // (first spatial axis, count)
-  for (int a = 0; a < op.d;) {
-    int f = 1, F = op.n[a];
-    // three-axis groups only for extents <= 12 (the kernels' K/N instantiations for f = 3)
-    while (a + f < op.d && F * op.n[a + f] <= 1024 &&
-           (f < 2 || (f == 2 && op.n[a] <= 12 && op.n[a + 1] <= 12 && op.n[a + 2] <= 12)))
-      F *= op.n[a + f++];
-    groups.emplace_back(a, f);
-    a += f;
-  }
-  EpiParams spec;
-  spec.kind = kind == SEP_APPLY ? EPI_SPEC_MUL : kind == SEP_SOLVE ? EPI_SPEC_DIV : EPI_SPEC_PHASE;
-  spec.ndims = v.nd;
-  for (int i = 0; i < v.nd; ++i) spec.ext[i] = v.ext[i];
-  for (int a = 0; a < op.d; ++a) spec.lam[a + v.cplx] = op.lam[a];
-  spec.shift = shift;
-  spec.dt = dt;
-  spec.cplx = v.cplx;
-  double* w = ctx.scratch[0];
-  const int ng = static_cast<int>(groups.size());
-  for (int dir = 0; dir < 2; ++dir) {
-    for (int g = 0; g < ng; ++g) {
-      const int a0 = groups[g].first, f = groups[g].second;
-      const double* mats[3];
-      int lda[3];
-      for (int j = 0; j < f; ++j) {
-        mats[j] = dir == 0 ? op.fwd[a0 + j] : op.bwd[a0 + j];
-        lda[j] = op.lda[a0 + j];
-      }
-      const bool last = g == ng - 1;
-      const double* src = (dir == 0 && g == 0) ? in : w;
-      double* dst = (dir == 1 && last) ? out : w;
-      EpiParams ep;
-      bool spectral = false;
-      if (dir == 0 && last) {
-        ep = spec;
-        spectral = true;
-      } else if (dir == 1 && last && (diag != nullptr || sigma != 0.0)) {
-        ep.kind = EPI_AXPY_DIAG;
-        ep.diag = diag;
-        ep.u = in;
-        ep.sigma = sigma;
-        ep.cplx = v.cplx;
-      }
-      launch_fused_small(ctx.stream, src, dst, v.nd, v.ext, a0 + v.cplx, f, mats, lda, ep,
-                         spectral);
-      ctx.ws.launches += 1;
-    }
-  }
 }
 
 // Even/odd folded operator (kronop_op_create_folded): per axis, fold into [u | v] halves, two
@@ -264,7 +207,7 @@ static void sep_transform_folded(kronop_ctx& ctx, const kronop_op& op, const dou
 // end, so after each direction the layout is the caller's again.
 static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out,
                               int cplx, SepKind kind, double shift, double dt, const double* diag,
-                              double sigma) {
+                              double sigma, bool bphase, const double* bfield, double bfactor) {
   const size_t nd = static_cast<size_t>(op.N) * (cplx ? 2 : 1);
   ensure_scratch(ctx, nd);
   std::vector<std::pair<int, int>> groups;
@@ -313,6 +256,10 @@ static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double
         e.diag = diag;
         e.u = in;
         e.sigma = sigma;
+      } else if (last && bphase) {
+        e.kind = EPI_BPHASE;
+        e.diag = bfield;
+        e.dt = bfactor;
       }
       ctx.ws.launches += launch_fused_rot(ctx.stream, src, dst, cplx, f, n, op.N, mats, lda, e);
       src = dst;
@@ -320,7 +267,15 @@ static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double
 }
 
 void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
-                   SepKind kind, double shift, double dt, const double* diag, double sigma) {
+                   SepKind kind, double shift, double dt, const double* diag, double sigma,
+                   bool bphase, const double* bfield, double bfactor) {
+  param_check(!bphase || (kind == SEP_PROPAGATE && cplx), "B phase: complex propagate only");
+  if (bphase && (op.folded || op.exec_prec >= KRONOP_PREC_FP64_OZAKI)) {
+    // paths without the fused epilogue: the phase as its own pass (k_phase)
+    sep_transform(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
+    launch_phase(ctx.stream, ctx.ws, out, bfield, bfactor, op.N);
+    return;
+  }
   if (op.exec_prec >= KRONOP_PREC_FP64_OZAKI && (kind != SEP_PROPAGATE || cplx)) {
     // kronop_op_set_precision: every transform of this operator on the INT8 path (ozaki.cu)
     const int epi = kind == SEP_SOLVE ? 1 : kind == SEP_APPLY ? 2 : 3;
@@ -333,14 +288,8 @@ void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, doubl
     return;
   }
   if (use_fused_small(op)) {
-    static const bool legacy = [] {
-      const char* e = getenv("KRONOP_FUSED_SMALL_LEGACY");  // A/B switch: in-place tiles
-      return e && e[0] == '1';
-    }();
-    if (legacy)
-      sep_transform_fused_small(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
-    else
-      sep_transform_rot(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma);
+    sep_transform_rot(ctx, op, in, out, cplx, kind, shift, dt, diag, sigma, bphase, bfield,
+                      bfactor);
     return;
   }
   View v = make_view(op.d, op.n, cplx);
@@ -367,6 +316,11 @@ void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, doubl
       ep.diag = diag;
       ep.u = in;
       ep.sigma = sigma;
+      ep.cplx = v.cplx;
+    } else if (k == 2 * d - 1 && bphase) {
+      ep.kind = EPI_BPHASE;
+      ep.diag = bfield;
+      ep.dt = bfactor;
       ep.cplx = v.cplx;
     }
     run_pass(ctx, cur, dst, v, axis + v.cplx, forward ? op.fwd[axis] : op.bwd[axis], op.lda[axis],
@@ -538,7 +492,6 @@ int kronop_ctx_create(int device, void* stream, kronop_ctx** out) {
       KCUDA(cudaMallocHost(&c->hscal, kScalarSlots * sizeof(double)));
       prime_mode_product_kernels();
       prime_mode_product_tma_kernels();
-      prime_fused_small_kernels();
       prime_fused_rot_kernels();
     } catch (...) {
       delete c;
@@ -1036,7 +989,9 @@ static void host_roundtrip(kronop_ctx* ctx, const kronop_op* op, const double* i
   if (kind == SEP_SOLVE) check_solve_shift(*ctx, *op, op->shift);
   const int d = op->d;
   const int nz = op->n[d - 1];
-  if (d < 2 || nz < 2 || op->folded) {
+  // the pipelined path below runs the FP64 DMMA passes itself; operators switched to another
+  // execution precision (kronop_op_set_precision) or folded ones take their own transform
+  if (d < 2 || nz < 2 || op->folded || op->exec_prec != KRONOP_PREC_FP64) {
     KCUDA(cudaMemcpyAsync(ctx->io[0], in_host, nd * sizeof(double), cudaMemcpyHostToDevice,
                           ctx->stream));
     sep_transform(*ctx, *op, ctx->io[0], ctx->io[1], cplx, kind, op->shift, dt, nullptr, 0.0);

@@ -2,6 +2,7 @@
 // by the C-ABI entry points (capi.cu) and the device-resident drivers (drivers.cu).
 #pragma once
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -91,6 +92,21 @@ double* pool_get(kronop_ctx& ctx, size_t n);
 void pool_put(kronop_ctx& ctx, double* p);
 void pool_trim(kronop_ctx& ctx);  // cudaFree every idle block
 
+// RAII device buffer from the context's block pool (pool_get / pool_put, capi.cu): drivers that
+// are called repeatedly (PCG, inverse iteration, GPE, evolve) reuse their vectors instead of a
+// cudaMalloc / cudaFree pair (which synchronises the device) per call.
+struct DBuf {
+  kronop_ctx* c = nullptr;
+  double* p = nullptr;
+  DBuf() = default;
+  DBuf(kronop_ctx& ctx, size_t n) : c(&ctx), p(pool_get(ctx, std::max<size_t>(n, 1))) {}
+  ~DBuf() {
+    if (p) pool_put(*c, p);
+  }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+};
+
 
 // Real view of a field: an optional leading re/im axis of extent 2, then the spatial axes.
 struct View {
@@ -115,12 +131,27 @@ void run_pass(kronop_ctx& ctx, const double* x, double* y, View& v, int raxis, c
 enum SepKind { SEP_APPLY = 0, SEP_SOLVE = 1, SEP_PROPAGATE = 2 };
 // out = T (f(lambda - shift) . (T^{-1} in)) [+ diag .* in - sigma in], f = x, / or exp(-i . dt).
 // in may alias out. Uses ctx.scratch.
+// bphase: complex propagate only -- the split-step B phase psi * exp(-i bfactor B) (B = bfield,
+// NULL = 1) applied to the result, fused into the last pass where the path allows.
 void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
-                   SepKind kind, double shift, double dt, const double* diag, double sigma);
+                   SepKind kind, double shift, double dt, const double* diag, double sigma,
+                   bool bphase = false, const double* bfield = nullptr, double bfactor = 0.0);
 // Singular-shift guard of SeparableOperator::solve (operators.cpp:44-52).
 void check_solve_shift(kronop_ctx& ctx, const kronop_op& op, double shift);
 
 IndexGeomHost mass_geom(const kronop_op& op);
+
+// driver kernels (drivers.cu) for the host-enqueued slab drivers (slab.cu)
+void launch_pcg_init(cudaStream_t s, Workspace& ws, PcgScalars* sc, const double* rz,
+                     const double* rr, double norm_b, double* history);
+void launch_pcg_alpha(cudaStream_t s, Workspace& ws, PcgScalars* sc);
+void launch_pcg_beta(cudaStream_t s, Workspace& ws, PcgScalars* sc);
+void launch_pcg_finish(cudaStream_t s, Workspace& ws, PcgScalars* sc, double* history);
+void launch_beta_square(cudaStream_t s, Workspace& ws, double* dg, const double* u, double beta,
+                        const double* v2, long long n);
+void launch_sub_scaled(cudaStream_t s, Workspace& ws, double* g, const double* a, const double* b,
+                       double c, long long n);
+void launch_square2(cudaStream_t s, Workspace& ws, double* sq, const double* u, long long n);
 void set_error(const std::string& msg);
 
 }  // namespace kronop_dev

@@ -14,6 +14,7 @@
 #include <chrono>
 #include <memory>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -37,21 +38,6 @@ int guard2(F&& f) {
     return KRONOP_ERUNTIME;
   }
 }
-
-// RAII device buffer from the context's block pool (pool_get / pool_put, capi.cu): drivers that
-// are called repeatedly (PCG, inverse iteration, GPE, evolve) reuse their vectors instead of a
-// cudaMalloc / cudaFree pair (which synchronises the device) per call.
-struct DBuf {
-  kronop_ctx* c = nullptr;
-  double* p = nullptr;
-  DBuf() = default;
-  DBuf(kronop_ctx& ctx, size_t n) : c(&ctx), p(pool_get(ctx, std::max<size_t>(n, 1))) {}
-  ~DBuf() {
-    if (p) pool_put(*c, p);
-  }
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-};
 
 // ------------------------------------------------------------------------ linear maps --
 static void apply_map(kronop_ctx& ctx, const kronop_linear_map& m, const double* in, double* out,
@@ -116,30 +102,61 @@ __global__ void k_pcg_beta(PcgScalars* sc) {  // pcg.cpp:60
   sc->beta = sc->rz_next / sc->rz;
 }
 
-__global__ void k_pcg_finish(PcgScalars* sc, double* history, cudaGraphConditionalHandle h) {
-  if (sc->active) {  // pcg.cpp:61-71
-    sc->rz = sc->rz_next;
-    sc->iterations += 1;
-    sc->rel = sc->preconditioned_norm ? sqrt(fabs(sc->rz)) / sc->pnorm0 : sqrt(sc->rr) / sc->norm_b;
-    if (sc->record_history) history[sc->history_len] = sc->rel;
-    sc->history_len += 1;
-    if (sc->rel < 0.99 * sc->best_rel) {
-      sc->best_rel = sc->rel;
-      sc->since = 0;
-      sc->improved = 1;
-    } else {
-      sc->since += 1;
-    }
-    // loop-top tests of the next iteration (pcg.cpp:45-50)
-    if (sc->rel <= sc->rel_tol) {
-      sc->converged = 1;
-      sc->active = 0;
-    } else if (sc->iterations >= sc->max_iter ||
-               (sc->stagnation_window > 0 && sc->since >= sc->stagnation_window)) {
-      sc->active = 0;
-    }
+// pcg.cpp:61-71 and the loop-top tests of the next iteration (pcg.cpp:45-50)
+__device__ void pcg_finish_body(PcgScalars* sc, double* history) {
+  if (!sc->active) return;
+  sc->rz = sc->rz_next;
+  sc->iterations += 1;
+  sc->rel = sc->preconditioned_norm ? sqrt(fabs(sc->rz)) / sc->pnorm0 : sqrt(sc->rr) / sc->norm_b;
+  if (sc->record_history) history[sc->history_len] = sc->rel;
+  sc->history_len += 1;
+  if (sc->rel < 0.99 * sc->best_rel) {
+    sc->best_rel = sc->rel;
+    sc->since = 0;
+    sc->improved = 1;
+  } else {
+    sc->since += 1;
   }
+  if (sc->rel <= sc->rel_tol) {
+    sc->converged = 1;
+    sc->active = 0;
+  } else if (sc->iterations >= sc->max_iter ||
+             (sc->stagnation_window > 0 && sc->since >= sc->stagnation_window)) {
+    sc->active = 0;
+  }
+}
+
+__global__ void k_pcg_finish(PcgScalars* sc, double* history, cudaGraphConditionalHandle h) {
+  pcg_finish_body(sc, history);
   cudaGraphSetConditional(h, sc->active ? 1u : 0u);
+}
+
+__global__ void k_pcg_finish_plain(PcgScalars* sc, double* history) {
+  pcg_finish_body(sc, history);
+}
+
+// Launchers of the PCG scalar / GPE kernels for the host-enqueued drivers of other translation
+// units (the slab-decomposed drivers, slab.cu).
+void launch_pcg_init(cudaStream_t s, Workspace& ws, PcgScalars* sc, const double* rz,
+                     const double* rr, double norm_b, double* history) {
+  k_pcg_init<<<1, 1, 0, s>>>(sc, rz, rr, norm_b, history);
+  KCUDA(cudaGetLastError());
+  ws.launches += 1;
+}
+void launch_pcg_alpha(cudaStream_t s, Workspace& ws, PcgScalars* sc) {
+  k_pcg_alpha<<<1, 1, 0, s>>>(sc);
+  KCUDA(cudaGetLastError());
+  ws.launches += 1;
+}
+void launch_pcg_beta(cudaStream_t s, Workspace& ws, PcgScalars* sc) {
+  k_pcg_beta<<<1, 1, 0, s>>>(sc);
+  KCUDA(cudaGetLastError());
+  ws.launches += 1;
+}
+void launch_pcg_finish(cudaStream_t s, Workspace& ws, PcgScalars* sc, double* history) {
+  k_pcg_finish_plain<<<1, 1, 0, s>>>(sc, history);
+  KCUDA(cudaGetLastError());
+  ws.launches += 1;
 }
 
 struct PcgWork {
@@ -489,6 +506,24 @@ static double gpe_energy_dev(kronop_ctx& c, const kronop_op& h, const double* di
   return 0.5 * quad + 0.25 * beta * quartic;
 }
 
+void launch_beta_square(cudaStream_t s, Workspace& ws, double* dg, const double* u, double beta,
+                        const double* v2, long long n) {
+  k_beta_square<<<kEltBlocks, 256, 0, s>>>(dg, u, beta, v2, n);
+  KCUDA(cudaGetLastError());
+  ws.launches += 1;
+}
+void launch_sub_scaled(cudaStream_t s, Workspace& ws, double* g, const double* a, const double* b,
+                       double c, long long n) {
+  k_sub_scaled<<<kEltBlocks, 256, 0, s>>>(g, a, b, c, n);
+  KCUDA(cudaGetLastError());
+  ws.launches += 1;
+}
+void launch_square2(cudaStream_t s, Workspace& ws, double* sq, const double* u, long long n) {
+  k_square2<<<kEltBlocks, 256, 0, s>>>(sq, u, n);
+  KCUDA(cudaGetLastError());
+  ws.launches += 1;
+}
+
 }  // namespace kronop_dev
 
 extern "C" {
@@ -674,24 +709,35 @@ static std::vector<Schedule> step_schedules(int composition, int m, double h) { 
 static void run_schedules(kronop_ctx& c, const kronop_op& a, const double* b_diag,
                           const std::vector<Schedule>& schedules, double* psi, int steps,
                           bool merge) {
+  // The A-propagation due before a B phase is deferred to it and fused: the phase runs in the
+  // epilogue of the propagate's last pass (EPI_BPHASE), saving a field round trip per B step.
+  // The operations and their order are those of splitting.cpp:53-82 (merge: A-times accumulate
+  // and flush before each B or at the end; no merge: each A-time is flushed on its own).
+  static const bool unfused = [] {
+    const char* e = getenv("KRONOP_BPHASE_FUSED");  // A/B switch: 0 = B phase as its own pass
+    return e && e[0] == '0';
+  }();
   double pending = 0.0;
-  auto propagate = [&](double t) {
-    if (t == 0.0) return;  // propagate(psi, 0) is a copy (operators.cpp:64)
-    sep_transform(c, a, psi, psi, 1, SEP_PROPAGATE, a.shift, t, nullptr, 0.0);
+  bool has_pending = false;
+  auto flush = [&](bool with_b, double factor) {
+    const double t = pending;
+    const bool prop = has_pending && t != 0.0;  // propagate(psi, 0) is a copy (operators.cpp:64)
+    pending = 0.0;
+    has_pending = false;
+    if (prop && with_b && !unfused) {
+      sep_transform(c, a, psi, psi, 1, SEP_PROPAGATE, a.shift, t, nullptr, 0.0, true, b_diag,
+                    factor);
+      return;
+    }
+    if (prop) sep_transform(c, a, psi, psi, 1, SEP_PROPAGATE, a.shift, t, nullptr, 0.0);
+    if (with_b) launch_phase(c.stream, c.ws, psi, b_diag, factor, a.N);
   };
   auto propagate_a = [&](double t) {
-    if (merge)
-      pending += t;
-    else
-      propagate(t);
+    if (!merge && has_pending) flush(false, 0.0);
+    pending += t;
+    has_pending = true;
   };
-  auto multiply_b = [&](double factor) {
-    if (merge && pending != 0.0) {
-      propagate(pending);
-      pending = 0.0;
-    }
-    launch_phase(c.stream, c.ws, psi, b_diag, factor, a.N);
-  };
+  auto multiply_b = [&](double factor) { flush(true, factor); };
   for (int step = 0; step < steps; ++step)
     for (const Schedule& s : schedules) {
       const int m = static_cast<int>(s.b_factors.size());
@@ -701,7 +747,7 @@ static void run_schedules(kronop_ctx& c, const kronop_op& a, const double* b_dia
       }
       propagate_a(s.a_times[m]);
     }
-  if (merge && pending != 0.0) propagate(pending);
+  flush(false, 0.0);
 }
 
 }  // namespace kronop_dev

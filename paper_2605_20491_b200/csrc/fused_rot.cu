@@ -8,7 +8,7 @@
 // so the next group's axes are again the fastest after c. After all groups the layout is back in
 // the original order (a full rotation), which is why a transform (forward groups, spectral
 // epilogue, backward groups) ends in the caller's layout. What this buys over contracting a group
-// in place (fused_small.cu): every tile a CTA reads is ONE contiguous chunk of the field
+// in place (an earlier design, measured 149 / 64 ms for 6D / 9D, since removed): every tile a CTA reads is ONE contiguous chunk of the field
 // ([Qt q][F][C], moved by a single cp.async.bulk into shared memory), and every tile it writes is
 // F runs of C * Qt contiguous doubles (64 B or more) stored straight from the DMMA accumulators of
 // the group's last axis - no strided 32-byte rows and no second shared-memory pass.
@@ -282,6 +282,13 @@ __device__ __forceinline__ void store_tile(const RotArgs& A, const double* tile,
           v.x = __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
           v.y = __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs));
         }
+      } else if (A.epi == EPI_BPHASE) {  // pointwise_phase (splitting.cpp:44-51), as k_phase
+        const double phase = A.diag ? __dmul_rn(-A.dt, A.diag[gi >> 1]) : -A.dt;
+        double sn, cs;
+        sincos(phase, &sn, &cs);
+        const double re = v.x, im = v.y;
+        v.x = __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
+        v.y = __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs));
       } else if (A.epi == EPI_AXPY_DIAG) {
         const double2 uu = *reinterpret_cast<const double2*>(A.u + gi);
         if (A.diag) {
@@ -441,15 +448,9 @@ constexpr size_t rot_smem_bytes() {
 
 template <int NF, int K4, int NT, int DN = 0>
 void launch_rot(cudaStream_t s, const RotArgs& a) {
-  static int grid_cap = [] {
-    KCUDA(cudaFuncSetAttribute(fused_rot_kernel<NF, K4, NT, DN>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(rot_smem_bytes<NF, K4, NT, DN>())));
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms;
-  }();
+  ensure_smem_attr(reinterpret_cast<const void*>(fused_rot_kernel<NF, K4, NT, DN>),
+                   rot_smem_bytes<NF, K4, NT, DN>());
+  const int grid_cap = device_sm_count();
   const long long grid = a.ntiles < grid_cap ? a.ntiles : grid_cap;
   fused_rot_kernel<NF, K4, NT, DN>
       <<<static_cast<unsigned>(grid), rt_threads<DN>(), rot_smem_bytes<NF, K4, NT, DN>(), s>>>(a);

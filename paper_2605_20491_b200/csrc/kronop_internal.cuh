@@ -6,6 +6,8 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -33,6 +35,27 @@ inline void param_check(bool ok, const std::string& msg) {
                              __FILE__ + ":" + std::to_string(__LINE__));                   \
   } while (0)
 
+// Opt-in dynamic shared memory is a per-device function attribute: set it once per (kernel,
+// device), so a process with contexts on several GPUs (kronop_slab_create) launches everywhere.
+inline void ensure_smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, std::unordered_map<int, size_t>> done;
+  int dev = 0;
+  KCUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[fn][dev];
+  if (have >= bytes) return;
+  KCUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bytes)));
+  have = bytes;
+}
+inline int device_sm_count() {
+  int dev = 0, v = 148;
+  KCUDA(cudaGetDevice(&dev));
+  KCUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+  return v;
+}
+
 // ------------------------------------------------------------ mode product --
 // One pass of the mode-k product on a field viewed as a real (pre x nk x post) array, axis 0
 // fastest:  Y[p, i, q] = sum_j A[i, j] X[p, j, q]  (proj/src/tensor.cpp:105-134).
@@ -49,6 +72,9 @@ enum EpiKind : int {
   EPI_SPEC_DIV = 2,    // y = acc / (lambda - shift)              operators.cpp:57
   EPI_SPEC_PHASE = 3,  // complex: y = acc * exp(-i (lambda - shift) dt)   operators.cpp:68-71
   EPI_AXPY_DIAG = 4,   // y = (acc + diag .* u) - sigma * u       operators.cpp:102, ground_state.cpp:70-72
+  // complex: y = acc * exp(-i dt B) with B = diag (spatial, NULL = 1), the split-step B phase
+  // (pointwise_phase, splitting.cpp:44-51) fused into the propagate's last backward pass
+  EPI_BPHASE = 5,
 };
 
 constexpr int kMaxDims = 10;  // 9 spatial axes + the complex component axis
@@ -66,6 +92,9 @@ struct EpiParams {
   const double* u = nullptr;     // the operator's input field (same layout as y)
   double sigma = 0.0;
   int cplx = 0;                  // real view has a leading re/im axis
+  // optional device flag (a PcgScalars::active of a host-enqueued driver loop): the pass is
+  // skipped when *active == 0, so speculatively enqueued iterations cost a launch, not a pass
+  const int* active = nullptr;
 };
 
 struct PassShape {
@@ -102,11 +131,6 @@ bool fused_rot_eligible(const double* x);
 int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f, const int* n,
                      long long N, const double* const* mats, const int* lda, const RotEpi& epi);
 
-// Fused small-extent multi-axis transform (fused_small.cu), used when every axis has n <= 32.
-void prime_fused_small_kernels();
-void launch_fused_small(cudaStream_t s, const double* x, double* y, int nd, const long long* ext,
-                        int axis, int f, const double* const* mats, const int* lda,
-                        const EpiParams& ep, bool spectral_last);
 bool mode_product_tma_eligible(const double* x, const PassShape& ps);
 void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const double* a_pad,
                              int lda, const PassShape& ps, const EpiParams& ep);

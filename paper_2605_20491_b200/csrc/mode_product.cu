@@ -114,6 +114,7 @@ __device__ __forceinline__ long long x_row_base(long long r, long long pre, long
 
 template <int BN, int LOADER, int VEC>
 __global__ void __launch_bounds__(NTHREADS, 1) mode_product_kernel(const KArgs args) {
+  if (args.ep.active && *args.ep.active == 0) return;
   using TC = TileCfg<BN>;
   using XL = XLayout<LOADER>;
   extern __shared__ __align__(128) double smem[];
@@ -290,6 +291,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) mode_product_kernel(const KArgs a
               }
               if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
             }
+            break;
+          }
+          case EPI_BPHASE: {
+            const double other = __shfl_xor_sync(0xffffffffu, val, 4);
+            if (ok) val = bphase_rotate(val, other, ep.diag, yi >> 1, ep.dt, (p & 1) != 0);
             break;
           }
           default:

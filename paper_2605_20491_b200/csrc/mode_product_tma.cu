@@ -169,10 +169,14 @@ __device__ __forceinline__ int chS(int g) { return ((g & 1) << 2) | (g >> 1); }
 // instruction cache when unrolled over 64 accumulators per thread):
 //   EK_GENERIC  every EpiParams kind (runtime dispatch; out-of-line per-element helpers)
 //   EK_STORE    plain store
+//   EK_MUL / EK_PHASE  the spectral multiply (apply) / phase (propagate: one sincos per (re, im)
+//               pair, both outputs from it) on the last real-view axis, same tables as EK_DIV
+//   EK_AXPY     + diag u - sigma u (FullOperator::apply's last pass): a row's u / diag loads are
+//               issued together before its stores (y may alias u, so the compiler cannot)
 //   EK_DIV      spectral divide on the last real-view axis (the solve's fused pass): per-warp
 //               tables of the row lambda partial sums and column eigenvalues, built before the K
 //               loop, and the divisions of one row batch issued together (div_rn_fast)
-enum { EK_GENERIC = 0, EK_STORE = 1, EK_DIV = 2 };
+enum { EK_GENERIC = 0, EK_STORE = 1, EK_DIV = 2, EK_MUL = 3, EK_PHASE = 4, EK_AXPY = 5 };
 
 struct TArgs {
   double* y;
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int col0 = (static_cast<int>(T - panel * ngroups) * CL + static_cast<int>(crank)) * BN;
     double* w_rowlam = s_tab + warp * C::WTAB;
     double* w_collam = w_rowlam + C::WTM;
-    if (EK == EK_DIV) {
+    if (EK == EK_DIV || EK == EK_MUL || EK == EK_PHASE) {
       // this warp's rows / columns of the tile: one index decomposition per row (32-bit: TMA
       // passes have R < 2^31) and one eigenvalue load per column, latency hidden behind the
       // first stage's wait; the warp owns its table (no CTA barrier couples the warps)
@@ -493,6 +497,86 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (rok && i < m) args.y[ybase + pre * static_cast<long long>(i)] = qv[jc][v];
           }
       }
+    } else if (EK == EK_MUL) {
+#pragma unroll
+      for (int j = 0; j < C::RT; ++j) {
+        const int lr = row_map<BN, LOADER>(j, g);
+        const long long r = row0 + wm * C::WTM + lr;
+        const bool rok = r < R;
+        const long long q = rok ? r / pre : 0;
+        const long long ybase = (rok ? r - q * pre : 0) + q * args.ldy;
+        const double lam_lo = w_rowlam[lr];
+#pragma unroll
+        for (int jc = 0; jc < C::CT; ++jc)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int lc = col_map<BN, LOADER>(jc, 2 * t + v);
+            const int i = col0 + wn * C::WTN + lc;
+            const double ls = __dsub_rn(__dadd_rn(lam_lo, w_collam[lc]), ep.shift);
+            if (rok && i < m)
+              args.y[ybase + pre * static_cast<long long>(i)] = __dmul_rn(acc[j][jc][v], ls);
+          }
+      }
+    } else if (EK == EK_PHASE) {
+      // rows j (re) and j + 1 (im) of a pair are the same spatial point (paired row maps, even
+      // pre, BM-aligned tiles): one sincos of -(lambda - shift) dt serves both (operators.cpp:68-71)
+#pragma unroll
+      for (int j = 0; j < C::RT; j += 2) {
+        const int lr = row_map<BN, LOADER>(j, g);
+        const long long r = row0 + wm * C::WTM + lr;
+        const bool rok = r < R;  // R and r are even: the partner row r + 1 is in range too
+        const long long q = rok ? r / pre : 0;
+        const long long ybase = (rok ? r - q * pre : 0) + q * args.ldy;
+        const double lam_lo = w_rowlam[lr];
+#pragma unroll
+        for (int jc = 0; jc < C::CT; ++jc)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int lc = col_map<BN, LOADER>(jc, 2 * t + v);
+            const int i = col0 + wn * C::WTN + lc;
+            const double ls = __dsub_rn(__dadd_rn(lam_lo, w_collam[lc]), ep.shift);
+            const double phase = __dmul_rn(-ls, ep.dt);
+            double sn, cs;
+            sincos(phase, &sn, &cs);
+            const double re = acc[j][jc][v], im = acc[j + 1][jc][v];
+            if (rok && i < m) {
+              const long long yi = ybase + pre * static_cast<long long>(i);
+              args.y[yi] = __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
+              args.y[yi + 1] = __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs));
+            }
+          }
+      }
+    } else if (EK == EK_AXPY) {
+      // (acc + diag .* u) - sigma u (operators.cpp:102; ground_state.cpp:70-72)
+#pragma unroll
+      for (int j = 0; j < C::RT; ++j) {
+        const long long r = row0 + wm * C::WTM + row_map<BN, LOADER>(j, g);
+        const bool rok = r < R;
+        const long long rr = rok ? r : 0;
+        const long long q = rr / pre;
+        const long long ybase = rr - q * pre + q * args.ldy;
+        long long yi[C::CT][2];
+        double uu[C::CT][2], dg[C::CT][2];
+#pragma unroll
+        for (int jc = 0; jc < C::CT; ++jc)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
+            const bool ok = rok && i < m;
+            yi[jc][v] = ok ? ybase + pre * static_cast<long long>(i) : -1;
+            uu[jc][v] = ok ? ep.u[yi[jc][v]] : 0.0;
+            dg[jc][v] = (ok && ep.diag) ? ep.diag[ep.cplx ? (yi[jc][v] >> 1) : yi[jc][v]] : 0.0;
+          }
+#pragma unroll
+        for (int jc = 0; jc < C::CT; ++jc)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            double val = acc[j][jc][v];
+            if (ep.diag) val = __dadd_rn(val, __dmul_rn(dg[jc][v], uu[jc][v]));
+            if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu[jc][v]));
+            if (yi[jc][v] >= 0) args.y[yi[jc][v]] = val;
+          }
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < C::RT; ++j) {
@@ -522,6 +606,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (ep.diag)
                   val = __dadd_rn(val, __dmul_rn(ep.diag[ep.cplx ? (yi >> 1) : yi], uu));
                 if (ep.sigma != 0.0) val = __dsub_rn(val, __dmul_rn(ep.sigma, uu));
+              } else if (ep.kind == EPI_BPHASE) {  // partner = tile j ^ 1, as for the phase
+                const double other = acc[j ^ 1][jc][v];
+                if (ok) val = bphase_rotate(val, other, ep.diag, yi >> 1, ep.dt, (j & 1) != 0);
               }
             }
             if (ok) args.y[yi] = val;
@@ -564,6 +651,13 @@ void set_attr_tma() {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
   KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, EK_DIV>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, EK_MUL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, EK_AXPY>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  if (LOADER != TL_CONTIG)
+    KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, LOADER != TL_CONTIG ? EK_PHASE : EK_GENERIC>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
   KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 2, EK_GENERIC>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
   KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 4, EK_GENERIC>,
@@ -647,11 +741,21 @@ void launch_tma(cudaStream_t s, int num_sms, long long ntiles_m, int ntiles_n,
     const long long blocks = tiles < num_sms ? tiles : num_sms;  // one CTA per SM
     const EpiParams& ep = ta.ep;
     const dim3 grid(static_cast<unsigned>(blocks));
+    const bool last_axis = ep.axis + 1 == ep.ndims && ep.lam[ep.axis] != nullptr;
     if (ep.kind == EPI_STORE)
       mode_product_tma_kernel<BN, LOADER, 1, EK_STORE><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(
           tmx, tmA, ta);
-    else if (ep.kind == EPI_SPEC_DIV && ep.axis + 1 == ep.ndims && ep.lam[ep.axis] != nullptr)
+    else if (ep.kind == EPI_SPEC_DIV && last_axis)
       mode_product_tma_kernel<BN, LOADER, 1, EK_DIV><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(
+          tmx, tmA, ta);
+    else if (ep.kind == EPI_SPEC_MUL && last_axis)
+      mode_product_tma_kernel<BN, LOADER, 1, EK_MUL><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(
+          tmx, tmA, ta);
+    else if (ep.kind == EPI_SPEC_PHASE && last_axis && ep.cplx && LOADER != TL_CONTIG)
+      mode_product_tma_kernel<BN, LOADER, 1, LOADER != TL_CONTIG ? EK_PHASE : EK_GENERIC>
+          <<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(tmx, tmA, ta);
+    else if (ep.kind == EPI_AXPY_DIAG)
+      mode_product_tma_kernel<BN, LOADER, 1, EK_AXPY><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(
           tmx, tmA, ta);
     else
       mode_product_tma_kernel<BN, LOADER, 1, EK_GENERIC><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(

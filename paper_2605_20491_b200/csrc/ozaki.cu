@@ -192,6 +192,11 @@ __device__ __forceinline__ void oz_drain(uint32_t tmem, int q, int hc, double (&
   }
 }
 
+// Row exponent marking a row (field run or matrix row) that holds a NaN / Inf: the slices of such
+// a row are meaningless, so every output that contracts it is stored as NaN -- FP64 arithmetic
+// (and the reference's Eigen GEMM) propagates non-finite values the same way.
+constexpr int OZ_NONFINITE = 1 << 29;
+
 // Epilogue, part 2: scale by 2^(ex+ey) / 127^2, the spectral divide (lambda summed in axis order
 // from 0.0, minus the shift, IEEE divide: operators.cpp:57), rotated FP64 store y[col * R + r].
 __device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, int lane,
@@ -221,6 +226,7 @@ __device__ __forceinline__ void oz_store(const OzArgs& a, long long r, int c0, i
     double val = (E > -1000 && E < 1000)
                      ? v0 * __longlong_as_double(static_cast<long long>(1023 + E) << 52)
                      : ldexp(v0, E);
+    if (er == OZ_NONFINITE || ec == OZ_NONFINITE) val = __longlong_as_double(0x7ff8000000000000LL);
     if (a.epi == 3) {  // partner row (re <-> im) is the neighbouring lane; as epilogue.cuh
       const double other = __shfl_xor_sync(0xffffffffu, val, 1);
       if (live && col < a.m) {
@@ -585,6 +591,7 @@ __global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict_
       const long long rq = gather ? (r < R ? r % Rh : 0) : r;
       const long long rc = gather ? (r < R ? r / Rh : 0) : 0;
       double amax = 0.0;
+      bool nonfinite = false;
       for (int k0 = 0; k0 < Kp; k0 += 256) {  // 8 independent loads in flight per lane
         double v[8];
 #pragma unroll
@@ -598,18 +605,21 @@ __global__ void __launch_bounds__(256) k_oz_split_rows(const double* __restrict_
         for (int u = 0; u < 8; ++u) {
           const int k = k0 + u * 32 + lane;
           if (k < Kp) {
-            srow[warp * ld + (k >> 4) * 17 + (k & 15)] = v[u];
-            amax = fmax(amax, fabs(v[u]));
+            const bool fin = isfinite(v[u]);
+            nonfinite = nonfinite || !fin;
+            srow[warp * ld + (k >> 4) * 17 + (k & 15)] = fin ? v[u] : 0.0;
+            amax = fmax(amax, fin ? fabs(v[u]) : 0.0);
           }
         }
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      nonfinite = __any_sync(0xffffffffu, nonfinite);
       int e = 0;
       if (amax > 0.0) frexp(amax, &e);  // amax < 2^e
       if (lane == 0) {
         sexp[warp] = e;
-        if (r < Rp) ex[r] = e;
+        if (r < Rp) ex[r] = nonfinite ? OZ_NONFINITE : e;
       }
     }
     __syncthreads();
@@ -652,13 +662,19 @@ __global__ void __launch_bounds__(256) k_oz_split_mat(const double* __restrict__
   const int nch = KB * 2;
   for (int r = w0; r < mp; r += nw) {
     double amax = 0.0;
+    bool nonfinite = false;
     if (r < m)
-      for (int k = lane; k < K; k += 32) amax = fmax(amax, fabs(M[r + static_cast<long long>(lda) * k]));
+      for (int k = lane; k < K; k += 32) {
+        const double v = M[r + static_cast<long long>(lda) * k];
+        nonfinite = nonfinite || !isfinite(v);
+        amax = fmax(amax, isfinite(v) ? fabs(v) : 0.0);
+      }
 #pragma unroll
     for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    nonfinite = __any_sync(0xffffffffu, nonfinite);
     int e = 0;
     if (amax > 0.0) frexp(amax, &e);
-    if (lane == 0) ex[r] = e;
+    if (lane == 0) ex[r] = nonfinite ? OZ_NONFINITE : e;
     const int p = r / P, rr = r - p * P;
     const double sc = ldexp(127.0, -e);
     for (int c = lane; c < nch; c += 32) {
@@ -666,7 +682,8 @@ __global__ void __launch_bounds__(256) k_oz_split_mat(const double* __restrict__
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int k = c * 16 + u;
-        const double v = (r < m && k < K) ? M[r + static_cast<long long>(lda) * k] : 0.0;
+        double v = (r < m && k < K) ? M[r + static_cast<long long>(lda) * k] : 0.0;
+        if (!isfinite(v)) v = 0.0;  // the row is marked OZ_NONFINITE
         t[u] = e > -900 ? v * sc : ldexp(v, -e) * 127.0;
       }
       uint32_t w[S][4];
@@ -689,12 +706,7 @@ void oz_split_rows(cudaStream_t st, const double* x, long long R, int K, int gat
   const long long Rp = (R + OZ_PAIR - 1) / OZ_PAIR * OZ_PAIR;  // whole 256-row pair panels
   const int nch = KB * 2;
   const size_t smem = static_cast<size_t>(8) * (nch * 17 + ((4 - nch) & 15)) * sizeof(double);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    KCUDA(cudaFuncSetAttribute(k_oz_split_rows<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
-    attr = smem;
-  }
+  if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(k_oz_split_rows<S>), smem);
   const long long groups = Rp / 8;
   const int per_sm = smem <= 72 * 1024 ? 3 : 1;
   const int blocks = static_cast<int>(groups < 148LL * per_sm * 4 ? groups : 148LL * per_sm * 4);
@@ -721,14 +733,8 @@ void oz_split_mat(cudaStream_t st, const double* M, int lda, int m, int K, int P
 template <int S>
 void oz_pass(cudaStream_t st, OzArgs a) {
   using G = OzGeom<S>;
-  static int sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    KCUDA(cudaFuncSetAttribute(oz_pass_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               G::SMEM));
-    return v;
-  }();
+  ensure_smem_attr(reinterpret_cast<const void*>(oz_pass_kernel<S>), G::SMEM);
+  const int sms = device_sm_count();
   const long long tiles = a.ntm * a.ntn;
   const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
   oz_pass_kernel<S><<<grid, OZ_THREADS, G::SMEM, st>>>(a);
@@ -764,14 +770,8 @@ void oz_encode_rows(CUtensorMap* map, const void* base, size_t bytes, int box_ro
 template <int S>
 void oz2_pass(cudaStream_t st, OzArgs a, size_t xbytes, size_t bbytes) {
   using G = Oz2Geom<S>;
-  static int sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    KCUDA(cudaFuncSetAttribute(oz2_pass_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               G::SMEM));
-    return v;
-  }();
+  ensure_smem_attr(reinterpret_cast<const void*>(oz2_pass_kernel<S>), G::SMEM);
+  const int sms = device_sm_count();
   CUtensorMap tx, tb;
   oz_encode_rows(&tx, a.xs, xbytes, G::A / 128);
   oz_encode_rows(&tb, a.bs, bbytes, G::B / 128);
@@ -1049,11 +1049,14 @@ void sep_ozaki(kronop_ctx& ctx, kronop_op& op, const double* in, double* out, in
 // initialise - the split matrices, the workspace for complex fields, the kernels' attributes -
 // is done here, by one throw-away transform of a zero field.
 void ozaki_prepare(kronop_ctx& ctx, kronop_op& op, int slices) {
-  const size_t n2 = 2 * static_cast<size_t>(op.N);
+  // one throw-away REAL transform splits the matrices and sizes the workspace for the real
+  // drivers (PCG, inverse iteration, GPE capture graphs and must not allocate); a complex field
+  // grows it later, outside any capture. In + out = 2 N doubles (a complex warm-up took 6 N).
+  const size_t n = static_cast<size_t>(op.N);
   double* z = nullptr;
-  KCUDA(cudaMallocAsync(&z, 2 * n2 * sizeof(double), ctx.stream));
-  KCUDA(cudaMemsetAsync(z, 0, n2 * sizeof(double), ctx.stream));
-  sep_ozaki(ctx, op, z, z + n2, 1, 3, op.shift, 0.0, nullptr, 0.0, slices);
+  KCUDA(cudaMallocAsync(&z, 2 * n * sizeof(double), ctx.stream));
+  KCUDA(cudaMemsetAsync(z, 0, n * sizeof(double), ctx.stream));
+  sep_ozaki(ctx, op, z, z + n, 0, 2, op.shift, 0.0, nullptr, 0.0, slices);
   KCUDA(cudaFreeAsync(z, ctx.stream));
   KCUDA(cudaStreamSynchronize(ctx.stream));
 }

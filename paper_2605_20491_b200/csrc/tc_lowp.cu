@@ -434,12 +434,7 @@ void encode_lowp_2d(CUtensorMap* map, const void* base, long long inner, long lo
 template <int PREC, int OUT_F64, int CL>
 void tc_launch(cudaStream_t s, unsigned grid, const CUtensorMap& tx, const CUtensorMap& tb,
                const TcArgs& a) {
-  static bool attr = [] {
-    KCUDA(cudaFuncSetAttribute(tc_pass_kernel<PREC, OUT_F64, CL>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
-    return true;
-  }();
-  (void)attr;
+  ensure_smem_attr(reinterpret_cast<const void*>(tc_pass_kernel<PREC, OUT_F64, CL>), TC_SMEM);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(TC_THREADS);
@@ -502,12 +497,7 @@ void tc_pass(cudaStream_t s, const void* x, const void* bmat, void* y, long long
   a.m = m;
   a.ntn = (m + TC_BN - 1) / TC_BN;
   a.ntm = (R + TC_BM - 1) / TC_BM;
-  static int sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
+  const int sms = device_sm_count();
   const long long tiles = ((a.ntm + cl - 1) / cl) * a.ntn * cl;  // CTAs worth of work
   long long g = tiles < sms ? tiles : sms;
   g = g / cl * cl;
@@ -806,12 +796,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 template <int PREC, int OUT_F64>
 void tc2_launch(cudaStream_t s, unsigned grid, const CUtensorMap& tx, const CUtensorMap& tb,
                 const TcArgs& a) {
-  static bool attr = [] {
-    KCUDA(cudaFuncSetAttribute(tc2_pass_kernel<PREC, OUT_F64>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM));
-    return true;
-  }();
-  (void)attr;
+  ensure_smem_attr(reinterpret_cast<const void*>(tc2_pass_kernel<PREC, OUT_F64>), T2_SMEM);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(TC_THREADS);
@@ -1053,14 +1038,9 @@ void t3_pass(cudaStream_t s, const float* xh, const float* xl, const float* bh, 
   a.m = m;
   a.ntn = (m + T3_BN - 1) / T3_BN;
   a.ntm = (R + TC_BM - 1) / TC_BM;
-  static int sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    KCUDA(cudaFuncSetAttribute(t3_pass_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, T3_SMEM));
-    KCUDA(cudaFuncSetAttribute(t3_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, T3_SMEM));
-    return v;
-  }();
+  ensure_smem_attr(reinterpret_cast<const void*>(t3_pass_kernel<0>), T3_SMEM);
+  ensure_smem_attr(reinterpret_cast<const void*>(t3_pass_kernel<1>), T3_SMEM);
+  const int sms = device_sm_count();
   const long long tiles = a.ntm * a.ntn;
   const unsigned grid = static_cast<unsigned>(tiles < sms ? tiles : sms);
   if (out_f64)

@@ -95,10 +95,10 @@ class SlabOperator:
         self.shift = shift
         self.diag = diag_slab
         nz, ny = self.shape[-1], self.shape[-2]
-        self.zs = split_extent(nz, self.P)
-        self.ys = split_extent(ny, self.P)
-        self.z0 = offsets(self.zs)
-        self.y0 = offsets(self.ys)
+        # the partition of the C-ABI slab operators (kronop_slab_plan, host code of libkronop.so)
+        self.zs, self.z0 = plan(nz, self.P)
+        self.ys, self.y0 = plan(ny, self.P)
+        assert self.zs == split_extent(nz, self.P) and self.z0 == offsets(self.zs)
         r = self.r
         self.R = int(np.prod(self.shape[:-2]))  # extent of the axes below d-2
         lamz = axes[-1].eigenvalues[self.z0[r]:self.z0[r] + self.zs[r]]
@@ -236,3 +236,205 @@ def slab_pcg(apply_a, precond, b, x, dot, rel_tol=1e-12, max_iter=500, stagnatio
         x.copy_(best_x)
         rel = best_rel
     return it_done, rel, converged
+
+
+# ------------------------------------------------------------ C-ABI slab operators --
+def plan(n: int, parts: int):
+    """kronop_slab_plan (host): the (extents, offsets) split of n planes into `parts` slabs, the
+    same split the device slab operators use."""
+    import ctypes as C
+    from . import _lib
+    e = (C.c_int * parts)()
+    o = (C.c_int * parts)()
+    _lib.check(_lib.lib().kronop_slab_plan(n, parts, e, o))
+    return list(e), list(o)
+
+
+class DeviceSlabOperator:
+    """SeparableOperator / FullOperator, pcg and the a_u GPE flow on slab-decomposed fields
+    through the C-ABI (kronop_slab_*, csrc/slab.cu).
+
+    In-process: `devices` lists the CUDA device of every part (distinct GPUs exchange over
+    NVLink peer copies; a repeated device gives virtual slabs on one GPU). NCCL: pass `ctx`
+    (this rank's api.Context), `rank`, `nranks` and the 128-byte `unique_id` (see nccl_unique_id).
+    Fields are lists of torch tensors, one per local part (this process's z-slabs)."""
+
+    def __init__(self, axes, shift: float = 0.0, mass=None, devices=None, ctx=None, rank=0,
+                 nranks=1, unique_id=None):
+        import ctypes as C
+        from . import _lib
+        from .api import _arr_of_ptrs
+        d = len(axes)
+        self.axes = list(axes)
+        self.shape = tuple(len(a.eigenvalues) for a in axes)
+        n = (C.c_int * d)(*self.shape)
+        keep = [np.asfortranarray(a.transform) for a in axes] + \
+               [np.asfortranarray(a.inverse_transform) for a in axes] + \
+               [np.ascontiguousarray(a.eigenvalues) for a in axes]
+        T, Ti, lam = (_arr_of_ptrs(keep[:d]), _arr_of_ptrs(keep[d:2 * d]),
+                      _arr_of_ptrs(keep[2 * d:]))
+        self.mass = [np.ascontiguousarray(m, dtype=np.float64) for m in mass] if mass else None
+        mp = _arr_of_ptrs(self.mass) if self.mass else None
+        h = C.c_void_p()
+        if ctx is None:
+            devs = list(devices or [0])
+            _lib.check(_lib.lib().kronop_slab_create(len(devs), (C.c_int * len(devs))(*devs), d, n,
+                                                     T, Ti, lam, mp, shift, C.byref(h)))
+        else:
+            self.ctx = ctx
+            _lib.check(_lib.lib().kronop_slab_create_nccl(ctx.h, bytes(unique_id), nranks, rank, d,
+                                                          n, T, Ti, lam, mp, shift, C.byref(h)))
+        self.h = h
+        P, nl, first = C.c_int(), C.c_int(), C.c_int()
+        _lib.check(_lib.lib().kronop_slab_info(h, C.byref(P), C.byref(nl), C.byref(first)))
+        self.P, self.nlocal, self.first = P.value, nl.value, first.value
+        self.parts = []
+        for i in range(self.nlocal):
+            dv, st = C.c_int(), C.c_void_p()
+            z0, nz, el = C.c_longlong(), C.c_longlong(), C.c_longlong()
+            _lib.check(_lib.lib().kronop_slab_part(h, i, C.byref(dv), C.byref(st), C.byref(z0),
+                                                   C.byref(nz), C.byref(el)))
+            self.parts.append({"device": dv.value, "stream": torch.cuda.ExternalStream(
+                st.value, device="cuda:%d" % dv.value), "z0": z0.value, "nz": nz.value,
+                "elems": el.value})
+
+    def close(self):
+        from . import _lib
+        if getattr(self, "h", None):
+            _lib.lib().kronop_slab_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- field helpers --
+    def plane_elems(self):
+        return int(np.prod(self.shape[:-1]))
+
+    def scatter(self, full: torch.Tensor):
+        """This process's z-slabs of a full field (host or device tensor, flat, axis 0 fastest)."""
+        pe = self.plane_elems()
+        out = []
+        for pt in self.parts:
+            sl = full[pt["z0"] * pe:(pt["z0"] + pt["nz"]) * pe]
+            out.append(sl.to("cuda:%d" % pt["device"]).contiguous().clone())
+        return out
+
+    def gather(self, parts) -> torch.Tensor:
+        """Concatenate local slabs (in-process: the whole field) on the first part's device."""
+        return torch.cat([p.to(parts[0].device) for p in parts])
+
+    def empty_like(self, parts):
+        return [torch.empty_like(p) for p in parts]
+
+    def _enter(self):
+        for pt in self.parts:
+            pt["stream"].wait_stream(torch.cuda.current_stream(pt["device"]))
+
+    def _leave(self):
+        for pt in self.parts:
+            torch.cuda.current_stream(pt["device"]).wait_stream(pt["stream"])
+
+    @staticmethod
+    def _ptrs(parts):
+        import ctypes as C
+        if parts is None:
+            return None
+        return (C.c_void_p * len(parts))(*[C.c_void_p(p.data_ptr()) for p in parts])
+
+    # -------------------------------------------------------------------- operators --
+    def set_shift(self, shift: float):
+        from . import _lib
+        _lib.check(_lib.lib().kronop_slab_set_shift(self.h, shift))
+
+    def apply(self, u, diag=None, sigma: float = 0.0, out=None):
+        from . import _lib
+        out = out or self.empty_like(u)
+        self._enter()
+        _lib.check(_lib.lib().kronop_slab_apply(self.h, self._ptrs(u), int(u[0].is_complex()),
+                                                self._ptrs(diag), sigma, self._ptrs(out)))
+        self._leave()
+        return out
+
+    def solve(self, b, out=None):
+        from . import _lib
+        out = out or self.empty_like(b)
+        self._enter()
+        _lib.check(_lib.lib().kronop_slab_solve(self.h, self._ptrs(b), int(b[0].is_complex()),
+                                                self._ptrs(out)))
+        self._leave()
+        return out
+
+    def propagate(self, psi, dt: float, out=None):
+        from . import _lib
+        out = out or self.empty_like(psi)
+        self._enter()
+        _lib.check(_lib.lib().kronop_slab_propagate(self.h, self._ptrs(psi), dt, self._ptrs(out)))
+        self._leave()
+        return out
+
+    def dot(self, a, b, weighted: bool = False) -> float:
+        import ctypes as C
+        from . import _lib
+        r = C.c_double()
+        self._enter()
+        _lib.check(_lib.lib().kronop_slab_dot(self.h, self._ptrs(a), self._ptrs(b), int(weighted),
+                                              C.byref(r)))
+        return r.value
+
+    def pcg(self, b, x, config, diag=None, sigma: float = 0.0):
+        """pcg(FullOperator{this, diag}.apply - sigma, this.solve, b, x&) (pcg.cpp:8-81);
+        x (list of part tensors) is the warm start and receives the solution."""
+        import ctypes as C
+        from . import _lib
+        from .api import PcgReport
+        cfg = _lib.PcgConfig(config.rel_tol, config.max_iter, int(config.record_history),
+                             int(config.preconditioned_norm), config.stagnation_window)
+        rep = _lib.PcgReport()
+        hist = np.zeros(config.max_iter + 1)
+        self._enter()
+        _lib.check(_lib.lib().kronop_slab_pcg(
+            self.h, self._ptrs(diag), sigma, self._ptrs(b), self._ptrs(x), C.byref(cfg),
+            C.byref(rep), hist.ctypes.data_as(C.POINTER(C.c_double))))
+        self._leave()
+        return PcgReport(rep.iterations, rep.final_residual, bool(rep.converged),
+                         list(hist[:rep.history_len]))
+
+    def gpe_au(self, beta: float, config, diag=None, initial=None):
+        """a_u gradient flow (gpe.cpp:55-165) on this Hamiltonian (+ diag = V2); returns
+        (state parts, api.GpeResult)."""
+        import ctypes as C
+        from . import _lib
+        from .api import GpeResult
+        gc = _lib.GpeConfig(1, config.step, config.metric_shift, config.energy_rel_tol,
+                            config.max_iterations,
+                            _lib.PcgConfig(config.inner.rel_tol, config.inner.max_iter,
+                                           int(config.inner.record_history),
+                                           int(config.inner.preconditioned_norm),
+                                           config.inner.stagnation_window),
+                            {"constant": 0, "eigenfunction": 1, "supplied": 2}[config.init],
+                            int(config.record_history))
+        res = _lib.GpeResult()
+        hist = np.zeros(5 * max(config.max_iterations, 1))
+        state = [torch.empty(pt["elems"], dtype=torch.float64, device="cuda:%d" % pt["device"])
+                 for pt in self.parts]
+        self._enter()
+        _lib.check(_lib.lib().kronop_slab_gpe_au(
+            self.h, self._ptrs(diag), beta, C.byref(gc), self._ptrs(initial), self._ptrs(state),
+            C.byref(res), hist.ctypes.data_as(C.POINTER(C.c_double))))
+        self._leave()
+        rows = [tuple(hist[5 * i:5 * i + 5]) for i in range(res.history_len)]
+        return state, GpeResult(state, res.energy, res.eigenvalue, res.iterations,
+                                res.linear_solves, bool(res.converged), rows)
+
+
+def nccl_unique_id() -> bytes:
+    """kronop_nccl_unique_id: 128 bytes for kronop_slab_create_nccl (create on rank 0, broadcast)."""
+    import ctypes as C
+    from . import _lib
+    buf = C.create_string_buffer(128)
+    _lib.check(_lib.lib().kronop_nccl_unique_id(buf))
+    return buf.raw
