@@ -713,9 +713,14 @@ static void run_schedules(kronop_ctx& c, const kronop_op& a, const double* b_dia
   // epilogue of the propagate's last pass (EPI_BPHASE), saving a field round trip per B step.
   // The operations and their order are those of splitting.cpp:53-82 (merge: A-times accumulate
   // and flush before each B or at the end; no merge: each A-time is flushed on its own).
+  // B phase fused into the propagate's last pass (EPI_BPHASE) only on request
+  // (KRONOP_BPHASE_FUSED=1): it is bit-identical, but measured slower on every config-5 grid
+  // (Strang steps/s, tools/microbench/bphase_bench.py: 9D n = 9 25.4 vs 29.5, 6D n = 29 15.5 vs
+  // 16.0, 3D 499^3 15.8 vs 16.8) -- the per-element sincos makes the latency-bound store phase
+  // of the contraction longer than the HBM-bound standalone phase pass it saves.
   static const bool unfused = [] {
-    const char* e = getenv("KRONOP_BPHASE_FUSED");  // A/B switch: 0 = B phase as its own pass
-    return e && e[0] == '0';
+    const char* e = getenv("KRONOP_BPHASE_FUSED");
+    return !(e && e[0] == '1');
   }();
   double pending = 0.0;
   bool has_pending = false;

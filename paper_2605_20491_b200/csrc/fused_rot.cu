@@ -38,10 +38,39 @@ namespace {
 // matrix lives in registers: 2 n^2 + O(n) registers per thread)
 template <int DN>
 // (n = 9: 7 warps, so the 648 fibers an axis of a 9D tile holds split into 3 nearly full rounds)
-__host__ __device__ constexpr int rt_threads() { return DN == 9 ? 224 : DN > 0 ? 256 : 512; }
+__host__ __device__ constexpr int rt_threads_default() { return DN == 9 ? 224 : DN > 0 ? 256 : 512; }
 constexpr int RT_MAXF = 3;
 constexpr int RT_STAGES = 3;
 constexpr int RT_TILE = 8192;  // doubles per stage (64 KB)
+// Compile-time knobs of the DFMA path (n <= 10), for A/B builds (tools/build_variant.py):
+// threads per CTA (0 = rt_threads_default), co-resident CTAs per SM, stages, doubles per stage.
+// Default: two 4-warp CTAs per SM with 2 stages of 48 KB each (the n x n matrix in registers
+// caps a CTA at ~224 registers per thread, so two CTAs is the most the register file holds; one
+// CTA's store phase overlaps the other's contraction). Measured (tools/microbench/rot_bench.py,
+// profiles/r02_rot_variants.json): 9D n = 9 propagate 27.15 -> 25.73 ms, 9D solve 17.3 -> 15.6
+// ms vs one 7-warp CTA with 3 x 64 KB stages; 96-thread CTAs and 4 stages were no better.
+#ifndef KRONOP_DF_THREADS
+#define KRONOP_DF_THREADS 128
+#endif
+#ifndef KRONOP_DF_CTAS
+#define KRONOP_DF_CTAS 2
+#endif
+#ifndef KRONOP_DF_STAGES
+#define KRONOP_DF_STAGES 2
+#endif
+#ifndef KRONOP_DF_TILE
+#define KRONOP_DF_TILE 6144
+#endif
+template <int DN>
+__host__ __device__ constexpr int rt_threads() {
+  return DN > 0 && KRONOP_DF_THREADS > 0 ? KRONOP_DF_THREADS : rt_threads_default<DN>();
+}
+template <int DN>
+__host__ __device__ constexpr int rt_ctas() { return DN > 0 ? KRONOP_DF_CTAS : 1; }
+template <int DN>
+__host__ __device__ constexpr int rt_stages() { return DN > 0 ? KRONOP_DF_STAGES : RT_STAGES; }
+template <int DN>
+__host__ __device__ constexpr int rt_tile() { return DN > 0 ? KRONOP_DF_TILE : RT_TILE; }
 
 struct RotArgs {
   const double* x;
@@ -318,8 +347,10 @@ __device__ __forceinline__ void store_tile(const RotArgs& A, const double* tile,
 }
 
 template <int NF, int K4, int NT, int DN>
-__global__ void __launch_bounds__(rt_threads<DN>(), 1) fused_rot_kernel(const __grid_constant__ RotArgs A) {
+__global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_kernel(const __grid_constant__ RotArgs A) {
   constexpr int THREADS = rt_threads<DN>();
+  constexpr int RT_STAGES = rt_stages<DN>();
+  constexpr int RT_TILE = rt_tile<DN>();
   constexpr int G = NT >= 3 ? 2 : (NT == 2 ? 2 : 4);  // 8 G NT independent DMMA chains per warp
   // DN > 0: DFMA path with n = DN on every group axis (matrices row-major, pitch DNP);
   // DN == 0: DMMA path (B fragments in fragment order)
@@ -442,15 +473,15 @@ __global__ void __launch_bounds__(rt_threads<DN>(), 1) fused_rot_kernel(const __
 template <int NF, int K4, int NT, int DN>
 constexpr size_t rot_smem_bytes() {
   constexpr int FRAG = DN > 0 ? DN * ((DN + 1) & ~1) : K4 * NT * 32;
-  return (static_cast<size_t>(RT_STAGES) * RT_TILE + NF * FRAG + 128) * sizeof(double) +
-         RT_STAGES * (2 * sizeof(uint64_t) + sizeof(int)) + 16;
+  return (static_cast<size_t>(rt_stages<DN>()) * rt_tile<DN>() + NF * FRAG + 128) * sizeof(double) +
+         rt_stages<DN>() * (2 * sizeof(uint64_t) + sizeof(int)) + 16;
 }
 
 template <int NF, int K4, int NT, int DN = 0>
 void launch_rot(cudaStream_t s, const RotArgs& a) {
   ensure_smem_attr(reinterpret_cast<const void*>(fused_rot_kernel<NF, K4, NT, DN>),
                    rot_smem_bytes<NF, K4, NT, DN>());
-  const int grid_cap = device_sm_count();
+  const int grid_cap = device_sm_count() * rt_ctas<DN>();
   const long long grid = a.ntiles < grid_cap ? a.ntiles : grid_cap;
   fused_rot_kernel<NF, K4, NT, DN>
       <<<static_cast<unsigned>(grid), rt_threads<DN>(), rot_smem_bytes<NF, K4, NT, DN>(), s>>>(a);
@@ -660,9 +691,32 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
   }
   param_check(maxn <= 32 && a.F <= 1024 && (f < 3 || maxn <= 12), "fused_rot: group too large");
   a.Q = N / a.F;
-  // C * Qt: the largest power of two >= 8 with C * Qt * F <= RT_TILE
+  bool same = true;
+  for (int j = 1; j < f; ++j) same = same && n[j] == n[0];
+  static const bool no_dfma = [] {
+    const char* e = getenv("KRONOP_ROT_NO_DFMA");  // A/B switch: DMMA for every extent
+    return e && e[0] == '1';
+  }();
+  const bool dfma_ok = same && maxn >= 2 && maxn <= 10 && !no_dfma;
+  // A/B switch for the phase (last forward) launch: 0 = epilogue fused into the 16-warp DMMA
+  // kernel; 1 = contraction on the epilogue-free kernels + the standalone spectral pass when the
+  // DFMA kernel serves the group; 2 (default) = that split for every extent (9D n = 9 propagate
+  // 29.7 -> 26.7 ms, 6D n = 29 51.7 -> 50.8 ms, bit-identical; tools/microbench/spec_split.py). The divide / multiply
+  // epilogues stay fused (measured: splitting them costs the extra field round trip)
+  static const int spec_split = [] {
+    const char* e = getenv("KRONOP_ROT_SPEC_SPLIT");
+    return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
+  }();
+  const bool spectral = epi.kind == EPI_SPEC_MUL || epi.kind == EPI_SPEC_DIV ||
+                        epi.kind == EPI_SPEC_PHASE;
+  const bool split = epi.kind == EPI_SPEC_PHASE && (spec_split == 2 || (spec_split == 1 && dfma_ok));
+  // every (f, n) has an instantiation; the group must fit a DFMA stage (C Qt >= 8)
+  const bool use_dfma = dfma_ok && (!spectral || split) && 8 * a.F <= KRONOP_DF_TILE;
+  // C * Qt: the largest power of two >= 8 with C * Qt * F <= the stage size of the path
+  const int tile_doubles = use_dfma ? KRONOP_DF_TILE : RT_TILE;
   int cqt = 8;
-  while (cqt * 2 * a.F <= RT_TILE && cqt < 64) cqt *= 2;
+  while (cqt * 2 * a.F <= tile_doubles && cqt < 64) cqt *= 2;
+  param_check(cqt * a.F <= RT_TILE, "fused_rot: group too large for a stage");
   a.lcq = 0;
   while ((1 << a.lcq) < cqt) ++a.lcq;
   a.Qt = cqt / a.C;
@@ -688,30 +742,11 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
     a.qext[j] = epi.qext[j];
     a.lam_q[j] = epi.lam_q[j];
   }
-  bool same = true;
-  for (int j = 1; j < f; ++j) same = same && n[j] == n[0];
-  static const bool no_dfma = [] {
-    const char* e = getenv("KRONOP_ROT_NO_DFMA");  // A/B switch: DMMA for every extent
-    return e && e[0] == '1';
-  }();
-  // A/B switch for the phase (last forward) launch: 0 = epilogue fused into the 16-warp DMMA
-  // kernel; 1 = contraction on the epilogue-free kernels + the standalone spectral pass when the
-  // DFMA kernel serves the group; 2 (default) = that split for every extent (9D n = 9 propagate
-  // 29.7 -> 26.7 ms, 6D n = 29 51.7 -> 50.8 ms, bit-identical; tools/microbench/spec_split.py). The divide / multiply
-  // epilogues stay fused (measured: splitting them costs the extra field round trip)
-  static const int spec_split = [] {
-    const char* e = getenv("KRONOP_ROT_SPEC_SPLIT");
-    return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
-  }();
-  const bool spectral = epi.kind == EPI_SPEC_MUL || epi.kind == EPI_SPEC_DIV ||
-                        epi.kind == EPI_SPEC_PHASE;
-  const bool dfma_ok = same && maxn >= 2 && maxn <= 10 && !no_dfma;
-  const bool split = epi.kind == EPI_SPEC_PHASE && (spec_split == 2 || (spec_split == 1 && dfma_ok));
   if (split) a.epi = EPI_STORE;
   // fused epilogue: the spectral launch keeps the 16-warp DMMA kernel (its store pass, one sincos
   // per pair, is latency bound and needs the warps more than the contraction needs DFMA)
   bool launched = false;
-  if (dfma_ok && (!spectral || split)) {
+  if (use_dfma) {
     launched = true;
     switch (f * 16 + maxn) {
 #define RT_DF(F, N) \

@@ -77,8 +77,8 @@ np.savez(sys.argv[1], **out)
 
 def test_fused_b_phase_is_bit_identical(tmp_path):
     """The split-step B phase fused into the propagate's last pass (EPI_BPHASE, DMMA / TMA /
-    small-extent kernels) gives bit-identical states to the standalone phase pass
-    (KRONOP_BPHASE_FUSED=0), for qHOP / Yoshida, merged or not."""
+    small-extent kernels; KRONOP_BPHASE_FUSED=1) gives bit-identical states to the standalone
+    phase pass (the default), for qHOP / Yoshida, merged or not."""
     import os
     import subprocess
     import sys
