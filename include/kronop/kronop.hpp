@@ -595,4 +595,107 @@ inline GpeResult gpe_gradient_flow(const GpeProblem& p, const GpeFlowConfig& con
   return out;
 }
 
+// ------------------------------------------ slab decomposition (kronop_slab_*, multi-GPU) --
+// SeparableOperator / FullOperator / pcg on fields cut into slabs of the slowest axis across the
+// GPUs of `devices` (one process; a repeated device gives virtual slabs on one GPU). Host fields
+// keep the reference's value semantics: scattered to the parts, transformed, gathered back.
+class SlabOperator {
+ public:
+  SlabOperator(const std::vector<int>& devices, std::vector<AxisEigens> axes, double shift = 0.0,
+               std::shared_ptr<const MassWeights> mass = nullptr)
+      : axes_(std::move(axes)) {
+    const int d = static_cast<int>(axes_.size());
+    std::vector<int> n(d);
+    std::vector<const double*> T(d), Ti(d), L(d), M(d);
+    for (int a = 0; a < d; ++a) {
+      n[a] = axes_[a].size();
+      T[a] = axes_[a].transform.data();
+      Ti[a] = axes_[a].inverse_transform.data();
+      L[a] = axes_[a].eigenvalues.data();
+      if (mass) M[a] = (*mass)[a].data();
+    }
+    kronop_slab* h = nullptr;
+    check(kronop_slab_create(static_cast<int>(devices.size()), devices.data(), d, n.data(),
+                             T.data(), Ti.data(), L.data(), mass ? M.data() : nullptr, shift, &h));
+    slab_.reset(h, [](kronop_slab* p) { kronop_slab_destroy(p); });
+    int nl = 0;
+    check(kronop_slab_info(h, nullptr, &nl, nullptr));
+    elems_.resize(nl);
+    for (int i = 0; i < nl; ++i)
+      check(kronop_slab_part(h, i, nullptr, nullptr, nullptr, nullptr, &elems_[i]));
+  }
+  int parts() const { return static_cast<int>(elems_.size()); }
+  void set_shift(double s) { check(kronop_slab_set_shift(slab_.get(), s)); }
+
+  template <typename S>
+  TensorField<S> apply(const TensorField<S>& u) const {  // operators.cpp:31-40
+    return run(u, [&](double* const* in, double* const* out) {
+      check(kronop_slab_apply(slab_.get(), in, is_complex_v<S>, nullptr, 0.0, out));
+    });
+  }
+  template <typename S>
+  TensorField<S> solve(const TensorField<S>& b) const {  // operators.cpp:42-61
+    return run(b, [&](double* const* in, double* const* out) {
+      check(kronop_slab_solve(slab_.get(), in, is_complex_v<S>, out));
+    });
+  }
+  ComplexField propagate(const ComplexField& psi, double dt) const {  // operators.cpp:63-75
+    return run(psi, [&](double* const* in, double* const* out) {
+      check(kronop_slab_propagate(slab_.get(), in, dt, out));
+    });
+  }
+  // pcg(FullOperator{this, diagonal}.apply, this.solve, b, x&) (pcg.cpp:8-81); x in/out
+  PcgReport pcg(const RealField* diagonal, const RealField& b, RealField& x,
+                const PcgConfig& cfg) const {
+    Parts db(*this, 1), dx(*this, 1), dd(*this, 1);
+    check(kronop_slab_scatter(slab_.get(), reinterpret_cast<const double*>(b.data()), 0, db.p.data()));
+    check(kronop_slab_scatter(slab_.get(), reinterpret_cast<const double*>(x.data()), 0, dx.p.data()));
+    if (diagonal)
+      check(kronop_slab_scatter(slab_.get(), diagonal->data(), 0, dd.p.data()));
+    kronop_pcg_config c{cfg.rel_tol, cfg.max_iter, cfg.record_history ? 1 : 0,
+                        cfg.preconditioned_norm ? 1 : 0, cfg.stagnation_window};
+    kronop_pcg_report r{};
+    std::vector<double> hist(static_cast<size_t>(cfg.max_iter) + 1);
+    check(kronop_slab_pcg(slab_.get(), diagonal ? dd.p.data() : nullptr, 0.0, db.p.data(),
+                          dx.p.data(), &c, &r, hist.data()));
+    check(kronop_slab_gather(slab_.get(), dx.p.data(), 0, x.data()));
+    PcgReport rep;
+    rep.iterations = r.iterations;
+    rep.final_residual = r.final_residual;
+    rep.converged = r.converged != 0;
+    if (cfg.record_history) rep.history.assign(hist.begin(), hist.begin() + r.history_len);
+    return rep;
+  }
+
+ private:
+  struct Parts {  // one device buffer per local part
+    const SlabOperator* o;
+    std::vector<double*> p;
+    Parts(const SlabOperator& op, int c) : o(&op), p(op.elems_.size(), nullptr) {
+      for (size_t i = 0; i < p.size(); ++i)
+        check(kronop_slab_field_alloc(op.slab_.get(), static_cast<int>(i),
+                                      static_cast<size_t>(op.elems_[i]) * c, &p[i]));
+    }
+    ~Parts() {
+      for (size_t i = 0; i < p.size(); ++i) kronop_slab_field_free(o->slab_.get(), static_cast<int>(i), p[i]);
+    }
+  };
+  template <typename S, class F>
+  TensorField<S> run(const TensorField<S>& in, F&& f) const {
+    constexpr int c = is_complex_v<S> ? 2 : 1;
+    Parts a(*this, c), b(*this, c);
+    check(kronop_slab_scatter(slab_.get(), reinterpret_cast<const double*>(in.data()),
+                              is_complex_v<S>, a.p.data()));
+    f(a.p.data(), b.p.data());
+    TensorField<S> out(in.shape());
+    check(kronop_slab_gather(slab_.get(), b.p.data(), is_complex_v<S>,
+                             reinterpret_cast<double*>(out.data())));
+    out.set_mass(in.mass());
+    return out;
+  }
+  std::vector<AxisEigens> axes_;
+  std::shared_ptr<kronop_slab> slab_;
+  std::vector<long long> elems_;
+};
+
 }  // namespace kronop

@@ -146,6 +146,10 @@ PROTOTYPES = {
     "kronop_slab_part": (I, [P, I, IP, C.POINTER(C.c_void_p), C.POINTER(C.c_longlong),
                              C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "kronop_slab_set_shift": (I, [P, D]),
+    "kronop_slab_field_alloc": (I, [P, I, C.c_size_t, P]),
+    "kronop_slab_field_free": (I, [P, I, P]),
+    "kronop_slab_scatter": (I, [P, DP, I, P]),
+    "kronop_slab_gather": (I, [P, P, I, DP]),
     "kronop_slab_synchronize": (I, [P]),
     "kronop_slab_apply": (I, [P, P, I, P, D, P]),
     "kronop_slab_solve": (I, [P, P, I, P]),

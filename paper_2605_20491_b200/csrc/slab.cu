@@ -1034,6 +1034,57 @@ int kronop_slab_part(const kronop_slab* s, int local, int* device, void** stream
   });
 }
 
+int kronop_slab_field_alloc(kronop_slab* s, int local, size_t doubles, double** out) {
+  return guard_slab([&] {
+    param_check(s && out && local >= 0 && local < static_cast<int>(s->parts.size()),
+                "slab_field_alloc: bad argument");
+    part_device(s->parts[local]);
+    KCUDA(cudaMalloc(out, std::max<size_t>(doubles, 1) * sizeof(double)));
+  });
+}
+
+int kronop_slab_field_free(kronop_slab* s, int local, double* p) {
+  return guard_slab([&] {
+    param_check(s && local >= 0 && local < static_cast<int>(s->parts.size()),
+                "slab_field_free: bad argument");
+    part_device(s->parts[local]);
+    KCUDA(cudaFree(p));
+  });
+}
+
+// host = the FULL field (all planes, axis 0 fastest); each local part gets / gives its planes
+int kronop_slab_scatter(kronop_slab* s, const double* host, int is_complex, double* const* parts) {
+  return guard_slab([&] {
+    param_check(s && host && parts, "slab_scatter: null argument");
+    const long long c = is_complex ? 2 : 1;
+    for (size_t i = 0; i < s->parts.size(); ++i) {
+      SlabPart& pt = s->parts[i];
+      part_device(pt);
+      const long long plane = zslab_elems(*s, pt.p) / std::max(1, s->zs[pt.p]);
+      KCUDA(cudaMemcpyAsync(parts[i], host + c * plane * s->z0[pt.p],
+                            c * zslab_elems(*s, pt.p) * sizeof(double), cudaMemcpyHostToDevice,
+                            pt.ctx->stream));
+    }
+    slab_sync(*s);
+  });
+}
+
+int kronop_slab_gather(kronop_slab* s, const double* const* parts, int is_complex, double* host) {
+  return guard_slab([&] {
+    param_check(s && host && parts, "slab_gather: null argument");
+    const long long c = is_complex ? 2 : 1;
+    for (size_t i = 0; i < s->parts.size(); ++i) {
+      SlabPart& pt = s->parts[i];
+      part_device(pt);
+      const long long plane = zslab_elems(*s, pt.p) / std::max(1, s->zs[pt.p]);
+      KCUDA(cudaMemcpyAsync(host + c * plane * s->z0[pt.p], parts[i],
+                            c * zslab_elems(*s, pt.p) * sizeof(double), cudaMemcpyDeviceToHost,
+                            pt.ctx->stream));
+    }
+    slab_sync(*s);
+  });
+}
+
 int kronop_slab_set_shift(kronop_slab* s, double shift) {
   return guard_slab([&] {
     param_check(s, "slab_set_shift: null slab");
