@@ -266,6 +266,85 @@ static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double
     }
 }
 
+// Rotated pass sequence for the large-extent path: every pass contracts the fastest axis after
+// the re/im axis and writes its output axis to the SLOWEST end (y = r + R i), so the next axis is
+// the fastest again and after d passes the layout is the original one. Every pass then reads
+// through the CONTIG (real) / CPLX0 (complex) TMA loader -- the STRIDED loader the passes on axes
+// 1..d-1 used ran at 89-90% of the DMMA pipe vs ~95% (profiles/r02_pass_a1.json; cuBLAS on the
+// same shapes, profiles/r02_cublas_passes.json: 61.1 / 61.5 / 61.9 ms vs 62.5 / 66.6 / 66.2 ms).
+// The last forward pass's rows enumerate axes 0..d-2 in order (the same rows as the unrotated
+// last-axis pass), so the fused spectral epilogue sums the eigenvalues exactly as before
+// (PassShape::rot); the last backward pass writes the original layout, so the FullOperator AXPY
+// and the B phase index u / V2 as before. The contraction order over k inside the DMMA differs
+// between the loaders' k permutations, so results agree with the axis-order passes to rounding
+// (KRONOP_ROTATE_PASSES=0 selects those; tests/test_gpu_switches.py).
+static bool rotated_passes_ok(const kronop_ctx& ctx, const kronop_op& op, const double* in,
+                              const double* out, const View& v) {
+  static const bool off = [] {
+    const char* e = getenv("KRONOP_ROTATE_PASSES");  // A/B switch: 0 = axis-order passes
+    return e && e[0] == '0';
+  }();
+  if (off || op.d < 2 || !mode_product_tma_enabled()) return false;
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!aligned(in) || !aligned(out) || !aligned(ctx.scratch[0]) || !aligned(ctx.scratch[1]))
+    return false;
+  for (int a = 0; a < op.d; ++a) {
+    if ((!v.cplx && op.n[a] % 2 != 0) || op.n[a] < 2) return false;  // CONTIG rows of even length
+    if (v.total() / op.n[a] > 0x7fffffffLL) return false;  // rows: TMA coordinates are 32-bit
+  }
+  return true;
+}
+
+static void sep_transform_rotated(kronop_ctx& ctx, const kronop_op& op, const double* in,
+                                  double* out, const View& v, SepKind kind, double shift,
+                                  double dt, const double* diag, double sigma, bool bphase,
+                                  const double* bfield, double bfactor) {
+  const int d = op.d;
+  const long long c = v.cplx ? 2 : 1;
+  const long long total = v.total();
+  const double* cur = in;
+  for (int k = 0; k < 2 * d; ++k) {
+    const bool forward = k < d;
+    const int axis = forward ? k : k - d;
+    double* dst = (k == 2 * d - 1) ? out : ctx.scratch[k % 2];
+    PassShape ps;
+    ps.pre = c;
+    ps.nk = op.n[axis];
+    ps.m = op.n[axis];
+    ps.post = total / (c * op.n[axis]);
+    ps.ldy = c;                   // ybase = r
+    ps.ycol = total / op.n[axis];  // output axis at the slow end
+    ps.rot = 1;
+    EpiParams ep;
+    if (k == d - 1) {  // the spectral epilogue, rows = axes 0..d-2 in order (as the unrotated pass)
+      ep.kind = kind == SEP_APPLY ? EPI_SPEC_MUL : kind == SEP_SOLVE ? EPI_SPEC_DIV : EPI_SPEC_PHASE;
+      ep.axis = d - 1 + v.cplx;
+      ep.ndims = v.nd;
+      for (int i = 0; i < v.nd; ++i) ep.ext[i] = v.ext[i];
+      for (int a = 0; a < d; ++a) ep.lam[a + v.cplx] = op.lam[a];
+      ep.shift = shift;
+      ep.dt = dt;
+      ep.cplx = v.cplx;
+    }
+    if (k == 2 * d - 1 && (diag != nullptr || sigma != 0.0)) {
+      ep.kind = EPI_AXPY_DIAG;
+      ep.diag = diag;
+      ep.u = in;
+      ep.sigma = sigma;
+      ep.cplx = v.cplx;
+    } else if (k == 2 * d - 1 && bphase) {
+      ep.kind = EPI_BPHASE;
+      ep.diag = bfield;
+      ep.dt = bfactor;
+      ep.cplx = v.cplx;
+    }
+    launch_mode_product(ctx.stream, cur, dst, forward ? op.fwd[axis] : op.bwd[axis],
+                        op.lda[axis], ps, ep);
+    ctx.ws.launches += 1;
+    cur = dst;
+  }
+}
+
 void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
                    SepKind kind, double shift, double dt, const double* diag, double sigma,
                    bool bphase, const double* bfield, double bfactor) {
@@ -296,6 +375,11 @@ void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, doubl
   ensure_scratch(ctx, static_cast<size_t>(v.total()));
   const int d = op.d;
   const double* cur = in;
+  if (rotated_passes_ok(ctx, op, in, out, v)) {
+    sep_transform_rotated(ctx, op, in, out, v, kind, shift, dt, diag, sigma, bphase, bfield,
+                          bfactor);
+    return;
+  }
   for (int k = 0; k < 2 * d; ++k) {
     const bool forward = k < d;
     const int axis = forward ? k : k - d;

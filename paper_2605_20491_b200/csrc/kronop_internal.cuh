@@ -103,6 +103,11 @@ struct PassShape {
   // q-strides of X and Y (doubles). 0 = dense (pre * nk, pre * m); larger values address a
   // sub-range of a longer axis (the even/odd halves of a folded axis).
   long long ldx = 0, ldy = 0;
+  // Rotated output (TMA kernel only): ycol = stride of the output index i (0 = pre), and rot = 1
+  // when the spectral eigenvalue sum runs over the full row index r (the rows enumerate the other
+  // axes in order: the layout of a pass that moves its contracted axis to the slowest end).
+  long long ycol = 0;
+  int rot = 0;
   long long ldx_eff() const { return ldx ? ldx : pre * nk; }
   long long ldy_eff() const { return ldy ? ldy : pre * m; }
 };
@@ -132,6 +137,7 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
                      long long N, const double* const* mats, const int* lda, const RotEpi& epi);
 
 bool mode_product_tma_eligible(const double* x, const PassShape& ps);
+bool mode_product_tma_enabled();  // false under KRONOP_DISABLE_TMA=1
 void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const double* a_pad,
                              int lda, const PassShape& ps, const EpiParams& ep);
 void launch_mode_product(cudaStream_t s, const double* x, double* y, const double* a_pad, int lda,

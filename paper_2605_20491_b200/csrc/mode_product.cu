@@ -355,19 +355,25 @@ void prime_mode_product_kernels() {
   set_attr<64, LD_STRIDED_K, 2>();
 }
 
+bool mode_product_tma_enabled() {
+  static const bool no_tma = [] {
+    const char* e = getenv("KRONOP_DISABLE_TMA");  // A/B switch for profiling the cp.async kernel
+    return e && e[0] == '1';
+  }();
+  return !no_tma;
+}
+
 void launch_mode_product(cudaStream_t s, const double* x, double* y, const double* a_pad, int lda,
                          const PassShape& ps, const EpiParams& ep) {
   param_check(ps.nk >= 1 && ps.m >= 1 && ps.pre >= 1 && ps.post >= 1,
               "mode_product: empty pass shape");
   param_check(lda >= pad_up(ps.m, kMatPadM), "mode_product: matrix leading dimension too small");
-  static const bool no_tma = [] {
-    const char* e = getenv("KRONOP_DISABLE_TMA");  // A/B switch for profiling the cp.async kernel
-    return e && e[0] == '1';
-  }();
-  if (!no_tma && mode_product_tma_eligible(x, ps)) {
+  if (mode_product_tma_enabled() && mode_product_tma_eligible(x, ps)) {
     launch_mode_product_tma(s, x, y, a_pad, lda, ps, ep);
     return;
   }
+  param_check((ps.ycol == 0 || ps.ycol == ps.pre) && !ps.rot,
+              "mode_product: rotated output needs the TMA kernel");
   KArgs ka;
   ka.x = x;
   ka.y = y;

@@ -183,6 +183,8 @@ struct TArgs {
   int x2d;  // STRIDED with post == 1: X is the 2-D (pre x nk) tensor map
   long long pre, post, R;
   long long ldy;  // q-stride of Y
+  long long ycol;  // stride of the output index i in Y (pre, or R for a rotated pass)
+  int rot;         // eigenvalue rows = full row index r (rotated pass)
   int nk, m;
   int ntiles_n;
   long long ntiles_m;
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int cs = chS(g);
   const EpiParams& ep = args.ep;
-  const long long pre = args.pre, R = args.R;
+  const long long pre = args.pre, R = args.R, ycol = args.ycol;
   const int m = args.m;
   const bool spectral =
       ep.kind == EPI_SPEC_MUL || ep.kind == EPI_SPEC_DIV || ep.kind == EPI_SPEC_PHASE;
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
       for (int k = lane; k < C::WTM; k += 32) {
         const long long r = row0 + wm * C::WTM + k;
-        w_rowlam[k] = r < R ? lambda_partial_low_ext(ep, r % pre, ep.axis) : 0.0;
+        w_rowlam[k] = r < R ? lambda_partial_low_ext(ep, args.rot ? r : r % pre, ep.axis) : 0.0;
       }
       const int c = col0 + wn * C::WTN + lane;
       w_collam[lane] = c < m ? ep.lam[ep.axis][c] : 0.0;
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
             const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
-            if (rok && i < m) args.y[ybase + pre * static_cast<long long>(i)] = qv[jc][v];
+            if (rok && i < m) args.y[ybase + ycol * static_cast<long long>(i)] = qv[jc][v];
           }
       }
     } else if (EK == EK_MUL) {
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int i = col0 + wn * C::WTN + lc;
             const double ls = __dsub_rn(__dadd_rn(lam_lo, w_collam[lc]), ep.shift);
             if (rok && i < m)
-              args.y[ybase + pre * static_cast<long long>(i)] = __dmul_rn(acc[j][jc][v], ls);
+              args.y[ybase + ycol * static_cast<long long>(i)] = __dmul_rn(acc[j][jc][v], ls);
           }
       }
     } else if (EK == EK_PHASE) {
@@ -540,7 +542,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             sincos(phase, &sn, &cs);
             const double re = acc[j][jc][v], im = acc[j + 1][jc][v];
             if (rok && i < m) {
-              const long long yi = ybase + pre * static_cast<long long>(i);
+              const long long yi = ybase + ycol * static_cast<long long>(i);
               args.y[yi] = __dsub_rn(__dmul_rn(re, cs), __dmul_rn(im, sn));
               args.y[yi + 1] = __dadd_rn(__dmul_rn(re, sn), __dmul_rn(im, cs));
             }
@@ -563,7 +565,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int v = 0; v < 2; ++v) {
             const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
             const bool ok = rok && i < m;
-            yi[jc][v] = ok ? ybase + pre * static_cast<long long>(i) : -1;
+            yi[jc][v] = ok ? ybase + ycol * static_cast<long long>(i) : -1;
             uu[jc][v] = ok ? ep.u[yi[jc][v]] : 0.0;
             dg[jc][v] = (ok && ep.diag) ? ep.diag[ep.cplx ? (yi[jc][v] >> 1) : yi[jc][v]] : 0.0;
           }
@@ -587,7 +589,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const long long p = rr - q * pre;
         const long long ybase = p + q * args.ldy;
         const double lam_lo =
-            (EK == EK_GENERIC && spectral) ? lambda_partial_low_ext(ep, p, ep.axis) : 0.0;
+            (EK == EK_GENERIC && spectral) ? lambda_partial_low_ext(ep, args.rot ? rr : p, ep.axis)
+                                            : 0.0;
 #pragma unroll
         for (int jc = 0; jc < C::CT; ++jc) {
 #pragma unroll
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
             const bool ok = rok && i < m;
             double val = acc[j][jc][v];
-            const long long yi = ybase + pre * static_cast<long long>(ok ? i : 0);
+            const long long yi = ybase + ycol * static_cast<long long>(ok ? i : 0);
             if (EK == EK_GENERIC) {
               if (spectral) {
                 // PHASE: the re/im partner (row r ^ 1) is this thread's tile j ^ 1 (paired maps)
@@ -793,6 +796,11 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
   ta.post = ps.post;
   ta.R = ps.pre * ps.post;
   ta.ldy = ps.ldy_eff();
+  ta.ycol = ps.ycol ? ps.ycol : ps.pre;
+  ta.rot = ps.rot;
+  param_check(!ps.rot || ep.axis + 1 >= ep.ndims || (ep.kind != EPI_SPEC_MUL &&
+              ep.kind != EPI_SPEC_DIV && ep.kind != EPI_SPEC_PHASE),
+              "mode_product: rotated pass with a spectral epilogue must be on the last axis");
   ta.nk = ps.nk;
   ta.m = ps.m;
   ta.ep = ep;

@@ -58,6 +58,8 @@ print("ok", kind)
 
 @pytest.mark.parametrize("var,val,kind", [
     ("KRONOP_DISABLE_TMA", "1", "fp64_3d"),           # cp.async pass kernel for every geometry
+    ("KRONOP_ROTATE_PASSES", "0", "fp64_3d"),         # axis-order passes (STRIDED TMA loader)
+    ("KRONOP_ROTATE_PASSES", "0", "fp64_254"),
     ("KRONOP_TMA_CLUSTER", "2", "fp64_254"),          # X multicast across 2-CTA clusters
     ("KRONOP_TMA_CLUSTER", "4", "fp64_254"),          # ... 4-CTA clusters
     ("KRONOP_DISABLE_FUSED_SMALL", "1", "small_6d"),  # generic per-axis passes for n <= 32
