@@ -61,16 +61,32 @@ constexpr int RT_TILE = 8192;  // doubles per stage (64 KB)
 #ifndef KRONOP_DF_TILE
 #define KRONOP_DF_TILE 6144
 #endif
+// the same knobs for the DMMA path (n > 10), for A/B builds
+#ifndef KRONOP_DM_THREADS
+#define KRONOP_DM_THREADS 512
+#endif
+#ifndef KRONOP_DM_CTAS
+#define KRONOP_DM_CTAS 1
+#endif
+#ifndef KRONOP_DM_STAGES
+#define KRONOP_DM_STAGES 3
+#endif
+#ifndef KRONOP_DM_TILE
+#define KRONOP_DM_TILE 8192
+#endif
 template <int DN>
 __host__ __device__ constexpr int rt_threads() {
-  return DN > 0 && KRONOP_DF_THREADS > 0 ? KRONOP_DF_THREADS : rt_threads_default<DN>();
+  return DN > 0 ? (KRONOP_DF_THREADS > 0 ? KRONOP_DF_THREADS : rt_threads_default<DN>())
+                : KRONOP_DM_THREADS;
 }
 template <int DN>
-__host__ __device__ constexpr int rt_ctas() { return DN > 0 ? KRONOP_DF_CTAS : 1; }
+__host__ __device__ constexpr int rt_ctas() { return DN > 0 ? KRONOP_DF_CTAS : KRONOP_DM_CTAS; }
 template <int DN>
-__host__ __device__ constexpr int rt_stages() { return DN > 0 ? KRONOP_DF_STAGES : RT_STAGES; }
+__host__ __device__ constexpr int rt_stages() {
+  return DN > 0 ? KRONOP_DF_STAGES : KRONOP_DM_STAGES;
+}
 template <int DN>
-__host__ __device__ constexpr int rt_tile() { return DN > 0 ? KRONOP_DF_TILE : RT_TILE; }
+__host__ __device__ constexpr int rt_tile() { return DN > 0 ? KRONOP_DF_TILE : KRONOP_DM_TILE; }
 
 struct RotArgs {
   const double* x;
@@ -254,6 +270,31 @@ __device__ __forceinline__ void axis_dfma(double* tile, const double (&M)[N][N],
   }
 }
 
+// The same with the stride and fiber count known at compile time (isotropic three-axis group,
+// C known, C Qt = 8): the fiber -> address map is a division by a constant and the strided
+// loads / stores take immediate offsets (the runtime version spent ~25% of its issue slots on
+// the float-reciprocal division and address arithmetic, profiles/r02_rot9.json).
+template <int N, int THREADS, int S, int NFIB>
+__device__ __forceinline__ void axis_dfma_ct(double* tile, const double (&M)[N][N], int tid) {
+  constexpr int Sm = S * N;
+#pragma unroll 1
+  for (int f = tid; f < NFIB; f += THREADS) {
+    double* p = tile + f + (f / S) * (Sm - S);
+    double x[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) x[k] = p[k * S];
+    double acc[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fma(M[i][k], x[k], acc[i]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) p[i * S] = acc[i];
+  }
+}
+
 // lambda of one output: the axes below the group (lam_low, per q), then the group axes in order
 // (axis order from 0.0, direct_sum_grid tensor.cpp:196-209).
 template <int NF>
@@ -346,7 +387,8 @@ __device__ __forceinline__ void store_tile(const RotArgs& A, const double* tile,
   }
 }
 
-template <int NF, int K4, int NT, int DN>
+// CC > 0 (DFMA, isotropic three-axis group with C = CC and C Qt = 8): compile-time geometry
+template <int NF, int K4, int NT, int DN, int CC = 0>
 __global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_kernel(const __grid_constant__ RotArgs A) {
   constexpr int THREADS = rt_threads<DN>();
   constexpr int RT_STAGES = rt_stages<DN>();
@@ -435,6 +477,16 @@ __global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_ker
       lam_low[tid] = lam;
     }
     mbar_wait(&full[s], (it / RT_STAGES) & 1);
+    if constexpr (DN > 0 && CC > 0 && NF == 3) {
+      if (!mloaded) load_matrix<DN>(Mreg, frags);
+      mloaded = true;
+      axis_dfma_ct<DN, THREADS, CC, 8 * DN * DN>(buf, Mreg, tid);
+      __syncthreads();
+      axis_dfma_ct<DN, THREADS, CC * DN, 8 * DN * DN>(buf, Mreg, tid);
+      __syncthreads();
+      axis_dfma_ct<DN, THREADS, CC * DN * DN, 8 * DN * DN>(buf, Mreg, tid);
+      __syncthreads();
+    } else {
     int S = A.C;
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
@@ -449,6 +501,7 @@ __global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_ker
                                          warp, lane);
       S *= m;
       __syncthreads();
+    }
     }
     store_tile<NF, THREADS>(A, buf, q0, qv, lam_low, tid);
     // No CTA barrier here: a warp that has stored its share moves on to the next tile's first
@@ -477,13 +530,13 @@ constexpr size_t rot_smem_bytes() {
          rt_stages<DN>() * (2 * sizeof(uint64_t) + sizeof(int)) + 16;
 }
 
-template <int NF, int K4, int NT, int DN = 0>
+template <int NF, int K4, int NT, int DN = 0, int CC = 0>
 void launch_rot(cudaStream_t s, const RotArgs& a) {
-  ensure_smem_attr(reinterpret_cast<const void*>(fused_rot_kernel<NF, K4, NT, DN>),
+  ensure_smem_attr(reinterpret_cast<const void*>(fused_rot_kernel<NF, K4, NT, DN, CC>),
                    rot_smem_bytes<NF, K4, NT, DN>());
   const int grid_cap = device_sm_count() * rt_ctas<DN>();
   const long long grid = a.ntiles < grid_cap ? a.ntiles : grid_cap;
-  fused_rot_kernel<NF, K4, NT, DN>
+  fused_rot_kernel<NF, K4, NT, DN, CC>
       <<<static_cast<unsigned>(grid), rt_threads<DN>(), rot_smem_bytes<NF, K4, NT, DN>(), s>>>(a);
   KCUDA(cudaGetLastError());
 }
@@ -713,10 +766,10 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
   // every (f, n) has an instantiation; the group must fit a DFMA stage (C Qt >= 8)
   const bool use_dfma = dfma_ok && (!spectral || split) && 8 * a.F <= KRONOP_DF_TILE;
   // C * Qt: the largest power of two >= 8 with C * Qt * F <= the stage size of the path
-  const int tile_doubles = use_dfma ? KRONOP_DF_TILE : RT_TILE;
+  const int tile_doubles = use_dfma ? KRONOP_DF_TILE : KRONOP_DM_TILE;
   int cqt = 8;
   while (cqt * 2 * a.F <= tile_doubles && cqt < 64) cqt *= 2;
-  param_check(cqt * a.F <= RT_TILE, "fused_rot: group too large for a stage");
+  param_check(cqt * a.F <= tile_doubles, "fused_rot: group too large for a stage");
   a.lcq = 0;
   while ((1 << a.lcq) < cqt) ++a.lcq;
   a.Qt = cqt / a.C;
@@ -746,7 +799,18 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
   // fused epilogue: the spectral launch keeps the 16-warp DMMA kernel (its store pass, one sincos
   // per pair, is latency bound and needs the warps more than the contraction needs DFMA)
   bool launched = false;
-  if (use_dfma) {
+  static const bool no_ct = [] {
+    const char* e = getenv("KRONOP_ROT_CT");  // A/B switch: 0 = runtime-geometry DFMA kernel
+    return e && e[0] == '0';
+  }();
+  if (use_dfma && f == 3 && maxn == 9 && a.uniform && cqt == 8 && !no_ct) {
+    launched = true;  // the config-5 9D group: compile-time geometry
+    if (a.C == 2)
+      launch_rot<3, 1, 1, 9, 2>(s, a);
+    else
+      launch_rot<3, 1, 1, 9, 1>(s, a);
+  }
+  if (use_dfma && !launched) {
     launched = true;
     switch (f * 16 + maxn) {
 #define RT_DF(F, N) \

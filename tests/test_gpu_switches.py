@@ -29,7 +29,7 @@ def rel(a, b):
 
 L, cells, k, d = {"fp64_3d": (8.0, 13, 5, 3), "fp64_254": (8.0, 51, 5, 3),
                   "small_6d": (5.0, 2, 3, 6), "small_9d": (3.0, 1, 4, 7),
-                  "lowp": (8.0, 13, 5, 3)}[kind]
+                  "lowp": (8.0, 13, 5, 3), "rot_9": (3.0, 2, 5, 6)}[kind]
 g = A.Grid.sem(L, cells, k, d)
 op = g.separable_operator(ctx, [lambda t: t * t] * d, shift=-0.25)
 b = K.seeded_field(g.shape, 5)
@@ -64,6 +64,7 @@ print("ok", kind)
     ("KRONOP_TMA_CLUSTER", "4", "fp64_254"),          # ... 4-CTA clusters
     ("KRONOP_DISABLE_FUSED_SMALL", "1", "small_6d"),  # generic per-axis passes for n <= 32
     ("KRONOP_ROT_NO_DFMA", "1", "small_9d"),          # DMMA instead of DFMA for n <= 10
+    ("KRONOP_ROT_CT", "0", "rot_9"),                  # runtime-geometry DFMA kernel for n = 9
     ("KRONOP_ROT_SPEC_SPLIT", "0", "small_9d"),       # phase fused into the contraction
     ("KRONOP_ROT_SPEC_SPLIT", "1", "small_6d"),       # standalone spectral pass everywhere
     ("KRONOP_TC_CLUSTER", "2", "lowp"),               # B multicast in the tcgen05 pass
