@@ -803,12 +803,12 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
     const char* e = getenv("KRONOP_ROT_CT");  // A/B switch: 0 = runtime-geometry DFMA kernel
     return e && e[0] == '0';
   }();
-  if (use_dfma && f == 3 && maxn == 9 && a.uniform && cqt == 8 && !no_ct) {
-    launched = true;  // the config-5 9D group: compile-time geometry
-    if (a.C == 2)
-      launch_rot<3, 1, 1, 9, 2>(s, a);
-    else
-      launch_rot<3, 1, 1, 9, 1>(s, a);
+  // the config-5 9D group of a real field: compile-time geometry (9D solve 15.7 -> 14.5 ms); for
+  // complex fields it measured slower (9D propagate 25.8 -> 30.2 ms), so they keep the runtime
+  // kernel (profiles/r02_rot_variants.json)
+  if (use_dfma && f == 3 && maxn == 9 && a.uniform && cqt == 8 && a.C == 1 && !no_ct) {
+    launched = true;
+    launch_rot<3, 1, 1, 9, 1>(s, a);
   }
   if (use_dfma && !launched) {
     launched = true;

@@ -64,7 +64,7 @@ print("ok", kind)
     ("KRONOP_TMA_CLUSTER", "4", "fp64_254"),          # ... 4-CTA clusters
     ("KRONOP_DISABLE_FUSED_SMALL", "1", "small_6d"),  # generic per-axis passes for n <= 32
     ("KRONOP_ROT_NO_DFMA", "1", "small_9d"),          # DMMA instead of DFMA for n <= 10
-    ("KRONOP_ROT_CT", "0", "rot_9"),                  # runtime-geometry DFMA kernel for n = 9
+    ("KRONOP_ROT_CT", "0", "rot_9"),                  # runtime-geometry DFMA kernel, real n = 9
     ("KRONOP_ROT_SPEC_SPLIT", "0", "small_9d"),       # phase fused into the contraction
     ("KRONOP_ROT_SPEC_SPLIT", "1", "small_6d"),       # standalone spectral pass everywhere
     ("KRONOP_TC_CLUSTER", "2", "lowp"),               # B multicast in the tcgen05 pass
