@@ -5,7 +5,7 @@ mode-product passes (T^{-1}), the fused spectral divide, 3 backward passes (T). 
 L = 8 (n = 1024), harmonic V1 = x^2 per axis, rhs = SplitMix64(seed = 1) uniform [-1, 1)
 (harness.cpp:184-189). Fields are 8 GiB each (>> 126 MB L2), so no L2 flush is needed.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kronop|reference] [--n 1024]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kronop|reference] [--extent 1024]
 
 --impl reference times the reference's CPU path on the host cores at the same 1024^3 workload (no
 scaling): the C++ -O3 -fopenmp restatement of tensor.cpp / operators.cpp in oracle/cpu (the
@@ -13,7 +13,7 @@ reference itself cannot be built here, Eigen3 is absent), one ful
 Multi-GPU (--gpus N self-launches torch.distributed.run; one rank per GPU): the same solve is
 slab-decomposed through the C-ABI (kronop_slab_create_nccl, csrc/slab.cu): axes 0-1
 local, two NCCL all-to-all transposes for the last axis; total work fixed => "scaling": "strong";
-time = max over ranks of CUDA-event time. --n 2048 selects the 2048^3 scaling grid (Q3 x 683).
+time = max over ranks of CUDA-event time. --extent 2048 selects the 2048^3 scaling grid (Q3 x 683).
 """
 import argparse
 import json
@@ -164,6 +164,8 @@ def cpu_reference_operator(n):
     the oracle's axis factorisation (numpy build_axis; harmonic V1, so the three axes are equal)."""
     from oracle import kronop_oracle as K
     from oracle import kronop_cpu as KC
+    # every host core, whatever OMP_NUM_THREADS a launcher set (torchrun sets 1 per rank)
+    KC.lib(os.cpu_count() or 1)
     ax = K.build_axis(K.assemble_sem(8.0, workload_config(n), workload_degree(n)), lambda t: t * t)
     return KC, KC.CpuOperator([ax] * 3)
 
@@ -195,7 +197,8 @@ def run_reference(args):
         "steps_requested": args.steps, "warmup": warm, "ms_per_step": t * 1e3,
         "step_ms": [round(x * 1e3, 1) for x in secs], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "3D (-Delta+V1)^-1 solve, harmonic V1, SEM Q5 205 cells L=8, n=%d" % n,
+        "config": {"workload": "3D (-Delta+V1)^-1 solve, harmonic V1, SEM Q%d %d cells L=8, n=%d"
+                               % (workload_degree(n), workload_config(n), n),
                    "n": n, "dof": N},
         "cpu_baseline": {"value": gdofs, "unit": "GDoF/s", "cores": cores, "kind": "port",
                          "sample": sample},
@@ -708,8 +711,8 @@ def run_kronop(args):
             "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "3D (-Delta+V1)^-1 solve, harmonic V1, SEM Q5 205 cells L=8, "
-                                   "n=%d (BASELINE configs[1])" % n,
+            "config": {"workload": "3D (-Delta+V1)^-1 solve, harmonic V1, SEM Q%d %d cells L=8, "
+                                   "n=%d (BASELINE configs[1])" % (workload_degree(n), cells, n),
                        "n": n, "dof": N, "parallelism": "replicas" if world > 1 else "single",
                        "l2": "inputs (8 GiB/field) larger than L2; no flush"},
             "tflops": 12.0 * n ** 4 / t_step / 1e12,
@@ -751,7 +754,7 @@ def run_kronop_slab(args):
     slab-decomposed through the C-ABI (kronop_slab_create_nccl, csrc/slab.cu): axes 0-1 local,
     two NCCL all-to-all transposes (grouped send / recv per plane) for the last axis. Total work
     fixed => "scaling": "strong"; time = max over ranks of the CUDA-event time on the rank's
-    stream. --n 2048 runs the 2048^3 scaling grid (Q3 x 683 cells, 64 GiB per field)."""
+    stream. --extent 2048 runs the 2048^3 scaling grid (Q3 x 683 cells, 64 GiB per field)."""
     import torch
     import torch.distributed as dist
     world, rank, local = dist_init()
@@ -856,7 +859,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kronop", choices=["kronop", "reference"])
-    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--extent", dest="n", type=int, default=1024,
+                    help="grid extent per axis (1024 = Q5 x 205 cells; 2048 = Q3 x 683 cells)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--slab", action="store_true", help="force the slab-decomposed path (any N)")
