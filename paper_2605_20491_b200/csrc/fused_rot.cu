@@ -74,6 +74,12 @@ constexpr int RT_TILE = 8192;  // doubles per stage (64 KB)
 #ifndef KRONOP_DM_TILE
 #define KRONOP_DM_TILE 8192
 #endif
+// DMMA path: the CTA's warps form KRONOP_DM_GROUPS independent groups that take alternate tiles,
+// each synchronising on its own named barrier, so one group's store phase and barrier waits
+// overlap the other's contraction (two CTAs per SM do not fit the shared memory)
+#ifndef KRONOP_DM_GROUPS
+#define KRONOP_DM_GROUPS 2
+#endif
 template <int DN>
 __host__ __device__ constexpr int rt_threads() {
   return DN > 0 ? (KRONOP_DF_THREADS > 0 ? KRONOP_DF_THREADS : rt_threads_default<DN>())
@@ -398,13 +404,29 @@ __global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_ker
   // DN == 0: DMMA path (B fragments in fragment order)
   constexpr int DNP = (DN + 1) & ~1;
   constexpr int FRAG = DN > 0 ? DN * DNP : K4 * NT * 32;  // doubles per axis
+  constexpr int GROUPS = DN > 0 ? 1 : KRONOP_DM_GROUPS;
+  constexpr int GT = THREADS / GROUPS;  // threads per group
   extern __shared__ __align__(128) double sm[];
   double* stages = sm;                                   // RT_STAGES x RT_TILE
   double* frags = stages + RT_STAGES * RT_TILE;          // NF x FRAG
-  double* lam_low2 = frags + NF * FRAG;                  // 2 x 64 (Qt), double-buffered per tile
-  uint64_t* full = reinterpret_cast<uint64_t*>(lam_low2 + 128);
+  double* lam_low2 = frags + NF * FRAG;  // 2 x 64 (Qt) per group (<= 4), double-buffered per tile
+  uint64_t* full = reinterpret_cast<uint64_t*>(lam_low2 + 512);
+  static_assert(GROUPS >= 1 && GROUPS <= 4 && THREADS % (32 * GROUPS) == 0, "warp groups");
   int* done = reinterpret_cast<int*>(full + RT_STAGES);  // per-stage count of warps finished
+  // per-stage count of loads issued: with several warp groups a group can reach the next use of
+  // a stage before the other group has consumed and refilled it, when the barrier would still
+  // show the parity of the use before (phases two apart look alike) -- so a group first waits
+  // until the load it needs has been issued
+  int* issued = done + RT_STAGES;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = tid / GT, gtid = tid - grp * GT, gwarp = gtid >> 5;
+  (void)warp;
+  auto gsync = [&]() {
+    if constexpr (GROUPS == 1)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(GT) : "memory");
+  };
   const int t = lane & 3;
   const bool spectral = A.epi == EPI_SPEC_MUL || A.epi == EPI_SPEC_DIV || A.epi == EPI_SPEC_PHASE;
 
@@ -444,6 +466,7 @@ __global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_ker
     for (int s = 0; s < RT_STAGES; ++s) {
       mbar_init(&full[s], 1);
       done[s] = 0;
+      issued[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -452,21 +475,27 @@ __global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_ker
   if (tid == 0)
     for (int s = 0; s < RT_STAGES; ++s) {
       const long long tile = blockIdx.x + static_cast<long long>(s) * gridDim.x;
-      if (tile < A.ntiles) issue_tile(A, tile, stages + s * RT_TILE, &full[s]);
+      if (tile < A.ntiles) {
+        issue_tile(A, tile, stages + s * RT_TILE, &full[s]);
+        issued[s] = 1;
+      }
     }
 
   const int tile_elems = A.Qt * A.C * A.F;
   double Mreg[DN > 0 ? DN : 1][DN > 0 ? DN : 1];  // DFMA path: the axis matrix in registers
   bool mloaded = false;
-  int it = 0;
-  for (long long tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++it) {
+  for (int kt = 0;; ++kt) {
+    const int it = kt * GROUPS + grp;  // this group's tiles: it = grp, grp + GROUPS, ...
+    const long long tile = blockIdx.x + static_cast<long long>(it) * gridDim.x;
+    if (tile >= A.ntiles) break;
     const int s = it % RT_STAGES;
     double* buf = stages + s * RT_TILE;
     const long long q0 = tile * A.Qt;
     const int qv = static_cast<int>(A.Q - q0 < A.Qt ? A.Q - q0 : A.Qt);
-    double* lam_low = lam_low2 + 64 * (it & 1);  // warps may still store the previous tile
-    if (spectral && tid < A.Qt) {  // lambda of the axes below the group, axis order from 0.0
-      long long q = q0 + tid;
+    // the group's warps may still store its previous tile
+    double* lam_low = lam_low2 + 64 * (2 * grp + (kt & 1));
+    if (spectral && gtid < A.Qt) {  // lambda of the axes below the group, axis order from 0.0
+      long long q = q0 + gtid;
       double lam = 0.0;
       for (int j = 0; j < A.nq; ++j) {
         const long long e = A.qext[j];
@@ -474,7 +503,13 @@ __global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_ker
         q /= e;
         lam = __dadd_rn(lam, A.lam_q[j][idx]);
       }
-      lam_low[tid] = lam;
+      lam_low[gtid] = lam;
+    }
+    if constexpr (GROUPS > 1) {
+      if (lane == 0)
+        while (*reinterpret_cast<volatile int*>(&issued[s]) <= it / RT_STAGES) {
+        }
+      __syncwarp();
     }
     mbar_wait(&full[s], (it / RT_STAGES) & 1);
     if constexpr (DN > 0 && CC > 0 && NF == 3) {
@@ -497,26 +532,28 @@ __global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_ker
         mloaded = true;
         axis_dfma<DN, THREADS>(buf, Mreg, S, tile_elems / DN, tid);
       } else
-        axis_inplace<K4, NT, G, THREADS>(buf, frags + j * FRAG, koff[j], m, S, tile_elems / m,
-                                         warp, lane);
+        axis_inplace<K4, NT, G, GT>(buf, frags + j * FRAG, koff[j], m, S, tile_elems / m,
+                                    gwarp, lane);
       S *= m;
-      __syncthreads();
+      gsync();
     }
     }
-    store_tile<NF, THREADS>(A, buf, q0, qv, lam_low, tid);
+    store_tile<NF, GT>(A, buf, q0, qv, lam_low, gtid);
     // No CTA barrier here: a warp that has stored its share moves on to the next tile's first
     // axis (another stage) while the others finish storing. The last warp to finish with stage
     // s refills it.
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
-      if (atomicAdd(&done[s], 1) == THREADS / 32 - 1) {
+      if (atomicAdd(&done[s], 1) == GT / 32 - 1) {
         done[s] = 0;
         __threadfence_block();
         const long long next = tile + static_cast<long long>(RT_STAGES) * gridDim.x;
         if (next < A.ntiles) {
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           issue_tile(A, next, buf, &full[s]);
+          __threadfence_block();
+          atomicAdd(&issued[s], 1);
         }
       }
     }
@@ -526,8 +563,8 @@ __global__ void __launch_bounds__(rt_threads<DN>(), rt_ctas<DN>()) fused_rot_ker
 template <int NF, int K4, int NT, int DN>
 constexpr size_t rot_smem_bytes() {
   constexpr int FRAG = DN > 0 ? DN * ((DN + 1) & ~1) : K4 * NT * 32;
-  return (static_cast<size_t>(rt_stages<DN>()) * rt_tile<DN>() + NF * FRAG + 128) * sizeof(double) +
-         rt_stages<DN>() * (2 * sizeof(uint64_t) + sizeof(int)) + 16;
+  return (static_cast<size_t>(rt_stages<DN>()) * rt_tile<DN>() + NF * FRAG + 512) * sizeof(double) +
+         rt_stages<DN>() * (2 * sizeof(uint64_t) + 2 * sizeof(int)) + 16;
 }
 
 template <int NF, int K4, int NT, int DN = 0, int CC = 0>
