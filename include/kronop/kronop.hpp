@@ -645,6 +645,36 @@ class SlabOperator {
     });
   }
   // pcg(FullOperator{this, diagonal}.apply, this.solve, b, x&) (pcg.cpp:8-81); x in/out
+  // gpe_gradient_flow, a_u flow (gpe.cpp:55-165) on the Hamiltonian this + diagonal (V2 or
+  // null); config.kind must be AdaptiveMetric, init Constant (or Supplied with `initial`).
+  // `state` receives the final state (host, value semantics).
+  GpeResult gpe_au(const RealField* diagonal, double beta, const GpeFlowConfig& config,
+                   RealField& state, const RealField* initial = nullptr) const {
+    Parts dd(*this, 1), di(*this, 1), ds(*this, 1);
+    if (diagonal)
+      check(kronop_slab_scatter(slab_.get(), diagonal->data(), 0, dd.p.data()));
+    if (initial)
+      check(kronop_slab_scatter(slab_.get(), initial->data(), 0, di.p.data()));
+    kronop_gpe_config c{KRONOP_GPE_AU, config.step, config.metric_shift, config.energy_rel_tol,
+                        config.max_iterations, config.inner.c(),
+                        config.init == GpeInit::Supplied ? KRONOP_GPE_INIT_SUPPLIED
+                                                         : KRONOP_GPE_INIT_CONSTANT,
+                        config.record_history ? 1 : 0};
+    kronop_gpe_result r{};
+    std::vector<double> hist(config.record_history ? 5 * static_cast<size_t>(config.max_iterations)
+                                                   : 0);
+    check(kronop_slab_gpe_au(slab_.get(), diagonal ? dd.p.data() : nullptr, beta, &c,
+                             initial ? di.p.data() : nullptr, ds.p.data(), &r,
+                             config.record_history ? hist.data() : nullptr));
+    check(kronop_slab_gather(slab_.get(), ds.p.data(), 0, state.data()));
+    GpeResult out{r.energy, r.eigenvalue, r.iterations, static_cast<long>(r.linear_solves),
+                  r.converged != 0, {}};
+    for (int i = 0; i < r.history_len; ++i)
+      out.history.push_back({static_cast<int>(hist[5 * i]), hist[5 * i + 1], hist[5 * i + 2],
+                             static_cast<long>(hist[5 * i + 3]), hist[5 * i + 4]});
+    return out;
+  }
+
   PcgReport pcg(const RealField* diagonal, const RealField& b, RealField& x,
                 const PcgConfig& cfg) const {
     Parts db(*this, 1), dx(*this, 1), dd(*this, 1);

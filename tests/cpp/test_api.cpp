@@ -258,6 +258,28 @@ int main() {
       CHECK(es < 1e-13 && ea < 1e-13 && ep < 1e-13);
       std::printf("ok slab P=%d solve %.2e apply %.2e propagate %.2e\n", P, es, ea, ep);
     }
+    // a_u GPE flow on 3 virtual slabs equals the single-device flow (gpe.cpp:118-157)
+    auto mass = std::make_shared<const MassWeights>(MassWeights{b.mass, b.mass, b.mass});
+    SeparableOperator ham(ctx, axes, 0.0, mass);
+    SeparableOperator lap(ctx, {build_axis(b, [](double) { return 0.0; }),
+                                build_axis(b, [](double) { return 0.0; }),
+                                build_axis(b, [](double) { return 0.0; })}, 0.0, mass);
+    GpeProblem prob{FullOperator{&ham, nullptr}, &lap, 10.0};
+    GpeFlowConfig cfg;
+    cfg.kind = GpeFlowKind::AdaptiveMetric;
+    cfg.step = 1.0;
+    cfg.energy_rel_tol = 1e-30;
+    cfg.max_iterations = 6;
+    cfg.init = GpeInit::Constant;
+    DeviceField<double> gst(ctx, Shape{n, n, n});
+    const GpeResult g1 = gpe_gradient_flow(prob, cfg, gst);
+    SlabOperator so(std::vector<int>(3, 0), axes, 0.0, mass);
+    RealField sst({n, n, n});
+    const GpeResult g3 = so.gpe_au(nullptr, 10.0, cfg, sst);
+    CHECK(g3.iterations == g1.iterations && g3.linear_solves == g1.linear_solves);
+    CHECK(std::abs(g3.energy - g1.energy) <= 1e-11 * std::abs(g1.energy));
+    std::printf("ok slab gpe_au E %.12f vs %.12f, %ld solves\n", g3.energy, g1.energy,
+                g3.linear_solves);
   }
 
   std::printf("all %d checks passed\n", g_checks);
