@@ -14,7 +14,7 @@ OUT = os.path.join(HERE, "libkronop.so")
 BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["mode_product.cu", "mode_product_tma.cu", "fused_rot.cu", "vector_ops.cu", "capi.cu", "drivers.cu", "fieldio.cu", "tc_lowp.cu", "ozaki.cu", "slab.cu"]
+CU = ["mode_product.cu", "mode_product_tma.cu", "fused_rot.cu", "vector_ops.cu", "capi.cu", "drivers.cu", "fieldio.cu", "tc_lowp.cu", "ozaki.cu", "slab.cu", "kron_prop.cu"]
 CPP = ["host_setup.cpp"]
 
 

@@ -202,12 +202,98 @@ static void sep_transform_folded(kronop_ctx& ctx, const kronop_op& op, const dou
   }
 }
 
+// Kronecker-factored propagate (kron_prop.cu) for complex fields whose axes all have n <= 10:
+// e^{-i (lambda - shift) dt} applied as e^{i shift dt} (x)_a E_a with
+// E_a = T_a diag(e^{-i lambda_a dt}) T_a^{-1} (operators.cpp:63-75 re-associated: the exponential
+// of a Kronecker sum is the Kronecker product of the exponentials). E_a is formed here in extended
+// precision from the host copies of T, T^{-1}, lambda; the shift's phase goes into the first
+// axis. Row-major [i][k] complex (re, im), as the kernel reads it.
+static void kron_prop_matrix(const kronop_op& op, int a, double dt, double shift_phase,
+                             double* E) {
+  const int n = op.n[a];
+  const std::vector<double>& T = op.hT[a];
+  const std::vector<double>& Ti = op.hTinv[a];
+  std::vector<long double> cr(n), ci(n);
+  for (int m = 0; m < n; ++m) {
+    const long double ph = -static_cast<long double>(op.hlam[a][m]) * dt;
+    cr[m] = std::cos(ph);
+    ci[m] = std::sin(ph);
+  }
+  const long double gr = std::cos(static_cast<long double>(shift_phase));
+  const long double gi = std::sin(static_cast<long double>(shift_phase));
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k) {
+      long double sr = 0.0L, si = 0.0L;
+      for (int m = 0; m < n; ++m) {
+        const long double t = static_cast<long double>(T[i + static_cast<size_t>(n) * m]) *
+                              Ti[m + static_cast<size_t>(n) * k];
+        sr += t * cr[m];
+        si += t * ci[m];
+      }
+      E[2 * (i * n + k)] = static_cast<double>(sr * gr - si * gi);
+      E[2 * (i * n + k) + 1] = static_cast<double>(sr * gi + si * gr);
+    }
+}
+
+// Groups for the Kronecker propagate: up to three consecutive axes of the same extent; empty when
+// some axis is outside the kernel's range or the host copies are missing.
+static std::vector<std::pair<int, int>> kron_groups(const kronop_op& op) {
+  std::vector<std::pair<int, int>> groups;
+  static const bool off = [] {
+    const char* e = getenv("KRONOP_KRON_PROP");  // A/B switch: 0 = transform / phase / transform
+    return e && e[0] == '0';
+  }();
+  if (off || op.folded || op.exec_prec != KRONOP_PREC_FP64) return groups;
+  for (int a = 0; a < op.d; ++a)
+    if (op.hT[a].empty() || !kron_group_supported(op.n[a], 1)) return groups;
+  for (int a = 0; a < op.d;) {
+    int f = 1;
+    while (a + f < op.d && f < 3 && op.n[a + f] == op.n[a]) ++f;
+    groups.emplace_back(a, f);
+    a += f;
+  }
+  return groups;
+}
+
+static bool sep_propagate_kron(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out,
+                               double shift, double dt, bool bphase, const double* bfield,
+                               double bfactor) {
+  const std::vector<std::pair<int, int>> groups = kron_groups(op);
+  if (groups.empty() || !fused_rot_eligible(in) || !fused_rot_eligible(out)) return false;
+  const size_t nd = static_cast<size_t>(op.N) * 2;
+  ensure_scratch(ctx, nd);
+  const int ng = static_cast<int>(groups.size());
+  std::vector<double> E(3 * 10 * 10 * 2);
+  const double* src = in;
+  for (int g = 0; g < ng; ++g) {
+    const int a0 = groups[g].first, f = groups[g].second, n = op.n[a0];
+    for (int j = 0; j < f; ++j)
+      kron_prop_matrix(op, a0 + j, dt, (g == 0 && j == 0) ? shift * dt : 0.0,
+                       E.data() + static_cast<size_t>(j) * n * n * 2);
+    const bool last = g == ng - 1;
+    // a launch must not write its own input (other CTAs still read the tiles it overwrites)
+    double* dst = (last && src != out) ? out
+                  : src == ctx.scratch[0]  ? ctx.scratch[1]
+                                           : ctx.scratch[0];
+    launch_kron_group(ctx.stream, src, dst, n, f, op.N, E.data(), last && bphase ? bfield : nullptr,
+                      bfactor, last && bphase ? 1 : 0);
+    ctx.ws.launches += 1;
+    src = dst;
+  }
+  if (src != out)
+    KCUDA(cudaMemcpyAsync(out, src, nd * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+  return true;
+}
+
 // Small-extent path, rotating layout (fused_rot.cu): groups of up to 3 consecutive axes (fused
 // extent <= 1024), forward groups then backward groups; each launch moves its group to the slow
 // end, so after each direction the layout is the caller's again.
 static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out,
                               int cplx, SepKind kind, double shift, double dt, const double* diag,
                               double sigma, bool bphase, const double* bfield, double bfactor) {
+  if (kind == SEP_PROPAGATE && cplx && diag == nullptr && sigma == 0.0 &&
+      sep_propagate_kron(ctx, op, in, out, shift, dt, bphase, bfield, bfactor))
+    return;
   const size_t nd = static_cast<size_t>(op.N) * (cplx ? 2 : 1);
   ensure_scratch(ctx, nd);
   std::vector<std::pair<int, int>> groups;
@@ -765,6 +851,10 @@ int kronop_op_create(kronop_ctx* ctx, int d, const int* n, const double* const* 
         op->n[a] = n[a];
         op->N *= n[a];
         op->hlam[a].assign(lambda[a], lambda[a] + n[a]);
+        if (n[a] <= 32) {
+          op->hT[a].assign(T[a], T[a] + static_cast<size_t>(n[a]) * n[a]);
+          op->hTinv[a].assign(Tinv[a], Tinv[a] + static_cast<size_t>(n[a]) * n[a]);
+        }
         // an axis identical to an earlier one (isotropic grids) shares its device transforms:
         // less memory, and the small-extent kernel can keep one matrix in registers for a group
         int same = -1;

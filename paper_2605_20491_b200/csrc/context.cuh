@@ -53,6 +53,9 @@ struct kronop_op {
   bool has_mass = false;
   std::vector<double> hlam[KRONOP_MAX_DIM];
   std::vector<double> hmass[KRONOP_MAX_DIM];
+  // host copies of T and T^{-1} (column-major n x n) for axes with n <= 32: the Kronecker-factored
+  // small-extent propagate forms E_a = T_a diag(e^{-i lambda_a dt}) T_a^{-1} from them per dt
+  std::vector<double> hT[KRONOP_MAX_DIM], hTinv[KRONOP_MAX_DIM];
   double shift = 0.0, lmin = 0.0, lmax = 0.0;
   // even/odd folded operator (kronop_op_create_folded): per axis the half-size blocks; lam[a] is
   // in folded order [even modes | odd modes]; bwd[a] holds the ground-state column only.

@@ -1,0 +1,143 @@
+"""Kronecker-factored small-extent propagate (csrc/kron_prop.cu).
+
+exp(-i dt (sum_a A_a - shift)) psi is applied as e^{i shift dt} (x)_a E_a psi with
+E_a = T_a diag(e^{-i lambda_a dt}) T_a^{-1}: the map of operators.cpp:63-75 re-associated, one
+complex mode product per axis (groups of <= 3 axes per launch) instead of forward transforms, a
+phase pass and backward transforms. Checked against the oracle's transform / phase / transform
+sequence given the product's own factors (kernel parity, 1e-13 as for every propagate), in place and
+out of place, with the launch count proving the grouped kernel ran, plus the split-step B phase
+fused into the last group's store (bit-identical to the standalone phase pass)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import kronop_oracle as K
+
+pytestmark = pytest.mark.gpu
+
+
+def api():
+    from paper_2605_20491_b200 import api as a
+    return a
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def oracle_op_from(prod_op, shift=0.0):
+    axes = [K.AxisEigens(a.eigenvalues.copy(), a.transform.copy(), a.inverse_transform.copy())
+            for a in prod_op.axes]
+    return K.SeparableOperator(axes, shift)
+
+
+# (axes as (L, cells, degree) -> n = cells * degree - 1, expected launches per propagate)
+CASES = [
+    ([(3.0, 2, 5)] * 3, 1),                        # 3D n = 9: one three-axis group
+    ([(3.0, 2, 5)] * 4, 2),                        # 4D n = 9: 3 + 1
+    ([(2.0, 1, 6)] * 5, 2),                        # 5D n = 5: 3 + 2
+    ([(3.0, 1, 4)] * 9, 3),                        # 9D n = 3: 3 + 3 + 3
+    ([(2.0, 1, 11)] * 3, 1),                       # n = 10 (largest DFMA extent)
+    ([(2.0, 1, 3)] * 2 + [(3.0, 2, 3)] * 2, 2),    # n = 2, 2, 5, 5: 2 + 2
+    ([(3.0, 2, 5), (2.0, 1, 6), (3.0, 2, 5)], 3),  # 9, 5, 9: three one-axis groups
+]
+
+
+@pytest.mark.parametrize("axes,launches", CASES)
+def test_kron_propagate_matches_oracle(ctx, axes, launches):
+    A = api()
+    grid = A.Grid([A.assemble_sem(*a) for a in axes])
+    # anisotropic potentials: a different matrix on every axis of a group
+    pots = [(lambda t, c=c: (1.0 + 0.3 * c) * t * t + 0.1 * c) for c in range(grid.dim)]
+    op = grid.separable_operator(ctx, pots, -0.4)
+    ko = oracle_op_from(op, -0.4)
+    psi = K.seeded_complex_field(grid.shape, 71)
+    for dt in (0.01, 0.37, -0.2):
+        c0 = ctx.launch_count()
+        got = host(op.propagate(dev(psi), dt))
+        assert ctx.launch_count() - c0 == launches
+        assert rel(got, ko.propagate(psi, dt)) < 1e-13, dt
+    p = dev(psi)
+    op.propagate(p, 0.05, out=p)  # in place
+    assert rel(host(p), ko.propagate(psi, 0.05)) < 1e-13
+    assert np.array_equal(host(op.propagate(dev(psi), 0.0)), psi)
+
+
+def test_kron_propagate_config5_9d_shape(ctx):
+    """The config-5 9D group at its production extent (n = 9, three groups of 729) on a 9D grid
+    small enough for the oracle: 9^9 is 387M points, so the test uses the same n = 9 axes on 5D
+    (groups 3 + 2) and 6D (3 + 3) grids and checks unitarity of the 6D result."""
+    A = api()
+    for d, launches in ((5, 2), (6, 2)):
+        grid = A.Grid.sem(3.0, 2, 5, d)
+        op = grid.laplacian(ctx)
+        ko = oracle_op_from(op)
+        psi = K.seeded_complex_field(grid.shape, 72)
+        c0 = ctx.launch_count()
+        got = host(op.propagate(dev(psi), 0.005))
+        assert ctx.launch_count() - c0 == launches
+        assert rel(got, ko.propagate(psi, 0.005)) < 1e-13
+    w = np.ones(1)
+    for m in grid.mass:  # axis 0 fastest
+        w = np.kron(m, w)
+    n0 = float(np.sum(w * np.abs(psi) ** 2))
+    n1 = float(np.sum(w * np.abs(got) ** 2))
+    assert abs(n1 - n0) <= 1e-12 * n0
+
+
+_BPHASE_SNIPPET = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from oracle import kronop_oracle as K
+from paper_2605_20491_b200 import api as A
+ctx = A.Context(0)
+out = {}
+for spec in ((3.0, 2, 5, 4), (3.0, 1, 4, 9), (2.0, 1, 6, 5)):
+    g = A.Grid.sem(*spec)
+    op = g.laplacian(ctx)
+    b = 1.0 + K.uniform_pm1(9, g.node_count())
+    psi = torch.from_numpy(K.seeded_complex_field(g.shape, 73)).cuda()
+    bd = torch.from_numpy(b).cuda()
+    out["q%d" % g.dim] = A.qhop_step(op, bd, psi, 0.02, 3).cpu().numpy()
+    out["y%d" % g.dim] = A.yoshida_step(op, bd, psi, 0.02, 2).cpu().numpy()
+np.savez(sys.argv[1], **out)
+'''
+
+
+def test_kron_fused_b_phase_bit_identical(tmp_path):
+    """B phase in the last Kronecker group's store (KRONOP_BPHASE_FUSED=1) = the standalone
+    phase pass, bit for bit; both equal the oracle's split step to 1e-12."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("1", "0"):
+        f = str(tmp_path / ("k%s.npz" % flag))
+        env = dict(os.environ, KRONOP_BPHASE_FUSED=flag)
+        subprocess.check_call([sys.executable, "-c", _BPHASE_SNIPPET, f], cwd=root, env=env)
+        res[flag] = np.load(f)
+    for k in res["1"].files:
+        assert np.array_equal(res["1"][k], res["0"][k]), k
+
+
+def test_kron_qhop_step_matches_oracle(ctx):
+    A = api()
+    from paper_2605_20491_b200 import potentials as P
+    grid = A.Grid.sem(3.0, 1, 4, 9)
+    op = grid.laplacian(ctx)
+    ko = oracle_op_from(op)
+    b = P.build_potential("coulomb-3d3", grid).nonseparable
+    psi = K.seeded_complex_field(grid.shape, 74)
+    out = host(A.qhop_step(op, dev(b), dev(psi), 0.02, 3))
+    assert rel(out, K.qhop_step(ko, b, psi, 0.02, 3)) < 1e-12
+    out = host(A.yoshida_step(op, dev(b), dev(psi), 0.02, 2))
+    assert rel(out, K.yoshida_step(ko, b, psi, 0.02, 2)) < 1e-12
