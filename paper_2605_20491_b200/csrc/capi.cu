@@ -235,6 +235,38 @@ static void kron_prop_matrix(const kronop_op& op, int a, double dt, double shift
     }
 }
 
+// Parity symmetry of an axis propagator: R E R = E (R: i -> n-1-i) to rounding (64 ulp of the
+// largest entry). Exact for a symmetric box with an even potential; E's asymmetry is then only
+// the rounding of T, T^{-1}.
+static bool kron_fold_symmetric(const double* E, int n) {
+  double emax = 0.0, dmax = 0.0;
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k) {
+      const double* a = E + 2 * (i * n + k);
+      const double* b = E + 2 * ((n - 1 - i) * n + (n - 1 - k));
+      emax = std::max(emax, std::max(std::abs(a[0]), std::abs(a[1])));
+      dmax = std::max(dmax, std::max(std::abs(a[0] - b[0]), std::abs(a[1] - b[1])));
+    }
+  return n >= 2 && dmax <= 64.0 * 2.220446049250313e-16 * emax;
+}
+
+// E (n x n complex, row-major) -> its parity blocks in place: Ae ((M+c) x (M+c)) then Ao (M x M),
+// M = n / 2, c = n % 2 (the layout kr_contract reads with FOLD).
+static void kron_fold_blocks(double* E, int n) {
+  const int M = n / 2, ME = M + n % 2;
+  std::vector<double> out(static_cast<size_t>(n) * n * 2, 0.0);
+  auto at = [&](int i, int k, int c) { return E[2 * (i * n + k) + c]; };
+  for (int i = 0; i < ME; ++i)
+    for (int k = 0; k < ME; ++k)
+      for (int c = 0; c < 2; ++c)
+        out[2 * (i * ME + k) + c] = k < M ? 0.5 * (at(i, k, c) + at(i, n - 1 - k, c)) : at(i, k, c);
+  for (int i = 0; i < M; ++i)
+    for (int k = 0; k < M; ++k)
+      for (int c = 0; c < 2; ++c)
+        out[2 * (ME * ME + i * M + k) + c] = 0.5 * (at(i, k, c) - at(i, n - 1 - k, c));
+  std::copy(out.begin(), out.end(), E);
+}
+
 // Groups for the Kronecker propagate: up to three consecutive axes of the same extent; empty when
 // some axis is outside the kernel's range or the host copies are missing.
 static std::vector<std::pair<int, int>> kron_groups(const kronop_op& op) {
@@ -263,19 +295,28 @@ static bool sep_propagate_kron(kronop_ctx& ctx, const kronop_op& op, const doubl
   const size_t nd = static_cast<size_t>(op.N) * 2;
   ensure_scratch(ctx, nd);
   const int ng = static_cast<int>(groups.size());
+  static const bool no_fold = [] {
+    const char* e = getenv("KRONOP_KRON_FOLD");  // A/B switch: 0 = dense E_a even when symmetric
+    return e && e[0] == '0';
+  }();
   std::vector<double> E(3 * 10 * 10 * 2);
   const double* src = in;
   for (int g = 0; g < ng; ++g) {
     const int a0 = groups[g].first, f = groups[g].second, n = op.n[a0];
-    for (int j = 0; j < f; ++j)
-      kron_prop_matrix(op, a0 + j, dt, (g == 0 && j == 0) ? shift * dt : 0.0,
-                       E.data() + static_cast<size_t>(j) * n * n * 2);
+    bool fold = !no_fold;
+    for (int j = 0; j < f; ++j) {
+      double* e = E.data() + static_cast<size_t>(j) * n * n * 2;
+      kron_prop_matrix(op, a0 + j, dt, (g == 0 && j == 0) ? shift * dt : 0.0, e);
+      fold = fold && kron_fold_symmetric(e, n);
+    }
+    if (fold)
+      for (int j = 0; j < f; ++j) kron_fold_blocks(E.data() + static_cast<size_t>(j) * n * n * 2, n);
     const bool last = g == ng - 1;
     // a launch must not write its own input (other CTAs still read the tiles it overwrites)
     double* dst = (last && src != out) ? out
                   : src == ctx.scratch[0]  ? ctx.scratch[1]
                                            : ctx.scratch[0];
-    launch_kron_group(ctx.stream, src, dst, n, f, op.N, E.data(), last && bphase ? bfield : nullptr,
+    launch_kron_group(ctx.stream, src, dst, n, f, fold, op.N, E.data(), last && bphase ? bfield : nullptr,
                       bfactor, last && bphase ? 1 : 0);
     ctx.ws.launches += 1;
     src = dst;

@@ -19,7 +19,7 @@
 //   consecutive values q of the other axes = QT contiguous planes of F = N^f complex values, and the
 //   output moves the group to the slowest end (complex index q + Q g), so after all groups the
 //   layout is the caller's again. Tiles arrive by cp.async.bulk (mbarrier complete_tx) into a
-//   2-stage ring; two CTAs per SM.
+//   3-stage ring; one CTA per SM, walking a contiguous range of tiles.
 // * The planes sit in shared memory with a pitch PPC = F + pad (complex units) chosen so that the
 //   16-byte (re, im) loads of every axis are bank-conflict free (the last axis walks q fastest, so
 //   its stores to HBM are runs of QT pairs).
@@ -41,13 +41,19 @@ namespace kronop_dev {
 
 namespace {
 
+// One CTA per SM with a 3-deep ring (one tile in compute, two in flight) measured fastest:
+// 9D n = 9 propagate 10.3 ms vs 11.9 ms for two CTAs x 2 stages and 10.5 ms for 1 x 4
+// (tools/microbench/kron_bench.py; profiles/r02_kron_variants.json).
 #ifndef KRONOP_KR_CTAS
-#define KRONOP_KR_CTAS 2
+#define KRONOP_KR_CTAS 1
 #endif
 #ifndef KRONOP_KR_STAGES
-#define KRONOP_KR_STAGES 2
+#define KRONOP_KR_STAGES 3
 #endif
-constexpr int KR_TILE_MAX = 6144;  // complex doubles x 2 per stage before padding (48 KB)
+#ifndef KRONOP_KR_TILE
+#define KRONOP_KR_TILE 6144
+#endif
+constexpr int KR_TILE_MAX = KRONOP_KR_TILE;  // doubles per stage before padding (48 KB)
 constexpr int KR_MAXN = 10;
 
 __host__ __device__ constexpr int kr_pow(int n, int f) { return f == 0 ? 1 : n * kr_pow(n, f - 1); }
@@ -62,7 +68,7 @@ struct KronCfg {
   static constexpr int QT = kr_qt(F, 1);     // planes per tile (power of two)
   static constexpr int PL = F / N;           // last axis' complex stride = fibers per plane
   static constexpr int FIB = QT * PL;        // complex fibers per axis per tile
-  static constexpr int THREADS = FIB >= 512 ? 512 : (kr_round32(FIB) < 64 ? 64 : kr_round32(FIB));
+  static constexpr int THREADS = FIB >= 1024 ? 1024 : (kr_round32(FIB) < 64 ? 64 : kr_round32(FIB));
   // plane pitch: 8 lanes of a 16-byte access phase see QT planes x (8 / QT) fibers on the last
   // axis, so the pitch must be = 8 / QT (mod 8) for QT <= 8 and odd beyond
   static constexpr int TGT = QT >= 8 ? 1 : 8 / QT;
@@ -79,7 +85,7 @@ struct KronArgs {
   const double* bfield;  // B phase in the last group's store (null = B == 1)
   double bfactor;
   int bphase;
-  double E[NF][N][N][2];  // E_j(i, k) = (re, im): output i, input k
+  double2 E[NF][N][N];  // E_j(i, k) = (re, im): output i, input k
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -130,30 +136,91 @@ __device__ __forceinline__ void kr_issue(const KronArgs<N, NF>& A, long long til
   }
 }
 
-// out_i = sum_k E_J(i, k) x_k, complex; E from the parameter space (constant-bank operands).
-// Each of the 2N accumulators is one fma chain in k order.
+// out_i = sum_k E_J(i, k) x_k, complex; E from the parameter space (uniform constant loads, 128
+// bits = one complex entry). Each of the 2N accumulators is one fma chain in k order.
+//
+// FOLD (every E_a commutes with the reflection R: i -> N-1-i, i.e. the axis' operator is parity
+// symmetric -- a symmetric box [-L, L] with an even V1, as every config-5 axis): E maps even
+// vectors to even and odd to odd, so with s_k = x_k + x_{N-1-k}, d_k = x_k - x_{N-1-k} (k < M =
+// N/2) and s_M = x_M (odd N)
+//   a = Ae s,  b = Ao d,   out_i = a_i + b_i,  out_{N-1-i} = a_i - b_i,  out_M = a_M (odd N)
+// with Ae_ik = (E_ik + E_i,N-1-k) / 2 (k < M), Ae_iM = E_iM and Ao_ik = (E_ik - E_i,N-1-k) / 2:
+// (M + N%2)^2 + M^2 complex products instead of N^2 (41 vs 81 at N = 9). The host forms Ae, Ao
+// (stored in E[J] as [Ae | Ao], row-major) and picks this form only when R E R = E to rounding.
 template <int N, int NF, int J>
+__device__ __forceinline__ double2 kr_e(const KronArgs<N, NF>& A, int flat) {
+  return A.E[J][flat / N][flat % N];
+}
+
+template <int N, int NF, int J, bool FOLD>
 __device__ __forceinline__ void kr_contract(const KronArgs<N, NF>& A, const double2 (&x)[N],
                                             double (&re)[N], double (&im)[N]) {
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    re[i] = 0.0;
-    im[i] = 0.0;
-  }
-#pragma unroll
-  for (int k = 0; k < N; ++k)
+  if constexpr (!FOLD) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const double er = A.E[J][i][k][0], ei = A.E[J][i][k][1];
-      re[i] = fma(er, x[k].x, re[i]);
-      re[i] = fma(-ei, x[k].y, re[i]);
-      im[i] = fma(er, x[k].y, im[i]);
-      im[i] = fma(ei, x[k].x, im[i]);
+      re[i] = 0.0;
+      im[i] = 0.0;
     }
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double2 e = A.E[J][i][k];  // one 128-bit uniform constant load
+        re[i] = fma(e.x, x[k].x, re[i]);
+        re[i] = fma(-e.y, x[k].y, re[i]);
+        im[i] = fma(e.x, x[k].y, im[i]);
+        im[i] = fma(e.y, x[k].x, im[i]);
+      }
+  } else {
+    constexpr int M = N / 2, ME = M + N % 2;
+    double2 sv[ME], dv[M > 0 ? M : 1];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      sv[k] = make_double2(x[k].x + x[N - 1 - k].x, x[k].y + x[N - 1 - k].y);
+      dv[k] = make_double2(x[k].x - x[N - 1 - k].x, x[k].y - x[N - 1 - k].y);
+    }
+    if constexpr (N % 2) sv[M] = x[M];
+    double ar[ME], ai[ME], br[M > 0 ? M : 1], bi[M > 0 ? M : 1];
+#pragma unroll
+    for (int i = 0; i < ME; ++i) ar[i] = ai[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) br[i] = bi[i] = 0.0;
+#pragma unroll
+    for (int k = 0; k < ME; ++k)
+#pragma unroll
+      for (int i = 0; i < ME; ++i) {
+        const double2 e = kr_e<N, NF, J>(A, i * ME + k);
+        ar[i] = fma(e.x, sv[k].x, ar[i]);
+        ar[i] = fma(-e.y, sv[k].y, ar[i]);
+        ai[i] = fma(e.x, sv[k].y, ai[i]);
+        ai[i] = fma(e.y, sv[k].x, ai[i]);
+      }
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const double2 e = kr_e<N, NF, J>(A, ME * ME + i * M + k);
+        br[i] = fma(e.x, dv[k].x, br[i]);
+        br[i] = fma(-e.y, dv[k].y, br[i]);
+        bi[i] = fma(e.x, dv[k].y, bi[i]);
+        bi[i] = fma(e.y, dv[k].x, bi[i]);
+      }
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      re[i] = ar[i] + br[i];
+      im[i] = ai[i] + bi[i];
+      re[N - 1 - i] = ar[i] - br[i];
+      im[N - 1 - i] = ai[i] - bi[i];
+    }
+    if constexpr (N % 2) {
+      re[M] = ar[M];
+      im[M] = ai[M];
+    }
+  }
 }
 
 // Group axis J < NF - 1, in place: fibers (lo < P, hg < H, qi) at lo + P N hg + PPC qi.
-template <int N, int NF, int J>
+template <int N, int NF, int J, bool FOLD>
 __device__ __forceinline__ void kr_axis(const KronArgs<N, NF>& A, double* buf, int tid) {
   using C = KronCfg<N, NF>;
   constexpr int P = kr_pow(N, J);
@@ -168,7 +235,7 @@ __device__ __forceinline__ void kr_axis(const KronArgs<N, NF>& A, double* buf, i
 #pragma unroll
     for (int k = 0; k < N; ++k) x[k] = p[k * P];
     double re[N], im[N];
-    kr_contract<N, NF, J>(A, x, re, im);
+    kr_contract<N, NF, J, FOLD>(A, x, re, im);
 #pragma unroll
     for (int i = 0; i < N; ++i) p[i * P] = make_double2(re[i], im[i]);
   }
@@ -176,7 +243,7 @@ __device__ __forceinline__ void kr_axis(const KronArgs<N, NF>& A, double* buf, i
 
 // Last group axis (J = NF - 1, stride PL), q fastest across the lanes; outputs go to HBM with the
 // group at the slowest end: complex index (q0 + qi) + Q (lo + PL i).
-template <int N, int NF>
+template <int N, int NF, bool FOLD, bool BPH>
 __device__ __forceinline__ void kr_last(const KronArgs<N, NF>& A, const double* buf, long long q0,
                                         int qv, int tid) {
   using C = KronCfg<N, NF>;
@@ -192,13 +259,13 @@ __device__ __forceinline__ void kr_last(const KronArgs<N, NF>& A, const double* 
 #pragma unroll
     for (int k = 0; k < N; ++k) x[k] = p[k * P];
     double re[N], im[N];
-    kr_contract<N, NF, NF - 1>(A, x, re, im);
+    kr_contract<N, NF, NF - 1, FOLD>(A, x, re, im);
     const long long o = q0 + qi + A.Q * lo;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const long long oi = o + A.Q * P * i;
       double vr = re[i], vi = im[i];
-      if (A.bphase) {  // pointwise_phase (splitting.cpp:44-51), the operations of k_phase
+      if constexpr (BPH) {  // pointwise_phase (splitting.cpp:44-51), the operations of k_phase
         const double phase = A.bfield ? __dmul_rn(-A.bfactor, A.bfield[oi]) : -A.bfactor;
         double sn, cs;
         sincos(phase, &sn, &cs);
@@ -211,55 +278,78 @@ __device__ __forceinline__ void kr_last(const KronArgs<N, NF>& A, const double* 
   }
 }
 
-template <int N, int NF, int J>
+template <int N, int NF, int J, bool FOLD>
 __device__ __forceinline__ void kr_inplace_axes(const KronArgs<N, NF>& A, double* buf, int tid) {
   if constexpr (J < NF - 1) {
-    kr_axis<N, NF, J>(A, buf, tid);
+    kr_axis<N, NF, J, FOLD>(A, buf, tid);
     __syncthreads();
-    kr_inplace_axes<N, NF, J + 1>(A, buf, tid);
+    kr_inplace_axes<N, NF, J + 1, FOLD>(A, buf, tid);
   }
 }
 
-template <int N, int NF>
+// Persistent CTA over a contiguous range of tiles, STAGES-deep ring of bulk-loaded stages.
+// There is no CTA barrier at the end of a tile: the last warp to finish with a stage refills it,
+// so fast warps start the next tile's first axis while slow ones still store. (A software-
+// pipelined variant -- the last axis of tile t after the first axis of tile t+1, split-phase
+// mbarriers between the axes -- measured slower, 15.1 vs 12.5 ms per 9D propagate: with two
+// tiles in compute the 2-stage ring has no stage left to prefetch into.)
+template <int N, int NF, bool FOLD, bool BPH>
 __global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, KRONOP_KR_CTAS)
     kron_rot_kernel(const __grid_constant__ KronArgs<N, NF> A) {
   using C = KronCfg<N, NF>;
   constexpr int STAGES = KRONOP_KR_STAGES;
+  constexpr int WARPS = C::THREADS / 32;
   extern __shared__ __align__(128) double sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * C::STAGE);
-  const int tid = threadIdx.x;
+  int* done = reinterpret_cast<int*>(full + STAGES);  // warps finished with a stage
+  const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      done[s] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // Each CTA walks a contiguous range of tiles: its writes then complete whole lines of every
+  // output run over consecutive tiles (the rotating copy measured 2.5 -> 3.1 TB/s at QT = 4
+  // against the interleaved order, tools/microbench/rot_copy.cu).
+  const long long per = (A.ntiles + gridDim.x - 1) / gridDim.x;
+  const long long t0 = blockIdx.x * per;
+  const long long t1 = t0 + per < A.ntiles ? t0 + per : A.ntiles;
   if (tid == 0)
-    for (int s = 0; s < STAGES; ++s) {
-      const long long tile = blockIdx.x + static_cast<long long>(s) * gridDim.x;
-      if (tile < A.ntiles) kr_issue(A, tile, sm + s * C::STAGE, &full[s]);
-    }
+    for (int s = 0; s < STAGES; ++s)
+      if (t0 + s < t1) kr_issue(A, t0 + s, sm + s * C::STAGE, &full[s]);
   for (int it = 0;; ++it) {
-    const long long tile = blockIdx.x + static_cast<long long>(it) * gridDim.x;
-    if (tile >= A.ntiles) break;
+    const long long tile = t0 + it;
+    if (tile >= t1) break;
     const int s = it % STAGES;
     double* buf = sm + s * C::STAGE;
+    // A warp runs at most one tile ahead of the slowest (the next tile's first axis barrier
+    // waits for every warp; one-axis groups: the refill waits for every warp), so the phase it
+    // waits for is never two ahead of the barrier's.
     mbar_wait(&full[s], (it / STAGES) & 1);
     const long long q0 = tile * C::QT;
     const int qv = static_cast<int>(A.Q - q0 < C::QT ? A.Q - q0 : C::QT);
-    kr_inplace_axes<N, NF, 0>(A, buf, tid);
-    kr_last<N, NF>(A, buf, q0, qv, tid);
-    __syncthreads();  // every thread is done with the stage (generic proxy) before the refill
-    if (tid == 0) {
-      const long long next = tile + static_cast<long long>(STAGES) * gridDim.x;
-      if (next < A.ntiles) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        kr_issue(A, next, buf, &full[s]);
+    kr_inplace_axes<N, NF, 0, FOLD>(A, buf, tid);
+    kr_last<N, NF, FOLD, BPH>(A, buf, q0, qv, tid);
+    const long long next = tile + STAGES;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&done[s], 1) == WARPS - 1) {
+        done[s] = 0;
+        __threadfence_block();
+        if (next < t1) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          kr_issue(A, next, buf, &full[s]);
+        }
       }
     }
   }
 }
 
-template <int N, int NF>
+template <int N, int NF, bool FOLD, bool BPH>
 void launch_kron(cudaStream_t s, const double* x, double* y, long long Ntot, const double* E,
                  const double* bfield, double bfactor, int bphase) {
   using C = KronCfg<N, NF>;
@@ -274,44 +364,60 @@ void launch_kron(cudaStream_t s, const double* x, double* y, long long Ntot, con
   a.bphase = bphase;
   std::memcpy(a.E, E, sizeof(a.E));
   const size_t smem = static_cast<size_t>(KRONOP_KR_STAGES) * C::STAGE * sizeof(double) +
-                      KRONOP_KR_STAGES * sizeof(uint64_t);
-  ensure_smem_attr(reinterpret_cast<const void*>(kron_rot_kernel<N, NF>), smem);
+                      KRONOP_KR_STAGES * sizeof(uint64_t) + KRONOP_KR_STAGES * sizeof(int);
+  ensure_smem_attr(reinterpret_cast<const void*>(kron_rot_kernel<N, NF, FOLD, BPH>), smem);
   const long long cap = static_cast<long long>(device_sm_count()) * KRONOP_KR_CTAS;
   const long long grid = a.ntiles < cap ? a.ntiles : cap;
-  kron_rot_kernel<N, NF><<<static_cast<unsigned>(grid), C::THREADS, smem, s>>>(a);
+  kron_rot_kernel<N, NF, FOLD, BPH><<<static_cast<unsigned>(grid), C::THREADS, smem, s>>>(a);
   KCUDA(cudaGetLastError());
 }
 
-template <int N>
-void launch_kron_n(cudaStream_t s, int f, const double* x, double* y, long long Ntot,
+template <int N, bool FOLD>
+void launch_kron_f(cudaStream_t s, int f, const double* x, double* y, long long Ntot,
                    const double* E, const double* bfield, double bfactor, int bphase) {
-  if (f == 1)
-    launch_kron<N, 1>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+  if (f == 1 && bphase)
+    launch_kron<N, 1, FOLD, true>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+  else if (f == 1)
+    launch_kron<N, 1, FOLD, false>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+  else if (f == 2 && bphase)
+    launch_kron<N, 2, FOLD, true>(s, x, y, Ntot, E, bfield, bfactor, bphase);
   else if (f == 2)
-    launch_kron<N, 2>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron<N, 2, FOLD, false>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+  else if (bphase)
+    launch_kron<N, 3, FOLD, true>(s, x, y, Ntot, E, bfield, bfactor, bphase);
   else
-    launch_kron<N, 3>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron<N, 3, FOLD, false>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+}
+
+template <int N>
+void launch_kron_n(cudaStream_t s, int f, bool fold, const double* x, double* y, long long Ntot,
+                   const double* E, const double* bfield, double bfactor, int bphase) {
+  if (fold)
+    launch_kron_f<N, true>(s, f, x, y, Ntot, E, bfield, bfactor, bphase);
+  else
+    launch_kron_f<N, false>(s, f, x, y, Ntot, E, bfield, bfactor, bphase);
 }
 
 }  // namespace
 
 bool kron_group_supported(int n, int f) { return n >= 2 && n <= KR_MAXN && f >= 1 && f <= 3; }
 
-void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, long long Ntot,
-                       const double* E, const double* bfield, double bfactor, int bphase) {
+void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, bool fold,
+                       long long Ntot, const double* E, const double* bfield, double bfactor,
+                       int bphase) {
   param_check(kron_group_supported(n, f), "kron propagate: unsupported group");
   param_check((reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0,
               "kron propagate: fields must be 16-byte aligned");
   switch (n) {
-    case 2: launch_kron_n<2>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 3: launch_kron_n<3>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 4: launch_kron_n<4>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 5: launch_kron_n<5>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 6: launch_kron_n<6>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 7: launch_kron_n<7>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 8: launch_kron_n<8>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 9: launch_kron_n<9>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    default: launch_kron_n<10>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 2: launch_kron_n<2>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 3: launch_kron_n<3>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 4: launch_kron_n<4>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 5: launch_kron_n<5>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 6: launch_kron_n<6>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 7: launch_kron_n<7>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 8: launch_kron_n<8>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 9: launch_kron_n<9>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    default: launch_kron_n<10>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
   }
 }
 

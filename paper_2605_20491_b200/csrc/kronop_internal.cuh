@@ -139,10 +139,12 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
 // Kronecker-factored complex propagate (kron_prop.cu): one launch contracts a group of f <= 3
 // consecutive axes of extent n (2..10) with the complex matrices E (f x n x n x (re, im), row i =
 // output, k = input) and moves the group to the slowest end (the rotating layout of fused_rot.cu).
-// bphase: the output is multiplied by exp(-i bfactor B) (B = bfield, null = 1).
+// bphase: the output is multiplied by exp(-i bfactor B) (B = bfield, null = 1). fold: E holds
+// the parity blocks [Ae | Ao] of R-symmetric axis matrices instead (see kr_contract).
 bool kron_group_supported(int n, int f);
-void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, long long Ntot,
-                       const double* E, const double* bfield, double bfactor, int bphase);
+void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, bool fold,
+                       long long Ntot, const double* E, const double* bfield, double bfactor,
+                       int bphase);
 
 bool mode_product_tma_eligible(const double* x, const PassShape& ps);
 bool mode_product_tma_enabled();  // false under KRONOP_DISABLE_TMA=1

@@ -51,12 +51,16 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("parity", ["even", "odd"])
 @pytest.mark.parametrize("axes,launches", CASES)
-def test_kron_propagate_matches_oracle(ctx, axes, launches):
+def test_kron_propagate_matches_oracle(ctx, axes, launches, parity):
+    """even: parity-symmetric axes (the folded Ae / Ao contraction); odd: a potential with an odd
+    part breaks the symmetry (dense E_a)."""
     A = api()
     grid = A.Grid([A.assemble_sem(*a) for a in axes])
     # anisotropic potentials: a different matrix on every axis of a group
-    pots = [(lambda t, c=c: (1.0 + 0.3 * c) * t * t + 0.1 * c) for c in range(grid.dim)]
+    odd = 0.35 if parity == "odd" else 0.0
+    pots = [(lambda t, c=c: (1.0 + 0.3 * c) * t * t + 0.1 * c + odd * t) for c in range(grid.dim)]
     op = grid.separable_operator(ctx, pots, -0.4)
     ko = oracle_op_from(op, -0.4)
     psi = K.seeded_complex_field(grid.shape, 71)
