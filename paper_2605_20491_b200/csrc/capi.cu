@@ -267,8 +267,10 @@ static void kron_fold_blocks(double* E, int n) {
   std::copy(out.begin(), out.end(), E);
 }
 
-// Groups for the Kronecker propagate: up to three consecutive axes of the same extent; empty when
-// some axis is outside the kernel's range or the host copies are missing.
+// Groups for the Kronecker propagate: up to three consecutive axes of the same extent n <= 10
+// (DFMA kernel), or up to two of the same extent 11..32 with n^2 <= 1024 (DMMA kernel, parity-
+// symmetric axes only); empty when some axis is outside that range or the host copies are
+// missing.
 static std::vector<std::pair<int, int>> kron_groups(const kronop_op& op) {
   std::vector<std::pair<int, int>> groups;
   static const bool off = [] {
@@ -279,8 +281,9 @@ static std::vector<std::pair<int, int>> kron_groups(const kronop_op& op) {
   for (int a = 0; a < op.d; ++a)
     if (op.hT[a].empty() || !kron_group_supported(op.n[a], 1)) return groups;
   for (int a = 0; a < op.d;) {
+    const int fmax = op.n[a] <= 10 ? 3 : 2;
     int f = 1;
-    while (a + f < op.d && f < 3 && op.n[a + f] == op.n[a]) ++f;
+    while (a + f < op.d && f < fmax && op.n[a + f] == op.n[a]) ++f;
     groups.emplace_back(a, f);
     a += f;
   }
@@ -292,32 +295,42 @@ static bool sep_propagate_kron(kronop_ctx& ctx, const kronop_op& op, const doubl
                                double bfactor) {
   const std::vector<std::pair<int, int>> groups = kron_groups(op);
   if (groups.empty() || !fused_rot_eligible(in) || !fused_rot_eligible(out)) return false;
-  const size_t nd = static_cast<size_t>(op.N) * 2;
-  ensure_scratch(ctx, nd);
-  const int ng = static_cast<int>(groups.size());
   static const bool no_fold = [] {
     const char* e = getenv("KRONOP_KRON_FOLD");  // A/B switch: 0 = dense E_a even when symmetric
     return e && e[0] == '0';
   }();
-  std::vector<double> E(3 * 10 * 10 * 2);
+  const int ng = static_cast<int>(groups.size());
+  // every group's matrices first: a group the kernels cannot take (an extent > 10 whose axis is
+  // not parity symmetric) sends the whole propagate to the transform / phase / transform path
+  constexpr size_t kSlot = 3 * 32 * 32 * 2;
+  std::vector<double> E(kSlot * ng);
+  std::vector<char> fold(ng);
+  for (int g = 0; g < ng; ++g) {
+    const int a0 = groups[g].first, f = groups[g].second, n = op.n[a0];
+    bool fl = !no_fold || kron_group_needs_fold(n);
+    for (int j = 0; j < f; ++j) {
+      double* e = E.data() + kSlot * g + static_cast<size_t>(j) * n * n * 2;
+      kron_prop_matrix(op, a0 + j, dt, (g == 0 && j == 0) ? shift * dt : 0.0, e);
+      fl = fl && kron_fold_symmetric(e, n);
+    }
+    if (!fl && kron_group_needs_fold(n)) return false;
+    if (fl)
+      for (int j = 0; j < f; ++j)
+        kron_fold_blocks(E.data() + kSlot * g + static_cast<size_t>(j) * n * n * 2, n);
+    fold[g] = fl;
+  }
+  const size_t nd = static_cast<size_t>(op.N) * 2;
+  ensure_scratch(ctx, nd);
   const double* src = in;
   for (int g = 0; g < ng; ++g) {
     const int a0 = groups[g].first, f = groups[g].second, n = op.n[a0];
-    bool fold = !no_fold;
-    for (int j = 0; j < f; ++j) {
-      double* e = E.data() + static_cast<size_t>(j) * n * n * 2;
-      kron_prop_matrix(op, a0 + j, dt, (g == 0 && j == 0) ? shift * dt : 0.0, e);
-      fold = fold && kron_fold_symmetric(e, n);
-    }
-    if (fold)
-      for (int j = 0; j < f; ++j) kron_fold_blocks(E.data() + static_cast<size_t>(j) * n * n * 2, n);
     const bool last = g == ng - 1;
     // a launch must not write its own input (other CTAs still read the tiles it overwrites)
     double* dst = (last && src != out) ? out
                   : src == ctx.scratch[0]  ? ctx.scratch[1]
                                            : ctx.scratch[0];
-    launch_kron_group(ctx.stream, src, dst, n, f, fold, op.N, E.data(), last && bphase ? bfield : nullptr,
-                      bfactor, last && bphase ? 1 : 0);
+    launch_kron_group(ctx.stream, src, dst, n, f, fold[g] != 0, op.N, E.data() + kSlot * g,
+                      last && bphase ? bfield : nullptr, bfactor, last && bphase ? 1 : 0);
     ctx.ws.launches += 1;
     src = dst;
   }

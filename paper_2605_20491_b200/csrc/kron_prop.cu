@@ -55,6 +55,7 @@ namespace {
 #endif
 constexpr int KR_TILE_MAX = KRONOP_KR_TILE;  // doubles per stage before padding (48 KB)
 constexpr int KR_MAXN = 10;
+constexpr int KD_MAXN = 32;
 
 __host__ __device__ constexpr int kr_pow(int n, int f) { return f == 0 ? 1 : n * kr_pow(n, f - 1); }
 __host__ __device__ constexpr int kr_qt(int F, int q) {
@@ -398,14 +399,304 @@ void launch_kron_n(cudaStream_t s, int f, bool fold, const double* x, double* y,
     launch_kron_f<N, false>(s, f, x, y, Ntot, E, bfield, bfactor, bphase);
 }
 
+// ------------------------------------------------------------------------------------------
+// Extents 11..32 (config 5: 6D n = 29): the same rotating group launch on the FP64 tensor cores.
+// Only the parity-folded form (every axis R-symmetric): per complex fiber the blocks
+// Ae ((M+c) x (M+c)) and Ao (M x M) are real 2(M+c) x 2(M+c) and 2M x 2M matrices over the
+// interleaved (re, im) components,
+//   [Re -Im]
+//   [Im  Re]  per complex entry,
+// contracted with mma.sync.m8n8k4.f64 (DMMA): 8 fibers per warp step (A = fiber components from
+// shared memory, B = matrix fragments staged once per CTA in fragment order), K = 2(M+c) / 2M
+// padded to 4, N padded to 8. At n = 29 that is 8 x 4 + 7 x 4 = 60 DMMA per 8 fibers against
+// 15 x 8 = 120 for the dense complex 58 x 58 matrix, and the same flops as ONE of the two real
+// 29 x 29 passes of the transform form -- so the fold halves the tensor work of a propagate on
+// top of the halved HBM traffic. Fold / unfold run in the warp that owns the fibers: s, d are
+// formed in place in shared memory (s_k at position k, d_k at N-1-k), and the outputs
+// y_i = a_i + b_i, y_{N-1-i} = a_i - b_i are formed from the accumulators, which hold a_i and b_i
+// of the same (fiber, i, re/im) in the same lane.
+#ifndef KRONOP_KD_STAGES
+#define KRONOP_KD_STAGES 3
+#endif
+#ifndef KRONOP_KD_WARPS
+#define KRONOP_KD_WARPS 16
+#endif
+constexpr int KD_SMEM_BUDGET = 220 * 1024;
+
+__host__ __device__ constexpr int kd_me(int n) { return n / 2 + n % 2; }
+__host__ __device__ constexpr int kd_frag(int n) {  // fragment doubles per axis (Ae + Ao blocks)
+  return ((2 * kd_me(n) + 3) / 4) * ((2 * kd_me(n) + 7) / 8) * 32 +
+         ((2 * (n / 2) + 3) / 4) * ((2 * (n / 2) + 7) / 8) * 32;
+}
+__host__ __device__ constexpr int kd_qt(int n, int nf, int q) {
+  return (q < 64 && KRONOP_KD_STAGES * 2 * (2 * q) * kr_pow(n, nf) * 8 + nf * kd_frag(n) * 8 + 256 <=
+                        KD_SMEM_BUDGET)
+             ? kd_qt(n, nf, 2 * q)
+             : q;
+}
+
+template <int N, int NF>
+struct KronDCfg {
+  static constexpr int F = kr_pow(N, NF);
+  static constexpr int QT = kd_qt(N, NF, 1);
+  static constexpr int PL = F / N;
+  static constexpr int FIB = QT * PL;
+  static constexpr int M = N / 2, ME = kd_me(N);
+  static constexpr int K4A = (2 * ME + 3) / 4, NTA = (2 * ME + 7) / 8;
+  static constexpr int K4B = (2 * M + 3) / 4, NTB = (2 * M + 7) / 8;
+  static constexpr int FRAG_A = K4A * NTA * 32, FRAG_B = K4B * NTB * 32;
+  static constexpr int FRAG = FRAG_A + FRAG_B;
+  static constexpr int STAGE = 2 * QT * F;  // doubles
+  static constexpr int THREADS = 32 * KRONOP_KD_WARPS;
+};
+
+template <int N, int NF>
+struct KronDArgs {
+  const double* x;
+  double* y;
+  long long Q;
+  long long ntiles;
+  const double* bfield;
+  double bfactor;
+  int bphase;
+  double2 E[NF][kd_me(N) * kd_me(N) + (N / 2) * (N / 2)];  // per axis [Ae | Ao], row-major
+};
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// One warp step on 8 fibers (g = lane / 4) of one axis: fold in place, the two block products,
+// unfold; in place (LAST = false) or to HBM with the group at the slow end (LAST = true).
+template <int N, int NF, int J, bool LAST>
+__device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, const double* frag,
+                                        int f0, long long q0, int qv, int lane) {
+  using C = KronDCfg<N, NF>;
+  constexpr int P = kr_pow(N, J);  // complex stride of the axis
+  constexpr int H = C::F / (P * N);
+  constexpr int M = C::M, ME = C::ME;
+  const int g = lane >> 2, t = lane & 3;
+  auto base_of = [&](int f, int& qi, int& lo) {  // complex offset of fiber f's element 0
+    if constexpr (LAST) {
+      qi = f % C::QT;
+      lo = f / C::QT;
+      return lo + qi * C::F;
+    } else {
+      lo = f % P;
+      const int hi = f / P;
+      qi = hi / H;
+      return lo + (hi % H) * (P * N) + qi * C::F;
+    }
+  };
+  double2* b2 = reinterpret_cast<double2*>(buf);
+  // fold: (x_k, x_{N-1-k}) -> (s_k, d_k) for the warp's 8 fibers
+  for (int it = lane; it < 8 * M; it += 32) {
+    const int gg = it / M, k = it - gg * M;
+    const int f = f0 + gg;
+    if (f < C::FIB) {
+      int qi, lo;
+      double2* p = b2 + base_of(f, qi, lo);
+      const double2 u = p[k * P], v = p[(N - 1 - k) * P];
+      p[k * P] = make_double2(u.x + v.x, u.y + v.y);
+      p[(N - 1 - k) * P] = make_double2(u.x - v.x, u.y - v.y);
+    }
+  }
+  __syncwarp();
+  const int f = f0 + g;
+  const bool fok = f < C::FIB;
+  int qi = 0, lo = 0;
+  const int fb = base_of(fok ? f : f0, qi, lo);
+  const double* src = buf + 2 * fb;
+  double acc_a[C::NTA][2], acc_b[C::NTB][2];
+#pragma unroll
+  for (int nt = 0; nt < C::NTA; ++nt) acc_a[nt][0] = acc_a[nt][1] = 0.0;
+#pragma unroll
+  for (int nt = 0; nt < C::NTB; ++nt) acc_b[nt][0] = acc_b[nt][1] = 0.0;
+  const double* fa = frag + lane;
+#pragma unroll
+  for (int kk = 0; kk < C::K4A; ++kk) {
+    const int kap = 4 * kk + t, k = kap >> 1;
+    const double a = k < ME ? src[2 * P * k + (kap & 1)] : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < C::NTA; ++nt) dmma884(acc_a[nt], a, fa[(kk * C::NTA + nt) * 32]);
+  }
+  const double* fbg = frag + C::FRAG_A + lane;
+#pragma unroll
+  for (int kk = 0; kk < C::K4B; ++kk) {
+    const int kap = 4 * kk + t, k = kap >> 1;
+    const double a = k < M ? src[2 * P * (N - 1 - k) + (kap & 1)] : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < C::NTB; ++nt) dmma884(acc_b[nt], a, fbg[(kk * C::NTB + nt) * 32]);
+  }
+  __syncwarp();  // every lane has read its fibers before any output overwrites them
+  if (!fok) return;
+  if constexpr (LAST) {
+    if (qi >= qv) return;
+  }
+  double2* y2 = reinterpret_cast<double2*>(A.y);
+  auto put = [&](int i, double re, double im) {
+    if constexpr (LAST) {
+      const long long oi = q0 + qi + A.Q * (lo + static_cast<long long>(P) * i);
+      if (A.bphase) {  // pointwise_phase (splitting.cpp:44-51), the operations of k_phase
+        const double phase = A.bfield ? __dmul_rn(-A.bfactor, A.bfield[oi]) : -A.bfactor;
+        double sn, cs;
+        sincos(phase, &sn, &cs);
+        const double r0 = re, i0 = im;
+        re = __dsub_rn(__dmul_rn(r0, cs), __dmul_rn(i0, sn));
+        im = __dadd_rn(__dmul_rn(r0, sn), __dmul_rn(i0, cs));
+      }
+      y2[oi] = make_double2(re, im);
+    } else {
+      b2[fb + i * P] = make_double2(re, im);
+    }
+  };
+#pragma unroll
+  for (int nt = 0; nt < C::NTA; ++nt) {
+    const int i = 4 * nt + t;
+    if (i < M) {
+      put(i, acc_a[nt][0] + acc_b[nt][0], acc_a[nt][1] + acc_b[nt][1]);
+      put(N - 1 - i, acc_a[nt][0] - acc_b[nt][0], acc_a[nt][1] - acc_b[nt][1]);
+    } else if (i < ME) {
+      put(i, acc_a[nt][0], acc_a[nt][1]);
+    }
+  }
+}
+
+template <int N, int NF, int J>
+__device__ __forceinline__ void kd_axis(const KronDArgs<N, NF>& A, double* buf, const double* frag,
+                                        long long q0, int qv, int warp, int lane) {
+  using C = KronDCfg<N, NF>;
+  constexpr bool LAST = J == NF - 1;
+  for (int f0 = warp * 8; f0 < C::FIB; f0 += 8 * KRONOP_KD_WARPS)
+    kd_step<N, NF, J, LAST>(A, buf, frag + J * C::FRAG, f0, q0, qv, lane);
+  if constexpr (!LAST) {
+    __syncthreads();
+    kd_axis<N, NF, J + 1>(A, buf, frag, q0, qv, warp, lane);
+  }
+}
+
+template <int N, int NF>
+__global__ void __launch_bounds__(32 * KRONOP_KD_WARPS, 1)
+    kron_dmma_kernel(const __grid_constant__ KronDArgs<N, NF> A) {
+  using C = KronDCfg<N, NF>;
+  constexpr int STAGES = KRONOP_KD_STAGES;
+  constexpr int WARPS = KRONOP_KD_WARPS;
+  extern __shared__ __align__(128) double sm[];
+  double* frag = sm + STAGES * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(frag + NF * C::FRAG);
+  int* done = reinterpret_cast<int*>(full + STAGES);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // B fragments: frag[j][(kk NT + nt) 32 + lane] = Mreal(8 nt + lane / 4, 4 kk + lane % 4)
+  for (int j = 0; j < NF; ++j)
+    for (int e = tid; e < C::FRAG; e += C::THREADS) {
+      const bool blk_a = e < C::FRAG_A;
+      const int ee = blk_a ? e : e - C::FRAG_A;
+      const int nts = blk_a ? C::NTA : C::NTB, dim = blk_a ? C::ME : C::M;
+      const int ln = ee & 31, rest = ee >> 5, nt = rest % nts, kk = rest / nts;
+      const int nu = 8 * nt + (ln >> 2), kap = 4 * kk + (ln & 3);
+      const int i = nu >> 1, k = kap >> 1, co = nu & 1, ci = kap & 1;
+      double v = 0.0;
+      if (i < dim && k < dim) {
+        const double2 z = blk_a ? A.E[j][i * C::ME + k] : A.E[j][C::ME * C::ME + i * C::M + k];
+        v = co == ci ? z.x : (co == 0 ? -z.y : z.y);
+      }
+      frag[j * C::FRAG + e] = v;
+    }
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      done[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const long long per = (A.ntiles + gridDim.x - 1) / gridDim.x;
+  const long long t0 = blockIdx.x * per;
+  const long long t1 = t0 + per < A.ntiles ? t0 + per : A.ntiles;
+  auto issue = [&](long long tile, double* dst, uint64_t* bar) {
+    const long long q0 = tile * C::QT;
+    const int qv = static_cast<int>(A.Q - q0 < C::QT ? A.Q - q0 : C::QT);
+    mbar_expect_tx(bar, static_cast<uint32_t>(qv) * C::F * 16u);
+    bulk_load(dst, A.x + 2LL * C::F * q0, static_cast<uint32_t>(qv) * C::F * 16u, bar);
+  };
+  if (tid == 0)
+    for (int s = 0; s < STAGES; ++s)
+      if (t0 + s < t1) issue(t0 + s, sm + s * C::STAGE, &full[s]);
+  for (int it = 0;; ++it) {
+    const long long tile = t0 + it;
+    if (tile >= t1) break;
+    const int s = it % STAGES;
+    double* buf = sm + s * C::STAGE;
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    const long long q0 = tile * C::QT;
+    const int qv = static_cast<int>(A.Q - q0 < C::QT ? A.Q - q0 : C::QT);
+    kd_axis<N, NF, 0>(A, buf, frag, q0, qv, warp, lane);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&done[s], 1) == WARPS - 1) {
+        done[s] = 0;
+        __threadfence_block();
+        if (tile + STAGES < t1) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          issue(tile + STAGES, buf, &full[s]);
+        }
+      }
+    }
+  }
+}
+
+template <int N, int NF>
+void launch_kron_dmma(cudaStream_t s, const double* x, double* y, long long Ntot, const double* E,
+                      const double* bfield, double bfactor, int bphase) {
+  using C = KronDCfg<N, NF>;
+  KronDArgs<N, NF> a;
+  std::memset(&a, 0, sizeof(a));
+  a.x = x;
+  a.y = y;
+  a.Q = Ntot / C::F;
+  a.ntiles = (a.Q + C::QT - 1) / C::QT;
+  a.bfield = bfield;
+  a.bfactor = bfactor;
+  a.bphase = bphase;
+  // E: per axis the N x N slot of the caller's buffer holds [Ae | Ao] (kron_fold_blocks)
+  constexpr int BLK = C::ME * C::ME + C::M * C::M;
+  for (int j = 0; j < NF; ++j)
+    std::memcpy(&a.E[j][0], E + static_cast<size_t>(j) * N * N * 2, BLK * sizeof(double2));
+  const size_t smem = (static_cast<size_t>(KRONOP_KD_STAGES) * C::STAGE + NF * C::FRAG) *
+                          sizeof(double) +
+                      KRONOP_KD_STAGES * (sizeof(uint64_t) + sizeof(int));
+  ensure_smem_attr(reinterpret_cast<const void*>(kron_dmma_kernel<N, NF>), smem);
+  const long long cap = device_sm_count();
+  const long long grid = a.ntiles < cap ? a.ntiles : cap;
+  kron_dmma_kernel<N, NF><<<static_cast<unsigned>(grid), C::THREADS, smem, s>>>(a);
+  KCUDA(cudaGetLastError());
+}
+
+template <int N>
+void launch_kron_dmma_n(cudaStream_t s, int f, const double* x, double* y, long long Ntot,
+                        const double* E, const double* bfield, double bfactor, int bphase) {
+  if (f == 1)
+    launch_kron_dmma<N, 1>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+  else
+    launch_kron_dmma<N, 2>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+}
+
 }  // namespace
 
-bool kron_group_supported(int n, int f) { return n >= 2 && n <= KR_MAXN && f >= 1 && f <= 3; }
+bool kron_group_supported(int n, int f) {
+  return (n >= 2 && n <= KR_MAXN && f >= 1 && f <= 3) ||
+         (n > KR_MAXN && n <= KD_MAXN && f >= 1 && f <= 2);
+}
+bool kron_group_needs_fold(int n) { return n > KR_MAXN; }
 
 void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, bool fold,
                        long long Ntot, const double* E, const double* bfield, double bfactor,
                        int bphase) {
   param_check(kron_group_supported(n, f), "kron propagate: unsupported group");
+  param_check(fold || n <= KR_MAXN, "kron propagate: extents > 10 need parity-symmetric axes");
   param_check((reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0,
               "kron propagate: fields must be 16-byte aligned");
   switch (n) {
@@ -417,7 +708,15 @@ void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f,
     case 7: launch_kron_n<7>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
     case 8: launch_kron_n<8>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
     case 9: launch_kron_n<9>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    default: launch_kron_n<10>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 10: launch_kron_n<10>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+#define KD_CASE(NN) \
+  case NN: launch_kron_dmma_n<NN>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    KD_CASE(11) KD_CASE(12) KD_CASE(13) KD_CASE(14) KD_CASE(15) KD_CASE(16) KD_CASE(17)
+    KD_CASE(18) KD_CASE(19) KD_CASE(20) KD_CASE(21) KD_CASE(22) KD_CASE(23) KD_CASE(24)
+    KD_CASE(25) KD_CASE(26) KD_CASE(27) KD_CASE(28) KD_CASE(29) KD_CASE(30) KD_CASE(31)
+    KD_CASE(32)
+#undef KD_CASE
+    default: break;
   }
 }
 

@@ -142,6 +142,7 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
 // bphase: the output is multiplied by exp(-i bfactor B) (B = bfield, null = 1). fold: E holds
 // the parity blocks [Ae | Ao] of R-symmetric axis matrices instead (see kr_contract).
 bool kron_group_supported(int n, int f);
+bool kron_group_needs_fold(int n);  // extents > 10 (DMMA kernel): parity-symmetric axes only
 void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, bool fold,
                        long long Ntot, const double* E, const double* bfield, double bfactor,
                        int bphase);
