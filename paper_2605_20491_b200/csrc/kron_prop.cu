@@ -421,6 +421,11 @@ void launch_kron_n(cudaStream_t s, int f, bool fold, const double* x, double* y,
 #ifndef KRONOP_KD_WARPS
 #define KRONOP_KD_WARPS 16
 #endif
+// the CTA's warps form KD_GROUPS groups that take alternate tiles, each synchronising on its own
+// named barrier, so one group's fold / unfold and barrier waits overlap the other's DMMA
+#ifndef KRONOP_KD_GROUPS
+#define KRONOP_KD_GROUPS 2
+#endif
 constexpr int KD_SMEM_BUDGET = 220 * 1024;
 
 __host__ __device__ constexpr int kd_me(int n) { return n / 2 + n % 2; }
@@ -566,14 +571,18 @@ __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, 
 
 template <int N, int NF, int J>
 __device__ __forceinline__ void kd_axis(const KronDArgs<N, NF>& A, double* buf, const double* frag,
-                                        long long q0, int qv, int warp, int lane) {
+                                        long long q0, int qv, int gwarp, int lane, int grp) {
   using C = KronDCfg<N, NF>;
   constexpr bool LAST = J == NF - 1;
-  for (int f0 = warp * 8; f0 < C::FIB; f0 += 8 * KRONOP_KD_WARPS)
+  constexpr int GW = KRONOP_KD_WARPS / KRONOP_KD_GROUPS;  // warps per group
+  for (int f0 = gwarp * 8; f0 < C::FIB; f0 += 8 * GW)
     kd_step<N, NF, J, LAST>(A, buf, frag + J * C::FRAG, f0, q0, qv, lane);
   if constexpr (!LAST) {
-    __syncthreads();
-    kd_axis<N, NF, J + 1>(A, buf, frag, q0, qv, warp, lane);
+    if constexpr (KRONOP_KD_GROUPS == 1)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(32 * GW) : "memory");
+    kd_axis<N, NF, J + 1>(A, buf, frag, q0, qv, gwarp, lane, grp);
   }
 }
 
@@ -586,8 +595,15 @@ __global__ void __launch_bounds__(32 * KRONOP_KD_WARPS, 1)
   extern __shared__ __align__(128) double sm[];
   double* frag = sm + STAGES * C::STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(frag + NF * C::FRAG);
-  int* done = reinterpret_cast<int*>(full + STAGES);
+  int* done = reinterpret_cast<int*>(full + STAGES);  // warps of the group finished with a stage
+  // loads issued per stage: a group can reach the next use of a stage before the other group has
+  // consumed and refilled it, when the mbarrier would still show the parity of the use before
+  // (phases two apart look alike) -- so it first waits until the load it needs has been issued
+  int* issued = done + STAGES;
+  constexpr int GROUPS = KRONOP_KD_GROUPS, GW = WARPS / GROUPS;
+  static_assert(WARPS % GROUPS == 0 && STAGES >= GROUPS, "warp groups");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp / GW, gwarp = warp - grp * GW;
   // B fragments: frag[j][(kk NT + nt) 32 + lane] = Mreal(8 nt + lane / 4, 4 kk + lane % 4)
   for (int j = 0; j < NF; ++j)
     for (int e = tid; e < C::FRAG; e += C::THREADS) {
@@ -604,14 +620,6 @@ __global__ void __launch_bounds__(32 * KRONOP_KD_WARPS, 1)
       }
       frag[j * C::FRAG + e] = v;
     }
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      done[s] = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
   const long long per = (A.ntiles + gridDim.x - 1) / gridDim.x;
   const long long t0 = blockIdx.x * per;
   const long long t1 = t0 + per < A.ntiles ? t0 + per : A.ntiles;
@@ -621,27 +629,48 @@ __global__ void __launch_bounds__(32 * KRONOP_KD_WARPS, 1)
     mbar_expect_tx(bar, static_cast<uint32_t>(qv) * C::F * 16u);
     bulk_load(dst, A.x + 2LL * C::F * q0, static_cast<uint32_t>(qv) * C::F * 16u, bar);
   };
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      done[s] = 0;
+      issued[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
   if (tid == 0)
     for (int s = 0; s < STAGES; ++s)
-      if (t0 + s < t1) issue(t0 + s, sm + s * C::STAGE, &full[s]);
-  for (int it = 0;; ++it) {
+      if (t0 + s < t1) {
+        issue(t0 + s, sm + s * C::STAGE, &full[s]);
+        issued[s] = 1;
+      }
+  for (int kt = 0;; ++kt) {
+    const int it = kt * GROUPS + grp;  // this group's tiles
     const long long tile = t0 + it;
     if (tile >= t1) break;
     const int s = it % STAGES;
     double* buf = sm + s * C::STAGE;
+    if constexpr (GROUPS > 1) {
+      if (lane == 0)
+        while (*reinterpret_cast<volatile int*>(&issued[s]) <= it / STAGES) {
+        }
+      __syncwarp();
+    }
     mbar_wait(&full[s], (it / STAGES) & 1);
     const long long q0 = tile * C::QT;
     const int qv = static_cast<int>(A.Q - q0 < C::QT ? A.Q - q0 : C::QT);
-    kd_axis<N, NF, 0>(A, buf, frag, q0, qv, warp, lane);
+    kd_axis<N, NF, 0>(A, buf, frag, q0, qv, gwarp, lane, grp);
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
-      if (atomicAdd(&done[s], 1) == WARPS - 1) {
+      if (atomicAdd(&done[s], 1) == GW - 1) {
         done[s] = 0;
         __threadfence_block();
         if (tile + STAGES < t1) {
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           issue(tile + STAGES, buf, &full[s]);
+          __threadfence_block();
+          atomicAdd(&issued[s], 1);
         }
       }
     }
@@ -667,7 +696,7 @@ void launch_kron_dmma(cudaStream_t s, const double* x, double* y, long long Ntot
     std::memcpy(&a.E[j][0], E + static_cast<size_t>(j) * N * N * 2, BLK * sizeof(double2));
   const size_t smem = (static_cast<size_t>(KRONOP_KD_STAGES) * C::STAGE + NF * C::FRAG) *
                           sizeof(double) +
-                      KRONOP_KD_STAGES * (sizeof(uint64_t) + sizeof(int));
+                      KRONOP_KD_STAGES * (sizeof(uint64_t) + 2 * sizeof(int));
   ensure_smem_attr(reinterpret_cast<const void*>(kron_dmma_kernel<N, NF>), smem);
   const long long cap = device_sm_count();
   const long long grid = a.ntiles < cap ? a.ntiles : cap;
