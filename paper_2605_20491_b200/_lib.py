@@ -113,6 +113,8 @@ PROTOTYPES = {
     "kronop_sep_solve_host": (I, [P, P, P, I, P]),
     "kronop_sep_apply_host": (I, [P, P, P, I, P]),
     "kronop_sep_propagate_host": (I, [P, P, P, D, P]),
+    "kronop_sep_solve_host_batch": (I, [P, P, I, P, I, P]),
+    "kronop_sep_propagate_host_batch": (I, [P, P, I, P, D, P]),
     "kronop_pcg": (I, [P, C.POINTER(LinearMap), C.POINTER(LinearMap), P, P,
                        C.POINTER(PcgConfig), C.POINTER(PcgReport), DP]),
     "kronop_inverse_iteration": (I, [P, P, P, C.POINTER(InverseIterationConfig), P, P,

@@ -470,6 +470,24 @@ class SeparableOperator:
                                           int(cplx), C.c_void_p(out.ctypes.data)))
         return out
 
+    def solve_host_batch(self, bs, outs, is_complex=None):
+        """kronop_sep_solve_host_batch: a list of host right-hand sides -> host solutions, the
+        copies of neighbouring items overlapped with each item's transform."""
+        cplx = np.iscomplexobj(bs[0]) if is_complex is None else is_complex
+        n = len(bs)
+        ins = (C.c_void_p * n)(*[b.ctypes.data for b in bs])
+        ous = (C.c_void_p * n)(*[o.ctypes.data for o in outs])
+        check(lib().kronop_sep_solve_host_batch(self.ctx.h, self.h, n, ins, int(cplx), ous))
+        return outs
+
+    def propagate_host_batch(self, psis, dt: float, outs):
+        n = len(psis)
+        ins = (C.c_void_p * n)(*[p.ctypes.data for p in psis])
+        ous = (C.c_void_p * n)(*[o.ctypes.data for o in outs])
+        check(lib().kronop_sep_propagate_host_batch(self.ctx.h, self.h, n, ins, C.c_double(dt),
+                                                    ous))
+        return outs
+
     def apply_host(self, u: np.ndarray, out: np.ndarray):
         check(lib().kronop_sep_apply_host(self.ctx.h, self.h, C.c_void_p(u.ctypes.data),
                                           int(np.iscomplexobj(u)), C.c_void_p(out.ctypes.data)))

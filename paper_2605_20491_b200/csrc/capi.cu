@@ -731,6 +731,12 @@ int kronop_ctx_destroy(kronop_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto p : ctx->scratch) if (p) cudaFree(p);
     for (auto p : ctx->io) if (p) cudaFree(p);
+    for (auto p : ctx->bio) if (p) cudaFree(p);
+    for (int p = 0; p < 2; ++p) {
+      if (ctx->ev_up[p]) cudaEventDestroy(ctx->ev_up[p]);
+      if (ctx->ev_comp[p]) cudaEventDestroy(ctx->ev_comp[p]);
+      if (ctx->ev_down[p]) cudaEventDestroy(ctx->ev_down[p]);
+    }
     for (auto& b : ctx->pool) cudaFree(b.p);
     if (ctx->tmp) cudaFree(ctx->tmp);
     if (ctx->ws.partials) cudaFree(ctx->ws.partials);
@@ -1307,6 +1313,85 @@ static void host_roundtrip(kronop_ctx* ctx, const kronop_op* op, const double* i
   }
   KCUDA(cudaStreamSynchronize(sout));
   KCUDA(cudaStreamSynchronize(sc));
+}
+
+// Batched host path: items alternate between two device (in, out) pairs; per item the upload
+// (copy stream 0) waits for the compute that last read its input buffer, the transform (compute
+// stream, the device path's own pass sequence) waits for the upload and for the download that
+// last read its output buffer, and the download (copy stream 1) waits for the transform.
+static void host_batch(kronop_ctx* ctx, const kronop_op* op, int count, const double* const* in,
+                       int cplx, double* const* out, SepKind kind, double dt) {
+  param_check(count >= 0 && (count == 0 || (in && out)), "host batch: bad arguments");
+  for (int i = 0; i < count; ++i) param_check(in[i] && out[i], "host batch: null field");
+  if (count == 0) return;
+  if (count == 1) {
+    host_roundtrip(ctx, op, in[0], cplx, out[0], kind, dt);
+    return;
+  }
+  const size_t nd = static_cast<size_t>(op->N) * (cplx ? 2 : 1);
+  if (kind == SEP_SOLVE) check_solve_shift(*ctx, *op, op->shift);
+  ensure_copy_engines(ctx);
+  if (!ctx->ev_up[0])
+    for (int p = 0; p < 2; ++p) {
+      KCUDA(cudaEventCreateWithFlags(&ctx->ev_up[p], cudaEventDisableTiming));
+      KCUDA(cudaEventCreateWithFlags(&ctx->ev_comp[p], cudaEventDisableTiming));
+      KCUDA(cudaEventCreateWithFlags(&ctx->ev_down[p], cudaEventDisableTiming));
+    }
+  if (nd > ctx->bio_cap) {
+    KCUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto& b : ctx->bio) {
+      if (b) KCUDA(cudaFree(b));
+      b = nullptr;
+    }
+    ctx->bio_cap = 0;
+    for (auto& b : ctx->bio) KCUDA(cudaMalloc(&b, nd * sizeof(double)));
+    ctx->bio_cap = nd;
+  }
+  ensure_scratch(*ctx, nd);
+  cudaStream_t sc = ctx->stream, sin = ctx->copy_stream[0], sout = ctx->copy_stream[1];
+  KCUDA(cudaEventRecord(ctx->ev_ready, sc));
+  KCUDA(cudaStreamWaitEvent(sin, ctx->ev_ready, 0));
+  KCUDA(cudaStreamWaitEvent(sout, ctx->ev_ready, 0));
+  const SepKind k = kind;
+  for (int i = 0; i < count; ++i) {
+    const int p = i & 1;
+    double* din = ctx->bio[p];
+    double* dout = ctx->bio[2 + p];
+    if (i >= 2) KCUDA(cudaStreamWaitEvent(sin, ctx->ev_comp[p], 0));  // item i-2 read din
+    KCUDA(cudaMemcpyAsync(din, in[i], nd * sizeof(double), cudaMemcpyHostToDevice, sin));
+    KCUDA(cudaEventRecord(ctx->ev_up[p], sin));
+    KCUDA(cudaStreamWaitEvent(sc, ctx->ev_up[p], 0));
+    if (i >= 2) KCUDA(cudaStreamWaitEvent(sc, ctx->ev_down[p], 0));  // item i-2 left dout
+    if (k == SEP_PROPAGATE && dt == 0.0)  // operators.cpp:64
+      KCUDA(cudaMemcpyAsync(dout, din, nd * sizeof(double), cudaMemcpyDeviceToDevice, sc));
+    else
+      sep_transform(*ctx, *op, din, dout, cplx, k, op->shift, dt, nullptr, 0.0);
+    KCUDA(cudaEventRecord(ctx->ev_comp[p], sc));
+    KCUDA(cudaStreamWaitEvent(sout, ctx->ev_comp[p], 0));
+    KCUDA(cudaMemcpyAsync(out[i], dout, nd * sizeof(double), cudaMemcpyDeviceToHost, sout));
+    KCUDA(cudaEventRecord(ctx->ev_down[p], sout));
+  }
+  KCUDA(cudaStreamSynchronize(sout));
+  KCUDA(cudaStreamSynchronize(sin));
+  KCUDA(cudaStreamSynchronize(sc));
+}
+
+int kronop_sep_solve_host_batch(kronop_ctx* ctx, const kronop_op* op, int count,
+                                const double* const* b_hosts, int is_complex,
+                                double* const* out_hosts) {
+  return guard([&] {
+    param_check(ctx && op, "solve: null argument");
+    host_batch(ctx, op, count, b_hosts, is_complex, out_hosts, SEP_SOLVE, 0.0);
+  });
+}
+
+int kronop_sep_propagate_host_batch(kronop_ctx* ctx, const kronop_op* op, int count,
+                                    const double* const* psi_hosts, double dt,
+                                    double* const* out_hosts) {
+  return guard([&] {
+    param_check(ctx && op, "propagate: null argument");
+    host_batch(ctx, op, count, psi_hosts, 1, out_hosts, SEP_PROPAGATE, dt);
+  });
 }
 
 int kronop_sep_solve_host(kronop_ctx* ctx, const kronop_op* op, const double* b_host,

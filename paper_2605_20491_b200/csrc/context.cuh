@@ -28,6 +28,11 @@ struct kronop_ctx {
   cudaEvent_t ev_in[kMaxChunks] = {};
   cudaEvent_t ev_out[kMaxChunks] = {};
   cudaEvent_t ev_ready = nullptr;
+  // batched host path (kronop_sep_*_host_batch): ping-pong device in / out fields and the
+  // upload / compute / download events of the two items in flight
+  double* bio[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t bio_cap = 0;
+  cudaEvent_t ev_up[2] = {}, ev_comp[2] = {}, ev_down[2] = {};
   // device block pool for driver vectors (stream-ordered reuse on `stream`; freed at destroy)
   struct Block {
     double* p;

@@ -181,6 +181,39 @@ def test_host_buffer_entry_points_pipelined(ctx, spec):
     assert rel(op.solve_host(psi, np.empty_like(psi)), ko.solve(psi)) < 1e-13
 
 
+@pytest.mark.parametrize("spec", [(8.0, 13, 5, 3), (3.0, 2, 5, 4)])
+def test_host_batch_entry_points(ctx, spec):
+    """kronop_sep_{solve,propagate}_host_batch: every item of a 5-item batch (distinct inputs,
+    real and complex, one output aliasing its own input) equals the oracle; 1- and 0-item
+    batches."""
+    A = api()
+    grid = A.Grid.sem(*spec)
+    op = _trap_op(A, ctx, grid, 0.25)
+    ko = oracle_op_from(op, 0.25)
+    n = grid.node_count()
+    bs = [K.uniform_pm1(90 + i, n) for i in range(5)]
+    outs = [np.empty_like(b) for b in bs]
+    outs[3] = bs[3]  # in place
+    ref3 = ko.solve(bs[3].copy())
+    refs = [ko.solve(b) for b in bs]
+    refs[3] = ref3
+    op.solve_host_batch(bs, outs)
+    for o, r in zip(outs, refs):
+        assert rel(o, r) < 1e-13
+    cs = [K.seeded_complex_field(grid.shape, 95 + i) for i in range(3)]
+    couts = [np.empty_like(c) for c in cs]
+    op.propagate_host_batch(cs, 0.07, couts)
+    for o, c in zip(couts, cs):
+        assert rel(o, ko.propagate(c, 0.07)) < 1e-13
+    op.solve_host_batch(cs[:2], couts[:2])
+    for o, c in zip(couts[:2], cs[:2]):
+        assert rel(o, ko.solve(c)) < 1e-13
+    one = [np.empty_like(bs[0])]
+    op.solve_host_batch(bs[:1], one)
+    assert rel(one[0], ko.solve(bs[0])) < 1e-13
+    op.solve_host_batch([], [])
+
+
 def test_full_operator_apply_with_v2_and_sigma(ctx):
     A = api()
     grid = A.Grid.sem(1.0, 7, 1, 3)  # 6^3, acceptance.cpp:131-200 instance
