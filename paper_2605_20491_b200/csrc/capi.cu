@@ -292,7 +292,7 @@ static std::vector<std::pair<int, int>> kron_groups(const kronop_op& op) {
 
 static bool sep_propagate_kron(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out,
                                double shift, double dt, bool bphase, const double* bfield,
-                               double bfactor) {
+                               double bfactor, const double* pre = nullptr) {
   const std::vector<std::pair<int, int>> groups = kron_groups(op);
   if (groups.empty() || !fused_rot_eligible(in) || !fused_rot_eligible(out)) return false;
   static const bool no_fold = [] {
@@ -330,13 +330,30 @@ static bool sep_propagate_kron(kronop_ctx& ctx, const kronop_op& op, const doubl
                   : src == ctx.scratch[0]  ? ctx.scratch[1]
                                            : ctx.scratch[0];
     launch_kron_group(ctx.stream, src, dst, n, f, fold[g] != 0, op.N, E.data() + kSlot * g,
-                      last && bphase ? bfield : nullptr, bfactor, last && bphase ? 1 : 0);
+                      last && bphase ? bfield : nullptr, bfactor, last && bphase ? 1 : 0,
+                      g == 0 ? pre : nullptr);
     ctx.ws.launches += 1;
     src = dst;
   }
   if (src != out)
     KCUDA(cudaMemcpyAsync(out, src, nd * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
   return true;
+}
+
+// psi <- e^{-i(A - shift) dt} (e^{-i factor B} psi) in place: the split-step's B phase followed
+// by its next A propagation, with the phase applied by the Kronecker kernel's first group as it
+// reads psi (pre_tab = the (cos, sin) table of k_phase's operations; bit-identical to the phase
+// pass followed by the propagate). Returns false when the propagate does not take the Kronecker
+// path (the caller then runs the phase pass and the propagate).
+bool kron_path_likely(const kronop_op& op) {
+  return op.exec_prec == KRONOP_PREC_FP64 && !op.folded && use_fused_small(op) &&
+         !kron_groups(op).empty();
+}
+
+bool sep_propagate_prephased(kronop_ctx& ctx, const kronop_op& op, double* psi, double shift,
+                             double dt, const double* pre_tab) {
+  if (op.exec_prec != KRONOP_PREC_FP64 || op.folded || !use_fused_small(op)) return false;
+  return sep_propagate_kron(ctx, op, psi, psi, shift, dt, false, nullptr, 0.0, pre_tab);
 }
 
 // Small-extent path, rotating layout (fused_rot.cu): groups of up to 3 consecutive axes (fused

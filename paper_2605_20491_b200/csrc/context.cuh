@@ -144,6 +144,14 @@ enum SepKind { SEP_APPLY = 0, SEP_SOLVE = 1, SEP_PROPAGATE = 2 };
 void sep_transform(kronop_ctx& ctx, const kronop_op& op, const double* in, double* out, int cplx,
                    SepKind kind, double shift, double dt, const double* diag, double sigma,
                    bool bphase = false, const double* bfield = nullptr, double bfactor = 0.0);
+// psi <- propagate(pointwise_phase(psi)) in place with the phase ((cos, sin) table pre_tab)
+// applied by the Kronecker propagate's first group as it reads psi; false (nothing enqueued)
+// when the propagate does not take the Kronecker path.
+bool sep_propagate_prephased(kronop_ctx& ctx, const kronop_op& op, double* psi, double shift,
+                             double dt, const double* pre_tab);
+// true when complex propagates of op take the Kronecker path (for steps whose E_a fold or are
+// small; sep_propagate_prephased has the final say per dt)
+bool kron_path_likely(const kronop_op& op);
 // Singular-shift guard of SeparableOperator::solve (operators.cpp:44-52).
 void check_solve_shift(kronop_ctx& ctx, const kronop_op& op, double shift);
 

@@ -722,6 +722,39 @@ static void run_schedules(kronop_ctx& c, const kronop_op& a, const double* b_dia
     const char* e = getenv("KRONOP_BPHASE_FUSED");
     return !(e && e[0] == '1');
   }();
+  // Default on the Kronecker path (small extents, config 5): a B phase is deferred to the A
+  // propagation that follows it and applied by that propagate's first group as it reads psi,
+  // from a (cos, sin) table per distinct B factor (k_phase's operations, so bit-identical): one
+  // field round trip and no per-element sincos per step. KRONOP_BPHASE_PRE=0 turns it off.
+  static const bool pre_off = [] {
+    const char* e = getenv("KRONOP_BPHASE_PRE");
+    return e && e[0] == '0';
+  }();
+  std::vector<double> factors;
+  for (const Schedule& sc : schedules)
+    for (double f : sc.b_factors)
+      if (std::find(factors.begin(), factors.end(), f) == factors.end()) factors.push_back(f);
+  bool use_pre = !pre_off && unfused && steps * schedules.size() > 1 && kron_path_likely(a);
+  if (use_pre) {  // the tables (2N doubles each) must leave room for the rest of the run
+    size_t free_b = 0, total_b = 0;
+    KCUDA(cudaMemGetInfo(&free_b, &total_b));
+    use_pre = factors.size() * 2.0 * a.N * sizeof(double) <= 0.5 * static_cast<double>(free_b);
+  }
+  std::vector<std::unique_ptr<DBuf>> tables(factors.size());
+  auto table_of = [&](double f) -> const double* {
+    const size_t i = std::find(factors.begin(), factors.end(), f) - factors.begin();
+    if (!tables[i]) {
+      tables[i] = std::make_unique<DBuf>(c, static_cast<size_t>(2 * a.N));
+      launch_phase_table(c.stream, c.ws, tables[i]->p, b_diag, f, a.N);
+    }
+    return tables[i]->p;
+  };
+  bool pending_b = false;
+  double pending_bf = 0.0;
+  auto apply_pending_b = [&]() {
+    if (pending_b) launch_phase(c.stream, c.ws, psi, b_diag, pending_bf, a.N);
+    pending_b = false;
+  };
   double pending = 0.0;
   bool has_pending = false;
   auto flush = [&](bool with_b, double factor) {
@@ -729,13 +762,26 @@ static void run_schedules(kronop_ctx& c, const kronop_op& a, const double* b_dia
     const bool prop = has_pending && t != 0.0;  // propagate(psi, 0) is a copy (operators.cpp:64)
     pending = 0.0;
     has_pending = false;
-    if (prop && with_b && !unfused) {
-      sep_transform(c, a, psi, psi, 1, SEP_PROPAGATE, a.shift, t, nullptr, 0.0, true, b_diag,
-                    factor);
-      return;
+    if (prop && pending_b &&
+        sep_propagate_prephased(c, a, psi, a.shift, t, table_of(pending_bf))) {
+      pending_b = false;  // B, then this A: done by the propagate
+    } else {
+      apply_pending_b();
+      if (prop && with_b && !unfused) {
+        sep_transform(c, a, psi, psi, 1, SEP_PROPAGATE, a.shift, t, nullptr, 0.0, true, b_diag,
+                      factor);
+        return;
+      }
+      if (prop) sep_transform(c, a, psi, psi, 1, SEP_PROPAGATE, a.shift, t, nullptr, 0.0);
     }
-    if (prop) sep_transform(c, a, psi, psi, 1, SEP_PROPAGATE, a.shift, t, nullptr, 0.0);
-    if (with_b) launch_phase(c.stream, c.ws, psi, b_diag, factor, a.N);
+    if (with_b) {
+      if (use_pre) {
+        pending_b = true;
+        pending_bf = factor;
+      } else {
+        launch_phase(c.stream, c.ws, psi, b_diag, factor, a.N);
+      }
+    }
   };
   auto propagate_a = [&](double t) {
     if (!merge && has_pending) flush(false, 0.0);
@@ -753,6 +799,7 @@ static void run_schedules(kronop_ctx& c, const kronop_op& a, const double* b_dia
       propagate_a(s.a_times[m]);
     }
   flush(false, 0.0);
+  apply_pending_b();
 }
 
 }  // namespace kronop_dev

@@ -86,6 +86,9 @@ struct KronArgs {
   const double* bfield;  // B phase in the last group's store (null = B == 1)
   double bfactor;
   int bphase;
+  // B phase of the step BEFORE this propagate, applied to the tile as it is read (first group
+  // only): pre[i] = (cos, sin) of -factor B_i, the table of k_phase's operations; null = none
+  const double2* pre;
   double2 E[NF][N][N];  // E_j(i, k) = (re, im): output i, input k
 };
 
@@ -118,6 +121,13 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
           "r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// psi * (cos, sin) with the operations of k_phase (vector_ops.cu), so a B phase applied here is
+// bit-identical to the standalone pass
+__device__ __forceinline__ double2 kr_rotate(double2 v, double2 cs) {
+  return make_double2(__dsub_rn(__dmul_rn(v.x, cs.x), __dmul_rn(v.y, cs.y)),
+                      __dadd_rn(__dmul_rn(v.x, cs.y), __dmul_rn(v.y, cs.x)));
 }
 
 // Bulk loads of tile `tile` (thread 0): one copy when the planes are unpadded, else one per plane.
@@ -222,7 +232,8 @@ __device__ __forceinline__ void kr_contract(const KronArgs<N, NF>& A, const doub
 
 // Group axis J < NF - 1, in place: fibers (lo < P, hg < H, qi) at lo + P N hg + PPC qi.
 template <int N, int NF, int J, bool FOLD>
-__device__ __forceinline__ void kr_axis(const KronArgs<N, NF>& A, double* buf, int tid) {
+__device__ __forceinline__ void kr_axis(const KronArgs<N, NF>& A, double* buf, long long q0,
+                                        int qv, int tid) {
   using C = KronCfg<N, NF>;
   constexpr int P = kr_pow(N, J);
   constexpr int H = C::F / (P * N);
@@ -235,6 +246,11 @@ __device__ __forceinline__ void kr_axis(const KronArgs<N, NF>& A, double* buf, i
     double2 x[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) x[k] = p[k * P];
+    if (J == 0 && A.pre && qi < qv) {  // the preceding B phase, on the original-layout input
+      const double2* ph = A.pre + (q0 + qi) * C::F + lo + hg * (P * N);
+#pragma unroll
+      for (int k = 0; k < N; ++k) x[k] = kr_rotate(x[k], __ldg(ph + k * P));
+    }
     double re[N], im[N];
     kr_contract<N, NF, J, FOLD>(A, x, re, im);
 #pragma unroll
@@ -259,6 +275,11 @@ __device__ __forceinline__ void kr_last(const KronArgs<N, NF>& A, const double* 
     double2 x[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) x[k] = p[k * P];
+    if (NF == 1 && A.pre) {  // one-axis group: this is also the first axis
+      const double2* ph = A.pre + (q0 + qi) * C::F + lo;
+#pragma unroll
+      for (int k = 0; k < N; ++k) x[k] = kr_rotate(x[k], __ldg(ph + k * P));
+    }
     double re[N], im[N];
     kr_contract<N, NF, NF - 1, FOLD>(A, x, re, im);
     const long long o = q0 + qi + A.Q * lo;
@@ -280,11 +301,12 @@ __device__ __forceinline__ void kr_last(const KronArgs<N, NF>& A, const double* 
 }
 
 template <int N, int NF, int J, bool FOLD>
-__device__ __forceinline__ void kr_inplace_axes(const KronArgs<N, NF>& A, double* buf, int tid) {
+__device__ __forceinline__ void kr_inplace_axes(const KronArgs<N, NF>& A, double* buf, long long q0,
+                                                int qv, int tid) {
   if constexpr (J < NF - 1) {
-    kr_axis<N, NF, J, FOLD>(A, buf, tid);
+    kr_axis<N, NF, J, FOLD>(A, buf, q0, qv, tid);
     __syncthreads();
-    kr_inplace_axes<N, NF, J + 1, FOLD>(A, buf, tid);
+    kr_inplace_axes<N, NF, J + 1, FOLD>(A, buf, q0, qv, tid);
   }
 }
 
@@ -332,7 +354,7 @@ __global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, KRONOP_KR_CTAS)
     mbar_wait(&full[s], (it / STAGES) & 1);
     const long long q0 = tile * C::QT;
     const int qv = static_cast<int>(A.Q - q0 < C::QT ? A.Q - q0 : C::QT);
-    kr_inplace_axes<N, NF, 0, FOLD>(A, buf, tid);
+    kr_inplace_axes<N, NF, 0, FOLD>(A, buf, q0, qv, tid);
     kr_last<N, NF, FOLD, BPH>(A, buf, q0, qv, tid);
     const long long next = tile + STAGES;
     __syncwarp();
@@ -352,7 +374,7 @@ __global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, KRONOP_KR_CTAS)
 
 template <int N, int NF, bool FOLD, bool BPH>
 void launch_kron(cudaStream_t s, const double* x, double* y, long long Ntot, const double* E,
-                 const double* bfield, double bfactor, int bphase) {
+                 const double* bfield, double bfactor, int bphase, const double* pre) {
   using C = KronCfg<N, NF>;
   KronArgs<N, NF> a;
   std::memset(&a, 0, sizeof(a));
@@ -363,6 +385,7 @@ void launch_kron(cudaStream_t s, const double* x, double* y, long long Ntot, con
   a.bfield = bfield;
   a.bfactor = bfactor;
   a.bphase = bphase;
+  a.pre = reinterpret_cast<const double2*>(pre);
   std::memcpy(a.E, E, sizeof(a.E));
   const size_t smem = static_cast<size_t>(KRONOP_KR_STAGES) * C::STAGE * sizeof(double) +
                       KRONOP_KR_STAGES * sizeof(uint64_t) + KRONOP_KR_STAGES * sizeof(int);
@@ -375,28 +398,30 @@ void launch_kron(cudaStream_t s, const double* x, double* y, long long Ntot, con
 
 template <int N, bool FOLD>
 void launch_kron_f(cudaStream_t s, int f, const double* x, double* y, long long Ntot,
-                   const double* E, const double* bfield, double bfactor, int bphase) {
+                   const double* E, const double* bfield, double bfactor, int bphase,
+                   const double* pre) {
   if (f == 1 && bphase)
-    launch_kron<N, 1, FOLD, true>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron<N, 1, FOLD, true>(s, x, y, Ntot, E, bfield, bfactor, bphase, pre);
   else if (f == 1)
-    launch_kron<N, 1, FOLD, false>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron<N, 1, FOLD, false>(s, x, y, Ntot, E, bfield, bfactor, bphase, pre);
   else if (f == 2 && bphase)
-    launch_kron<N, 2, FOLD, true>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron<N, 2, FOLD, true>(s, x, y, Ntot, E, bfield, bfactor, bphase, pre);
   else if (f == 2)
-    launch_kron<N, 2, FOLD, false>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron<N, 2, FOLD, false>(s, x, y, Ntot, E, bfield, bfactor, bphase, pre);
   else if (bphase)
-    launch_kron<N, 3, FOLD, true>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron<N, 3, FOLD, true>(s, x, y, Ntot, E, bfield, bfactor, bphase, pre);
   else
-    launch_kron<N, 3, FOLD, false>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron<N, 3, FOLD, false>(s, x, y, Ntot, E, bfield, bfactor, bphase, pre);
 }
 
 template <int N>
 void launch_kron_n(cudaStream_t s, int f, bool fold, const double* x, double* y, long long Ntot,
-                   const double* E, const double* bfield, double bfactor, int bphase) {
+                   const double* E, const double* bfield, double bfactor, int bphase,
+                   const double* pre) {
   if (fold)
-    launch_kron_f<N, true>(s, f, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron_f<N, true>(s, f, x, y, Ntot, E, bfield, bfactor, bphase, pre);
   else
-    launch_kron_f<N, false>(s, f, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron_f<N, false>(s, f, x, y, Ntot, E, bfield, bfactor, bphase, pre);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -464,6 +489,7 @@ struct KronDArgs {
   const double* bfield;
   double bfactor;
   int bphase;
+  const double2* pre;  // as KronArgs::pre
   double2 E[NF][kd_me(N) * kd_me(N) + (N / 2) * (N / 2)];  // per axis [Ae | Ao], row-major
 };
 
@@ -496,16 +522,58 @@ __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, 
     }
   };
   double2* b2 = reinterpret_cast<double2*>(buf);
-  // fold: (x_k, x_{N-1-k}) -> (s_k, d_k) for the warp's 8 fibers
-  for (int it = lane; it < 8 * M; it += 32) {
-    const int gg = it / M, k = it - gg * M;
-    const int f = f0 + gg;
-    if (f < C::FIB) {
-      int qi, lo;
-      double2* p = b2 + base_of(f, qi, lo);
-      const double2 u = p[k * P], v = p[(N - 1 - k) * P];
-      p[k * P] = make_double2(u.x + v.x, u.y + v.y);
-      p[(N - 1 - k) * P] = make_double2(u.x - v.x, u.y - v.y);
+  // fold: (x_k, x_{N-1-k}) -> (s_k, d_k) for the warp's 8 fibers; on the group's first axis the
+  // preceding B phase (A.pre) is applied to the inputs first, the center element included
+  const bool pre = J == 0 && A.pre != nullptr;
+  constexpr int ITER = (8 * ME + 31) / 32;
+  if (pre) {
+    // the table entries of all the lane's items are loaded first (2 ITER loads in flight), then
+    // the fold: one global-load latency per warp step instead of one per item
+    double2 pu[ITER], pv[ITER];
+#pragma unroll
+    for (int j = 0; j < ITER; ++j) {
+      const int it = lane + 32 * j, gg = it / ME, k = it - gg * ME;
+      const int f = f0 + gg;
+      pu[j] = pv[j] = make_double2(1.0, 0.0);
+      if (it < 8 * ME && f < C::FIB) {
+        int qi, lo;
+        const int fb = base_of(f, qi, lo);
+        if (qi < qv) {
+          // tile-local complex offset fb + k P is the global one minus q0 F (plane pitch F)
+          const double2* ph = A.pre + q0 * C::F + fb;
+          pu[j] = __ldg(ph + k * P);
+          if (k < M) pv[j] = __ldg(ph + (N - 1 - k) * P);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < ITER; ++j) {
+      const int it = lane + 32 * j, gg = it / ME, k = it - gg * ME;
+      const int f = f0 + gg;
+      if (it < 8 * ME && f < C::FIB) {
+        int qi, lo;
+        double2* p = b2 + base_of(f, qi, lo);
+        const double2 u = kr_rotate(p[k * P], pu[j]);
+        if (k < M) {
+          const double2 v = kr_rotate(p[(N - 1 - k) * P], pv[j]);
+          p[k * P] = make_double2(u.x + v.x, u.y + v.y);
+          p[(N - 1 - k) * P] = make_double2(u.x - v.x, u.y - v.y);
+        } else {
+          p[k * P] = u;  // center (odd N), phased
+        }
+      }
+    }
+  } else {
+    for (int it = lane; it < 8 * M; it += 32) {
+      const int gg = it / M, k = it - gg * M;
+      const int f = f0 + gg;
+      if (f < C::FIB) {
+        int qi, lo;
+        double2* p = b2 + base_of(f, qi, lo);
+        const double2 u = p[k * P], v = p[(N - 1 - k) * P];
+        p[k * P] = make_double2(u.x + v.x, u.y + v.y);
+        p[(N - 1 - k) * P] = make_double2(u.x - v.x, u.y - v.y);
+      }
     }
   }
   __syncwarp();
@@ -679,7 +747,7 @@ __global__ void __launch_bounds__(32 * KRONOP_KD_WARPS, 1)
 
 template <int N, int NF>
 void launch_kron_dmma(cudaStream_t s, const double* x, double* y, long long Ntot, const double* E,
-                      const double* bfield, double bfactor, int bphase) {
+                      const double* bfield, double bfactor, int bphase, const double* pre) {
   using C = KronDCfg<N, NF>;
   KronDArgs<N, NF> a;
   std::memset(&a, 0, sizeof(a));
@@ -690,6 +758,7 @@ void launch_kron_dmma(cudaStream_t s, const double* x, double* y, long long Ntot
   a.bfield = bfield;
   a.bfactor = bfactor;
   a.bphase = bphase;
+  a.pre = reinterpret_cast<const double2*>(pre);
   // E: per axis the N x N slot of the caller's buffer holds [Ae | Ao] (kron_fold_blocks)
   constexpr int BLK = C::ME * C::ME + C::M * C::M;
   for (int j = 0; j < NF; ++j)
@@ -706,11 +775,12 @@ void launch_kron_dmma(cudaStream_t s, const double* x, double* y, long long Ntot
 
 template <int N>
 void launch_kron_dmma_n(cudaStream_t s, int f, const double* x, double* y, long long Ntot,
-                        const double* E, const double* bfield, double bfactor, int bphase) {
+                        const double* E, const double* bfield, double bfactor, int bphase,
+                   const double* pre) {
   if (f == 1)
-    launch_kron_dmma<N, 1>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron_dmma<N, 1>(s, x, y, Ntot, E, bfield, bfactor, bphase, pre);
   else
-    launch_kron_dmma<N, 2>(s, x, y, Ntot, E, bfield, bfactor, bphase);
+    launch_kron_dmma<N, 2>(s, x, y, Ntot, E, bfield, bfactor, bphase, pre);
 }
 
 }  // namespace
@@ -723,23 +793,23 @@ bool kron_group_needs_fold(int n) { return n > KR_MAXN; }
 
 void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, bool fold,
                        long long Ntot, const double* E, const double* bfield, double bfactor,
-                       int bphase) {
+                       int bphase, const double* pre) {
   param_check(kron_group_supported(n, f), "kron propagate: unsupported group");
   param_check(fold || n <= KR_MAXN, "kron propagate: extents > 10 need parity-symmetric axes");
   param_check((reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0,
               "kron propagate: fields must be 16-byte aligned");
   switch (n) {
-    case 2: launch_kron_n<2>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 3: launch_kron_n<3>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 4: launch_kron_n<4>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 5: launch_kron_n<5>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 6: launch_kron_n<6>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 7: launch_kron_n<7>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 8: launch_kron_n<8>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 9: launch_kron_n<9>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
-    case 10: launch_kron_n<10>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase); break;
+    case 2: launch_kron_n<2>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
+    case 3: launch_kron_n<3>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
+    case 4: launch_kron_n<4>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
+    case 5: launch_kron_n<5>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
+    case 6: launch_kron_n<6>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
+    case 7: launch_kron_n<7>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
+    case 8: launch_kron_n<8>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
+    case 9: launch_kron_n<9>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
+    case 10: launch_kron_n<10>(s, f, fold, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
 #define KD_CASE(NN) \
-  case NN: launch_kron_dmma_n<NN>(s, f, x, y, Ntot, E, bfield, bfactor, bphase); break;
+  case NN: launch_kron_dmma_n<NN>(s, f, x, y, Ntot, E, bfield, bfactor, bphase, pre); break;
     KD_CASE(11) KD_CASE(12) KD_CASE(13) KD_CASE(14) KD_CASE(15) KD_CASE(16) KD_CASE(17)
     KD_CASE(18) KD_CASE(19) KD_CASE(20) KD_CASE(21) KD_CASE(22) KD_CASE(23) KD_CASE(24)
     KD_CASE(25) KD_CASE(26) KD_CASE(27) KD_CASE(28) KD_CASE(29) KD_CASE(30) KD_CASE(31)

@@ -143,9 +143,11 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
 // the parity blocks [Ae | Ao] of R-symmetric axis matrices instead (see kr_contract).
 bool kron_group_supported(int n, int f);
 bool kron_group_needs_fold(int n);  // extents > 10 (DMMA kernel): parity-symmetric axes only
+// pre: (cos, sin) table of the B phase that precedes this propagate (first group only; null =
+// none), applied to the input as it is read.
 void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, bool fold,
                        long long Ntot, const double* E, const double* bfield, double bfactor,
-                       int bphase);
+                       int bphase, const double* pre);
 
 bool mode_product_tma_eligible(const double* x, const PassShape& ps);
 bool mode_product_tma_enabled();  // false under KRONOP_DISABLE_TMA=1

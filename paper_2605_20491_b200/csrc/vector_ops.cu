@@ -288,6 +288,26 @@ void launch_phase(cudaStream_t s, Workspace& ws, double* psi, const double* b, d
   KCUDA(cudaGetLastError());
 }
 
+// (cos, sin) of the B phase -factor * b[i] with k_phase's operations: the table a Kronecker
+// propagate reads to apply the preceding B step to its input (bit-identical to k_phase).
+__global__ void k_phase_table(double* tab, const double* b, double factor, long long n) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += stride) {
+    const double phase = b ? __dmul_rn(-factor, b[i]) : -factor;
+    double sn, cs;
+    sincos(phase, &sn, &cs);
+    reinterpret_cast<double2*>(tab)[i] = make_double2(cs, sn);
+  }
+}
+
+void launch_phase_table(cudaStream_t s, Workspace& ws, double* tab, const double* b,
+                        double factor, long long n) {
+  k_phase_table<<<kEltBlocks, kThreads, 0, s>>>(tab, b, factor, n);
+  ws.launches += 1;
+  KCUDA(cudaGetLastError());
+}
+
 // out[i] = generator(multi-index of i): 0 = mass product, 1 = direct sum (from 0.0), 2 = product
 struct GenArgs {
   IndexGeom geom;

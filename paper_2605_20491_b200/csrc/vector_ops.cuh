@@ -42,6 +42,8 @@ void launch_div_by(cudaStream_t s, Workspace& ws, double* y, const double* x, lo
                    const double* nrm_dev, int take_sqrt);
 void launch_mul_diag(cudaStream_t s, Workspace& ws, double* y, const double* x, const double* d,
                      long long n, int cplx);
+void launch_phase_table(cudaStream_t s, Workspace& ws, double* tab, const double* b,
+                        double factor, long long n);
 void launch_phase(cudaStream_t s, Workspace& ws, double* psi, const double* b, double factor,
                   long long n);
 void launch_generate(cudaStream_t s, Workspace& ws, double* out, const IndexGeomHost& g,

@@ -124,25 +124,34 @@ for spec in ((3.0, 2, 5, 4), (3.0, 1, 4, 9), (2.0, 1, 6, 5)):
     bd = torch.from_numpy(b).cuda()
     out["q%d" % g.dim] = A.qhop_step(op, bd, psi, 0.02, 3).cpu().numpy()
     out["y%d" % g.dim] = A.yoshida_step(op, bd, psi, 0.02, 2).cpu().numpy()
+    for m in (1, 3):
+        st, err, steps = A.evolve(A.SplitSpec(quad_points=m, dt=0.01, total_time=0.05,
+                                              merge_across_steps=bool(m == 1)),
+                                  op, bd, psi, stationary_eigenvalue=0.0)
+        out["e%d_%d" % (g.dim, m)] = st.cpu().numpy()
 np.savez(sys.argv[1], **out)
 '''
 
 
 def test_kron_fused_b_phase_bit_identical(tmp_path):
-    """B phase in the last Kronecker group's store (KRONOP_BPHASE_FUSED=1) = the standalone
-    phase pass, bit for bit; both equal the oracle's split step to 1e-12."""
+    """The split-step B phase three ways, bit for bit the same states (qHOP / Yoshida steps,
+    merged and unmerged evolve): deferred into the next Kronecker propagate's first group from a
+    (cos, sin) table (the default), as the standalone phase pass (KRONOP_BPHASE_PRE=0), and in the
+    last group's store of the propagate before it (KRONOP_BPHASE_FUSED=1)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for flag in ("1", "0"):
-        f = str(tmp_path / ("k%s.npz" % flag))
-        env = dict(os.environ, KRONOP_BPHASE_FUSED=flag)
+    for name, env_add in (("pre", {}), ("standalone", {"KRONOP_BPHASE_PRE": "0"}),
+                          ("post", {"KRONOP_BPHASE_FUSED": "1"})):
+        f = str(tmp_path / ("k%s.npz" % name))
+        env = dict(os.environ, **env_add)
         subprocess.check_call([sys.executable, "-c", _BPHASE_SNIPPET, f], cwd=root, env=env)
-        res[flag] = np.load(f)
-    for k in res["1"].files:
-        assert np.array_equal(res["1"][k], res["0"][k]), k
+        res[name] = np.load(f)
+    for k in res["pre"].files:
+        assert np.array_equal(res["pre"][k], res["standalone"][k]), k
+        assert np.array_equal(res["post"][k], res["standalone"][k]), k
 
 
 def test_kron_qhop_step_matches_oracle(ctx):

@@ -1,5 +1,6 @@
-"""Strang (qHOP M = 1, merge) steps/s on the config-5 grids with the B phase fused into the
-propagate's last pass (default) or as its own pass (KRONOP_BPHASE_FUSED=0)."""
+"""Strang (qHOP M = 1, merge) steps/s on the config-5 grids: the B phase applied by the next
+Kronecker propagate's first group (default), as its own pass (KRONOP_BPHASE_PRE=0), or in the
+last pass of the propagate before it (KRONOP_BPHASE_FUSED=1)."""
 import json, os, sys, time
 import numpy as np
 import torch
@@ -7,7 +8,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 from paper_2605_20491_b200 import api as A, potentials as P
 
 ctx = A.Context(0)
-res = {"fused": os.environ.get("KRONOP_BPHASE_FUSED", "1")}
+res = {"pre": os.environ.get("KRONOP_BPHASE_PRE", "1"),
+       "post_fused": os.environ.get("KRONOP_BPHASE_FUSED", "0")}
 for name, (L, cells, k, d) in {"9d": (3.0, 2, 5, 9), "6d": (5.0, 3, 10, 6), "3d499": (8.0, 100, 5, 3)}.items():
     g = A.Grid.sem(L, cells, k, d)
     lap = g.laplacian(ctx)
