@@ -473,8 +473,8 @@ class SeparableOperator:
     def solve_host_batch(self, bs, outs, is_complex=None):
         """kronop_sep_solve_host_batch: a list of host right-hand sides -> host solutions, the
         copies of neighbouring items overlapped with each item's transform."""
-        cplx = np.iscomplexobj(bs[0]) if is_complex is None else is_complex
         n = len(bs)
+        cplx = (n > 0 and np.iscomplexobj(bs[0])) if is_complex is None else is_complex
         ins = (C.c_void_p * n)(*[b.ctypes.data for b in bs])
         ous = (C.c_void_p * n)(*[o.ctypes.data for o in outs])
         check(lib().kronop_sep_solve_host_batch(self.ctx.h, self.h, n, ins, int(cplx), ous))

@@ -372,6 +372,92 @@ __global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, KRONOP_KR_CTAS)
   }
 }
 
+// Paired-tile variant (groups whose tile has QT < 8 planes, i.e. 9D n = 9: 64-byte output runs).
+// A CTA takes its tiles two at a time: both tiles' group axes, the last one included, are applied
+// in place in shared memory, then the pair is written out as F runs of 2 QT consecutive q
+// (128 bytes at QT = 4) -- the rotating copy moved 3.1 TB/s with 64-byte runs and 4.5 TB/s with
+// 128-byte ones (tools/microbench/rot_copy.cu). 4 stages: one pair in compute, the next in flight.
+// Stages sit one complex apart (pitch STAGE + 2 doubles) so the 16-byte reads of the write-out,
+// 8 lanes = one g over 4 planes of each tile, are bank-conflict free.
+#ifndef KRONOP_KR_PAIR
+#define KRONOP_KR_PAIR 1
+#endif
+template <int N, int NF>
+struct KronPairCfg {
+  using C = KronCfg<N, NF>;
+  static constexpr int STAGES = 4;
+  static constexpr int PITCH = C::STAGE + 2;  // doubles between stages
+};
+
+template <int N, int NF, bool FOLD, bool BPH>
+__global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, 1)
+    kron_rot_pair_kernel(const __grid_constant__ KronArgs<N, NF> A) {
+  using C = KronCfg<N, NF>;
+  using PC = KronPairCfg<N, NF>;
+  constexpr int STAGES = PC::STAGES;
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * PC::PITCH);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // contiguous, even-aligned tile range per CTA (a pair's first q is a multiple of 2 QT)
+  long long per = (A.ntiles + gridDim.x - 1) / gridDim.x;
+  per += per & 1;
+  const long long t0 = blockIdx.x * per;
+  const long long t1 = t0 + per < A.ntiles ? t0 + per : A.ntiles;
+  if (tid == 0)
+    for (int s = 0; s < STAGES; ++s)
+      if (t0 + s < t1) kr_issue(A, t0 + s, sm + s * PC::PITCH, &full[s]);
+  for (int it = 0;; it += 2) {
+    const long long tile = t0 + it;
+    if (tile >= t1) break;
+    const int nt = tile + 1 < t1 ? 2 : 1;
+    const long long q0 = tile * C::QT;
+    for (int u = 0; u < nt; ++u) {
+      const int s = (it + u) % STAGES;
+      double* buf = sm + s * PC::PITCH;
+      mbar_wait(&full[s], ((it + u) / STAGES) & 1);
+      const long long qu = q0 + u * C::QT;
+      const int qv = static_cast<int>(A.Q - qu < C::QT ? A.Q - qu : C::QT);
+      kr_inplace_axes<N, NF, 0, FOLD>(A, buf, qu, qv, tid);
+      kr_axis<N, NF, NF - 1, FOLD>(A, buf, qu, qv, tid);  // the last axis, in place
+      __syncthreads();
+    }
+    // write-out: item = (g, qq), qq = 2 QT consecutive q fastest; 16 bytes per item
+    const int qn = static_cast<int>(A.Q - q0 < nt * C::QT ? A.Q - q0 : nt * C::QT);
+    const double2* b0 = reinterpret_cast<const double2*>(sm + (it % STAGES) * PC::PITCH);
+    const double2* b1 = reinterpret_cast<const double2*>(sm + ((it + 1) % STAGES) * PC::PITCH);
+    double2* y2 = reinterpret_cast<double2*>(A.y);
+    constexpr int QQ = 2 * C::QT;
+#pragma unroll 4
+    for (int e = tid; e < C::F * QQ; e += C::THREADS) {
+      const int qq = e % QQ, g = e / QQ;
+      if (qq >= qn) continue;
+      const int qi = qq % C::QT;
+      double2 v = (qq < C::QT ? b0 : b1)[qi * C::PPC + g];
+      const long long oi = q0 + qq + A.Q * g;
+      if constexpr (BPH) {  // pointwise_phase (splitting.cpp:44-51), the operations of k_phase
+        const double phase = A.bfield ? __dmul_rn(-A.bfactor, A.bfield[oi]) : -A.bfactor;
+        double sn, cs;
+        sincos(phase, &sn, &cs);
+        v = kr_rotate(v, make_double2(cs, sn));
+      }
+      y2[oi] = v;
+    }
+    __syncthreads();  // both stages read (generic proxy) before their refills
+    if (tid == 0)
+      for (int u = 0; u < 2; ++u)
+        if (tile + u + STAGES < t1) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          const int s = (it + u) % STAGES;
+          kr_issue(A, tile + u + STAGES, sm + s * PC::PITCH, &full[s]);
+        }
+  }
+}
+
 template <int N, int NF, bool FOLD, bool BPH>
 void launch_kron(cudaStream_t s, const double* x, double* y, long long Ntot, const double* E,
                  const double* bfield, double bfactor, int bphase, const double* pre) {
@@ -387,6 +473,19 @@ void launch_kron(cudaStream_t s, const double* x, double* y, long long Ntot, con
   a.bphase = bphase;
   a.pre = reinterpret_cast<const double2*>(pre);
   std::memcpy(a.E, E, sizeof(a.E));
+  if constexpr (KRONOP_KR_PAIR && NF >= 2 && C::QT < 8 &&
+                KronPairCfg<N, NF>::STAGES * KronPairCfg<N, NF>::PITCH * 8 + 64 <= 227 * 1024) {
+    using PC = KronPairCfg<N, NF>;
+    const size_t smem = static_cast<size_t>(PC::STAGES) * PC::PITCH * sizeof(double) +
+                        PC::STAGES * sizeof(uint64_t);
+    ensure_smem_attr(reinterpret_cast<const void*>(kron_rot_pair_kernel<N, NF, FOLD, BPH>), smem);
+    const long long cap = device_sm_count();
+    const long long grid = (a.ntiles + 1) / 2 < cap ? (a.ntiles + 1) / 2 : cap;
+    kron_rot_pair_kernel<N, NF, FOLD, BPH>
+        <<<static_cast<unsigned>(grid), C::THREADS, smem, s>>>(a);
+    KCUDA(cudaGetLastError());
+    return;
+  }
   const size_t smem = static_cast<size_t>(KRONOP_KR_STAGES) * C::STAGE * sizeof(double) +
                       KRONOP_KR_STAGES * sizeof(uint64_t) + KRONOP_KR_STAGES * sizeof(int);
   ensure_smem_attr(reinterpret_cast<const void*>(kron_rot_kernel<N, NF, FOLD, BPH>), smem);
