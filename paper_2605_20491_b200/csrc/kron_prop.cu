@@ -663,15 +663,34 @@ __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, 
       }
     }
   } else {
-    for (int it = lane; it < 8 * M; it += 32) {
-      const int gg = it / M, k = it - gg * M;
-      const int f = f0 + gg;
-      if (f < C::FIB) {
-        int qi, lo;
-        double2* p = b2 + base_of(f, qi, lo);
-        const double2 u = p[k * P], v = p[(N - 1 - k) * P];
-        p[k * P] = make_double2(u.x + v.x, u.y + v.y);
-        p[(N - 1 - k) * P] = make_double2(u.x - v.x, u.y - v.y);
+    // all of the lane's pairs are loaded before any is folded (ILP over the shared-memory
+    // latency; the loop form stalled on each LDS)
+    constexpr int IT2 = (8 * M + 31) / 32;
+    constexpr int BATCH = 2;  // pairs in flight per lane (more spilled at 128 registers)
+#pragma unroll
+    for (int j0 = 0; j0 < IT2; j0 += BATCH) {
+      double2 uu[BATCH], vv[BATCH];
+      int off[BATCH];
+#pragma unroll
+      for (int jj = 0; jj < BATCH; ++jj) {
+        const int it = lane + 32 * (j0 + jj), gg = it / M, k = it - gg * M;
+        const int f = f0 + gg;
+        off[jj] = -1;
+        if (j0 + jj < IT2 && it < 8 * M && f < C::FIB) {
+          int qi, lo;
+          off[jj] = base_of(f, qi, lo) + k * P;
+          uu[jj] = b2[off[jj]];
+          vv[jj] = b2[off[jj] + (N - 1 - 2 * k) * P];
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < BATCH; ++jj) {
+        if (off[jj] >= 0) {
+          const int k = (lane + 32 * (j0 + jj)) % M;
+          b2[off[jj]] = make_double2(uu[jj].x + vv[jj].x, uu[jj].y + vv[jj].y);
+          b2[off[jj] + (N - 1 - 2 * k) * P] =
+              make_double2(uu[jj].x - vv[jj].x, uu[jj].y - vv[jj].y);
+        }
       }
     }
   }
