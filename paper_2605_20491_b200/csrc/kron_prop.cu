@@ -600,10 +600,15 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 
 // One warp step on 8 fibers (g = lane / 4) of one axis: fold in place, the two block products,
 // unfold; in place (LAST = false) or to HBM with the group at the slow end (LAST = true).
+#ifndef KRONOP_KD_G
+#define KRONOP_KD_G 1  // fiber octets per warp step (B fragments reused across them)
+#endif
 template <int N, int NF, int J, bool LAST>
 __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, const double* frag,
                                         int f0, long long q0, int qv, int lane) {
   using C = KronDCfg<N, NF>;
+  constexpr int G = KRONOP_KD_G;
+  constexpr int FW = 8 * G;        // fibers per warp step
   constexpr int P = kr_pow(N, J);  // complex stride of the axis
   constexpr int H = C::F / (P * N);
   constexpr int M = C::M, ME = C::ME;
@@ -621,10 +626,10 @@ __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, 
     }
   };
   double2* b2 = reinterpret_cast<double2*>(buf);
-  // fold: (x_k, x_{N-1-k}) -> (s_k, d_k) for the warp's 8 fibers; on the group's first axis the
+  // fold: (x_k, x_{N-1-k}) -> (s_k, d_k) for the warp's fibers; on the group's first axis the
   // preceding B phase (A.pre) is applied to the inputs first, the center element included
   const bool pre = J == 0 && A.pre != nullptr;
-  constexpr int ITER = (8 * ME + 31) / 32;
+  constexpr int ITER = (FW * ME + 31) / 32;
   if (pre) {
     // the table entries of all the lane's items are loaded first (2 ITER loads in flight), then
     // the fold: one global-load latency per warp step instead of one per item
@@ -634,7 +639,7 @@ __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, 
       const int it = lane + 32 * j, gg = it / ME, k = it - gg * ME;
       const int f = f0 + gg;
       pu[j] = pv[j] = make_double2(1.0, 0.0);
-      if (it < 8 * ME && f < C::FIB) {
+      if (it < FW * ME && f < C::FIB) {
         int qi, lo;
         const int fb = base_of(f, qi, lo);
         if (qi < qv) {
@@ -649,7 +654,7 @@ __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, 
     for (int j = 0; j < ITER; ++j) {
       const int it = lane + 32 * j, gg = it / ME, k = it - gg * ME;
       const int f = f0 + gg;
-      if (it < 8 * ME && f < C::FIB) {
+      if (it < FW * ME && f < C::FIB) {
         int qi, lo;
         double2* p = b2 + base_of(f, qi, lo);
         const double2 u = kr_rotate(p[k * P], pu[j]);
@@ -663,9 +668,9 @@ __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, 
       }
     }
   } else {
-    // all of the lane's pairs are loaded before any is folded (ILP over the shared-memory
-    // latency; the loop form stalled on each LDS)
-    constexpr int IT2 = (8 * M + 31) / 32;
+    // the lane's pairs are loaded in batches before they are folded (ILP over the
+    // shared-memory latency; the loop form stalled on each LDS)
+    constexpr int IT2 = (FW * M + 31) / 32;
     constexpr int BATCH = 2;  // pairs in flight per lane (more spilled at 128 registers)
 #pragma unroll
     for (int j0 = 0; j0 < IT2; j0 += BATCH) {
@@ -676,7 +681,7 @@ __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, 
         const int it = lane + 32 * (j0 + jj), gg = it / M, k = it - gg * M;
         const int f = f0 + gg;
         off[jj] = -1;
-        if (j0 + jj < IT2 && it < 8 * M && f < C::FIB) {
+        if (j0 + jj < IT2 && it < FW * M && f < C::FIB) {
           int qi, lo;
           off[jj] = base_of(f, qi, lo) + k * P;
           uu[jj] = b2[off[jj]];
@@ -695,62 +700,86 @@ __device__ __forceinline__ void kd_step(const KronDArgs<N, NF>& A, double* buf, 
     }
   }
   __syncwarp();
-  const int f = f0 + g;
-  const bool fok = f < C::FIB;
-  int qi = 0, lo = 0;
-  const int fb = base_of(fok ? f : f0, qi, lo);
-  const double* src = buf + 2 * fb;
-  double acc_a[C::NTA][2], acc_b[C::NTB][2];
+  bool fok[G];
+  int qis[G], los[G], fbs[G];
+  const double* src[G];
 #pragma unroll
-  for (int nt = 0; nt < C::NTA; ++nt) acc_a[nt][0] = acc_a[nt][1] = 0.0;
+  for (int gg = 0; gg < G; ++gg) {
+    const int f = f0 + 8 * gg + g;
+    fok[gg] = f < C::FIB;
+    fbs[gg] = base_of(fok[gg] ? f : f0, qis[gg], los[gg]);
+    src[gg] = buf + 2 * fbs[gg];
+  }
+  double acc_a[G][C::NTA][2], acc_b[G][C::NTB][2];
 #pragma unroll
-  for (int nt = 0; nt < C::NTB; ++nt) acc_b[nt][0] = acc_b[nt][1] = 0.0;
+  for (int gg = 0; gg < G; ++gg) {
+#pragma unroll
+    for (int nt = 0; nt < C::NTA; ++nt) acc_a[gg][nt][0] = acc_a[gg][nt][1] = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < C::NTB; ++nt) acc_b[gg][nt][0] = acc_b[gg][nt][1] = 0.0;
+  }
   const double* fa = frag + lane;
 #pragma unroll
   for (int kk = 0; kk < C::K4A; ++kk) {
     const int kap = 4 * kk + t, k = kap >> 1;
-    const double a = k < ME ? src[2 * P * k + (kap & 1)] : 0.0;
+    double a[G];
 #pragma unroll
-    for (int nt = 0; nt < C::NTA; ++nt) dmma884(acc_a[nt], a, fa[(kk * C::NTA + nt) * 32]);
+    for (int gg = 0; gg < G; ++gg) a[gg] = k < ME ? src[gg][2 * P * k + (kap & 1)] : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < C::NTA; ++nt) {
+      const double b = fa[(kk * C::NTA + nt) * 32];
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) dmma884(acc_a[gg][nt], a[gg], b);
+    }
   }
   const double* fbg = frag + C::FRAG_A + lane;
 #pragma unroll
   for (int kk = 0; kk < C::K4B; ++kk) {
     const int kap = 4 * kk + t, k = kap >> 1;
-    const double a = k < M ? src[2 * P * (N - 1 - k) + (kap & 1)] : 0.0;
+    double a[G];
 #pragma unroll
-    for (int nt = 0; nt < C::NTB; ++nt) dmma884(acc_b[nt], a, fbg[(kk * C::NTB + nt) * 32]);
+    for (int gg = 0; gg < G; ++gg)
+      a[gg] = k < M ? src[gg][2 * P * (N - 1 - k) + (kap & 1)] : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < C::NTB; ++nt) {
+      const double b = fbg[(kk * C::NTB + nt) * 32];
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) dmma884(acc_b[gg][nt], a[gg], b);
+    }
   }
   __syncwarp();  // every lane has read its fibers before any output overwrites them
-  if (!fok) return;
-  if constexpr (LAST) {
-    if (qi >= qv) return;
-  }
   double2* y2 = reinterpret_cast<double2*>(A.y);
-  auto put = [&](int i, double re, double im) {
-    if constexpr (LAST) {
-      const long long oi = q0 + qi + A.Q * (lo + static_cast<long long>(P) * i);
-      if (A.bphase) {  // pointwise_phase (splitting.cpp:44-51), the operations of k_phase
-        const double phase = A.bfield ? __dmul_rn(-A.bfactor, A.bfield[oi]) : -A.bfactor;
-        double sn, cs;
-        sincos(phase, &sn, &cs);
-        const double r0 = re, i0 = im;
-        re = __dsub_rn(__dmul_rn(r0, cs), __dmul_rn(i0, sn));
-        im = __dadd_rn(__dmul_rn(r0, sn), __dmul_rn(i0, cs));
-      }
-      y2[oi] = make_double2(re, im);
-    } else {
-      b2[fb + i * P] = make_double2(re, im);
-    }
-  };
 #pragma unroll
-  for (int nt = 0; nt < C::NTA; ++nt) {
-    const int i = 4 * nt + t;
-    if (i < M) {
-      put(i, acc_a[nt][0] + acc_b[nt][0], acc_a[nt][1] + acc_b[nt][1]);
-      put(N - 1 - i, acc_a[nt][0] - acc_b[nt][0], acc_a[nt][1] - acc_b[nt][1]);
-    } else if (i < ME) {
-      put(i, acc_a[nt][0], acc_a[nt][1]);
+  for (int gg = 0; gg < G; ++gg) {
+    if (!fok[gg]) continue;
+    if constexpr (LAST) {
+      if (qis[gg] >= qv) continue;
+    }
+    auto put = [&](int i, double re, double im) {
+      if constexpr (LAST) {
+        const long long oi = q0 + qis[gg] + A.Q * (los[gg] + static_cast<long long>(P) * i);
+        if (A.bphase) {  // pointwise_phase (splitting.cpp:44-51), the operations of k_phase
+          const double phase = A.bfield ? __dmul_rn(-A.bfactor, A.bfield[oi]) : -A.bfactor;
+          double sn, cs;
+          sincos(phase, &sn, &cs);
+          const double r0 = re, i0 = im;
+          re = __dsub_rn(__dmul_rn(r0, cs), __dmul_rn(i0, sn));
+          im = __dadd_rn(__dmul_rn(r0, sn), __dmul_rn(i0, cs));
+        }
+        y2[oi] = make_double2(re, im);
+      } else {
+        b2[fbs[gg] + i * P] = make_double2(re, im);
+      }
+    };
+#pragma unroll
+    for (int nt = 0; nt < C::NTA; ++nt) {
+      const int i = 4 * nt + t;
+      if (i < M) {
+        put(i, acc_a[gg][nt][0] + acc_b[gg][nt][0], acc_a[gg][nt][1] + acc_b[gg][nt][1]);
+        put(N - 1 - i, acc_a[gg][nt][0] - acc_b[gg][nt][0], acc_a[gg][nt][1] - acc_b[gg][nt][1]);
+      } else if (i < ME) {
+        put(i, acc_a[gg][nt][0], acc_a[gg][nt][1]);
+      }
     }
   }
 }
@@ -761,7 +790,7 @@ __device__ __forceinline__ void kd_axis(const KronDArgs<N, NF>& A, double* buf, 
   using C = KronDCfg<N, NF>;
   constexpr bool LAST = J == NF - 1;
   constexpr int GW = KRONOP_KD_WARPS / KRONOP_KD_GROUPS;  // warps per group
-  for (int f0 = gwarp * 8; f0 < C::FIB; f0 += 8 * GW)
+  for (int f0 = gwarp * 8 * KRONOP_KD_G; f0 < C::FIB; f0 += 8 * KRONOP_KD_G * GW)
     kd_step<N, NF, J, LAST>(A, buf, frag + J * C::FRAG, f0, q0, qv, lane);
   if constexpr (!LAST) {
     if constexpr (KRONOP_KD_GROUPS == 1)
