@@ -185,3 +185,33 @@ def test_kron_large_step_falls_back(ctx):
     got = host(op.propagate(dev(psi), 0.003))
     assert ctx.launch_count() - c0 == 2
     assert rel(got, ko.propagate(psi, 0.003)) < 1e-13
+
+
+@pytest.mark.parametrize("name", ["9d_n9", "6d_n29"])
+def test_kron_config5_full_size_matches_transform_passes(ctx, name):
+    """BASELINE configs[4] at its own size (9^9 = 3.9e8 and 29^6 = 5.9e8 complex DoF, beyond the
+    oracle): the Kronecker propagate against the transform / phase / transform sequence built from
+    single passes of the same operator (kronop_op_pass_ex: forward axes 0..d-1 with the phase
+    epilogue on the last, backward axes 0..d-1 -- the kernels the oracle parity tests pin at small
+    sizes), relative l2 within 1e-13, and the mass norm preserved."""
+    A = api()
+    L, cells, k, d = {"9d_n9": (3.0, 2, 5, 9), "6d_n29": (5.0, 3, 10, 6)}[name]
+    grid = A.Grid.sem(L, cells, k, d)
+    op = grid.laplacian(ctx)
+    N = grid.node_count()
+    psi = torch.view_as_complex(A.splitmix_uniform(ctx, 7, 2 * N).view(-1, 2))
+    dt = 0.005
+    c0 = ctx.launch_count()
+    got = op.propagate(psi, dt)
+    assert ctx.launch_count() - c0 == 3
+    cur = psi
+    for a in range(d):
+        cur = op.transform_pass_ex(cur, a, True, "phase" if a == d - 1 else "store", dt=dt)
+    for a in range(d):
+        cur = op.transform_pass_ex(cur, a, False)
+    diff = float(torch.linalg.norm(got - cur) / torch.linalg.norm(cur))
+    assert diff < 1e-13, diff
+    w = A.mass_field(ctx, grid.shape, grid.mass)
+    n0 = float(torch.sum(w * psi.abs() ** 2))
+    n1 = float(torch.sum(w * got.abs() ** 2))
+    assert abs(n1 - n0) <= 1e-12 * n0
