@@ -458,8 +458,9 @@ def secondary_metrics(A, P, ctx, device):
                       "kinetic step), dt = 0.005, Kronecker-factored: %d group launches, no "
                       "phase pass" % (d, n, launches)}
         del o
-        # Strang (qHOP M = 1, merged) with B = a separable harmonic trap on the grid: per step
-        # one A propagation and one B phase pass
+        # Strang (qHOP M = 1, merged, dt = 0.005, T = 0.1 as in the config) with B = a separable
+        # harmonic trap on the grid: per step one A propagation with the previous B phase as its
+        # prologue
         try:
             b = torch.from_numpy(np.ascontiguousarray(
                 P.separable_sum(g, P.build_potential("harmonic", g)))).to(device)
@@ -467,7 +468,7 @@ def secondary_metrics(A, P, ctx, device):
                      lap, b, psi, stationary_eigenvalue=0.0)
             torch.cuda.synchronize()
             e0.record(ctx.stream)
-            st, err, steps = A.evolve(A.SplitSpec(quad_points=1, dt=0.005, total_time=0.05,
+            st, err, steps = A.evolve(A.SplitSpec(quad_points=1, dt=0.005, total_time=0.1,
                                                   merge_across_steps=True),
                                       lap, b, psi, stationary_eigenvalue=0.0)
             e1.record(ctx.stream)
