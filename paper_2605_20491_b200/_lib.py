@@ -145,6 +145,7 @@ PROTOTYPES = {
     "kronop_slab_create_nccl": (I, [P, C.c_char_p, I, I, I, IP, P, P, P, P, D, P]),
     "kronop_slab_destroy": (I, [P]),
     "kronop_slab_info": (I, [P, IP, IP, IP]),
+    "kronop_slab_stats": (I, [P, C.POINTER(C.c_longlong)]),
     "kronop_slab_part": (I, [P, I, IP, C.POINTER(C.c_void_p), C.POINTER(C.c_longlong),
                              C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "kronop_slab_set_shift": (I, [P, D]),

@@ -97,7 +97,23 @@ struct EpiParams {
   const int* active = nullptr;
 };
 
+// Exchange-fused output of a pass (slab decomposition, slab.cu): the output columns i are split
+// into consecutive ranges [i0[k], i0[k+1]) owned by destination part k, and element (p, i, q)
+// (p < pre, q < post) is stored at dst[k] + (i - i0[k]) * ccol[k] + p + q * cq[k] -- straight into
+// the part's slab buffer (peer memory over NVLink, or the same device), so the pass that precedes
+// a slab transpose IS the transpose.
+constexpr int kMaxSplit = 8;
+struct SplitDst {
+  int parts = 0;
+  int i0[kMaxSplit + 1] = {};
+  double* dst[kMaxSplit] = {};
+  long long ccol[kMaxSplit] = {};
+  long long cq[kMaxSplit] = {};
+};
+
 struct PassShape {
+  // exchange-fused store (TMA kernel, EPI_STORE only); null = the pass's own output y
+  const SplitDst* split = nullptr;
   long long pre = 1, post = 1;
   int nk = 0, m = 0;
   // q-strides of X and Y (doubles). 0 = dense (pre * nk, pre * m); larger values address a

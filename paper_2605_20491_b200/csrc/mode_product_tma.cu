@@ -176,7 +176,10 @@ __device__ __forceinline__ int chS(int g) { return ((g & 1) << 2) | (g >> 1); }
 //   EK_DIV      spectral divide on the last real-view axis (the solve's fused pass): per-warp
 //               tables of the row lambda partial sums and column eigenvalues, built before the K
 //               loop, and the divisions of one row batch issued together (div_rn_fast)
-enum { EK_GENERIC = 0, EK_STORE = 1, EK_DIV = 2, EK_MUL = 3, EK_PHASE = 4, EK_AXPY = 5 };
+//   EK_SPLIT    plain store into the destination parts of a slab exchange (SplitDst): the
+//               per-column destination is resolved once per tile, the rows stay coalesced
+enum { EK_GENERIC = 0, EK_STORE = 1, EK_DIV = 2, EK_MUL = 3, EK_PHASE = 4, EK_AXPY = 5,
+       EK_SPLIT = 6 };
 
 struct TArgs {
   double* y;
@@ -189,6 +192,7 @@ struct TArgs {
   int ntiles_n;
   long long ntiles_m;
   EpiParams ep;
+  SplitDst split;  // EK_SPLIT
 };
 
 template <int BN, int LOADER>
@@ -579,6 +583,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (yi[jc][v] >= 0) args.y[yi[jc][v]] = val;
           }
       }
+    } else if (EK == EK_SPLIT) {
+      // destination of each of the thread's columns (one range lookup per column per tile)
+      double* cb[C::CT][2];
+      long long cqv[C::CT][2];
+#pragma unroll
+      for (int jc = 0; jc < C::CT; ++jc)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int i = col0 + wn * C::WTN + col_map<BN, LOADER>(jc, 2 * t + v);
+          int k = 0;
+          while (k + 1 < args.split.parts && i >= args.split.i0[k + 1]) ++k;
+          cb[jc][v] = i < m ? args.split.dst[k] + (i - args.split.i0[k]) * args.split.ccol[k]
+                            : nullptr;
+          cqv[jc][v] = args.split.cq[k];
+        }
+#pragma unroll
+      for (int j = 0; j < C::RT; ++j) {
+        const long long r = row0 + wm * C::WTM + row_map<BN, LOADER>(j, g);
+        if (r >= R) continue;
+        const long long q = r / pre;
+        const long long p = r - q * pre;
+#pragma unroll
+        for (int jc = 0; jc < C::CT; ++jc)
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            if (cb[jc][v]) cb[jc][v][p + q * cqv[jc][v]] = acc[j][jc][v];
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < C::RT; ++j) {
@@ -658,6 +689,8 @@ void set_attr_tma() {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
   KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, EK_AXPY>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, EK_SPLIT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
   if (LOADER != TL_CONTIG)
     KCUDA(cudaFuncSetAttribute(mode_product_tma_kernel<BN, LOADER, 1, LOADER != TL_CONTIG ? EK_PHASE : EK_GENERIC>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
@@ -728,7 +761,7 @@ void launch_tma(cudaStream_t s, int num_sms, long long ntiles_m, int ntiles_n,
   const long long tiles = ntiles_m * ntiles_n;
   int cl = 1;
   for (int c : {4, 2}) {
-    if (c != forced) continue;
+    if (c != forced || ta.split.parts > 0) continue;  // the cluster kernels store plainly
     if (ntiles_n % c != 0 || tiles < 4LL * num_sms) continue;
     const int g = c == 4 ? cluster_grid<BN, LOADER, 4>(num_sms) : cluster_grid<BN, LOADER, 2>(num_sms);
     if (g >= num_sms - (forced ? num_sms : 0) && g > 0) {
@@ -745,7 +778,10 @@ void launch_tma(cudaStream_t s, int num_sms, long long ntiles_m, int ntiles_n,
     const EpiParams& ep = ta.ep;
     const dim3 grid(static_cast<unsigned>(blocks));
     const bool last_axis = ep.axis + 1 == ep.ndims && ep.lam[ep.axis] != nullptr;
-    if (ep.kind == EPI_STORE)
+    if (ta.split.parts > 0)
+      mode_product_tma_kernel<BN, LOADER, 1, EK_SPLIT><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(
+          tmx, tmA, ta);
+    else if (ep.kind == EPI_STORE)
       mode_product_tma_kernel<BN, LOADER, 1, EK_STORE><<<grid, NTHREADS, Cfg<BN>::SMEM, s>>>(
           tmx, tmA, ta);
     else if (ep.kind == EPI_SPEC_DIV && last_axis)
@@ -798,6 +834,10 @@ void launch_mode_product_tma(cudaStream_t s, const double* x, double* y, const d
   ta.ldy = ps.ldy_eff();
   ta.ycol = ps.ycol ? ps.ycol : ps.pre;
   ta.rot = ps.rot;
+  ta.split = ps.split ? *ps.split : SplitDst{};
+  param_check(!ps.split || (ep.kind == EPI_STORE && !ps.rot && ps.split->parts >= 1 &&
+                            ps.split->parts <= kMaxSplit),
+              "mode_product: exchange-fused store needs a plain, unrotated pass");
   param_check(!ps.rot || ep.axis + 1 >= ep.ndims || (ep.kind != EPI_SPEC_MUL &&
               ep.kind != EPI_SPEC_DIV && ep.kind != EPI_SPEC_PHASE),
               "mode_product: rotated pass with a spectral epilogue must be on the last axis");

@@ -173,6 +173,8 @@ struct SlabPart {
   double* mass[KRONOP_MAX_DIM] = {};  // full per-axis mass weights (or null)
   double* zx = nullptr;               // exchange buffer, z-slab layout
   size_t zx_cap = 0;
+  double* yx = nullptr;               // receive buffer of the fused z -> y exchange, y-slab layout
+  size_t yx_cap = 0;
   double* red = nullptr;              // partials ring [kSlabRing][kSlabSlots] + gathered
   double* gathered = nullptr;         // NCCL: [P][kSlabSlots]
   const double** srcs = nullptr;      // device array of P pointers (this ring slot's sources)
@@ -193,6 +195,7 @@ struct kronop_slab {
   bool nccl = false;
   ncclComm_t comm = nullptr;
   int ring = 0;  // next partials ring slot
+  long long fused_transforms = 0;  // applications whose transposes were exchange-fused passes
 };
 
 namespace kronop_dev {
@@ -355,12 +358,191 @@ static void ensure_part_buffers(kronop_slab& s, int c) {
   }
 }
 
+// Exchange-fused transform (in-process transport): the pass before each slab transpose stores
+// its output columns straight into the destination parts' slab buffers (SplitDst epilogue of the
+// TMA pass kernel: NVLink peer stores for distinct GPUs, plain stores for virtual slabs), so the
+// transposes cost no copy and no extra HBM round trip, and the transfer overlaps the pass's
+// math tile by tile:
+//   forward passes 0..d-3 (local) | barrier | pass d-2 -> every part's y-slab receive buffer (yx)
+//   | barrier | pass d-1 forward + spectral (local) | pass d-1 backward -> every part's z-slab
+//   buffer (zx) | barrier | backward passes 0..d-2 (local)
+// Used when both transpose passes take the TMA kernel on every part (KRONOP_SLAB_FUSED=0: the
+// copy exchange). The NCCL transport keeps grouped send / recv.
+static bool slab_fused_ok(kronop_slab& s, const std::vector<const double*>& in, int c) {
+  static const bool off = [] {
+    const char* e = getenv("KRONOP_SLAB_FUSED");
+    return e && e[0] == '0';
+  }();
+  if (off || s.nccl || s.d < 2 || static_cast<int>(s.parts.size()) > kMaxSplit ||
+      !mode_product_tma_enabled())
+    return false;
+  const int d = s.d;
+  for (size_t i = 0; i < s.parts.size(); ++i) {
+    const SlabPart& pt = s.parts[i];
+    PassShape a;
+    a.pre = s.R * c;
+    a.nk = a.m = s.n[d - 2];
+    a.post = s.zs[pt.p];
+    const double* x0 = d - 2 == 0 ? in[i] : pt.ctx->scratch[(d - 3) % 2];
+    PassShape b;
+    b.pre = s.R * c * s.ys[pt.p];
+    b.nk = b.m = s.n[d - 1];
+    b.post = 1;
+    if (!mode_product_tma_eligible(x0, a) || !mode_product_tma_eligible(pt.ctx->scratch[1], b))
+      return false;
+  }
+  return true;
+}
+
+static void slab_transform_fused(kronop_slab& s, const std::vector<const double*>& in,
+                                 const std::vector<double*>& out, int cplx, const SlabEpi& e) {
+  const int c = cplx ? 2 : 1;
+  const int d = s.d;
+  const long long Rc = s.R * c;
+  const int ny = s.n[d - 2];
+  for (auto& pt : s.parts) {
+    part_device(pt);
+    const size_t yneed = static_cast<size_t>(yslab_elems(s, pt.p)) * c;
+    if (yneed > pt.yx_cap) {
+      KCUDA(cudaStreamSynchronize(pt.ctx->stream));
+      if (pt.yx) KCUDA(cudaFree(pt.yx));
+      pt.yx = nullptr;
+      KCUDA(cudaMalloc(&pt.yx, yneed * sizeof(double)));
+      pt.yx_cap = yneed;
+    }
+  }
+  // forward passes on axes 0..d-3 (local)
+  std::vector<const double*> cur(s.parts.size());
+  for (size_t i = 0; i < s.parts.size(); ++i) {
+    SlabPart& pt = s.parts[i];
+    part_device(pt);
+    kronop_ctx& ctx = *pt.ctx;
+    int shp[KRONOP_MAX_DIM];
+    for (int a = 0; a < d - 1; ++a) shp[a] = s.n[a];
+    shp[d - 1] = s.zs[pt.p];
+    View v = make_view(d, shp, cplx);
+    cur[i] = in[i];
+    for (int a = 0; a < d - 2; ++a) {
+      double* dst = ctx.scratch[a % 2];
+      EpiParams ep;
+      ep.active = e.active ? e.active[i] : nullptr;
+      run_pass(ctx, cur[i], dst, v, a + v.cplx, pt.fwd[a], pt.lda[a], s.n[a], ep);
+      cur[i] = dst;
+    }
+  }
+  barrier_a(s);  // every part's receive buffer is free (its last reader was the previous call)
+  // pass d-2 = the z -> y transpose: column y of part p's output goes to part q = owner(y) at
+  // yx_q[(z0_p + z) ys_q Rc + (y - y0_q) Rc + r]
+  for (size_t i = 0; i < s.parts.size(); ++i) {
+    SlabPart& pt = s.parts[i];
+    part_device(pt);
+    SplitDst sd;
+    sd.parts = static_cast<int>(s.parts.size());
+    for (size_t k = 0; k < s.parts.size(); ++k) {
+      const SlabPart& q = s.parts[k];
+      sd.i0[k] = s.y0[q.p];
+      sd.dst[k] = q.yx + static_cast<long long>(s.z0[pt.p]) * s.ys[q.p] * Rc;
+      sd.ccol[k] = Rc;
+      sd.cq[k] = static_cast<long long>(s.ys[q.p]) * Rc;
+    }
+    sd.i0[s.parts.size()] = ny;
+    PassShape ps;
+    ps.pre = Rc;
+    ps.nk = ps.m = ny;
+    ps.post = s.zs[pt.p];
+    ps.split = &sd;
+    EpiParams ep;
+    ep.active = e.active ? e.active[i] : nullptr;
+    launch_mode_product(pt.ctx->stream, cur[i], pt.zx, pt.fwd[d - 2], pt.lda[d - 2], ps, ep);
+    pt.ctx->ws.launches += 1;
+  }
+  barrier_a(s);  // every part's y-slab is complete
+  // forward axis d-1 + spectral epilogue (local), then backward axis d-1 = the y -> z transpose:
+  // column z of part q's output goes to part p = owner(z) at zx_p[(z - z0_p) ny Rc + y0_q Rc + r']
+  for (size_t i = 0; i < s.parts.size(); ++i) {
+    SlabPart& pt = s.parts[i];
+    part_device(pt);
+    kronop_ctx& ctx = *pt.ctx;
+    int shp[KRONOP_MAX_DIM];
+    for (int a = 0; a < d - 2; ++a) shp[a] = s.n[a];
+    shp[d - 2] = s.ys[pt.p];
+    shp[d - 1] = s.n[d - 1];
+    View v = make_view(d, shp, cplx);
+    EpiParams ep;
+    ep.kind = e.kind;
+    ep.axis = d - 1 + v.cplx;
+    ep.ndims = v.nd;
+    for (int k = 0; k < v.nd; ++k) ep.ext[k] = v.ext[k];
+    for (int a = 0; a < d; ++a) ep.lam[a + v.cplx] = pt.lam[a];
+    ep.lam[d - 2 + v.cplx] = pt.lam[d - 2] + s.y0[pt.p];  // this part's rows of axis d-2
+    ep.shift = e.shift;
+    ep.dt = e.dt;
+    ep.cplx = v.cplx;
+    ep.active = e.active ? e.active[i] : nullptr;
+    run_pass(ctx, pt.yx, ctx.scratch[1], v, d - 1 + v.cplx, pt.fwd[d - 1], pt.lda[d - 1],
+             s.n[d - 1], ep);
+    SplitDst sd;
+    sd.parts = static_cast<int>(s.parts.size());
+    for (size_t k = 0; k < s.parts.size(); ++k) {
+      const SlabPart& p = s.parts[k];
+      sd.i0[k] = s.z0[p.p];
+      sd.dst[k] = p.zx + static_cast<long long>(s.y0[pt.p]) * Rc;
+      sd.ccol[k] = static_cast<long long>(ny) * Rc;
+      sd.cq[k] = 0;
+    }
+    sd.i0[s.parts.size()] = s.n[d - 1];
+    PassShape ps;
+    ps.pre = Rc * s.ys[pt.p];
+    ps.nk = ps.m = s.n[d - 1];
+    ps.post = 1;
+    ps.split = &sd;
+    EpiParams st;
+    st.active = ep.active;
+    launch_mode_product(ctx.stream, ctx.scratch[1], ctx.scratch[0], pt.bwd[d - 1],
+                        pt.lda[d - 1], ps, st);
+    ctx.ws.launches += 1;
+  }
+  barrier_a(s);  // every part's z-slab is complete
+  // backward passes on axes 0..d-2, the last with the FullOperator AXPY epilogue
+  for (size_t i = 0; i < s.parts.size(); ++i) {
+    SlabPart& pt = s.parts[i];
+    part_device(pt);
+    kronop_ctx& ctx = *pt.ctx;
+    int shp[KRONOP_MAX_DIM];
+    for (int a = 0; a < d - 1; ++a) shp[a] = s.n[a];
+    shp[d - 1] = s.zs[pt.p];
+    View v = make_view(d, shp, cplx);
+    const double* src = pt.zx;
+    for (int a = 0; a < d - 1; ++a) {
+      const bool last = a == d - 2;
+      double* dst = last ? out[i] : ctx.scratch[a % 2];
+      EpiParams ep;
+      ep.active = e.active ? e.active[i] : nullptr;
+      const double* dg = e.diag.empty() ? nullptr : e.diag[i];
+      if (last && (dg != nullptr || e.sigma != 0.0)) {
+        ep.kind = EPI_AXPY_DIAG;
+        ep.diag = dg;
+        ep.u = in[i];
+        ep.sigma = e.sigma;
+        ep.cplx = v.cplx;
+      }
+      run_pass(ctx, src, dst, v, a + v.cplx, pt.bwd[a], pt.lda[a], s.n[a], ep);
+      src = dst;
+    }
+  }
+}
+
 // out = T (f(lambda - shift) . T^{-1} in) [+ diag .* in - sigma in] on every local part's slab
 static void slab_transform(kronop_slab& s, const std::vector<const double*>& in,
                            const std::vector<double*>& out, int cplx, const SlabEpi& e) {
   const int c = cplx ? 2 : 1;
   const int d = s.d;
   ensure_part_buffers(s, c);
+  if (slab_fused_ok(s, in, c)) {
+    slab_transform_fused(s, in, out, cplx, e);
+    ++s.fused_transforms;
+    return;
+  }
   std::vector<const double*> zsrc(s.parts.size()), ysrc(s.parts.size());
   std::vector<double*> ydst(s.parts.size()), zdst(s.parts.size());
   // forward passes on axes 0..d-2 (z-slab), ending in zx
@@ -999,6 +1181,7 @@ int kronop_slab_destroy(kronop_slab* s) {
       cudaFree(pt.mass[a]);
     }
     cudaFree(pt.zx);
+    cudaFree(pt.yx);
     cudaFree(pt.red);
     cudaFree(pt.gathered);
     for (auto* p : pt.srcs_ring) cudaFree(p);
@@ -1017,6 +1200,13 @@ int kronop_slab_info(const kronop_slab* s, int* nparts, int* nlocal, int* first_
     if (nparts) *nparts = s->P;
     if (nlocal) *nlocal = static_cast<int>(s->parts.size());
     if (first_part) *first_part = s->parts.empty() ? 0 : s->parts[0].p;
+  });
+}
+
+int kronop_slab_stats(const kronop_slab* s, long long* fused_transforms) {
+  return guard_slab([&] {
+    param_check(s, "slab_stats: null slab");
+    if (fused_transforms) *fused_transforms = s->fused_transforms;
   });
 }
 

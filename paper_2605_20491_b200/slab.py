@@ -314,6 +314,14 @@ class DeviceSlabOperator:
     def plane_elems(self):
         return int(np.prod(self.shape[:-1]))
 
+    def fused_transforms(self) -> int:
+        """kronop_slab_stats: applications whose transposes ran as exchange-fused passes."""
+        import ctypes as C
+        from . import _lib
+        v = C.c_longlong()
+        _lib.check(_lib.lib().kronop_slab_stats(self.h, C.byref(v)))
+        return v.value
+
     def scatter(self, full: torch.Tensor):
         """This process's z-slabs of a full field (host or device tensor, flat, axis 0 fastest)."""
         pe = self.plane_elems()

@@ -172,3 +172,61 @@ def test_nccl_slab_one_rank(ctx):
     rep = so.pcg(bs, xs, A.PcgConfig(rel_tol=1e-10))
     assert rep.converged and rep.iterations == 1  # exact preconditioner
     so.close()
+
+
+_FUSED_SNIPPET = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from oracle import kronop_oracle as K
+from paper_2605_20491_b200 import api as A, slab as S
+ctx = A.Context(0)
+out = {}
+for g, P in (((3, 11, 3), 3), ((3, 3, 4), 2), ((3, 11, 3), 4)):
+    grid = A.Grid.sem(8.0, *g)
+    op = grid.separable_operator(ctx, [lambda t: t * t] * grid.dim, shift=-0.3)
+    so = S.DeviceSlabOperator(op.axes, shift=-0.3, mass=grid.mass, devices=[0] * P)
+    b = K.seeded_field(grid.shape, 11)
+    v2 = K.seeded_field(grid.shape, 12) + 2.0
+    psi = K.seeded_complex_field(grid.shape, 13)
+    bs, v2s = so.scatter(torch.from_numpy(b)), so.scatter(torch.from_numpy(v2))
+    ps = so.scatter(torch.from_numpy(psi))
+    key = "%d_%d_%d_%d" % (g + (P,))
+    out["s" + key] = so.gather(so.solve(bs)).cpu().numpy()
+    out["a" + key] = so.gather(so.apply(bs, diag=v2s, sigma=0.7)).cpu().numpy()
+    out["p" + key] = so.gather(so.propagate(ps, 0.02)).cpu().numpy()
+    out["n" + key] = np.array([so.fused_transforms()])
+    so.close()
+np.savez(sys.argv[1], **out)
+'''
+
+
+def test_virtual_slab_fused_exchange_bitwise(ctx, tmp_path):
+    """The exchange-fused transposes (the pass before each transpose storing straight into the
+    destination parts' slab buffers, SplitDst epilogue of the TMA pass kernel) give bit-identical
+    solve / FullOperator apply / propagate to the copy exchange (KRONOP_SLAB_FUSED=0) on
+    TMA-eligible virtual-slab grids (32^3 over 3 and 4 uneven parts, 8^4 over 2), ran fused for
+    every application, and match the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for name, env_add in (("fused", {}), ("copy", {"KRONOP_SLAB_FUSED": "0"})):
+        f = str(tmp_path / ("s%s.npz" % name))
+        subprocess.check_call([sys.executable, "-c", _FUSED_SNIPPET, f], cwd=root,
+                              env=dict(os.environ, **env_add))
+        res[name] = np.load(f)
+    for k in res["fused"].files:
+        if k.startswith("n"):
+            assert res["fused"][k][0] == 3, k  # solve, apply, propagate: all fused
+            assert res["copy"][k][0] == 0, k
+        else:
+            assert np.array_equal(res["fused"][k], res["copy"][k]), k
+    A = api()
+    grid = A.Grid.sem(8.0, 3, 11, 3)
+    op = grid.separable_operator(ctx, [lambda t: t * t] * 3, shift=-0.3)
+    ko = oracle_op(op, -0.3)
+    b = K.seeded_field(grid.shape, 11)
+    assert rel(res["fused"]["s3_11_3_3"], ko.solve(b)) < 1e-13
+    psi = K.seeded_complex_field(grid.shape, 13)
+    assert rel(res["fused"]["p3_11_3_3"], ko.propagate(psi, 0.02)) < 1e-13
