@@ -610,6 +610,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int v = 0; v < 2; ++v)
             if (cb[jc][v]) cb[jc][v][p + q * cqv[jc][v]] = acc[j][jc][v];
       }
+      // the stores may go to another GPU (NVLink peer memory, possibly mapped from another
+      // process): order them before whatever signals the peer next (the exchange barrier)
+      __threadfence_system();
     } else {
 #pragma unroll
       for (int j = 0; j < C::RT; ++j) {

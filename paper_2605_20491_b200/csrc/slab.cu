@@ -196,6 +196,13 @@ struct kronop_slab {
   ncclComm_t comm = nullptr;
   int ring = 0;  // next partials ring slot
   long long fused_transforms = 0;  // applications whose transposes were exchange-fused passes
+  // NCCL transport: the peers' receive buffers mapped into this process (CUDA IPC), so the
+  // exchange-fused passes store into them over NVLink. 0 = not set up yet, 1 = on, -1 = off
+  // (IPC unavailable or the collective self-check failed: grouped send / recv instead)
+  int ipc = 0;
+  std::vector<double*> peer_yx, peer_zx;  // [P], own buffers at this rank
+  std::vector<void*> ipc_opened;
+  double* bar = nullptr;                   // barrier all-gather buffer (1 + P doubles)
 };
 
 namespace kronop_dev {
@@ -368,28 +375,154 @@ static void ensure_part_buffers(kronop_slab& s, int c) {
 //   buffer (zx) | barrier | backward passes 0..d-2 (local)
 // Used when both transpose passes take the TMA kernel on every part (KRONOP_SLAB_FUSED=0: the
 // copy exchange). The NCCL transport keeps grouped send / recv.
-static bool slab_fused_ok(kronop_slab& s, const std::vector<const double*>& in, int c) {
+// stream-ordered barrier of the NCCL transport: an all-gather of one double per rank completes
+// on a rank only when every rank's stream has reached it
+static void nccl_barrier(kronop_slab& s) {
+  SlabPart& me = s.parts[0];
+  KNCCL(g_nccl.AllGather(s.bar, s.bar + 1, 1, ncclDouble, s.comm, me.ctx->stream));
+}
+
+__global__ void k_ipc_probe(double* const* dsts, int P, int rank) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < P) dsts[q][rank] = static_cast<double>(rank + 1);
+}
+
+// One-time, collective (every rank calls it at the same transform): allocate the receive
+// buffers at complex size (they never move afterwards), exchange their CUDA IPC handles over
+// NCCL, open the peers', and check the mapping end to end (every rank writes its id into every
+// rank's buffer through the mapped pointers, all-gather barrier, every rank reads them back);
+// all ranks then agree on the outcome, so a failure anywhere falls back everywhere.
+static void slab_ipc_setup(kronop_slab& s) {
+  SlabPart& me = s.parts[0];
+  part_device(me);
+  cudaStream_t st = me.ctx->stream;
+  const int P = s.P, r = me.p;
+  bool ok = true;
+  try {
+    KCUDA(cudaMalloc(&s.bar, (1 + P) * sizeof(double)));
+    KCUDA(cudaMemsetAsync(s.bar, 0, (1 + P) * sizeof(double), st));
+    const size_t zneed = static_cast<size_t>(zslab_elems(s, r)) * 2;
+    const size_t yneed = static_cast<size_t>(yslab_elems(s, r)) * 2;
+    KCUDA(cudaStreamSynchronize(st));
+    if (me.zx_cap < zneed) {
+      if (me.zx) KCUDA(cudaFree(me.zx));
+      me.zx = nullptr;
+      KCUDA(cudaMalloc(&me.zx, zneed * sizeof(double)));
+      me.zx_cap = zneed;
+    }
+    if (me.yx_cap < yneed) {
+      if (me.yx) KCUDA(cudaFree(me.yx));
+      me.yx = nullptr;
+      KCUDA(cudaMalloc(&me.yx, yneed * sizeof(double)));
+      me.yx_cap = yneed;
+    }
+  } catch (...) {
+    ok = false;
+  }
+  // handle exchange (every rank takes part, whatever its local outcome)
+  struct Handles {
+    cudaIpcMemHandle_t y, z;
+    int ok;
+  };
+  Handles mine{};
+  if (ok) {
+    ok = cudaIpcGetMemHandle(&mine.y, me.yx) == cudaSuccess &&
+         cudaIpcGetMemHandle(&mine.z, me.zx) == cudaSuccess;
+    (void)cudaGetLastError();
+  }
+  mine.ok = ok ? 1 : 0;
+  unsigned char* dh = nullptr;
+  KCUDA(cudaMalloc(&dh, sizeof(Handles) * (1 + P)));
+  KCUDA(cudaMemcpyAsync(dh, &mine, sizeof(Handles), cudaMemcpyHostToDevice, st));
+  KNCCL(g_nccl.AllGather(dh, dh + sizeof(Handles), sizeof(Handles), ncclUint8, s.comm, st));
+  std::vector<Handles> all(P);
+  KCUDA(cudaMemcpyAsync(all.data(), dh + sizeof(Handles), sizeof(Handles) * P,
+                        cudaMemcpyDeviceToHost, st));
+  KCUDA(cudaStreamSynchronize(st));
+  for (const Handles& h : all) ok = ok && h.ok;
+  s.peer_yx.assign(P, nullptr);
+  s.peer_zx.assign(P, nullptr);
+  if (ok) {
+    for (int q = 0; q < P && ok; ++q) {
+      if (q == r) {
+        s.peer_yx[q] = me.yx;
+        s.peer_zx[q] = me.zx;
+        continue;
+      }
+      void *py = nullptr, *pz = nullptr;
+      ok = cudaIpcOpenMemHandle(&py, all[q].y, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      if (ok) s.ipc_opened.push_back(py);
+      ok = ok && cudaIpcOpenMemHandle(&pz, all[q].z, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      if (pz) s.ipc_opened.push_back(pz);
+      (void)cudaGetLastError();
+      s.peer_yx[q] = static_cast<double*>(py);
+      s.peer_zx[q] = static_cast<double*>(pz);
+    }
+  }
+  // probe through the mapping: rank r writes r + 1 into slot r of every rank's y buffer
+  double** dptrs = nullptr;
+  KCUDA(cudaMalloc(&dptrs, P * sizeof(double*)));
+  if (ok) {
+    KCUDA(cudaMemcpyAsync(dptrs, s.peer_yx.data(), P * sizeof(double*), cudaMemcpyHostToDevice,
+                          st));
+    k_ipc_probe<<<1, 32 * ((P + 31) / 32), 0, st>>>(dptrs, P, r);
+    ok = cudaGetLastError() == cudaSuccess;
+  }
+  nccl_barrier(s);
+  std::vector<double> got(P, 0.0);
+  if (ok) {
+    KCUDA(cudaMemcpyAsync(got.data(), me.yx, P * sizeof(double), cudaMemcpyDeviceToHost, st));
+    KCUDA(cudaStreamSynchronize(st));
+    for (int q = 0; q < P; ++q) ok = ok && got[q] == static_cast<double>(q + 1);
+  }
+  // agreement: every rank's verdict
+  Handles verdict{};
+  verdict.ok = ok ? 1 : 0;
+  KCUDA(cudaMemcpyAsync(dh, &verdict, sizeof(Handles), cudaMemcpyHostToDevice, st));
+  KNCCL(g_nccl.AllGather(dh, dh + sizeof(Handles), sizeof(Handles), ncclUint8, s.comm, st));
+  KCUDA(cudaMemcpyAsync(all.data(), dh + sizeof(Handles), sizeof(Handles) * P,
+                        cudaMemcpyDeviceToHost, st));
+  KCUDA(cudaStreamSynchronize(st));
+  for (const Handles& h : all) ok = ok && h.ok;
+  KCUDA(cudaFree(dh));
+  KCUDA(cudaFree(dptrs));
+  s.ipc = ok ? 1 : -1;
+}
+
+// Exchange-fused transform (in-process transport, or NCCL with the peers' buffers mapped by CUDA
+// IPC): the pass before each slab transpose stores its output columns straight into the
+// destination parts' slab buffers (SplitDst epilogue of the TMA pass kernel: NVLink peer stores
+// for distinct GPUs, plain stores for virtual slabs), so the transposes cost no copy and no extra
+// HBM round trip, and the transfer overlaps the pass's math tile by tile:
+//   forward passes 0..d-3 (local) | barrier | pass d-2 -> every part's y-slab receive buffer (yx)
+//   | barrier | pass d-1 forward + spectral (local) | pass d-1 backward -> every part's z-slab
+//   buffer (zx) | barrier | backward passes 0..d-2 (local)
+// (barriers: cross-stream events in process, a one-double NCCL all-gather across processes).
+// Used when both transpose passes take the TMA kernel on every part -- decided from the global
+// slab geometry, so all ranks decide alike (KRONOP_SLAB_FUSED=0: the copy / send-recv exchange).
+static bool slab_fused_ok(kronop_slab& s, int c) {
   static const bool off = [] {
     const char* e = getenv("KRONOP_SLAB_FUSED");
     return e && e[0] == '0';
   }();
-  if (off || s.nccl || s.d < 2 || static_cast<int>(s.parts.size()) > kMaxSplit ||
-      !mode_product_tma_enabled())
-    return false;
+  if (off || s.d < 2 || s.P > kMaxSplit || !mode_product_tma_enabled()) return false;
   const int d = s.d;
-  for (size_t i = 0; i < s.parts.size(); ++i) {
-    const SlabPart& pt = s.parts[i];
+  for (int p = 0; p < s.P; ++p) {  // every part's geometry (all fields are 16-byte aligned here)
     PassShape a;
     a.pre = s.R * c;
     a.nk = a.m = s.n[d - 2];
-    a.post = s.zs[pt.p];
-    const double* x0 = d - 2 == 0 ? in[i] : pt.ctx->scratch[(d - 3) % 2];
+    a.post = s.zs[p];
     PassShape b;
-    b.pre = s.R * c * s.ys[pt.p];
+    b.pre = s.R * c * s.ys[p];
     b.nk = b.m = s.n[d - 1];
     b.post = 1;
-    if (!mode_product_tma_eligible(x0, a) || !mode_product_tma_eligible(pt.ctx->scratch[1], b))
+    const double* aligned = reinterpret_cast<const double*>(static_cast<uintptr_t>(256));
+    if (!mode_product_tma_eligible(aligned, a) || !mode_product_tma_eligible(aligned, b))
       return false;
+  }
+  if (s.nccl) {
+    if (s.ipc == 0) slab_ipc_setup(s);
+    return s.ipc > 0;
   }
   return true;
 }
@@ -400,17 +533,35 @@ static void slab_transform_fused(kronop_slab& s, const std::vector<const double*
   const int d = s.d;
   const long long Rc = s.R * c;
   const int ny = s.n[d - 2];
-  for (auto& pt : s.parts) {
-    part_device(pt);
-    const size_t yneed = static_cast<size_t>(yslab_elems(s, pt.p)) * c;
-    if (yneed > pt.yx_cap) {
-      KCUDA(cudaStreamSynchronize(pt.ctx->stream));
-      if (pt.yx) KCUDA(cudaFree(pt.yx));
-      pt.yx = nullptr;
-      KCUDA(cudaMalloc(&pt.yx, yneed * sizeof(double)));
-      pt.yx_cap = yneed;
+  if (!s.nccl)
+    for (auto& pt : s.parts) {
+      part_device(pt);
+      const size_t yneed = static_cast<size_t>(yslab_elems(s, pt.p)) * c;
+      if (yneed > pt.yx_cap) {
+        KCUDA(cudaStreamSynchronize(pt.ctx->stream));
+        if (pt.yx) KCUDA(cudaFree(pt.yx));
+        pt.yx = nullptr;
+        KCUDA(cudaMalloc(&pt.yx, yneed * sizeof(double)));
+        pt.yx_cap = yneed;
+      }
+    }
+  // destination buffers of every part (the local ones, or the IPC-mapped peers')
+  std::vector<double*> yx(s.P, nullptr), zx(s.P, nullptr);
+  if (s.nccl) {
+    yx = s.peer_yx;
+    zx = s.peer_zx;
+  } else {
+    for (auto& pt : s.parts) {
+      yx[pt.p] = pt.yx;
+      zx[pt.p] = pt.zx;
     }
   }
+  auto barrier = [&]() {
+    if (s.nccl)
+      nccl_barrier(s);
+    else
+      barrier_a(s);
+  };
   // forward passes on axes 0..d-3 (local)
   std::vector<const double*> cur(s.parts.size());
   for (size_t i = 0; i < s.parts.size(); ++i) {
@@ -422,6 +573,12 @@ static void slab_transform_fused(kronop_slab& s, const std::vector<const double*
     shp[d - 1] = s.zs[pt.p];
     View v = make_view(d, shp, cplx);
     cur[i] = in[i];
+    if ((reinterpret_cast<uintptr_t>(cur[i]) & 15) != 0) {  // TMA needs 16-byte aligned rows
+      double* t = ensure_tmp(ctx, static_cast<size_t>(zslab_elems(s, pt.p)) * c);
+      KCUDA(cudaMemcpyAsync(t, cur[i], zslab_elems(s, pt.p) * c * sizeof(double),
+                            cudaMemcpyDeviceToDevice, ctx.stream));
+      cur[i] = t;
+    }
     for (int a = 0; a < d - 2; ++a) {
       double* dst = ctx.scratch[a % 2];
       EpiParams ep;
@@ -430,22 +587,21 @@ static void slab_transform_fused(kronop_slab& s, const std::vector<const double*
       cur[i] = dst;
     }
   }
-  barrier_a(s);  // every part's receive buffer is free (its last reader was the previous call)
+  barrier();  // every part's receive buffer is free (its last reader was the previous call)
   // pass d-2 = the z -> y transpose: column y of part p's output goes to part q = owner(y) at
   // yx_q[(z0_p + z) ys_q Rc + (y - y0_q) Rc + r]
   for (size_t i = 0; i < s.parts.size(); ++i) {
     SlabPart& pt = s.parts[i];
     part_device(pt);
     SplitDst sd;
-    sd.parts = static_cast<int>(s.parts.size());
-    for (size_t k = 0; k < s.parts.size(); ++k) {
-      const SlabPart& q = s.parts[k];
-      sd.i0[k] = s.y0[q.p];
-      sd.dst[k] = q.yx + static_cast<long long>(s.z0[pt.p]) * s.ys[q.p] * Rc;
-      sd.ccol[k] = Rc;
-      sd.cq[k] = static_cast<long long>(s.ys[q.p]) * Rc;
+    sd.parts = s.P;
+    for (int q = 0; q < s.P; ++q) {
+      sd.i0[q] = s.y0[q];
+      sd.dst[q] = yx[q] + static_cast<long long>(s.z0[pt.p]) * s.ys[q] * Rc;
+      sd.ccol[q] = Rc;
+      sd.cq[q] = static_cast<long long>(s.ys[q]) * Rc;
     }
-    sd.i0[s.parts.size()] = ny;
+    sd.i0[s.P] = ny;
     PassShape ps;
     ps.pre = Rc;
     ps.nk = ps.m = ny;
@@ -456,7 +612,7 @@ static void slab_transform_fused(kronop_slab& s, const std::vector<const double*
     launch_mode_product(pt.ctx->stream, cur[i], pt.zx, pt.fwd[d - 2], pt.lda[d - 2], ps, ep);
     pt.ctx->ws.launches += 1;
   }
-  barrier_a(s);  // every part's y-slab is complete
+  barrier();  // every part's y-slab is complete
   // forward axis d-1 + spectral epilogue (local), then backward axis d-1 = the y -> z transpose:
   // column z of part q's output goes to part p = owner(z) at zx_p[(z - z0_p) ny Rc + y0_q Rc + r']
   for (size_t i = 0; i < s.parts.size(); ++i) {
@@ -482,15 +638,14 @@ static void slab_transform_fused(kronop_slab& s, const std::vector<const double*
     run_pass(ctx, pt.yx, ctx.scratch[1], v, d - 1 + v.cplx, pt.fwd[d - 1], pt.lda[d - 1],
              s.n[d - 1], ep);
     SplitDst sd;
-    sd.parts = static_cast<int>(s.parts.size());
-    for (size_t k = 0; k < s.parts.size(); ++k) {
-      const SlabPart& p = s.parts[k];
-      sd.i0[k] = s.z0[p.p];
-      sd.dst[k] = p.zx + static_cast<long long>(s.y0[pt.p]) * Rc;
-      sd.ccol[k] = static_cast<long long>(ny) * Rc;
-      sd.cq[k] = 0;
+    sd.parts = s.P;
+    for (int p = 0; p < s.P; ++p) {
+      sd.i0[p] = s.z0[p];
+      sd.dst[p] = zx[p] + static_cast<long long>(s.y0[pt.p]) * Rc;
+      sd.ccol[p] = static_cast<long long>(ny) * Rc;
+      sd.cq[p] = 0;
     }
-    sd.i0[s.parts.size()] = s.n[d - 1];
+    sd.i0[s.P] = s.n[d - 1];
     PassShape ps;
     ps.pre = Rc * s.ys[pt.p];
     ps.nk = ps.m = s.n[d - 1];
@@ -502,7 +657,7 @@ static void slab_transform_fused(kronop_slab& s, const std::vector<const double*
                         pt.lda[d - 1], ps, st);
     ctx.ws.launches += 1;
   }
-  barrier_a(s);  // every part's z-slab is complete
+  barrier();  // every part's z-slab is complete
   // backward passes on axes 0..d-2, the last with the FullOperator AXPY epilogue
   for (size_t i = 0; i < s.parts.size(); ++i) {
     SlabPart& pt = s.parts[i];
@@ -538,7 +693,7 @@ static void slab_transform(kronop_slab& s, const std::vector<const double*>& in,
   const int c = cplx ? 2 : 1;
   const int d = s.d;
   ensure_part_buffers(s, c);
-  if (slab_fused_ok(s, in, c)) {
+  if (slab_fused_ok(s, c)) {
     slab_transform_fused(s, in, out, cplx, e);
     ++s.fused_transforms;
     return;
@@ -1189,6 +1344,8 @@ int kronop_slab_destroy(kronop_slab* s) {
     if (pt.ev_b) cudaEventDestroy(pt.ev_b);
     if (pt.own_ctx) kronop_ctx_destroy(pt.ctx);
   }
+  for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (s->bar) cudaFree(s->bar);
   if (s->comm) g_nccl.CommDestroy(s->comm);
   delete s;
   return KRONOP_OK;

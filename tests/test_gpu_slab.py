@@ -230,3 +230,26 @@ def test_virtual_slab_fused_exchange_bitwise(ctx, tmp_path):
     assert rel(res["fused"]["s3_11_3_3"], ko.solve(b)) < 1e-13
     psi = K.seeded_complex_field(grid.shape, 13)
     assert rel(res["fused"]["p3_11_3_3"], ko.propagate(psi, 0.02)) < 1e-13
+
+
+def test_nccl_slab_one_rank_fused_exchange(ctx):
+    """The NCCL transport's exchange-fused path at one rank: the CUDA IPC setup (receive buffers
+    at complex size, handle all-gather over NCCL, the collective write-through probe and the
+    agreement) runs, every application is fused, and solve / propagate match the single-device
+    path (at P ranks the same code maps the peers' buffers and stores into them over NVLink)."""
+    A, S = api(), slabmod()
+    import torch.cuda.nccl  # noqa: F401
+    grid = A.Grid.sem(8.0, 3, 11, 3)  # 32^3: both transposes TMA-eligible
+    op = grid.separable_operator(ctx, [lambda t: t * t] * 3, shift=-0.3)
+    so = S.DeviceSlabOperator(op.axes, shift=-0.3, ctx=ctx, rank=0, nranks=1,
+                              unique_id=S.nccl_unique_id())
+    b = A.splitmix_uniform(ctx, 1, grid.node_count())
+    x = op.solve(b)
+    xs = so.gather(so.solve(so.scatter(b)))
+    assert float(torch.linalg.norm(xs - x) / torch.linalg.norm(x)) < 1e-13
+    psi = torch.view_as_complex(A.splitmix_uniform(ctx, 2, 2 * grid.node_count()).view(-1, 2))
+    p = op.propagate(psi, 0.02)
+    ps = so.gather(so.propagate(so.scatter(psi), 0.02))
+    assert float(torch.linalg.norm(ps - p) / torch.linalg.norm(p)) < 1e-13
+    assert so.fused_transforms() == 2
+    so.close()
