@@ -773,7 +773,18 @@ int kronop_ctx_destroy(kronop_ctx* ctx) {
 int kronop_ctx_trim(kronop_ctx* ctx) {
   return guard([&] {
     param_check(ctx != nullptr, "ctx_trim: null context");
-    pool_trim(*ctx);
+    pool_trim(*ctx);  // synchronises the stream
+    // the host-path staging (single and batched entry points) is re-made on the next call
+    for (auto& p : ctx->io) {
+      if (p) KCUDA(cudaFree(p));
+      p = nullptr;
+    }
+    ctx->io_cap = 0;
+    for (auto& b : ctx->bio) {
+      if (b) KCUDA(cudaFree(b));
+      b = nullptr;
+    }
+    ctx->bio_cap = 0;
   });
 }
 
