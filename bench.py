@@ -51,16 +51,19 @@ def load_peaks():
 
 def load_pass_traffic():
     """DRAM bytes per 1024^3 pass of the dominant kernel from the committed `ncu --set full`
-    capture of the current kernels (dram__bytes_read.sum + dram__bytes_write.sum of the axis-1
-    STRIDED pass, profiles/r02_pass_a1.json), else round 1's, else None."""
+    capture of the current kernels (dram__bytes_read.sum + dram__bytes_write.sum of the first
+    pass of the rotated solve -- the CONTIG TMA instance every pass of the solve runs,
+    profiles/r02_rotated_pass.json; else the axis-order STRIDED pass, r02_pass_a1.json), else
+    round 1's, else None."""
     def gb(v):
         return float(v.split()[0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Tbyte": 1e12}[v.split()[1]]
-    try:
-        with open(os.path.join(ROOT, "profiles", "r02_pass_a1.json")) as f:
-            k = json.load(f)["kernels"][0]
-        return gb(k["dram_read"]) + gb(k["dram_write"])
-    except (OSError, KeyError, ValueError, IndexError):
-        pass
+    for name in ("r02_rotated_pass.json", "r02_pass_a1.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                k = json.load(f)["kernels"][0]
+            return gb(k["dram_read"]) + gb(k["dram_write"])
+        except (OSError, KeyError, ValueError, IndexError):
+            pass
     try:
         with open(os.path.join(ROOT, "profiles", "r01_ncu_full_pass1024.json")) as f:
             m = json.load(f)
