@@ -382,15 +382,38 @@ __global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, KRONOP_KR_CTAS)
 #ifndef KRONOP_KR_PAIR
 #define KRONOP_KR_PAIR 1
 #endif
+// KRONOP_KR_PAIR_HALVES = 2: the CTA has two halves of C::THREADS threads, each contracting one
+// tile of the pair at the same time (named barriers per half), all threads writing the pair out
+// (build knob; at 704 threads the contraction gets 80 registers and spills ~900 bytes, so the
+// default is one team of 11 warps)
+#ifndef KRONOP_KR_PAIR_HALVES
+#define KRONOP_KR_PAIR_HALVES 1
+#endif
 template <int N, int NF>
 struct KronPairCfg {
   using C = KronCfg<N, NF>;
   static constexpr int STAGES = 4;
   static constexpr int PITCH = C::STAGE + 2;  // doubles between stages
+  static constexpr int HALVES = KRONOP_KR_PAIR_HALVES;
+  static constexpr int THREADS = HALVES * C::THREADS;
 };
 
+// the group's axes of one tile, in place, by C::THREADS threads (htid) synchronising on their
+// own named barrier (id 1 + half) -- or the whole CTA when the pair is done by one team
+template <int N, int NF, int J, bool FOLD, int HALVES>
+__device__ __forceinline__ void kr_axes_team(const KronArgs<N, NF>& A, double* buf, long long q0,
+                                             int qv, int htid, int half) {
+  using C = KronCfg<N, NF>;
+  kr_axis<N, NF, J, FOLD>(A, buf, q0, qv, htid);
+  if constexpr (HALVES == 1)
+    __syncthreads();
+  else
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + half), "n"(C::THREADS) : "memory");
+  if constexpr (J + 1 < NF) kr_axes_team<N, NF, J + 1, FOLD, HALVES>(A, buf, q0, qv, htid, half);
+}
+
 template <int N, int NF, bool FOLD, bool BPH>
-__global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, 1)
+__global__ void __launch_bounds__(KronPairCfg<N, NF>::THREADS, 1)
     kron_rot_pair_kernel(const __grid_constant__ KronArgs<N, NF> A) {
   using C = KronCfg<N, NF>;
   using PC = KronPairCfg<N, NF>;
@@ -398,6 +421,8 @@ __global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, 1)
   extern __shared__ __align__(128) double sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * PC::PITCH);
   const int tid = threadIdx.x;
+  const int half = PC::HALVES == 1 ? 0 : tid / C::THREADS;
+  const int htid = tid - half * C::THREADS;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -416,16 +441,16 @@ __global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, 1)
     if (tile >= t1) break;
     const int nt = tile + 1 < t1 ? 2 : 1;
     const long long q0 = tile * C::QT;
-    for (int u = 0; u < nt; ++u) {
+    for (int u = PC::HALVES == 1 ? 0 : half; u < nt; u += PC::HALVES) {
       const int s = (it + u) % STAGES;
       double* buf = sm + s * PC::PITCH;
       mbar_wait(&full[s], ((it + u) / STAGES) & 1);
       const long long qu = q0 + u * C::QT;
       const int qv = static_cast<int>(A.Q - qu < C::QT ? A.Q - qu : C::QT);
-      kr_inplace_axes<N, NF, 0, FOLD>(A, buf, qu, qv, tid);
-      kr_axis<N, NF, NF - 1, FOLD>(A, buf, qu, qv, tid);  // the last axis, in place
-      __syncthreads();
+      // every group axis, the last one included, in place
+      kr_axes_team<N, NF, 0, FOLD, PC::HALVES>(A, buf, qu, qv, htid, half);
     }
+    if constexpr (PC::HALVES > 1) __syncthreads();  // both tiles contracted
     // write-out: item = (g, qq), qq = 2 QT consecutive q fastest; 16 bytes per item
     const int qn = static_cast<int>(A.Q - q0 < nt * C::QT ? A.Q - q0 : nt * C::QT);
     const double2* b0 = reinterpret_cast<const double2*>(sm + (it % STAGES) * PC::PITCH);
@@ -433,7 +458,7 @@ __global__ void __launch_bounds__(KronCfg<N, NF>::THREADS, 1)
     double2* y2 = reinterpret_cast<double2*>(A.y);
     constexpr int QQ = 2 * C::QT;
 #pragma unroll 4
-    for (int e = tid; e < C::F * QQ; e += C::THREADS) {
+    for (int e = tid; e < C::F * QQ; e += PC::THREADS) {
       const int qq = e % QQ, g = e / QQ;
       if (qq >= qn) continue;
       const int qi = qq % C::QT;
@@ -482,7 +507,7 @@ void launch_kron(cudaStream_t s, const double* x, double* y, long long Ntot, con
     const long long cap = device_sm_count();
     const long long grid = (a.ntiles + 1) / 2 < cap ? (a.ntiles + 1) / 2 : cap;
     kron_rot_pair_kernel<N, NF, FOLD, BPH>
-        <<<static_cast<unsigned>(grid), C::THREADS, smem, s>>>(a);
+        <<<static_cast<unsigned>(grid), PC::THREADS, smem, s>>>(a);
     KCUDA(cudaGetLastError());
     return;
   }
