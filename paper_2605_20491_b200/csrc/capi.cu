@@ -356,6 +356,73 @@ bool sep_propagate_prephased(kronop_ctx& ctx, const kronop_op& op, double* psi, 
   return sep_propagate_kron(ctx, op, psi, psi, shift, dt, false, nullptr, 0.0, pre_tab);
 }
 
+// Real fields whose axes all have n <= 10 (the config-5 9D solves / applies of inverse
+// iteration): the transform form on kron_real_kernel (kron_prop.cu) -- the real axis matrices as
+// kernel parameters, 1 CTA x 3 stages over contiguous tile ranges; the same operations and
+// order as fused_rot's DFMA path (identical results, KRONOP_KRON_REAL=0 selects fused_rot).
+static bool sep_transform_real_kron(kronop_ctx& ctx, const kronop_op& op, const double* in,
+                                    double* out, SepKind kind, double shift, const double* diag,
+                                    double sigma) {
+  static const bool off = [] {
+    const char* e = getenv("KRONOP_KRON_REAL");
+    return e && e[0] == '0';
+  }();
+  if (off || op.folded || op.exec_prec != KRONOP_PREC_FP64 || kind == SEP_PROPAGATE) return false;
+  if (!fused_rot_eligible(in)) return false;
+  for (int a = 0; a < op.d; ++a)
+    if (op.hT[a].empty() || !kron_real_supported(op.n[a], 1)) return false;
+  std::vector<std::pair<int, int>> groups;
+  for (int a = 0; a < op.d;) {
+    int f = 1;
+    while (a + f < op.d && f < 3 && op.n[a + f] == op.n[a]) ++f;
+    groups.emplace_back(a, f);
+    a += f;
+  }
+  const size_t nd = static_cast<size_t>(op.N);
+  ensure_scratch(ctx, nd);
+  const int ng = static_cast<int>(groups.size());
+  std::vector<double> M(3 * 10 * 10);
+  const double* src = in;
+  int k = 0;
+  for (int dir = 0; dir < 2; ++dir)
+    for (int g = 0; g < ng; ++g, ++k) {
+      const int a0 = groups[g].first, f = groups[g].second, n = op.n[a0];
+      const bool last = dir == 1 && g == ng - 1;
+      for (int j = 0; j < f; ++j) {
+        const std::vector<double>& T = dir == 0 ? op.hTinv[a0 + j] : op.hT[a0 + j];
+        for (int i = 0; i < n; ++i)
+          for (int kk = 0; kk < n; ++kk)
+            M[(j * n + i) * n + kk] = T[i + static_cast<size_t>(n) * kk];  // column-major
+      }
+      KronRealLaunch L;
+      L.x = src;
+      L.y = last ? out : ctx.scratch[k % 2];
+      L.Ntot = op.N;
+      L.n = n;
+      L.f = f;
+      L.M = M.data();
+      if (dir == 0 && g == ng - 1) {
+        L.epi = kind == SEP_SOLVE ? 1 : 2;
+        L.shift = shift;
+        for (int j = 0; j < f; ++j) L.lam_g[j] = op.lam[a0 + j];
+        L.nq = a0;
+        for (int j = 0; j < a0; ++j) {
+          L.qext[j] = op.n[j];
+          L.lam_q[j] = op.lam[j];
+        }
+      } else if (last && (diag != nullptr || sigma != 0.0)) {
+        L.epi = 3;
+        L.diag = diag;
+        L.u = in;
+        L.sigma = sigma;
+      }
+      launch_kron_real_group(ctx.stream, L);
+      ctx.ws.launches += 1;
+      src = L.y;
+    }
+  return true;
+}
+
 // Small-extent path, rotating layout (fused_rot.cu): groups of up to 3 consecutive axes (fused
 // extent <= 1024), forward groups then backward groups; each launch moves its group to the slow
 // end, so after each direction the layout is the caller's again.
@@ -365,6 +432,7 @@ static void sep_transform_rot(kronop_ctx& ctx, const kronop_op& op, const double
   if (kind == SEP_PROPAGATE && cplx && diag == nullptr && sigma == 0.0 &&
       sep_propagate_kron(ctx, op, in, out, shift, dt, bphase, bfield, bfactor))
     return;
+  if (!cplx && sep_transform_real_kron(ctx, op, in, out, kind, shift, diag, sigma)) return;
   const size_t nd = static_cast<size_t>(op.N) * (cplx ? 2 : 1);
   ensure_scratch(ctx, nd);
   std::vector<std::pair<int, int>> groups;

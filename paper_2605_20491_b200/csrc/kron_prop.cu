@@ -955,6 +955,257 @@ void launch_kron_dmma_n(cudaStream_t s, int f, const double* x, double* y, long 
     launch_kron_dmma<N, 2>(s, x, y, Ntot, E, bfield, bfactor, bphase, pre);
 }
 
+// ------------------------------------------------------------------------------------------
+// Real fields, transform form (solve / apply / FullOperator apply of the small-extent operators,
+// e.g. the config-5 ground states by inverse iteration): the same rotating group launch on DFMA
+// with the REAL axis matrix (T^{-1} forward, T backward) as kernel parameters, one thread per
+// real fiber, 8 planes per tile (64-byte output runs), 1 CTA x 3 stages over a contiguous tile
+// range. Epilogues: the spectral divide / multiply on the last forward group (lambda summed in
+// axis order from 0.0: the axes below the group per q, then the group axes -- direct_sum_grid
+// tensor.cpp:196-209) and the V2 / sigma AXPY on the last backward group (operators.cpp:102),
+// the operations and accumulation order of fused_rot.cu's DFMA path, so results are identical.
+constexpr int KRE_STORE = 0, KRE_DIV = 1, KRE_MUL = 2, KRE_AXPY = 3;
+
+template <int N, int NF>
+struct KronRCfg {
+  static constexpr int F = kr_pow(N, NF);
+  static constexpr int QT = kr_qt(F, 1) * 2 > 256 ? 256 : kr_qt(F, 1) * 2;  // 8 B elements
+  static constexpr int PL = F / N;
+  static constexpr int FIB = QT * PL;
+  static constexpr int THREADS = FIB >= 1024 ? 1024 : (kr_round32(FIB) < 64 ? 64 : kr_round32(FIB));
+  // planes unpadded: a tile is ONE contiguous chunk (8-byte elements: a per-plane bulk copy of
+  // an odd-extent plane would be neither a 16-byte multiple nor 16-byte aligned)
+  static constexpr int PPR = F;
+  static constexpr int STAGE = QT * PPR;
+};
+
+template <int N, int NF>
+struct KronRArgs {
+  const double* x;
+  double* y;
+  long long Q, ntiles;
+  double shift, sigma;
+  const double* diag;  // AXPY: V2 (null = none), original layout
+  const double* u;     // AXPY: the operator's input, original layout
+  const double* lam_g[3];
+  int nq;
+  long long qext[KRONOP_MAX_DIM];
+  const double* lam_q[KRONOP_MAX_DIM];
+  double M[NF][N][N];  // M_j(i, k): output i, input k
+};
+
+template <int N, int NF, int J>
+__device__ __forceinline__ void kre_contract(const KronRArgs<N, NF>& A, const double (&x)[N],
+                                             double (&o)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) o[i] = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int i = 0; i < N; ++i) o[i] = fma(A.M[J][i][k], x[k], o[i]);
+}
+
+template <int N, int NF, int J>
+__device__ __forceinline__ void kre_axis(const KronRArgs<N, NF>& A, double* buf, int tid) {
+  using C = KronRCfg<N, NF>;
+  constexpr int P = kr_pow(N, J);
+  constexpr int H = C::F / (P * N);
+#pragma unroll 1
+  for (int f = tid; f < C::FIB; f += C::THREADS) {
+    const int lo = f % P, hi = f / P;
+    const int hg = hi % H, qi = hi / H;
+    double* p = buf + lo + hg * (P * N) + qi * C::PPR;
+    double x[N], o[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) x[k] = p[k * P];
+    kre_contract<N, NF, J>(A, x, o);
+#pragma unroll
+    for (int i = 0; i < N; ++i) p[i * P] = o[i];
+  }
+}
+
+template <int N, int NF, int J>
+__device__ __forceinline__ void kre_inplace(const KronRArgs<N, NF>& A, double* buf, int tid) {
+  if constexpr (J < NF - 1) {
+    kre_axis<N, NF, J>(A, buf, tid);
+    __syncthreads();
+    kre_inplace<N, NF, J + 1>(A, buf, tid);
+  }
+}
+
+template <int N, int NF, int EPI>
+__device__ __forceinline__ void kre_last(const KronRArgs<N, NF>& A, const double* buf,
+                                         const double* lam_low, long long q0, int qv, int tid) {
+  using C = KronRCfg<N, NF>;
+  constexpr int P = C::PL;
+#pragma unroll 1
+  for (int f = tid; f < C::FIB; f += C::THREADS) {
+    const int qi = f % C::QT, lo = f / C::QT;
+    if (qi >= qv) continue;
+    const double* p = buf + lo + qi * C::PPR;
+    double x[N], o[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) x[k] = p[k * P];
+    kre_contract<N, NF, NF - 1>(A, x, o);
+    const long long ob = q0 + qi + A.Q * lo;
+    double lam_lo_g = 0.0;
+    if constexpr (EPI == KRE_DIV || EPI == KRE_MUL) {
+      // the group axes below the last one, in axis order after the axes below the group
+      lam_lo_g = lam_low[qi];
+      int r = lo;
+#pragma unroll
+      for (int j = 0; j < NF - 1; ++j) {
+        lam_lo_g = __dadd_rn(lam_lo_g, A.lam_g[j][r % N]);
+        r /= N;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const long long oi = ob + A.Q * P * i;
+      double v = o[i];
+      if constexpr (EPI == KRE_DIV || EPI == KRE_MUL) {
+        const double ls = __dsub_rn(__dadd_rn(lam_lo_g, A.lam_g[NF - 1][i]), A.shift);
+        v = EPI == KRE_MUL ? __dmul_rn(v, ls) : __ddiv_rn(v, ls);
+      } else if constexpr (EPI == KRE_AXPY) {
+        const double uu = A.u[oi];
+        if (A.diag) v = __dadd_rn(v, __dmul_rn(A.diag[oi], uu));
+        if (A.sigma != 0.0) v = __dsub_rn(v, __dmul_rn(A.sigma, uu));
+      }
+      A.y[oi] = v;
+    }
+  }
+}
+
+template <int N, int NF, int EPI>
+__global__ void __launch_bounds__(KronRCfg<N, NF>::THREADS, 1)
+    kron_real_kernel(const __grid_constant__ KronRArgs<N, NF> A) {
+  using C = KronRCfg<N, NF>;
+  constexpr int STAGES = 3;
+  constexpr int WARPS = C::THREADS / 32;
+  extern __shared__ __align__(128) double sm[];
+  double* lam_low2 = sm + STAGES * C::STAGE;  // 2 x QT: lambda of the axes below, per tile
+  uint64_t* full = reinterpret_cast<uint64_t*>(lam_low2 + 2 * C::QT);
+  int* done = reinterpret_cast<int*>(full + STAGES);
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      done[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const long long per = (A.ntiles + gridDim.x - 1) / gridDim.x;
+  const long long t0 = blockIdx.x * per;
+  const long long t1 = t0 + per < A.ntiles ? t0 + per : A.ntiles;
+  auto issue = [&](long long tile, double* dst, uint64_t* bar) {
+    const long long q0 = tile * C::QT;
+    const int qv = static_cast<int>(A.Q - q0 < C::QT ? A.Q - q0 : C::QT);
+    // one bulk copy of an even number of doubles (16-byte multiple; the tile start is 16-byte
+    // aligned since QT F is even or the tile is the first); an odd last element (partial last
+    // tile) through the generic proxy before the arrive
+    const uint32_t doubles = static_cast<uint32_t>(qv) * C::F;
+    const double* src = A.x + static_cast<long long>(C::F) * q0;
+    if (doubles & 1u) dst[doubles - 1] = src[doubles - 1];
+    const uint32_t bulk = (doubles & ~1u) * 8u;
+    mbar_expect_tx(bar, bulk);
+    if (bulk) bulk_load(dst, src, bulk, bar);
+  };
+  if (tid == 0)
+    for (int s = 0; s < STAGES; ++s)
+      if (t0 + s < t1) issue(t0 + s, sm + s * C::STAGE, &full[s]);
+  for (int it = 0;; ++it) {
+    const long long tile = t0 + it;
+    if (tile >= t1) break;
+    const int s = it % STAGES;
+    double* buf = sm + s * C::STAGE;
+    const long long q0 = tile * C::QT;
+    const int qv = static_cast<int>(A.Q - q0 < C::QT ? A.Q - q0 : C::QT);
+    double* lam_low = lam_low2 + (it & 1) * C::QT;
+    if constexpr (EPI == KRE_DIV || EPI == KRE_MUL) {
+      if (tid < qv) {  // lambda of the axes below the group, axis order from 0.0
+        long long q = q0 + tid;
+        double lam = 0.0;
+        for (int j = 0; j < A.nq; ++j) {
+          const long long e = A.qext[j];
+          const long long idx = q % e;
+          q /= e;
+          lam = __dadd_rn(lam, A.lam_q[j][idx]);
+        }
+        lam_low[tid] = lam;
+      }
+    }
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    kre_inplace<N, NF, 0>(A, buf, tid);
+    if constexpr (NF == 1 && (EPI == KRE_DIV || EPI == KRE_MUL)) __syncthreads();  // lam_low
+    kre_last<N, NF, EPI>(A, buf, lam_low, q0, qv, tid);
+    const long long next = tile + STAGES;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&done[s], 1) == WARPS - 1) {
+        done[s] = 0;
+        __threadfence_block();
+        if (next < t1) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          issue(next, buf, &full[s]);
+        }
+      }
+    }
+  }
+}
+
+template <int N, int NF, int EPI>
+void launch_kron_real(cudaStream_t s, const KronRealLaunch& L) {
+  using C = KronRCfg<N, NF>;
+  KronRArgs<N, NF> a;
+  std::memset(&a, 0, sizeof(a));
+  a.x = L.x;
+  a.y = L.y;
+  a.Q = L.Ntot / C::F;
+  a.ntiles = (a.Q + C::QT - 1) / C::QT;
+  a.shift = L.shift;
+  a.sigma = L.sigma;
+  a.diag = L.diag;
+  a.u = L.u;
+  for (int j = 0; j < NF; ++j) a.lam_g[j] = L.lam_g[j];
+  a.nq = L.nq;
+  for (int j = 0; j < L.nq; ++j) {
+    a.qext[j] = L.qext[j];
+    a.lam_q[j] = L.lam_q[j];
+  }
+  for (int j = 0; j < NF; ++j)
+    for (int i = 0; i < N; ++i)
+      for (int k = 0; k < N; ++k) a.M[j][i][k] = L.M[(j * N + i) * N + k];
+  const size_t smem = (3 * static_cast<size_t>(C::STAGE) + 2 * C::QT) * sizeof(double) +
+                      3 * (sizeof(uint64_t) + sizeof(int));
+  ensure_smem_attr(reinterpret_cast<const void*>(kron_real_kernel<N, NF, EPI>), smem);
+  const long long cap = device_sm_count();
+  const long long grid = a.ntiles < cap ? a.ntiles : cap;
+  kron_real_kernel<N, NF, EPI><<<static_cast<unsigned>(grid), C::THREADS, smem, s>>>(a);
+  KCUDA(cudaGetLastError());
+}
+
+template <int N, int NF>
+void launch_kron_real_e(cudaStream_t s, const KronRealLaunch& L) {
+  switch (L.epi) {
+    case KRE_DIV: launch_kron_real<N, NF, KRE_DIV>(s, L); break;
+    case KRE_MUL: launch_kron_real<N, NF, KRE_MUL>(s, L); break;
+    case KRE_AXPY: launch_kron_real<N, NF, KRE_AXPY>(s, L); break;
+    default: launch_kron_real<N, NF, KRE_STORE>(s, L); break;
+  }
+}
+
+template <int N>
+void launch_kron_real_n(cudaStream_t s, const KronRealLaunch& L) {
+  if (L.f == 1)
+    launch_kron_real_e<N, 1>(s, L);
+  else if (L.f == 2)
+    launch_kron_real_e<N, 2>(s, L);
+  else
+    launch_kron_real_e<N, 3>(s, L);
+}
+
 }  // namespace
 
 bool kron_group_supported(int n, int f) {
@@ -962,6 +1213,25 @@ bool kron_group_supported(int n, int f) {
          (n > KR_MAXN && n <= KD_MAXN && f >= 1 && f <= 2);
 }
 bool kron_group_needs_fold(int n) { return n > KR_MAXN; }
+
+bool kron_real_supported(int n, int f) { return n >= 2 && n <= KR_MAXN && f >= 1 && f <= 3; }
+
+void launch_kron_real_group(cudaStream_t s, const KronRealLaunch& L) {
+  param_check(kron_real_supported(L.n, L.f), "small-extent real transform: unsupported group");
+  param_check((reinterpret_cast<uintptr_t>(L.x) & 15u) == 0,
+              "small-extent real transform: input must be 16-byte aligned");
+  switch (L.n) {
+    case 2: launch_kron_real_n<2>(s, L); break;
+    case 3: launch_kron_real_n<3>(s, L); break;
+    case 4: launch_kron_real_n<4>(s, L); break;
+    case 5: launch_kron_real_n<5>(s, L); break;
+    case 6: launch_kron_real_n<6>(s, L); break;
+    case 7: launch_kron_real_n<7>(s, L); break;
+    case 8: launch_kron_real_n<8>(s, L); break;
+    case 9: launch_kron_real_n<9>(s, L); break;
+    default: launch_kron_real_n<10>(s, L); break;
+  }
+}
 
 void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, bool fold,
                        long long Ntot, const double* E, const double* bfield, double bfactor,

@@ -159,6 +159,27 @@ int launch_fused_rot(cudaStream_t s, const double* x, double* y, int cplx, int f
 // the parity blocks [Ae | Ao] of R-symmetric axis matrices instead (see kr_contract).
 bool kron_group_supported(int n, int f);
 bool kron_group_needs_fold(int n);  // extents > 10 (DMMA kernel): parity-symmetric axes only
+// Real-field transform-form group launch (kron_prop.cu, kron_real_kernel): one group of f <= 3
+// consecutive axes of extent n <= 10, real matrices M (f x n x n row-major: output i, input k),
+// rotating layout; epi 0 store, 1 spectral divide, 2 spectral multiply (last forward group:
+// lambda = the nq axes below the group (qext / lam_q) then the group axes lam_g, minus shift),
+// 3 AXPY (+ diag u - sigma u, last backward group).
+struct KronRealLaunch {
+  const double* x = nullptr;
+  double* y = nullptr;
+  long long Ntot = 0;
+  int n = 0, f = 0, epi = 0;
+  const double* M = nullptr;
+  double shift = 0.0, sigma = 0.0;
+  const double* diag = nullptr;
+  const double* u = nullptr;
+  const double* lam_g[3] = {};
+  int nq = 0;
+  long long qext[KRONOP_MAX_DIM] = {};
+  const double* lam_q[KRONOP_MAX_DIM] = {};
+};
+bool kron_real_supported(int n, int f);
+void launch_kron_real_group(cudaStream_t s, const KronRealLaunch& L);
 // pre: (cos, sin) table of the B phase that precedes this propagate (first group only; null =
 // none), applied to the input as it is read.
 void launch_kron_group(cudaStream_t s, const double* x, double* y, int n, int f, bool fold,

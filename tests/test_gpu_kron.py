@@ -215,3 +215,62 @@ def test_kron_config5_full_size_matches_transform_passes(ctx, name):
     n0 = float(torch.sum(w * psi.abs() ** 2))
     n1 = float(torch.sum(w * got.abs() ** 2))
     assert abs(n1 - n0) <= 1e-12 * n0
+
+
+_REAL_SNIPPET = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from oracle import kronop_oracle as K
+from paper_2605_20491_b200 import api as A
+ctx = A.Context(0)
+out = {}
+for axes in ([(3.0, 2, 5)] * 3, [(3.0, 2, 5)] * 4, [(2.0, 1, 6)] * 5, [(3.0, 1, 4)] * 9,
+             [(3.0, 2, 5), (2.0, 1, 6), (3.0, 2, 5)], [(3.0, 2, 5)] * 6):
+    g = A.Grid([A.assemble_sem(*a) for a in axes])
+    pots = [(lambda t, c=c: (1.0 + 0.3 * c) * t * t + 0.1 * c + 0.2 * t) for c in range(g.dim)]
+    op = g.separable_operator(ctx, pots, -0.4)
+    n = g.node_count()
+    b = torch.from_numpy(K.uniform_pm1(81, n)).cuda()
+    v2 = torch.from_numpy(K.uniform_pm1(82, n) + 2.0).cuda()
+    key = "x".join(str(s) for s in g.shape)
+    c0 = ctx.launch_count()
+    out["s" + key] = op.solve(b).cpu().numpy()
+    out["n" + key] = np.array([ctx.launch_count() - c0])
+    out["a" + key] = op.apply(b).cpu().numpy()
+    out["f" + key] = A.FullOperator(op, v2).apply(b, sigma=0.3).cpu().numpy()
+    x = b.clone()
+    op.solve(x, out=x)  # in place
+    out["i" + key] = x.cpu().numpy()
+np.savez(sys.argv[1], **out)
+'''
+
+
+def test_kron_real_transform_bitwise(tmp_path):
+    """Real fields with every extent <= 10 (solve / apply / FullOperator apply, in place too) on
+    kron_real_kernel equal fused_rot's DFMA path (KRONOP_KRON_REAL=0) bit for bit -- same
+    operations in the same order -- on 6 grids incl. mixed extents and 9D; and match the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for name, env_add in (("kron", {}), ("rot", {"KRONOP_KRON_REAL": "0"})):
+        f = str(tmp_path / ("r%s.npz" % name))
+        subprocess.check_call([sys.executable, "-c", _REAL_SNIPPET, f], cwd=root,
+                              env=dict(os.environ, **env_add))
+        res[name] = np.load(f)
+    for k in res["kron"].files:
+        if k.startswith("n"):
+            continue
+        assert np.array_equal(res["kron"][k], res["rot"][k]), k
+    A = api()
+    grid = A.Grid([A.assemble_sem(3.0, 2, 5)] * 3)
+    import torch as _t  # noqa: F401
+    from paper_2605_20491_b200 import api as _A  # noqa: F401
+    ctx = A.Context(0)
+    pots = [(lambda t, c=c: (1.0 + 0.3 * c) * t * t + 0.1 * c + 0.2 * t) for c in range(3)]
+    op = grid.separable_operator(ctx, pots, -0.4)
+    ko = oracle_op_from(op, -0.4)
+    b = K.uniform_pm1(81, grid.node_count())
+    assert rel(res["kron"]["s9x9x9"], ko.solve(b)) < 1e-13
+    assert rel(res["kron"]["a9x9x9"], ko.apply(b)) < 1e-13

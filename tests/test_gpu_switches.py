@@ -68,6 +68,7 @@ print("ok", kind)
     ("KRONOP_ROT_SPEC_SPLIT", "0", "small_9d"),       # phase fused into the contraction
     ("KRONOP_KRON_PROP", "0", "small_9d"),            # transform / phase / transform propagate
     ("KRONOP_KRON_FOLD", "0", "rot_9"),               # dense E_a on parity-symmetric axes
+    ("KRONOP_KRON_REAL", "0", "rot_9"),               # fused_rot DFMA for real small-extent fields
     ("KRONOP_ROT_SPEC_SPLIT", "1", "small_6d"),       # standalone spectral pass everywhere
     ("KRONOP_TC_CLUSTER", "2", "lowp"),               # B multicast in the tcgen05 pass
     ("KRONOP_TC_2SM", "0", "lowp"),                   # 1-SM tcgen05 kernels
