@@ -875,8 +875,12 @@ def run_kronop_slab(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "3D (-Delta+V1)^-1 solve, harmonic V1, SEM Q%d %d cells L=8, "
                                    "n=%d, slab-decomposed over %d GPUs through kronop_slab_* "
-                                   "(NCCL, 2 all-to-all per solve)"
+                                   "(NCCL ranks, 2 transposes per solve)"
                                    % (workload_degree(n), workload_config(n), n, world),
+                       "exchange": ("fused: the pass before each transpose stores into the peers' "
+                                    "CUDA-IPC-mapped slab buffers (%d solves fused)"
+                                    % so.fused_transforms() if so.fused_transforms() > 0 else
+                                    "NCCL grouped send / recv"),
                        "n": n, "dof": N, "parallelism": "slab%d" % world,
                        "l2": "inputs larger than L2; no flush"},
             "tflops": tfl,
