@@ -71,7 +71,8 @@ class Context:
         check(lib().kronop_ctx_synchronize(self.h))
 
     def trim(self):
-        """Return the idle driver work buffers (kronop_ctx_trim) to the device."""
+        """Return the idle driver work buffers and the host-path staging (kronop_ctx_trim) to
+        the device."""
         check(lib().kronop_ctx_trim(self.h))
 
     def launch_count(self) -> int:
