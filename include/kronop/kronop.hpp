@@ -345,6 +345,24 @@ class SeparableOperator {
     out.set_mass(b.mass());
     return out;
   }
+  // a caller's loop of solve() over host fields as one call (kronop_sep_solve_host_batch): the
+  // copies of neighbouring right-hand sides overlap each one's transform
+  template <typename S>
+  std::vector<TensorField<S>> solve(const std::vector<TensorField<S>>& bs) const {
+    std::vector<TensorField<S>> outs;
+    outs.reserve(bs.size());
+    std::vector<const double*> in;
+    std::vector<double*> out;
+    for (const auto& b : bs) {
+      outs.emplace_back(b.shape());
+      outs.back().set_mass(b.mass());
+      in.push_back(reinterpret_cast<const double*>(b.data()));
+      out.push_back(reinterpret_cast<double*>(outs.back().data()));
+    }
+    check(kronop_sep_solve_host_batch(ctx_->get(), op_.get(), static_cast<int>(bs.size()),
+                                      in.data(), is_complex_v<S>, out.data()));
+    return outs;
+  }
   ComplexField propagate(const ComplexField& psi, double dt) const {
     ComplexField out(psi.shape());
     check(kronop_sep_propagate_host(ctx_->get(), op_.get(),

@@ -73,6 +73,26 @@ int main() {
       den += rhs[k] * rhs[k];
     }
     CHECK(std::sqrt(num / den) < 1e-12);
+    // the batched form (kronop_sep_solve_host_batch) equals solve() item by item
+    {
+      std::vector<RealField> bs;
+      for (int i = 0; i < 3; ++i) {
+        RealField r({n, n});
+        for (std::size_t k = 0; k < r.size(); ++k) r[k] = uniform(s);
+        bs.push_back(r);
+      }
+      const std::vector<RealField> xs = op.solve(bs);
+      CHECK(xs.size() == 3);
+      for (int i = 0; i < 3; ++i) {
+        const RealField xi = op.solve(bs[i]);
+        double dn = 0, dd = 0;
+        for (std::size_t k = 0; k < xi.size(); ++k) {
+          dn += (xs[i][k] - xi[k]) * (xs[i][k] - xi[k]);
+          dd += xi[k] * xi[k];
+        }
+        CHECK(std::sqrt(dn / dd) < 1e-15);
+      }
+    }
     op.set_shift(axes[0].eigenvalues[1] + axes[1].eigenvalues[3]);
     bool threw = false;
     try {
