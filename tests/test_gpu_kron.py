@@ -274,3 +274,30 @@ def test_kron_real_transform_bitwise(tmp_path):
     b = K.uniform_pm1(81, grid.node_count())
     assert rel(res["kron"]["s9x9x9"], ko.solve(b)) < 1e-13
     assert rel(res["kron"]["a9x9x9"], ko.apply(b)) < 1e-13
+
+
+def test_kron_paths_deterministic(ctx):
+    """Every new pipelined kernel path rerun 6 times gives bit-identical fields (a shared-memory or
+    stage-reuse race in the ring / done-counter / paired write-out logic would show up as a
+    run-to-run difference): the paired 9-point DFMA propagate, the DMMA n = 29 propagate, the
+    B-phase prologue inside evolve, the real small-extent solve and FullOperator apply
+    (acceptance.cpp:647-687 asks reruns to agree to 1e-12)."""
+    A = api()
+    runs = {}
+    for spec in ((3.0, 2, 5, 4), (5.0, 3, 10, 3), (2.0, 1, 6, 5)):
+        g = A.Grid.sem(*spec)
+        lap = g.laplacian(ctx)
+        op = g.separable_operator(ctx, [lambda t: t * t] * g.dim, shift=-0.5)
+        N = g.node_count()
+        psi = torch.view_as_complex(A.splitmix_uniform(ctx, 3, 2 * N).view(-1, 2))
+        b = 1.0 + A.splitmix_uniform(ctx, 4, N)
+        spec_ev = A.SplitSpec(quad_points=3, dt=0.005, total_time=0.02, merge_across_steps=False)
+        for rep in range(6):
+            st, _, _ = A.evolve(spec_ev, lap, b, psi, stationary_eigenvalue=0.0)
+            outs = [lap.propagate(psi, 0.005), st, op.solve(b),
+                    A.FullOperator(op, b).apply(b, sigma=0.3)]
+            if rep == 0:
+                runs[spec] = [o.clone() for o in outs]
+            else:
+                for o, r in zip(outs, runs[spec]):
+                    assert torch.equal(o, r), spec
