@@ -456,7 +456,8 @@ def secondary_metrics(A, P, ctx, device):
                          "frac": max(t_fp64, t_hbm) / t,
                          "note": "fp64 bound = the reference algorithm's flops (8 d n N) at the "
                                  "measured DGEMM rate; hbm bound = the launches' field round "
-                                 "trips at the measured copy bandwidth"},
+                                 "trips at the measured copy bandwidth",
+                         "own_algorithm": own_bound(d, n, N, t, t_hbm)},
             "config": "exp(-i dt (-Delta)) on %dD SEM n=%d complex128 (BASELINE configs[4] "
                       "kinetic step), dt = 0.005, Kronecker-factored: %d group launches, no "
                       "phase pass" % (d, n, launches)}
@@ -484,6 +485,21 @@ def secondary_metrics(A, P, ctx, device):
         del lap, psi
         torch.cuda.empty_cache()
     return out
+
+
+def own_bound(d, n, N, t, t_hbm):
+    """Roofline of the algorithm the Kronecker propagate actually runs on the config-5 grids (the
+    axes are parity-symmetric, so the folded blocks: per complex fiber and axis (M+c)^2 + M^2
+    complex multiply-adds = 8 ((M+c)^2 + M^2) flops, M = n / 2), at the FP64 instruction peak of
+    the unit it runs on (DFMA for n <= 10, DMMA above; profiles/r01_fp64_instr_peak.txt) against
+    the same HBM bound."""
+    m, me = n // 2, n // 2 + n % 2
+    flops = d * (N / n) * 8.0 * (me * me + m * m)
+    peak, unit = (33.92, "DFMA") if n <= 10 else (36.97, "DMMA")
+    t_fp = flops / (peak * 1e12)
+    return {"flops": flops, "peak_tflops": peak, "unit": unit, "fp64_bound_ms": t_fp * 1e3,
+            "hbm_bound_ms": t_hbm * 1e3, "bound": "fp64" if t_fp >= t_hbm else "hbm",
+            "frac": max(t_fp, t_hbm) / t}
 
 
 def folded_variant(A, grid, pot, ctx, b, x, bn, xn, op_dense, steps, world, local):
