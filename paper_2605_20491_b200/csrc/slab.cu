@@ -200,6 +200,7 @@ struct kronop_slab {
   // exchange-fused passes store into them over NVLink. 0 = not set up yet, 1 = on, -1 = off
   // (IPC unavailable or the collective self-check failed: grouped send / recv instead)
   int ipc = 0;
+  int ipc_c = 0;                           // field kind (1 real, 2 complex) the mapping was sized for
   std::vector<double*> peer_yx, peer_zx;  // [P], own buffers at this rank
   std::vector<void*> ipc_opened;
   double* bar = nullptr;                   // barrier all-gather buffer (1 + P doubles)
@@ -392,30 +393,47 @@ __global__ void k_ipc_probe(double* const* dsts, int P, int rank) {
 // NCCL, open the peers', and check the mapping end to end (every rank writes its id into every
 // rank's buffer through the mapped pointers, all-gather barrier, every rank reads them back);
 // all ranks then agree on the outcome, so a failure anywhere falls back everywhere.
-static void slab_ipc_setup(kronop_slab& s) {
+// Grow a receive buffer to `need` doubles without losing the old one on failure (false: out of
+// memory, old buffer kept -- the caller falls back to the copy / send-recv exchange).
+static bool grow_buffer(double*& p, size_t& cap, size_t need) {
+  if (cap >= need) return true;
+  double* q = nullptr;
+  if (cudaMalloc(&q, need * sizeof(double)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  if (p) KCUDA(cudaFree(p));
+  p = q;
+  cap = need;
+  return true;
+}
+
+// (Re)run for a field kind c larger than the mapped buffers were sized for (c = 2 after real
+// transforms); every rank reaches it at the same transform, so it stays collective.
+static void slab_ipc_setup(kronop_slab& s, int c) {
   SlabPart& me = s.parts[0];
   part_device(me);
   cudaStream_t st = me.ctx->stream;
   const int P = s.P, r = me.p;
-  bool ok = true;
-  try {
+  KCUDA(cudaStreamSynchronize(st));
+  if (!s.bar) {
     KCUDA(cudaMalloc(&s.bar, (1 + P) * sizeof(double)));
     KCUDA(cudaMemsetAsync(s.bar, 0, (1 + P) * sizeof(double), st));
-    const size_t zneed = static_cast<size_t>(zslab_elems(s, r)) * 2;
-    const size_t yneed = static_cast<size_t>(yslab_elems(s, r)) * 2;
+  }
+  // a re-setup: every rank drops its mappings of the peers' buffers, and all have dropped them
+  // before anyone frees a buffer it exported
+  const bool had = !s.ipc_opened.empty() || s.ipc > 0;
+  for (void* p : s.ipc_opened) cudaIpcCloseMemHandle(p);
+  s.ipc_opened.clear();
+  if (had) {
+    nccl_barrier(s);
     KCUDA(cudaStreamSynchronize(st));
-    if (me.zx_cap < zneed) {
-      if (me.zx) KCUDA(cudaFree(me.zx));
-      me.zx = nullptr;
-      KCUDA(cudaMalloc(&me.zx, zneed * sizeof(double)));
-      me.zx_cap = zneed;
-    }
-    if (me.yx_cap < yneed) {
-      if (me.yx) KCUDA(cudaFree(me.yx));
-      me.yx = nullptr;
-      KCUDA(cudaMalloc(&me.yx, yneed * sizeof(double)));
-      me.yx_cap = yneed;
-    }
+  }
+  bool ok = true;
+  try {
+    const size_t zneed = static_cast<size_t>(zslab_elems(s, r)) * c;
+    const size_t yneed = static_cast<size_t>(yslab_elems(s, r)) * c;
+    ok = grow_buffer(me.zx, me.zx_cap, zneed) && grow_buffer(me.yx, me.yx_cap, yneed);
   } catch (...) {
     ok = false;
   }
@@ -487,6 +505,7 @@ static void slab_ipc_setup(kronop_slab& s) {
   KCUDA(cudaFree(dh));
   KCUDA(cudaFree(dptrs));
   s.ipc = ok ? 1 : -1;
+  s.ipc_c = c;
 }
 
 // Exchange-fused transform (in-process transport, or NCCL with the peers' buffers mapped by CUDA
@@ -521,8 +540,18 @@ static bool slab_fused_ok(kronop_slab& s, int c) {
       return false;
   }
   if (s.nccl) {
-    if (s.ipc == 0) slab_ipc_setup(s);
+    if (s.ipc == 0 || (s.ipc > 0 && c > s.ipc_c)) slab_ipc_setup(s, c);
     return s.ipc > 0;
+  }
+  // in process: the y-slab receive buffers (one slab more than the copy exchange needs); out of
+  // memory -> the copy exchange
+  for (auto& pt : s.parts) {
+    part_device(pt);
+    const size_t yneed = static_cast<size_t>(yslab_elems(s, pt.p)) * c;
+    if (pt.yx_cap < yneed) {
+      KCUDA(cudaStreamSynchronize(pt.ctx->stream));
+      if (!grow_buffer(pt.yx, pt.yx_cap, yneed)) return false;
+    }
   }
   return true;
 }
@@ -533,18 +562,6 @@ static void slab_transform_fused(kronop_slab& s, const std::vector<const double*
   const int d = s.d;
   const long long Rc = s.R * c;
   const int ny = s.n[d - 2];
-  if (!s.nccl)
-    for (auto& pt : s.parts) {
-      part_device(pt);
-      const size_t yneed = static_cast<size_t>(yslab_elems(s, pt.p)) * c;
-      if (yneed > pt.yx_cap) {
-        KCUDA(cudaStreamSynchronize(pt.ctx->stream));
-        if (pt.yx) KCUDA(cudaFree(pt.yx));
-        pt.yx = nullptr;
-        KCUDA(cudaMalloc(&pt.yx, yneed * sizeof(double)));
-        pt.yx_cap = yneed;
-      }
-    }
   // destination buffers of every part (the local ones, or the IPC-mapped peers')
   std::vector<double*> yx(s.P, nullptr), zx(s.P, nullptr);
   if (s.nccl) {
@@ -692,8 +709,11 @@ static void slab_transform(kronop_slab& s, const std::vector<const double*>& in,
                            const std::vector<double*>& out, int cplx, const SlabEpi& e) {
   const int c = cplx ? 2 : 1;
   const int d = s.d;
+  // the fused-exchange decision first: on the NCCL transport it may (collectively) re-map the
+  // receive buffers, which must not be reallocated under the peers' mappings
+  const bool fused = slab_fused_ok(s, c);
   ensure_part_buffers(s, c);
-  if (slab_fused_ok(s, c)) {
+  if (fused) {
     slab_transform_fused(s, in, out, cplx, e);
     ++s.fused_transforms;
     return;
