@@ -734,7 +734,13 @@ static void run_schedules(kronop_ctx& c, const kronop_op& a, const double* b_dia
   for (const Schedule& sc : schedules)
     for (double f : sc.b_factors)
       if (std::find(factors.begin(), factors.end(), f) == factors.end()) factors.push_back(f);
-  bool use_pre = !pre_off && unfused && steps * schedules.size() > 1 && kron_path_likely(a);
+  // worth it when the B phases outnumber the tables to make (one pass each): every run with more
+  // than one step, and single qHOP / Yoshida steps with repeated factors
+  long long nb = 0;
+  for (const Schedule& sc : schedules) nb += static_cast<long long>(sc.b_factors.size());
+  nb *= steps;
+  bool use_pre = !pre_off && unfused && nb > static_cast<long long>(factors.size()) &&
+                 kron_path_likely(a);
   if (use_pre) {  // the tables (2N doubles each) must leave room for the rest of the run
     size_t free_b = 0, total_b = 0;
     KCUDA(cudaMemGetInfo(&free_b, &total_b));
